@@ -1,0 +1,184 @@
+/*
+ * rfb.h -- C ABI of the B200 Radiant Foam hot path (librfb.so, sm_100a).
+ *
+ * Plain pointers and sizes only.  Every pointer is a DEVICE pointer unless
+ * marked (host); `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream).  Calls enqueue work on `stream` and return without
+ * synchronising.  Return value: 0 (RFB_OK) on success, RFB_EINVAL (-1) for an
+ * argument error, or a positive cudaError_t from the launch.
+ *
+ * Each entry point replaces one reference operator (paths are relative to
+ * the reference tree pkg/src/rfoam/):
+ *
+ *   rfb_pack_scene      diffrender/render.py:49-54  scene_arrays()  (+ the
+ *                        int64 -> int32 CSR narrowing and the per-site
+ *                        {x,y,z,sigma} record the kernels gather)
+ *   rfb_softplus        foam.py:22-25               softplus()  (device-side
+ *                        activation for device-resident training; the parity
+ *                        shim uploads the host numpy value instead)
+ *   rfb_camera_rays     tracer/camera.py:66-92      CameraModel.ray_directions()
+ *                        (pinhole branch, lines 80-83/91-92)
+ *   rfb_locate          geometry/adjacency.py:85-100 nearest_site()
+ *                        (greedy walk on the CSR; same distance expression
+ *                        and lowest-id tie rule as _grid_nearest 140-203)
+ *   rfb_render_rays     tracer/kernels.py:199-247   render_rays()
+ *                        (walk_ray 76-162 + sh_basis_into 38-58 +
+ *                        cell_color 61-73 + composite_segments 165-196)
+ *   rfb_render_image    diffrender/render.py:128-149 render_image() (fused
+ *                        ray generation + shared-origin start cell + render,
+ *                        over a list of image tiles for multi-GPU sharding)
+ *   rfb_backward_rays   diffrender/render.py:152-221 render_rays_with_gradients()
+ *                        (backward_ray 250-337 + face_t_gradient 340-369)
+ *   rfb_train_batch     tracer/kernels.py:372-453   train_batch()
+ *                        (+ quantile_backward_ray 456-567)
+ *
+ * Per-ray status semantics are the reference's (tracer/kernels.py:11-21):
+ * 0 ok, 2 step limit, 3 cycle; failed rays render the background with
+ * residual 1, wsum 0 and contribute no gradient.
+ */
+#ifndef RFB_H
+#define RFB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RFB_OK 0
+#define RFB_EINVAL (-1)
+
+#define RFB_STATUS_OK 0
+#define RFB_STATUS_STEP_LIMIT 2
+#define RFB_STATUS_CYCLE 3
+
+#define RFB_ABI_VERSION 1
+
+/* Device-resident scene, produced by rfb_pack_scene. */
+typedef struct rfb_scene {
+    int64_t n_sites;
+    int64_t n_edges;
+    const double *site4;      /* [n_sites][4]: x, y, z, sigma (activated density) */
+    const int32_t *offsets;   /* [n_sites + 1] CSR row starts */
+    const int32_t *neighbors; /* [n_edges] ascending per site */
+    const double *sh;         /* [n_sites][48], index k*3 + ch (render.py:53) */
+    int32_t sh_degree;        /* 0: read the DC band only (exact when bands 1..15 are
+                                 all zero), 3: all 16 bands */
+    int32_t pad_;
+    double background[3];     /* (host value) */
+} rfb_scene;
+
+/* Walk parameters (tracer/rays.py:12-14). */
+typedef struct rfb_params {
+    double epsilon;       /* early-termination transmittance, 0 disables */
+    double width_floor;   /* WIDTH_FLOOR_SCALE * diagonal */
+    int32_t step_limit;   /* hard per-ray cell cap */
+    int32_t lanes_per_ray;/* 0 = library default; 1, 2, 4, 8, 16 or 32 lanes cooperate
+                             on one ray (forward only) */
+} rfb_params;
+
+/* A batch of rays (render.py:57-125 arguments). */
+typedef struct rfb_rays {
+    int64_t m;
+    const double *origins;     /* [m][3] */
+    const double *directions;  /* [m][3], unit length */
+    const double *t_min;       /* [m] */
+    const double *t_max;       /* [m] */
+    const int32_t *start_sites;/* [m] */
+} rfb_rays;
+
+/* Forward outputs.  rgb/residual/wsum are float32 unless f64_outputs != 0,
+ * in which case they are float64.  Nullable fields are skipped. */
+typedef struct rfb_fwd_out {
+    void *rgb;                 /* [m][3] (required) */
+    void *residual;            /* [m] nullable */
+    void *wsum;                /* [m] nullable */
+    int8_t *status;            /* [m] nullable */
+    int32_t *nseg;             /* [m] nullable: recorded segments per ray */
+    int32_t *ray_counters;     /* [m][2] nullable: cells stepped, neighbour visits */
+    unsigned long long *counters; /* [2] nullable: totals, ACCUMULATED (kernels.py:8-9) */
+    int32_t f64_outputs;
+    int32_t seg_capacity;      /* > 0 enables the segment dump below */
+    int32_t *seg_cells;        /* [m][seg_capacity] */
+    double *seg_t0;            /* [m][seg_capacity] */
+    double *seg_t1;            /* [m][seg_capacity] */
+} rfb_fwd_out;
+
+/* Gradient accumulators (ACCUMULATED, like the reference's += buffers).
+ * One flat float32 allocation of n_sites * 52 floats is the intended layout:
+ * site4g = [n][4] (dpos x, y, z, dsigma) followed by sh = [n][48]. */
+typedef struct rfb_grads {
+    float *site4g;  /* [n][4]: dL/dposition (3) and dL/dsigma (activated) */
+    float *sh;      /* [n][48] */
+} rfb_grads;
+
+/* Pinhole camera (camera.py:20-60). pose is row-major world-from-camera. */
+typedef struct rfb_camera {
+    double pose[16]; /* (host value) */
+    int32_t width;
+    int32_t height;
+    double focal;
+    double cx;
+    double cy;
+} rfb_camera;
+
+int rfb_abi_version(void);
+const char *rfb_error_string(int code); /* (host) static string */
+int rfb_device_ok(void);                /* 1 when an sm_100 device is current */
+
+/* positions [n][3] f64, sigma [n] f64, offsets [n+1] i64, neighbors [E] i64
+ * -> site4 [n][4] f64, offsets32 [n+1], neighbors32 [E]. */
+int rfb_pack_scene(const double *positions, const double *sigma, const int64_t *offsets,
+                   const int64_t *neighbors, int64_t n_sites, int64_t n_edges, double *site4,
+                   int32_t *offsets32, int32_t *neighbors32, void *stream);
+
+/* out[k] = softplus_10(raw[k]); optionally also written into site4[k][3]. */
+int rfb_softplus(const double *raw, int64_t n, double *out, double *site4_sigma, void *stream);
+
+/* dirs [pix_count][3] f64 for row-major pixels pix_begin .. pix_begin+count-1. */
+int rfb_camera_rays(const rfb_camera *camera, int64_t pix_begin, int64_t pix_count,
+                    double *dirs, void *stream);
+
+/* out[q] = nearest site to queries[q] (greedy CSR walk from seed_site). */
+int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t seed_site,
+               int32_t *out, void *stream);
+
+int rfb_render_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,
+                    const rfb_fwd_out *out, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Renders the listed tile_w x tile_h pixel tiles (tile id = ty * tiles_x + tx,
+ * tiles_x = ceil(W / tile_w)) of the frame; outputs are full-frame [H*W]
+ * arrays indexed by pixel (row-major), untouched outside the listed tiles.
+ * start_site < 0: locate the camera position's nearest site on device from
+ * seed site 0.  t_max <= 0: render.py:72-76 fallback computed by the caller. */
+int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb_params *params,
+                     double t_min, double t_max, int32_t start_site, const int32_t *tile_ids,
+                     int64_t n_tiles, int32_t tile_w, int32_t tile_h, const rfb_fwd_out *out,
+                     void *workspace, size_t workspace_bytes, void *stream);
+
+/* Workspace bytes needed by the calls above for m rays (kind: 0 forward,
+ * 1 backward/train). */
+size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind);
+
+/* Forward + reverse pass for arbitrary colour adjoints [m][3] f64.  out.rgb
+ * receives the forward colour; gradients accumulate into grads. */
+int rfb_backward_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,
+                      const double *adjoints, const rfb_fwd_out *out, const rfb_grads *grads,
+                      void *workspace, size_t workspace_bytes, void *stream);
+
+/* Fused training pass: L2 adjoint 2*rgb_scale*(rgb - target) plus, when
+ * quantile_scale > 0, n_pairs Monte-Carlo quantile pairs per ray
+ * (u_pairs [m][n_pairs][2] f64).  loss [2] f64 ACCUMULATES (sum sq err,
+ * sum quantile terms) like loss_w in kernels.py:433,445. */
+int rfb_train_batch(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,
+                    const double *targets, double rgb_scale, double quantile_scale,
+                    const double *u_pairs, int32_t n_pairs, double weight_floor,
+                    const rfb_fwd_out *out, const rfb_grads *grads, double *loss,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RFB_H */

@@ -1,0 +1,370 @@
+"""Device-resident scene and the torch-level calls into librfb.so.
+
+PyTorch is plumbing here: it owns device memory and streams; all compute is
+in the sm_100a kernels behind the C ABI (include/rfb.h).  Layout in HBM
+(DESIGN.md §3):
+
+* ``site4``    float64 [n, 4]  x, y, z, sigma  -- one 32-byte record per site,
+                                the only per-neighbour gather of the walk;
+* ``offsets``  int32 [n+1], ``neighbors`` int32 [E]  -- the reference CSR
+                                (ascending per site), narrowed from int64;
+* ``sh``       float64 [n, 48] -- index k*3+ch as render.py:53;
+* gradients    float32 [n, 52] -- ``[n,4]`` (dpos xyz, dsigma) then ``[n,48]``
+                                (dSH); one flat buffer so a single NCCL
+                                all-reduce covers it.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .scene import softplus
+
+DEFAULT_EPSILON = 1e-3     # tracer/rays.py:12
+DEFAULT_STEP_LIMIT = 4096  # tracer/rays.py:13
+WIDTH_FLOOR_SCALE = 1e-12  # tracer/rays.py:14
+DEFAULT_LANES = 1
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def sh_degree_of(sh_coeffs: np.ndarray) -> int:
+    """0 when bands 1..15 are all exactly zero (the DC-only kernel is then
+    bit-identical), else 3."""
+    return 0 if not np.any(sh_coeffs.reshape(len(sh_coeffs), 16, 3)[:, 1:, :]) else 3
+
+
+class DeviceScene:
+    """Kernel-ready copy of a scene on one GPU (render.py:49-54 scene_arrays).
+
+    sigma is activated on the host with the reference's numpy softplus
+    (foam.py:22-25) so it is bit-identical; ``set_raw_density`` activates on
+    device instead (device-resident training).
+    """
+
+    def __init__(self, scene, device=None, sh_degree=None):
+        adj = scene.require_adjacency()
+        sh = np.asarray(scene.sh_coeffs, dtype=np.float64).reshape(len(adj.positions), 48)
+        self._init(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density), sh,
+                   scene.background, adj.bbox_lo, adj.bbox_hi, device, sh_degree)
+
+    @classmethod
+    def from_arrays(cls, positions, offsets, neighbors, sigma, sh_flat, background, device=None,
+                    sh_degree=None):
+        """Flat kernel arrays as passed to kernels.render_rays (kernels.py:199-209)."""
+        self = cls.__new__(cls)
+        pos = np.asarray(positions, dtype=np.float64)
+        self._init(pos, offsets, neighbors, sigma, sh_flat, background, pos.min(axis=0),
+                   pos.max(axis=0), device, sh_degree)
+        return self
+
+    def _init(self, positions, offsets, neighbors, sigma, sh_flat, background, bbox_lo, bbox_hi,
+              device, sh_degree):
+        self.lib = _lib.load()
+        self.device = torch.device(device or "cuda")
+        pos = np.ascontiguousarray(positions, dtype=np.float64)
+        n = len(pos)
+        self.n_sites = n
+        self.n_edges = int(len(neighbors))
+        self.bbox_lo = np.asarray(bbox_lo, dtype=np.float64)
+        self.bbox_hi = np.asarray(bbox_hi, dtype=np.float64)
+        self.diagonal = float(np.linalg.norm(self.bbox_hi - self.bbox_lo))
+        self.center = 0.5 * (self.bbox_lo + self.bbox_hi)
+        self.width_floor = WIDTH_FLOOR_SCALE * self.diagonal
+        self.background = np.asarray(background, dtype=np.float64).copy()
+        sh = np.ascontiguousarray(np.asarray(sh_flat, dtype=np.float64).reshape(n, 48))
+        self.sh_degree = sh_degree_of(sh) if sh_degree is None else int(sh_degree)
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        dev = self.device
+        with torch.cuda.device(dev):
+            self.site4 = torch.empty((n, 4), dtype=torch.float64, device=dev)
+            self.offsets = torch.empty(n + 1, dtype=torch.int32, device=dev)
+            self.neighbors = torch.empty(max(self.n_edges, 1), dtype=torch.int32, device=dev)
+            self.sh = torch.from_numpy(sh).to(dev)
+            pos_d = torch.from_numpy(pos).to(dev)
+            sig_d = torch.from_numpy(sigma).to(dev)
+            off_d = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
+            nbr_d = torch.from_numpy(np.ascontiguousarray(neighbors, dtype=np.int64)).to(dev)
+            _lib.check(self.lib.rfb_pack_scene(
+                _ptr(pos_d), _ptr(sig_d), _ptr(off_d), _ptr(nbr_d), n, self.n_edges,
+                _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors), _stream()),
+                "rfb_pack_scene")
+            torch.cuda.current_stream().synchronize()
+        self._c = _lib.rfb_scene()
+        self._refresh_struct()
+
+    def _refresh_struct(self):
+        c = self._c
+        c.n_sites = self.n_sites
+        c.n_edges = self.n_edges
+        c.site4 = self.site4.data_ptr()
+        c.offsets = self.offsets.data_ptr()
+        c.neighbors = self.neighbors.data_ptr()
+        c.sh = self.sh.data_ptr()
+        c.sh_degree = self.sh_degree
+        for k in range(3):
+            c.background[k] = float(self.background[k])
+
+    @property
+    def c(self):
+        return ctypes.byref(self._c)
+
+    # -- device-resident updates (training) ------------------------------
+    def set_raw_density(self, raw: torch.Tensor, stream=None):
+        raw = raw.to(self.device, torch.float64).contiguous()
+        _lib.check(self.lib.rfb_softplus(_ptr(raw), self.n_sites, None,
+                                         ctypes.c_void_p(self.site4.data_ptr() + 24),
+                                         _stream(stream)), "rfb_softplus")
+
+    def default_t_max(self, origins: np.ndarray) -> float:
+        """Batch fallback t_max (render.py:72-76)."""
+        o = np.asarray(origins, dtype=np.float64).reshape(-1, 3)
+        return float(np.linalg.norm(o - self.center, axis=1).max() + 2.0 * self.diagonal + 1.0)
+
+    def locate(self, queries: torch.Tensor, seed: int = 0, stream=None) -> torch.Tensor:
+        q = queries.to(self.device, torch.float64).contiguous()
+        m = q.shape[0]
+        out = torch.empty(m, dtype=torch.int32, device=self.device)
+        _lib.check(self.lib.rfb_locate(self.c, _ptr(q), m, int(seed), _ptr(out), _stream(stream)),
+                   "rfb_locate")
+        return out
+
+
+def make_params(epsilon=DEFAULT_EPSILON, width_floor=0.0, step_limit=DEFAULT_STEP_LIMIT,
+                lanes_per_ray=DEFAULT_LANES):
+    p = _lib.rfb_params()
+    p.epsilon = float(epsilon)
+    p.width_floor = float(width_floor)
+    p.step_limit = int(step_limit)
+    p.lanes_per_ray = int(lanes_per_ray)
+    return p
+
+
+@dataclass
+class ForwardResult:
+    rgb: torch.Tensor
+    residual: torch.Tensor
+    wsum: torch.Tensor
+    status: torch.Tensor
+    nseg: torch.Tensor | None = None
+    ray_counters: torch.Tensor | None = None
+    counters: torch.Tensor | None = None
+    seg_cells: torch.Tensor | None = None
+    seg_t0: torch.Tensor | None = None
+    seg_t1: torch.Tensor | None = None
+
+
+class Workspace:
+    """Grow-only device scratch (no allocation on the steady-state path)."""
+
+    def __init__(self, device):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self.buf
+
+
+def alloc_forward(m: int, device, f64=False, per_ray=True, seg_capacity=0) -> ForwardResult:
+    fdt = torch.float64 if f64 else torch.float32
+    r = ForwardResult(
+        rgb=torch.empty((m, 3), dtype=fdt, device=device),
+        residual=torch.empty(m, dtype=fdt, device=device),
+        wsum=torch.empty(m, dtype=fdt, device=device),
+        status=torch.empty(m, dtype=torch.int8, device=device),
+        counters=torch.zeros(2, dtype=torch.int64, device=device),
+    )
+    if per_ray:
+        r.nseg = torch.empty(m, dtype=torch.int32, device=device)
+        r.ray_counters = torch.empty((m, 2), dtype=torch.int32, device=device)
+    if seg_capacity > 0:
+        r.seg_cells = torch.full((m, seg_capacity), -1, dtype=torch.int32, device=device)
+        r.seg_t0 = torch.zeros((m, seg_capacity), dtype=torch.float64, device=device)
+        r.seg_t1 = torch.zeros((m, seg_capacity), dtype=torch.float64, device=device)
+    return r
+
+
+def fwd_struct(r: ForwardResult) -> _lib.rfb_fwd_out:
+    o = _lib.rfb_fwd_out()
+    o.rgb = r.rgb.data_ptr()
+    o.residual = r.residual.data_ptr() if r.residual is not None else None
+    o.wsum = r.wsum.data_ptr() if r.wsum is not None else None
+    o.status = r.status.data_ptr() if r.status is not None else None
+    o.nseg = r.nseg.data_ptr() if r.nseg is not None else None
+    o.ray_counters = r.ray_counters.data_ptr() if r.ray_counters is not None else None
+    o.counters = r.counters.data_ptr() if r.counters is not None else None
+    o.f64_outputs = 1 if r.rgb.dtype == torch.float64 else 0
+    if r.seg_cells is not None:
+        o.seg_capacity = r.seg_cells.shape[1]
+        o.seg_cells = r.seg_cells.data_ptr()
+        o.seg_t0 = r.seg_t0.data_ptr()
+        o.seg_t1 = r.seg_t1.data_ptr()
+    else:
+        o.seg_capacity = 0
+    return o
+
+
+def rays_struct(origins, directions, t_min, t_max, start) -> _lib.rfb_rays:
+    r = _lib.rfb_rays()
+    r.m = origins.shape[0]
+    r.origins = origins.data_ptr()
+    r.directions = directions.data_ptr()
+    r.t_min = t_min.data_ptr()
+    r.t_max = t_max.data_ptr()
+    r.start_sites = start.data_ptr()
+    return r
+
+
+def camera_struct(camera) -> _lib.rfb_camera:
+    c = _lib.rfb_camera()
+    pose = np.asarray(camera.pose, dtype=np.float64).reshape(16)
+    for k in range(16):
+        c.pose[k] = float(pose[k])
+    c.width = int(camera.width)
+    c.height = int(camera.height)
+    c.focal = float(camera.focal)
+    c.cx = float(camera.cx)
+    c.cy = float(camera.cy)
+    return c
+
+
+def render_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start, *,
+                       epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
+                       per_ray=True, seg_capacity=0, lanes_per_ray=DEFAULT_LANES,
+                       workspace: Workspace | None = None, out: ForwardResult | None = None,
+                       stream=None) -> ForwardResult:
+    """rfb_render_rays on device tensors (kernels.py:199-247)."""
+    m = origins.shape[0]
+    res = out or alloc_forward(m, ds.device, f64=f64, per_ray=per_ray, seg_capacity=seg_capacity)
+    ws = (workspace or Workspace(ds.device)).get(256)
+    p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
+    rays = rays_struct(origins, directions, t_min, t_max, start)
+    o = fwd_struct(res)
+    _lib.check(ds.lib.rfb_render_rays(ds.c, ctypes.byref(rays), ctypes.byref(p), ctypes.byref(o),
+                                      _ptr(ws), ws.numel(), _stream(stream)), "rfb_render_rays")
+    return res
+
+
+def tile_grid(width: int, height: int, tile_w: int = 32, tile_h: int = 32):
+    tiles_x = (width + tile_w - 1) // tile_w
+    tiles_y = (height + tile_h - 1) // tile_h
+    return tiles_x, tiles_y
+
+
+def render_image_device(ds: DeviceScene, camera, *, epsilon=DEFAULT_EPSILON,
+                        step_limit=DEFAULT_STEP_LIMIT, t_max=None, start_site=-1, tile_ids=None,
+                        tile_w=32, tile_h=32, f64=False, per_ray=False,
+                        lanes_per_ray=DEFAULT_LANES, workspace: Workspace | None = None,
+                        out: ForwardResult | None = None, stream=None) -> ForwardResult:
+    """Fused ray generation + render over a tile list (render.py:128-149)."""
+    W, H = int(camera.width), int(camera.height)
+    m = W * H
+    if tile_ids is None:
+        tx, ty = tile_grid(W, H, tile_w, tile_h)
+        tile_ids = torch.arange(tx * ty, dtype=torch.int32, device=ds.device)
+    res = out or alloc_forward(m, ds.device, f64=f64, per_ray=per_ray)
+    ws = (workspace or Workspace(ds.device)).get(256)
+    if t_max is None:
+        t_max = ds.default_t_max(np.asarray(camera.pose)[:3, 3][None, :])
+    p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
+    cam = camera_struct(camera)
+    o = fwd_struct(res)
+    _lib.check(ds.lib.rfb_render_image(ds.c, ctypes.byref(cam), ctypes.byref(p), 0.0, float(t_max),
+                                       int(start_site), _ptr(tile_ids), int(tile_ids.numel()),
+                                       int(tile_w), int(tile_h), ctypes.byref(o), _ptr(ws),
+                                       ws.numel(), _stream(stream)), "rfb_render_image")
+    return res
+
+
+class GradBuffers:
+    """Flat float32 [n, 52] gradient accumulator: view ``g4`` [n,4]
+    (dpos xyz, dsigma) and ``sh`` [n,48] (rfb_grads)."""
+
+    def __init__(self, n: int, device):
+        self.n = n
+        self.flat = torch.zeros(n * 52, dtype=torch.float32, device=device)
+        self.g4 = self.flat[: 4 * n].view(n, 4)
+        self.sh = self.flat[4 * n:].view(n, 48)
+
+    def zero_(self):
+        self.flat.zero_()
+
+    def struct(self):
+        g = _lib.rfb_grads()
+        g.site4g = self.g4.data_ptr()
+        g.sh = self.sh.data_ptr()
+        return g
+
+    @property
+    def d_position(self):
+        return self.g4[:, :3]
+
+    @property
+    def d_sigma(self):
+        return self.g4[:, 3]
+
+
+def backward_workspace_bytes(ds: DeviceScene, m: int, step_limit: int) -> int:
+    return int(ds.lib.rfb_workspace_bytes(int(m), int(step_limit), 1))
+
+
+def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start, adjoints,
+                         grads: GradBuffers, *, epsilon=DEFAULT_EPSILON,
+                         step_limit=DEFAULT_STEP_LIMIT, f64=False,
+                         workspace: Workspace | None = None, out: ForwardResult | None = None,
+                         stream=None) -> ForwardResult:
+    """rfb_backward_rays (render.py:152-221 generic adjoint)."""
+    m = origins.shape[0]
+    res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
+    ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
+    p = make_params(epsilon, ds.width_floor, step_limit, 1)
+    rays = rays_struct(origins, directions, t_min, t_max, start)
+    o = fwd_struct(res)
+    g = grads.struct()
+    adj = adjoints.to(ds.device, torch.float64).contiguous()
+    _lib.check(ds.lib.rfb_backward_rays(ds.c, ctypes.byref(rays), ctypes.byref(p), _ptr(adj),
+                                        ctypes.byref(o), ctypes.byref(g), _ptr(ws), ws.numel(),
+                                        _stream(stream)), "rfb_backward_rays")
+    return res
+
+
+def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start, targets,
+                       grads: GradBuffers, loss: torch.Tensor, *, rgb_scale: float,
+                       quantile_scale: float = 0.0, u_pairs=None, weight_floor: float = 1e-4,
+                       epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
+                       workspace: Workspace | None = None, out: ForwardResult | None = None,
+                       stream=None) -> ForwardResult:
+    """rfb_train_batch (kernels.py:372-453).  ``loss`` float64 [2] accumulates."""
+    m = origins.shape[0]
+    res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
+    ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
+    p = make_params(epsilon, ds.width_floor, step_limit, 1)
+    rays = rays_struct(origins, directions, t_min, t_max, start)
+    o = fwd_struct(res)
+    g = grads.struct()
+    n_pairs = 0
+    up = None
+    if quantile_scale > 0.0:
+        up = u_pairs.to(ds.device, torch.float64).contiguous()
+        n_pairs = up.shape[1]
+    _lib.check(ds.lib.rfb_train_batch(ds.c, ctypes.byref(rays), ctypes.byref(p), _ptr(targets),
+                                      float(rgb_scale), float(quantile_scale), _ptr(up), n_pairs,
+                                      float(weight_floor), ctypes.byref(o), ctypes.byref(g),
+                                      _ptr(loss), _ptr(ws), ws.numel(), _stream(stream)),
+               "rfb_train_batch")
+    return res

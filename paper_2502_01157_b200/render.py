@@ -1,0 +1,304 @@
+"""Drop-in replacements for the reference's Python render entry points.
+
+Same names, argument meaning, defaults, return types and error behaviour as
+rfoam/diffrender/render.py and rfoam/tracer/rays.py; the arithmetic runs in
+librfb.so on the current CUDA device.  Host numpy arrays go in and come out
+(fp64, like the reference); pass ``device_scene=`` to reuse a resident
+scene instead of uploading it on every call (the reference re-derives its
+kernel arrays on every call too, render.py:49-54).
+
+  render_ray_batch            render.py:57-125
+  render_image                render.py:128-149
+  render_rays_with_gradients  render.py:152-221
+  trace                       rays.py:81-115
+  RenderStats                 render.py:27-46
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as dv
+from .errors import CycleDetected, ShapeMismatch, StepLimit
+from .scene import GradientBuffer, softplus, softplus_grad
+
+DEFAULT_EPSILON = dv.DEFAULT_EPSILON
+DEFAULT_STEP_LIMIT = dv.DEFAULT_STEP_LIMIT
+WIDTH_FLOOR_SCALE = dv.WIDTH_FLOOR_SCALE
+
+STATUS_OK = 0
+STATUS_STEP_LIMIT = 2
+STATUS_CYCLE = 3
+
+
+@dataclass
+class RenderStats:
+    rays: int = 0
+    cells_stepped: int = 0
+    neighbor_visits: int = 0
+    grid_queries: int = 0
+    failed_rays: int = 0
+    seconds: float = 0.0
+
+    @property
+    def rays_per_sec(self):
+        return self.rays / self.seconds if self.seconds > 0 else 0.0
+
+    def merge(self, other):
+        self.rays += other.rays
+        self.cells_stepped += other.cells_stepped
+        self.neighbor_visits += other.neighbor_visits
+        self.grid_queries += other.grid_queries
+        self.failed_rays += other.failed_rays
+        self.seconds += other.seconds
+
+
+@dataclass
+class Ray:
+    """rays.py:17-36 (validated single ray)."""
+    origin: np.ndarray
+    direction: np.ndarray
+    t_min: float = 0.0
+    t_max: float = np.inf
+
+    def __post_init__(self):
+        self.origin = np.asarray(self.origin, dtype=np.float64)
+        self.direction = np.asarray(self.direction, dtype=np.float64)
+        if self.origin.shape != (3,) or self.direction.shape != (3,):
+            raise ShapeMismatch("ray origin/direction must be 3-vectors")
+        norm = float(np.linalg.norm(self.direction))
+        if abs(norm - 1.0) > 1e-6:
+            raise ValueError(f"ray direction not unit length (|d| = {norm:g})")
+        if not (0.0 <= self.t_min < self.t_max):
+            raise ValueError("require 0 <= t_min < t_max")
+
+    def at(self, t):
+        return self.origin + t * self.direction
+
+
+@dataclass
+class RaySegments:
+    """rays.py:39-57."""
+    cells: np.ndarray
+    t_entry: np.ndarray
+    t_exit: np.ndarray
+    residual_transmittance: float
+    status: int = STATUS_OK
+
+    def __len__(self):
+        return len(self.cells)
+
+    def widths(self):
+        return self.t_exit - self.t_entry
+
+    def midpoints(self, ray):
+        mid = 0.5 * (self.t_entry + self.t_exit)
+        return ray.origin[None, :] + mid[:, None] * ray.direction[None, :]
+
+
+def _default_t_max(adj, ray):
+    """rays.py:118-120."""
+    to_center = 0.5 * (adj.bbox_lo + adj.bbox_hi) - ray.origin
+    return float(np.linalg.norm(to_center) + 2.0 * adj.diagonal + 1.0)
+
+
+def _device_scene(scene, device_scene):
+    if device_scene is not None:
+        return device_scene
+    return dv.DeviceScene(scene)
+
+
+def _to_dev(a, dtype, device):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=dtype)).to(device, non_blocking=False)
+
+
+def render_ray_batch(scene, origins, directions, t_min=None, t_max=None, start_sites=None,
+                     epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, workers=None,
+                     stats=None, return_wsum=False, device_scene=None,
+                     lanes_per_ray=dv.DEFAULT_LANES):
+    """Forward-render arbitrary rays; returns (rgb, residual, status[, wsum]).
+
+    ``workers`` is accepted for signature compatibility (the GPU has no
+    worker pool).  Start cells: one device point location when all origins
+    coincide, else one per ray (render.py:78-90).
+    """
+    ds = _device_scene(scene, device_scene)
+    dev = ds.device
+    origins = np.ascontiguousarray(origins, dtype=np.float64)
+    directions = np.ascontiguousarray(directions, dtype=np.float64)
+    m = len(origins)
+    if t_min is None:
+        t_min = np.zeros(m)
+    if t_max is None:
+        t_max = np.full(m, np.nan)
+    t_min = np.ascontiguousarray(t_min, dtype=np.float64)
+    t_max = np.ascontiguousarray(t_max, dtype=np.float64)
+    if m > 0:
+        fallback = ds.default_t_max(origins)
+        t_max = np.where(np.isfinite(t_max), t_max, fallback)
+    o_d = _to_dev(origins.reshape(m, 3), np.float64, dev)
+    d_d = _to_dev(directions.reshape(m, 3), np.float64, dev)
+    tmin_d = _to_dev(t_min, np.float64, dev)
+    tmax_d = _to_dev(t_max, np.float64, dev)
+    if start_sites is None:
+        if m > 0 and np.ptp(origins, axis=0).max() == 0.0:
+            s0 = ds.locate(o_d[:1])
+            start_d = s0.expand(m).contiguous()
+            grid_queries = 1
+        elif m > 0:
+            seed = int(ds.locate(o_d[:1]).item())
+            start_d = ds.locate(o_d, seed=seed)
+            grid_queries = m
+        else:
+            start_d = torch.empty(0, dtype=torch.int32, device=dev)
+            grid_queries = 0
+    else:
+        start_d = _to_dev(start_sites, np.int32, dev)
+        grid_queries = 0
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    res = dv.render_rays_device(ds, o_d, d_d, tmin_d, tmax_d, start_d, epsilon=epsilon,
+                                step_limit=step_limit, f64=True, per_ray=False,
+                                lanes_per_ray=lanes_per_ray)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    rgb = res.rgb.cpu().numpy()
+    residual = res.residual.cpu().numpy()
+    status = res.status.cpu().numpy()
+    if stats is not None:
+        cnt = res.counters.cpu().numpy()
+        stats.merge(RenderStats(rays=m, cells_stepped=int(cnt[0]), neighbor_visits=int(cnt[1]),
+                                grid_queries=grid_queries,
+                                failed_rays=int((status != STATUS_OK).sum()), seconds=dt))
+    if return_wsum:
+        return rgb, residual, status, res.wsum.cpu().numpy()
+    return rgb, residual, status
+
+
+def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT,
+                 workers=None, stats=None, weight_check=False, device_scene=None,
+                 lanes_per_ray=dv.DEFAULT_LANES):
+    """Render a full frame; returns (H, W, 3) float64 image [, wsum, residual].
+
+    Ray generation, the shared-origin start cell and the walk all run on the
+    device in one pass (rfb_render_image).
+    """
+    ds = _device_scene(scene, device_scene)
+    if camera.kind != "pinhole":
+        dirs = camera.ray_directions()
+        origins = np.broadcast_to(camera.position, (len(dirs), 3)).copy()
+        out = render_ray_batch(scene, origins, dirs, epsilon=epsilon, step_limit=step_limit,
+                               stats=stats, return_wsum=weight_check, device_scene=ds)
+        img = out[0].reshape(camera.height, camera.width, 3)
+        if weight_check:
+            return (img, out[3].reshape(camera.height, camera.width),
+                    out[1].reshape(camera.height, camera.width))
+        return img
+    H, W = camera.height, camera.width
+    torch.cuda.synchronize(ds.device)
+    t0 = time.perf_counter()
+    res = dv.render_image_device(ds, camera, epsilon=epsilon, step_limit=step_limit, f64=True,
+                                 lanes_per_ray=lanes_per_ray)
+    torch.cuda.synchronize(ds.device)
+    dt = time.perf_counter() - t0
+    img = res.rgb.cpu().numpy().reshape(H, W, 3)
+    if stats is not None:
+        cnt = res.counters.cpu().numpy()
+        status = res.status.cpu().numpy()
+        stats.merge(RenderStats(rays=H * W, cells_stepped=int(cnt[0]),
+                                neighbor_visits=int(cnt[1]), grid_queries=1,
+                                failed_rays=int((status != STATUS_OK).sum()), seconds=dt))
+    if weight_check:
+        return (img, res.wsum.cpu().numpy().reshape(H, W), res.residual.cpu().numpy().reshape(H, W))
+    return img
+
+
+def render_rays_with_gradients(scene, origins, directions, adjoints, t_min=None, t_max=None,
+                               start_sites=None, epsilon=DEFAULT_EPSILON,
+                               step_limit=DEFAULT_STEP_LIMIT, grad=None, device_scene=None):
+    """Forward+backward for arbitrary per-ray colour adjoints; returns
+    (rgb (m,3) f64, GradientBuffer).  Gradients accumulate into ``grad``."""
+    ds = _device_scene(scene, device_scene)
+    adj = scene.require_adjacency()
+    dev = ds.device
+    origins = np.ascontiguousarray(origins, dtype=np.float64)
+    directions = np.ascontiguousarray(directions, dtype=np.float64)
+    adjoints = np.ascontiguousarray(adjoints, dtype=np.float64)
+    m = len(origins)
+    if t_min is None:
+        t_min = np.zeros(m)
+    t_min = np.ascontiguousarray(t_min, dtype=np.float64)
+    if t_max is None:
+        t_max = np.array([_default_t_max(adj, Ray(origins[k], directions[k])) for k in range(m)])
+    t_max = np.ascontiguousarray(t_max, dtype=np.float64)
+    o_d = _to_dev(origins.reshape(m, 3), np.float64, dev)
+    d_d = _to_dev(directions.reshape(m, 3), np.float64, dev)
+    if start_sites is None:
+        # host expression o + t_min*d (render.py:175-176), evaluated in numpy
+        # for bit-identical query points, then located on device
+        q = _to_dev(origins + t_min[:, None] * directions, np.float64, dev)
+        seed = int(ds.locate(q[:1]).item()) if m else 0
+        start_d = ds.locate(q, seed=seed)
+    else:
+        start_d = _to_dev(start_sites, np.int32, dev)
+    n = ds.n_sites
+    if grad is None:
+        grad = GradientBuffer(n)
+    gb = dv.GradBuffers(n, dev)
+    res = dv.backward_rays_device(ds, o_d, d_d, _to_dev(t_min, np.float64, dev),
+                                  _to_dev(t_max, np.float64, dev), start_d,
+                                  _to_dev(adjoints.reshape(m, 3), np.float64, dev), gb,
+                                  epsilon=epsilon, step_limit=step_limit, f64=True)
+    torch.cuda.synchronize(dev)
+    g4 = gb.g4.double().cpu().numpy()
+    dsh = gb.sh.double().cpu().numpy()
+    grad.d_position += g4[:, :3]
+    grad.d_sh += dsh.reshape(n, 16, 3)
+    grad.d_raw_density += g4[:, 3] * softplus_grad(scene.raw_density)
+    return res.rgb.cpu().numpy(), grad
+
+
+def trace(scene, ray, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, start_site=None,
+          counters=None, device_scene=None):
+    """Walk one ray (rays.py:81-115); raises StepLimit / CycleDetected."""
+    ds = _device_scene(scene, device_scene)
+    adj = scene.require_adjacency()
+    dev = ds.device
+    t_max = ray.t_max
+    if not np.isfinite(t_max):
+        t_max = _default_t_max(adj, ray)
+    o_d = _to_dev(ray.origin[None, :], np.float64, dev)
+    d_d = _to_dev(ray.direction[None, :], np.float64, dev)
+    if start_site is None:
+        start_d = ds.locate(_to_dev(ray.at(ray.t_min)[None, :], np.float64, dev))
+    else:
+        start_d = torch.tensor([int(start_site)], dtype=torch.int32, device=dev)
+    res = dv.render_rays_device(ds, o_d, d_d, _to_dev([ray.t_min], np.float64, dev),
+                                _to_dev([t_max], np.float64, dev), start_d, epsilon=epsilon,
+                                step_limit=step_limit, f64=True, per_ray=True,
+                                seg_capacity=step_limit)
+    torch.cuda.synchronize(dev)
+    status = int(res.status.item())
+    nseg = int(res.nseg.item())
+    if counters is not None:
+        rc = res.ray_counters.cpu().numpy()[0]
+        counters[0, 0] += int(rc[0])
+        counters[0, 1] += int(rc[1])
+    if status == STATUS_STEP_LIMIT:
+        raise StepLimit(f"ray exceeded {step_limit} cells")
+    if status == STATUS_CYCLE:
+        raise CycleDetected("walk stalled; same cell revisited without advancing")
+    cells = res.seg_cells[0, :nseg].cpu().numpy().astype(np.int64)
+    t0 = res.seg_t0[0, :nseg].cpu().numpy()
+    t1 = res.seg_t1[0, :nseg].cpu().numpy()
+    # walk_ray's residual is exp(log_T) (kernels.py:142); recompute it on the
+    # host from the recorded segments with the same accumulation order.
+    sig = softplus(scene.raw_density)
+    log_T = 0.0
+    for c, a, b in zip(cells, t0, t1):
+        log_T -= sig[c] * (b - a)
+    return RaySegments(cells, t0, t1, float(np.exp(log_T)), status)

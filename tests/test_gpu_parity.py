@@ -1,0 +1,207 @@
+"""CUDA path (librfb.so through the C ABI) vs the CPU oracle and the
+reference's golden vectors.
+
+Bars (BASELINE.json north_star): per-ray visited-cell sequences, segment
+depths, counters and status bit-exact; images within 1e-4 abs (the kernels
+composite in fp64, so the observed gap is ~1e-15); gradients within 1e-3
+relative per tensor, measured as max|d - ref| / max|ref| (the device
+accumulates in fp32 with unordered atomics).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_scene, golden_scene_arrays, load_golden
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+FRAMES = ["frame_2k_deg3", "frame_2k_deg3_eps0_orbit", "frame_10k_deg0", "frame_3k_surface"]
+IMG_TOL = 1e-4
+GRAD_RTOL = 1e-3
+
+
+def rel_err(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    den = np.abs(b).max()
+    return float(np.abs(a - b).max() / den) if den > 0 else float(np.abs(a).max())
+
+
+def _dev(a, dt=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
+
+
+def frame_rays(g):
+    sa = golden_scene_arrays(g)
+    dirs = g["dirs"]
+    m = len(dirs)
+    origin = g["pose"][:3, 3]
+    start = int(orc.nearest_sites(sa.positions, origin[None, :])[0])
+    t_max = float(np.linalg.norm(origin - sa.center) + 2.0 * sa.diagonal + 1.0)
+    return sa, np.broadcast_to(origin, (m, 3)).copy(), dirs, start, t_max
+
+
+@pytest.mark.parametrize("lanes", [1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("name", FRAMES)
+def test_render_rays_bit_exact_walk(cuda_ok, name, lanes):
+    from paper_2502_01157_b200 import device as dv
+
+    g = load_golden(name)
+    sa, origins, dirs, start, t_max = frame_rays(g)
+    m = len(dirs)
+    eps = float(g["epsilon"])
+    ds = dv.DeviceScene(golden_scene(g))
+    cap = 512
+    res = dv.render_rays_device(ds, _dev(origins), _dev(dirs), _dev(np.zeros(m)),
+                                _dev(np.full(m, t_max)), _dev(np.full(m, start), torch.int32),
+                                epsilon=eps, f64=True, per_ray=True, seg_capacity=cap,
+                                lanes_per_ray=lanes)
+    torch.cuda.synchronize()
+    ref = orc.render_rays(sa, origins, dirs, 0.0, t_max, start, epsilon=eps)
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    np.testing.assert_array_equal(res.nseg.cpu().numpy(), ref["nseg"])
+    np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
+    np.testing.assert_array_equal(res.counters.cpu().numpy(), ref["counters"].sum(axis=0))
+    H, W = int(g["height"]), int(g["width"])
+    rgb = res.rgb.cpu().numpy()
+    assert np.abs(rgb - ref["rgb"]).max() <= IMG_TOL
+    assert np.abs(rgb.reshape(H, W, 3) - g["img"]).max() <= IMG_TOL
+    assert np.abs(res.wsum.cpu().numpy() - ref["wsum"]).max() <= IMG_TOL
+    assert np.abs(res.residual.cpu().numpy() - ref["residual"]).max() <= IMG_TOL
+    # every ray's visited-cell sequence and segment depths, bit for bit
+    cells = res.seg_cells.cpu().numpy()
+    t0 = res.seg_t0.cpu().numpy()
+    t1 = res.seg_t1.cpu().numpy()
+    for q in range(m):
+        c, a, b, st, _, _ = orc.walk_ray(sa, origins[q], dirs[q], 0.0, t_max, start, epsilon=eps)
+        L = min(len(c), cap)
+        np.testing.assert_array_equal(cells[q, :L], c[:L])
+        np.testing.assert_array_equal(t0[q, :L], a[:L])
+        np.testing.assert_array_equal(t1[q, :L], b[:L])
+
+
+@pytest.mark.parametrize("name", FRAMES)
+def test_render_image_matches_reference(cuda_ok, name):
+    from paper_2502_01157_b200 import render
+    from paper_2502_01157_b200.camera import PINHOLE, CameraModel
+    from paper_2502_01157_b200.render import RenderStats
+
+    g = load_golden(name)
+    cam = CameraModel(PINHOLE, int(g["width"]), int(g["height"]), float(g["focal"]), g["pose"])
+    stats = RenderStats()
+    img, wsum, resid = render.render_image(golden_scene(g), cam, epsilon=float(g["epsilon"]),
+                                           stats=stats, weight_check=True)
+    assert np.abs(img - g["img"]).max() <= IMG_TOL
+    assert np.abs(wsum - g["wsum"]).max() <= IMG_TOL
+    assert np.abs(resid - g["residual"]).max() <= IMG_TOL
+    st = g["stats"]
+    assert (stats.rays, stats.cells_stepped, stats.neighbor_visits, stats.failed_rays) == tuple(st)
+
+
+@pytest.mark.parametrize("name", FRAMES)
+def test_render_ray_batch_api(cuda_ok, name):
+    from paper_2502_01157_b200 import render
+
+    g = load_golden(name)
+    origin = g["pose"][:3, 3]
+    m = len(g["dirs"])
+    rgb, residual, status, wsum = render.render_ray_batch(
+        golden_scene(g), np.broadcast_to(origin, (m, 3)), g["dirs"], epsilon=float(g["epsilon"]),
+        return_wsum=True)
+    H, W = int(g["height"]), int(g["width"])
+    assert rgb.dtype == np.float64 and status.dtype == np.int8
+    assert np.abs(rgb.reshape(H, W, 3) - g["img"]).max() <= IMG_TOL
+    np.testing.assert_array_equal(status, g["status"])
+
+
+def test_camera_rays_device_bit_exact(cuda_ok):
+    g = load_golden("frame_2k_deg3")
+    from paper_2502_01157_b200.camera import PINHOLE, CameraModel
+
+    cam = CameraModel(PINHOLE, int(g["width"]), int(g["height"]), float(g["focal"]), g["pose"])
+    d = cam.ray_directions_device().cpu().numpy()
+    np.testing.assert_array_equal(d, g["dirs"])
+
+
+def test_locate_matches_exact_nearest(cuda_ok):
+    from paper_2502_01157_b200 import device as dv
+
+    g = load_golden("frame_2k_deg3")
+    ds = dv.DeviceScene(golden_scene(g))
+    pos = g["positions"]
+    rng = np.random.default_rng(5)
+    nbr = g["neighbors"]
+    off = g["offsets"]
+    i = rng.integers(0, len(pos), 200)
+    j = nbr[off[i]]  # a Delaunay neighbour: the midpoint is an exact tie
+    q = np.concatenate([rng.uniform(-1.2, 1.2, (2000, 3)), rng.uniform(-6, 6, (500, 3)),
+                        pos[rng.integers(0, len(pos), 200)], 0.5 * (pos[i] + pos[j])])
+    got = ds.locate(_dev(q)).cpu().numpy()
+    ref = orc.nearest_sites(pos, q)
+    np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name", ["grad_2k_deg3", "grad_2k_deg3_inside_eps0"])
+def test_backward_matches_reference(cuda_ok, name):
+    from paper_2502_01157_b200 import render
+
+    g = load_golden(name)
+    rgb, grad = render.render_rays_with_gradients(golden_scene(g), g["origins"], g["dirs"],
+                                                  g["adjoints"], epsilon=float(g["epsilon"]))
+    assert np.abs(rgb - g["rgb"]).max() <= IMG_TOL
+    assert rel_err(grad.d_sh.reshape(-1, 48), g["d_sh"]) <= GRAD_RTOL
+    assert rel_err(grad.d_position, g["d_position"]) <= GRAD_RTOL
+    assert rel_err(grad.d_raw_density, g["d_raw_density"]) <= GRAD_RTOL
+
+
+@pytest.mark.parametrize("name", ["train_2k_deg3_q", "train_3k_surface_q"])
+def test_train_batch_matches_reference(cuda_ok, name):
+    from paper_2502_01157_b200 import device as dv
+
+    g = load_golden(name)
+    ds = dv.DeviceScene(golden_scene(g))
+    m = len(g["origins"])
+    gb = dv.GradBuffers(ds.n_sites, ds.device)
+    loss = torch.zeros(2, dtype=torch.float64, device="cuda")
+    res = dv.train_batch_device(ds, _dev(g["origins"]), _dev(g["dirs"]), _dev(np.zeros(m)),
+                                _dev(g["t_max"]), _dev(g["start"], torch.int32),
+                                _dev(g["targets"]), gb, loss, rgb_scale=float(g["rgb_scale"]),
+                                quantile_scale=float(g["quantile_scale"]),
+                                u_pairs=_dev(g["u_pairs"]), weight_floor=1e-4,
+                                epsilon=float(g["epsilon"]), f64=True)
+    torch.cuda.synchronize()
+    assert np.abs(res.rgb.cpu().numpy() - g["out_rgb"]).max() <= IMG_TOL
+    np.testing.assert_array_equal(res.status.cpu().numpy(), g["out_status"])
+    np.testing.assert_array_equal(res.counters.cpu().numpy(), g["counters"].sum(axis=0))
+    lw = g["loss_w"].sum(axis=0)
+    np.testing.assert_allclose(loss.cpu().numpy(), lw, rtol=1e-9)
+    g4 = gb.g4.double().cpu().numpy()
+    assert rel_err(g4[:, 3], g["d_sigma_w"].sum(axis=0)) <= GRAD_RTOL
+    assert rel_err(g4[:, :3], g["d_pos_w"].sum(axis=0)) <= GRAD_RTOL
+    assert rel_err(gb.sh.double().cpu().numpy(), g["d_sh_w"].sum(axis=0)) <= GRAD_RTOL
+
+
+def test_empty_and_step_limit(cuda_ok):
+    from paper_2502_01157_b200 import device as dv
+
+    g = load_golden("frame_2k_deg3")
+    sa, origins, dirs, start, t_max = frame_rays(g)
+    ds = dv.DeviceScene(golden_scene(g))
+    e = torch.empty((0, 3), dtype=torch.float64, device="cuda")
+    z = torch.empty(0, dtype=torch.float64, device="cuda")
+    res = dv.render_rays_device(ds, e, e, z, z, torch.empty(0, dtype=torch.int32, device="cuda"))
+    assert res.rgb.shape == (0, 3)
+    # step_limit 5: most rays fail with status 2 and render the background
+    m = 256
+    res = dv.render_rays_device(ds, _dev(origins[:m]), _dev(dirs[:m]), _dev(np.zeros(m)),
+                                _dev(np.full(m, t_max)), _dev(np.full(m, start), torch.int32),
+                                step_limit=5, f64=True)
+    torch.cuda.synchronize()
+    ref = orc.render_rays(sa, origins[:m], dirs[:m], 0.0, t_max, start, step_limit=5)
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    assert (ref["status"] == 2).any()
+    np.testing.assert_array_equal(res.rgb.cpu().numpy()[ref["status"] == 2],
+                                  np.broadcast_to(g["background"], ((ref["status"] == 2).sum(), 3)))
+    np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
