@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark: rays/s of the Radiant Foam hot path on B200 (BASELINE.json).
+
+Workload (N=1): config 2 -- synthetic 1M-site foam (seed 1,
+SH degree 3, uniform in [-1,1]^3, fp32-exact sites, Qhull CSR), pinhole
+camera at (0,0,3) looking at the origin, camera_angle_x 0.9, 1920x1080,
+epsilon 1e-3, step_limit 4096.  One step = one full forward frame
+(rfb_render_image: ray generation + start cell + walk + SH-3 colour +
+compositing).  ``fwd_bwd`` reports config 3 on the same scene: one step =
+rfb_train_batch over every pixel of the view (L2 adjoint, quantile off) plus,
+for N>1, the NCCL all-reduce of the per-site gradient buffer.
+
+Multi-GPU (torchrun, one rank per GPU): every step renders N views (view k =
+orbit pose k-1, view 0 = the config-2 camera); each view's 32x32 tiles are
+interleaved round-robin over the ranks (scene replicated) and the frames are
+summed onto rank 0.  Training: rank r trains on view r and the flat fp32
+gradient buffer is all-reduced.  Per-rank work is fixed as N grows:
+"scaling": "weak".
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier +
+synchronize, timed with CUDA events on the launching stream, max over ranks.
+The scene (482 MB) is larger than L2 (126 MB).  nvidia-smi clocks are
+sampled during the timed region.  ``e2e`` times the public API
+(render.render_image with a resident scene: camera in, (H,W,3) float64 image
+copied to host) including the device->host copy of the image.
+
+--impl reference: the reference algorithm's CPU implementation on the host
+cores (the C oracle port of rfoam/tracer/kernels.py, every host thread), on
+a bounded row sample of the same frame.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "rays/sec fwd and fwd+bwd (1M-site foam, 1080p) at 1/2/4/8 B200; % of gather roofline"
+UNIT = "rays/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-sites", type=int, default=1_000_000)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--lanes", type=int, default=0, help="lanes per ray (0 = library default)")
+    ap.add_argument("--no-fwd-bwd", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-row-stride", type=int, default=8)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def make_views(n_views, W, H):
+    from paper_2502_01157_b200.camera import PINHOLE, CameraModel, look_at, orbit_poses
+
+    poses = [look_at((0.0, 0.0, 3.0), (0.0, 0.0, 0.0))]
+    poses += orbit_poses(np.zeros(3), 3.0, 0.3, 8)
+    return [CameraModel.from_angle_x(PINHOLE, W, H, 0.9, poses[k % len(poses)])
+            for k in range(n_views)]
+
+
+def algorithmic_bytes(C, V, N, m, sh_bytes):
+    """B_f = 24C + 16V + S_b N + 12 per ray (totals here)."""
+    return 24.0 * C + 16.0 * V + sh_bytes * N + 12.0 * m
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """CPU reference arm: the oracle port on all host threads (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    line = cpu_baseline_measure(args, steps=args.steps, warmup=min(args.warmup, 1))
+    out = {"metric": METRIC, "value": line["value"], "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "impl": "reference",
+           "ms_per_step": line["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "config 2: 1M-site foam, SH deg 3, 1920x1080 forward",
+                      "sample": line["sample"], "n_sites": args.n_sites},
+           "cpu_baseline": {"value": line["value"], "unit": UNIT, "cores": line["cores"],
+                            "kind": "port", "sample": line["sample"]},
+           "e2e": {"value": line["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline_measure(args, steps=1, warmup=0, scene=None):
+    from oracle import oracle as orc
+    from paper_2502_01157_b200.scene import softplus
+    from paper_2502_01157_b200.synthetic import make_foam
+
+    if scene is None:
+        scene = make_foam(args.n_sites, args.seed, 3)
+    adj = scene.adjacency
+    sa = orc.SceneArrays(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density),
+                         scene.sh_coeffs.reshape(-1, 48), scene.background)
+    cam = make_views(1, args.width, args.height)[0]
+    rows = np.arange(0, args.height, args.cpu_row_stride)
+    rr, cc = np.meshgrid(rows, np.arange(args.width), indexing="ij")
+    dirs = cam.ray_directions(rr.reshape(-1), cc.reshape(-1))
+    m = len(dirs)
+    origin = cam.position
+    start = int(orc.nearest_sites(sa.positions, origin[None, :])[0])
+    t_max = float(np.linalg.norm(origin - sa.center) + 2.0 * sa.diagonal + 1.0)
+    threads = os.cpu_count() or 1
+    origins = np.broadcast_to(origin, (m, 3)).copy()
+    for _ in range(warmup):
+        orc.render_rays(sa, origins[:4096], dirs[:4096], 0.0, t_max, start, threads=threads)
+    times = []
+    for _ in range(max(steps, 1)):
+        t0 = time.perf_counter()
+        orc.render_rays(sa, origins, dirs, 0.0, t_max, start, threads=threads)
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    return {"value": m / dt, "ms_per_step": dt * 1e3, "cores": threads,
+            "sample": f"every {args.cpu_row_stride}th row of the 1920x1080 frame "
+                      f"({m} rays/step, {len(times)} steps, C oracle port, {threads} threads)"}
+
+
+# ---------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200 import render as rd
+    from paper_2502_01157_b200.synthetic import make_foam
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    W, H = args.width, args.height
+    lanes = args.lanes if args.lanes > 0 else dv.DEFAULT_LANES
+    t_build = time.perf_counter()
+    scene = make_foam(args.n_sites, args.seed, 3, verbose=(rank == 0))
+    ds = dv.DeviceScene(scene, device=dev)
+    build_s = time.perf_counter() - t_build
+    views = make_views(world, W, H)
+    tx, ty = dv.tile_grid(W, H, 32, 32)
+    all_tiles = np.arange(tx * ty, dtype=np.int32)
+    my_tiles = torch.from_numpy(all_tiles[rank::world].copy()).to(dev)
+    ws = dv.Workspace(dev)
+    frames = [dv.alloc_forward(W * H, dev, per_ray=False) for _ in views]
+    stream = torch.cuda.current_stream()
+
+    def fwd_step():
+        for k, cam in enumerate(views):
+            if world > 1:
+                frames[k].rgb.zero_()
+            dv.render_image_device(ds, cam, tile_ids=my_tiles, lanes_per_ray=lanes, workspace=ws,
+                                   out=frames[k])
+        if world > 1:
+            for fr in frames:
+                dist.reduce(fr.rgb, dst=0)
+
+    # -- untimed: counters for the roofline (view 0, full frame) ------------------
+    probe = dv.render_image_device(ds, views[0], per_ray=True, lanes_per_ray=lanes, workspace=ws)
+    torch.cuda.synchronize()
+    C_tot, V_tot = [int(x) for x in probe.counters.cpu().tolist()]
+    N_tot = int(probe.nseg.to(torch.int64).sum().item())
+    failed = int((probe.status != 0).sum().item())
+    m0 = W * H
+    sh_bytes = 192 if ds.sh_degree == 3 else 12
+    bytes_per_frame = algorithmic_bytes(C_tot, V_tot, N_tot, m0, sh_bytes)
+
+    # -- forward timing ------------------------------------------------------------
+    for _ in range(args.warmup):
+        fwd_step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    if rank == 0:
+        clk.start()
+        time.sleep(0.3)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    ev0.record(stream)
+    for s in range(args.steps):
+        kev[s][0].record(stream)
+        fwd_step()
+        kev[s][1].record(stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    fwd_ms = ev0.elapsed_time(ev1)
+    kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    clocks = clk.stop() if rank == 0 else None
+    t = torch.tensor([fwd_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    fwd_ms = float(t.item())
+    rays_total = args.steps * W * H * len(views)
+    fwd_value = rays_total / (fwd_ms / 1e3)
+
+    # -- fwd+bwd timing (config 3) -------------------------------------------------
+    fb = None
+    if not args.no_fwd_bwd:
+        cam = views[rank]
+        dirs = cam.ray_directions_device(device=dev)
+        m = dirs.shape[0]
+        origins = torch.from_numpy(np.broadcast_to(cam.position, (m, 3)).copy()).to(dev)
+        start = ds.locate(origins[:1]).expand(m).contiguous()
+        t_min = torch.zeros(m, dtype=torch.float64, device=dev)
+        t_max = torch.full((m,), ds.default_t_max(cam.position[None, :]), dtype=torch.float64,
+                           device=dev)
+        rng = np.random.default_rng(11)
+        targets = torch.from_numpy(rng.uniform(0.0, 1.0, (m, 3))).to(dev)
+        gb = dv.GradBuffers(ds.n_sites, dev)
+        loss = torch.zeros(2, dtype=torch.float64, device=dev)
+        out_fb = dv.alloc_forward(m, dev, per_ray=True)
+        rgb_scale = 1.0 / (3.0 * m * world)
+        wsb = dv.Workspace(dev)
+
+        def fb_step():
+            gb.zero_()
+            loss.zero_()
+            dv.train_batch_device(ds, origins, dirs, t_min, t_max, start, targets, gb, loss,
+                                  rgb_scale=rgb_scale, workspace=wsb, out=out_fb)
+            if world > 1:
+                dist.all_reduce(gb.flat)
+                dist.all_reduce(loss)
+
+        for _ in range(args.warmup):
+            fb_step()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        clk2 = ClockSampler(local)
+        if rank == 0:
+            clk2.start()
+            time.sleep(0.3)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            fb_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        fb_ms = e0.elapsed_time(e1)
+        clocks_fb = clk2.stop() if rank == 0 else None
+        t = torch.tensor([fb_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        fb_ms = float(t.item())
+        fb = {"value": args.steps * m * world / (fb_ms / 1e3), "unit": UNIT,
+              "ms_per_step": fb_ms / args.steps,
+              "workload": "config 3: 1080p forward+backward (L2 adjoint, quantile off), "
+                          "per-site fp32 gradients" + (", NCCL all-reduce" if world > 1 else ""),
+              "cells_per_ray": int(out_fb.ray_counters[:, 0].sum().item()) / m,
+              "loss_rgb": float(loss[0].item()) / (3.0 * m * world),
+              "clocks": clocks_fb}
+
+    # -- e2e through the public API (rank 0 view, host image out) -----------------
+    e2e = None
+    if not args.no_e2e and world == 1:
+        cam = views[0]
+        rd.render_image(scene, cam, device_scene=ds, lanes_per_ray=lanes)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(3, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            img = rd.render_image(scene, cam, device_scene=ds, lanes_per_ray=lanes)
+            ts.append(time.perf_counter() - t0)
+        e2e = {"value": W * H / float(np.median(ts)), "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": int(img.nbytes),
+               "api": "render.render_image(scene, camera, device_scene=ds) -> (H,W,3) f64 host"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cb = cpu_baseline_measure(args, steps=1, warmup=1, scene=scene)
+            cpu = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": "port",
+                   "sample": cb["sample"]}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port",
+                   "sample": f"failed: {e}"}
+
+    peak, peak_kind = peaks()
+    achieved = bytes_per_frame * len(views) / world / (kernel_ms / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get("k_render_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    out = {
+        "metric": METRIC, "value": fwd_value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": fwd_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (SURVEY.md §8d foam generator; random-init scene, no dataset)",
+        "config": {"workload": "config 2: 1M-site foam (seed 1), SH deg 3, 1920x1080 forward "
+                               "render per view, camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
+                   "n_sites": args.n_sites, "n_edges": ds.n_edges, "views_per_step": len(views),
+                   "tiles": "32x32 interleaved over ranks", "lanes_per_ray": lanes,
+                   "l2": "inputs larger than L2 (scene 482 MB vs 126 MB L2); no flush",
+                   "cells_per_ray": C_tot / m0, "neighbor_visits_per_ray": V_tot / m0,
+                   "segments_per_ray": N_tot / m0, "failed_rays": failed,
+                   "scene_build_s": round(build_s, 1)},
+        "fwd_bwd": fb,
+        "e2e": e2e,
+        "gpu_launches": 2 * args.steps * len(views),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "k_render (walk + SH + composite)",
+                     "algorithmic_bytes_per_launch": bytes_per_frame,
+                     "launch_ms": kernel_ms},
+        "cpu_baseline": cpu,
+        "clocks": clocks,
+    }
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -53,9 +53,15 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 1
+#define RFB_ABI_VERSION 2
 
-/* Device-resident scene, produced by rfb_pack_scene. */
+/* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
+ *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
+ *  packed (packed != 0, positions exactly representable in fp32): per-site
+ *   32-byte cell headers {float x,y,z; int k0; double sigma; int k1;
+ *   float cmax} and per-edge 16-byte records {float xj,yj,zj; int j} in CSR
+ *   order, plus fp32 SH (sh32) with the fp64 table kept for the exact clamp
+ *   fallback.  The generic arrays are always present (backward, locate). */
 typedef struct rfb_scene {
     int64_t n_sites;
     int64_t n_edges;
@@ -63,9 +69,12 @@ typedef struct rfb_scene {
     const int32_t *offsets;   /* [n_sites + 1] CSR row starts */
     const int32_t *neighbors; /* [n_edges] ascending per site */
     const double *sh;         /* [n_sites][48], index k*3 + ch (render.py:53) */
+    const void *cells;        /* packed: [n_sites] 32-byte headers (nullable) */
+    const void *edges;        /* packed: [n_edges] 16-byte records (nullable) */
+    const float *sh32;        /* packed: [n_sites][3][16] fp32 channel-major copy of sh (nullable) */
+    int32_t packed;           /* 1: use cells/edges/sh32 for the walk */
     int32_t sh_degree;        /* 0: read the DC band only (exact when bands 1..15 are
                                  all zero), 3: all 16 bands */
-    int32_t pad_;
     double background[3];     /* (host value) */
 } rfb_scene;
 
@@ -127,14 +136,20 @@ int rfb_abi_version(void);
 const char *rfb_error_string(int code); /* (host) static string */
 int rfb_device_ok(void);                /* 1 when an sm_100 device is current */
 
-/* positions [n][3] f64, sigma [n] f64, offsets [n+1] i64, neighbors [E] i64
- * -> site4 [n][4] f64, offsets32 [n+1], neighbors32 [E]. */
-int rfb_pack_scene(const double *positions, const double *sigma, const int64_t *offsets,
-                   const int64_t *neighbors, int64_t n_sites, int64_t n_edges, double *site4,
-                   int32_t *offsets32, int32_t *neighbors32, void *stream);
+/* Build the device layout from fp64/int64 device arrays:
+ * positions [n][3], sigma [n], sh [n][48], offsets [n+1], neighbors [E]
+ * -> site4 [n][4] f64, offsets32 [n+1], neighbors32 [E] and, when
+ * cells/edges/sh32 are non-NULL, the packed layout (caller guarantees the
+ * positions are exactly representable in fp32). */
+int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
+                   const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
+                   int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
+                   void *cells, void *edges, float *sh32, void *stream);
 
-/* out[k] = softplus_10(raw[k]); optionally also written into site4[k][3]. */
-int rfb_softplus(const double *raw, int64_t n, double *out, double *site4_sigma, void *stream);
+/* sigma = softplus_10(raw) for device-resident training, written to out
+ * (nullable), site4[:,3] (nullable) and the packed headers (nullable). */
+int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void *cells,
+                 void *stream);
 
 /* dirs [pix_count][3] f64 for row-major pixels pix_begin .. pix_begin+count-1. */
 int rfb_camera_rays(const rfb_camera *camera, int64_t pix_begin, int64_t pix_count,

@@ -1,6 +1,7 @@
 // rfb.cu -- sm_100a kernels and the C ABI (include/rfb.h) of the Radiant Foam
 // hot path.  See DESIGN.md for the data layout and the roofline of each
-// kernel; every kernel cites the reference function it replaces.
+// kernel; every kernel cites the reference function it replaces (paths are
+// relative to the reference tree pkg/src/rfoam/).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -12,7 +13,11 @@
 
 namespace rfb {
 
-__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+constexpr unsigned kFull = 0xffffffffu;
+#ifndef RFB_F32_FILTER
+#define RFB_F32_FILTER 1
+#endif
+constexpr bool kUseF32Filter = RFB_F32_FILTER != 0;
 
 // ---------------------------------------------------------------------------
 // Ray sources: explicit arrays (render.py:57-125) or a pinhole camera over a
@@ -23,7 +28,7 @@ struct ArrayRays {
     const int32_t *start;
     int64_t m;
     __device__ __forceinline__ int64_t count() const { return m; }
-    // returns output index (pixel / ray id) or -1 when the slot is padding
+    // returns the output index (ray id / pixel) or -1 for a padding slot
     __device__ __forceinline__ int64_t get(int64_t q, Ray &r) const {
         r.ox = origins[3 * q];
         r.oy = origins[3 * q + 1];
@@ -45,8 +50,8 @@ struct CameraParams {
     int32_t width, height;
 };
 
-// camera.py:78-92 pinhole branch; fma order reproduces numpy's
-// `d_cam @ R.T` bit-for-bit (checked in tests/test_camera.py).
+// camera.py:78-92 pinhole branch; the fma order reproduces numpy's
+// `d_cam @ R.T` bit-for-bit (tests/test_gpu_parity.py).
 __device__ __forceinline__ void pinhole_dir(const CameraParams &c, int64_t row, int64_t col,
                                             double &dx, double &dy, double &dz) {
     double u = ((double)col + 0.5 - c.cx) / c.focal;
@@ -90,14 +95,6 @@ struct TileRays {
     }
 };
 
-struct DevScene {
-    const double4 *site4;
-    const int32_t *off;
-    const int32_t *nbr;
-    const double *sh;
-    double bg[3];
-};
-
 struct FwdOut {
     void *rgb, *residual, *wsum;
     int8_t *status;
@@ -117,27 +114,115 @@ __device__ __forceinline__ void store_out(void *p, int64_t idx, double v, int32_
         reinterpret_cast<float *>(p)[idx] = (float)v;
 }
 
+__device__ __forceinline__ void write_fwd(const FwdOut &O, int64_t q, int status, double cr,
+                                          double cg, double cb, double resid, double wsum,
+                                          int32_t nseg, int32_t cells, int32_t visits) {
+    store_out(O.rgb, 3 * q, cr, O.f64);
+    store_out(O.rgb, 3 * q + 1, cg, O.f64);
+    store_out(O.rgb, 3 * q + 2, cb, O.f64);
+    if (O.residual) store_out(O.residual, q, resid, O.f64);
+    if (O.wsum) store_out(O.wsum, q, wsum, O.f64);
+    if (O.status) O.status[q] = (int8_t)status;
+    if (O.nseg) O.nseg[q] = nseg;
+    if (O.ray_counters) {
+        O.ray_counters[2 * q] = cells;
+        O.ray_counters[2 * q + 1] = visits;
+    }
+}
+
 // ---------------------------------------------------------------------------
-// Forward: walk (kernels.py:76-162) with compositing fused per recorded
-// segment (composite_segments 165-196, same operation order, so the result is
-// identical to compositing after the walk).  G lanes cooperate on one ray.
+// The walk (tracer/kernels.py:101-162), executed by the G lanes of a ray
+// group.  rec(index, cell, header, t0, t1) is called for every recorded
+// segment, in order.  Returns the status code.
 // ---------------------------------------------------------------------------
-template <int G, int SHDEG, class Src>
-__global__ void __launch_bounds__(256) k_render(DevScene S, Src src, double epsilon,
+template <int G, bool PACKED, class Rec>
+__device__ __forceinline__ int walk(const SceneView<PACKED> &S, const Ray &r, double epsilon,
+                                    double log_eps, double width_floor, int32_t step_limit,
+                                    int gl, unsigned gmask, int32_t &nseg, int32_t &cells,
+                                    int32_t &visits, Rec &&rec) {
+    int32_t i = r.start;
+    double entry = r.t_min, log_T = 0.0;
+    int32_t zero_adv = 0, steps = 0;
+    const float df[3] = {(float)r.dx, (float)r.dy, (float)r.dz};
+    nseg = 0;
+    cells = 0;
+    visits = 0;
+    for (;;) {
+        steps += 1;
+        if (steps > step_limit) return RFB_STATUS_STEP_LIMIT;
+        cells += 1;
+        Cell c = S.cell(i);
+        visits += c.k1 - c.k0;
+        double best_t;
+        int32_t best_j;
+        if constexpr (PACKED && kUseF32Filter)
+            exit_face_f32<G>(S, c, c.hf, r, entry, df, gl, gmask, best_t, best_j);
+        else
+            exit_face<G, PACKED>(S, c, r, gl, gmask, best_t, best_j);
+        if (best_j < 0 || best_t >= r.t_max) {  // hull exit or far plane
+            if (r.t_max > entry) {
+                log_T -= c.sigma * (r.t_max - entry);
+                rec(nseg, i, c, entry, r.t_max);
+                nseg += 1;
+            }
+            return RFB_STATUS_OK;
+        }
+        if (best_t < entry) best_t = entry;
+        if (best_t - entry > width_floor) {
+            log_T -= c.sigma * (best_t - entry);
+            rec(nseg, i, c, entry, best_t);
+            nseg += 1;
+            entry = best_t;
+            zero_adv = 0;
+            if (below_epsilon(log_T, epsilon, log_eps)) return RFB_STATUS_OK;
+            if (nseg >= step_limit) return RFB_STATUS_STEP_LIMIT;
+        } else {
+            zero_adv += 1;
+            if (zero_adv > kZeroAdvanceLimit) return RFB_STATUS_CYCLE;
+        }
+        i = best_j;
+    }
+}
+
+// fp32 copy of the ray's 16 SH basis values and sum |basis| (fp64) for the
+// colour rounding bound.
+__device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
+    double basis[16];
+    sh_basis(r.dx, r.dy, r.dz, basis);
+    double bsum = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        basis_f[k] = (float)basis[k];
+        bsum += fabs(basis[k]);
+    }
+    return bsum;
+}
+
+// ---------------------------------------------------------------------------
+// Forward: walk with compositing fused per recorded segment
+// (composite_segments kernels.py:165-196, same operation order, so the
+// result equals compositing after the walk).  Warps fetch 32/G rays at a
+// time from a global counter (persistent grid).
+// ---------------------------------------------------------------------------
+#ifndef RFB_FWD_MINB
+#define RFB_FWD_MINB 2
+#endif
+template <int G, int SHDEG, bool PACKED, class Src>
+__global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> S, Src src, double epsilon,
                                                 double log_eps, double width_floor,
                                                 int32_t step_limit, FwdOut O,
                                                 unsigned long long *ray_counter) {
-    constexpr int RPW = 32 / G;  // rays per warp
+    constexpr int RPW = 32 / G;
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
-    const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const int64_t total = src.count();
     unsigned long long my_cells = 0, my_visits = 0;
 
     for (;;) {
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(ray_counter, (unsigned long long)RPW);
-        base = __shfl_sync(0xffffffffu, base, 0);
+        base = __shfl_sync(kFull, base, 0);
         if ((int64_t)base >= total) break;
         int64_t q = (int64_t)base + lane / G;
         if (q >= total) continue;
@@ -145,115 +230,54 @@ __global__ void __launch_bounds__(256) k_render(DevScene S, Src src, double epsi
         int64_t oidx = src.get(q, r);
         if (oidx < 0) continue;
 
-        double basis[16];
-        if (SHDEG > 0)
-            sh_basis(r.dx, r.dy, r.dz, basis);
-        else
-            basis[0] = kC0;
-
-        int32_t i = r.start;
-        double entry = r.t_min, log_T = 0.0;
-        int32_t nseg = 0, zero_adv = 0, steps = 0;
-        int status = RFB_STATUS_OK;
-        double T = 1.0, wsum = 0.0, cr = 0.0, cg = 0.0, cb = 0.0;
-        int32_t cells = 0, visits = 0;
-        const bool dump = O.seg_cap > 0;
-
-        // Record one segment and composite it (kernels.py:137-141/147-151 +
-        // 179-189).
-        auto record = [&](int32_t cell, double t0, double t1) {
-            double sig = __ldg(&S.site4[cell].w);
-            double delta = t1 - t0;
-            log_T -= sig * delta;
-            double alpha = 1.0 - exp(-sig * delta);
-            double col[3];
-            cell_color<SHDEG>(S.sh, cell, basis, col);
-            double w = T * alpha;
-            wsum += w;
-            cr += w * col[0];
-            cg += w * col[1];
-            cb += w * col[2];
-            T *= 1.0 - alpha;
-            if (dump && nseg < O.seg_cap && gl == 0) {
-                int64_t o = oidx * O.seg_cap + nseg;
-                O.seg_cells[o] = cell;
-                O.seg_t0[o] = t0;
-                O.seg_t1[o] = t1;
-            }
-            nseg += 1;
-        };
-
-        for (;;) {
-            steps += 1;
-            if (steps > step_limit) {
-                status = RFB_STATUS_STEP_LIMIT;
-                break;
-            }
-            cells += 1;
-            double4 xi = ld_site(S.site4 + i);
-            int32_t k0 = __ldg(S.off + i), k1 = __ldg(S.off + i + 1);
-            visits += k1 - k0;
-            double best_t;
-            int32_t best_j;
-            exit_face<G>(S.site4, S.nbr, k0, k1, xi, r, gl, gmask, best_t, best_j);
-            if (best_j < 0 || best_t >= r.t_max) {
-                if (r.t_max > entry) record(i, entry, r.t_max);
-                break;
-            }
-            if (best_t < entry) best_t = entry;
-            if (best_t - entry > width_floor) {
-                record(i, entry, best_t);
-                entry = best_t;
-                zero_adv = 0;
-                if (below_epsilon(log_T, epsilon, log_eps)) break;
-                if (nseg >= step_limit) {
-                    status = RFB_STATUS_STEP_LIMIT;
-                    break;
-                }
-            } else {
-                zero_adv += 1;
-                if (zero_adv > kZeroAdvanceLimit) {
-                    status = RFB_STATUS_CYCLE;
-                    break;
-                }
-            }
-            i = best_j;
+        float basis[16];
+        double bsum;
+        if (SHDEG > 0) {
+            bsum = basis_setup(r, basis);
+        } else {
+            basis[0] = (float)kC0;
+            bsum = kC0;
         }
-
+        const double dir[3] = {r.dx, r.dy, r.dz};
+        double T = 1.0, wsum = 0.0, cr = 0.0, cg = 0.0, cb = 0.0;
+        const bool dump = O.seg_cap > 0;
+        int32_t nseg, cells, visits;
+        int status = walk<G, PACKED>(
+            S, r, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells, visits,
+            [&](int32_t s, int32_t cell, const Cell &c, double t0, double t1) {
+                double delta = t1 - t0;
+                double alpha = 1.0 - exp(-c.sigma * delta);
+                double col[3];
+                cell_color<SHDEG, PACKED>(S, cell, c.cmax, basis, dir, bsum, col);
+                double w = T * alpha;
+                wsum += w;
+                cr += w * col[0];
+                cg += w * col[1];
+                cb += w * col[2];
+                T *= 1.0 - alpha;
+                if (dump && s < O.seg_cap && gl == 0) {
+                    int64_t o = oidx * O.seg_cap + s;
+                    O.seg_cells[o] = cell;
+                    O.seg_t0[o] = t0;
+                    O.seg_t1[o] = t1;
+                }
+            });
         if (gl == 0) {
             my_cells += (unsigned long long)cells;
             my_visits += (unsigned long long)visits;
-            double resid;
-            if (status != RFB_STATUS_OK) {  // kernels.py:230-236
-                cr = S.bg[0];
-                cg = S.bg[1];
-                cb = S.bg[2];
-                resid = 1.0;
-                wsum = 0.0;
-            } else {
-                cr += T * S.bg[0];
-                cg += T * S.bg[1];
-                cb += T * S.bg[2];
-                resid = T;
-            }
-            store_out(O.rgb, 3 * oidx, cr, O.f64);
-            store_out(O.rgb, 3 * oidx + 1, cg, O.f64);
-            store_out(O.rgb, 3 * oidx + 2, cb, O.f64);
-            if (O.residual) store_out(O.residual, oidx, resid, O.f64);
-            if (O.wsum) store_out(O.wsum, oidx, wsum, O.f64);
-            if (O.status) O.status[oidx] = (int8_t)status;
-            if (O.nseg) O.nseg[oidx] = nseg;
-            if (O.ray_counters) {
-                O.ray_counters[2 * oidx] = cells;
-                O.ray_counters[2 * oidx + 1] = visits;
-            }
+            if (status != RFB_STATUS_OK)  // kernels.py:230-236
+                write_fwd(O, oidx, status, S.bg[0], S.bg[1], S.bg[2], 1.0, 0.0, nseg, cells,
+                          visits);
+            else
+                write_fwd(O, oidx, status, cr + T * S.bg[0], cg + T * S.bg[1], cb + T * S.bg[2],
+                          T, wsum, nseg, cells, visits);
         }
     }
     if (O.counters) {
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            my_cells += __shfl_xor_sync(0xffffffffu, my_cells, off);
-            my_visits += __shfl_xor_sync(0xffffffffu, my_visits, off);
+            my_cells += __shfl_xor_sync(kFull, my_cells, off);
+            my_visits += __shfl_xor_sync(kFull, my_visits, off);
         }
         if (lane == 0) {
             atomicAdd(O.counters, my_cells);
@@ -263,16 +287,23 @@ __global__ void __launch_bounds__(256) k_render(DevScene S, Src src, double epsi
 }
 
 // ---------------------------------------------------------------------------
-// Backward / training: one thread per ray.  The walk records each segment
-// (cell | clamp mask, exit depth, transmittance after it, colour) into a
-// per-thread slot of the workspace; the reverse pass (backward_ray,
-// kernels.py:250-337) and the quantile pairs (456-567) then read it back.
+// Backward / training.  Each warp takes 32 rays.  Every lane walks its ray
+// (recording the segments into its slot of the workspace and compositing),
+// then the warp runs the reverse pass (backward_ray, kernels.py:267-337)
+// cooperatively: each iteration selects the farthest pending segment's cell,
+// every lane whose current segment is in that cell processes it, and the
+// gradients of that cell are summed across the group before ONE atomic per
+// value (dpos+dsigma as a float4, dSH as two coalesced 32-lane reductions
+// into the cell's 48-float row).  Coherent rays share cells, so this
+// replaces ~32 contended atomics by one.  Per-lane segment order and
+// arithmetic are exactly the reference's; only the summation order of the
+// fp32 accumulators changes.
 // ---------------------------------------------------------------------------
 struct Scratch {
-    int32_t *cell;  // [cap][slots]: cell id | mask << 29
-    double *t1;     // [cap][slots]: exit depth (entry of s = exit of s-1)
-    double *tb;     // [cap][slots]: T_before[s+1] = prod exp(-sigma*delta)
-    float *col;     // [cap][3][slots]
+    int32_t *cell;  // [cap][slots]: cell id | clamp mask << 29
+    double *t1;     // [cap][slots]: exit depth (the entry of s+1)
+    double *tb;     // [cap][slots]: T_before[s+1] = prod exp(-sigma*delta) (kernels.py:270-275)
+    float *col;     // [3*cap][slots]: clamped colour
     int64_t slots;
 };
 
@@ -281,66 +312,66 @@ struct Grads {
     float *sh;  // [n][48]
 };
 
-__device__ __forceinline__ void add_pos(float *g4, int32_t i, double x, double y, double z) {
-    float *p = g4 + 4 * (int64_t)i;
-    atomicAdd(p, (float)x);
-    atomicAdd(p + 1, (float)y);
-    atomicAdd(p + 2, (float)z);
+__device__ __forceinline__ void red4(float *p, float a, float b, float c, float d) {
+    atomicAdd(reinterpret_cast<float4 *>(p), make_float4(a, b, c, d));
 }
 
-// kernels.py:340-369
-__device__ __forceinline__ void face_t_gradient(const double4 *__restrict__ site4, int32_t i,
-                                                int32_t j, const Ray &r, double t, double dt,
-                                                float *g4) {
+// kernels.py:340-369 -> contributions to x_i (gi) and x_j (gj).
+__device__ __forceinline__ bool face_grad(const double4 *__restrict__ site4, int32_t i,
+                                          int32_t j, const Ray &r, double t, double dt,
+                                          double *gi, double *gj) {
     double4 xi = ld_site(site4 + i), xj = ld_site(site4 + j);
     double nx = xj.x - xi.x, ny = xj.y - xi.y, nz = xj.z - xi.z;
     double denom = r.dx * nx + r.dy * ny + r.dz * nz;
-    if (denom == 0.0) return;
+    if (denom == 0.0) return false;
     double mx = 0.5 * (xi.x + xj.x), my = 0.5 * (xi.y + xj.y), mz = 0.5 * (xi.z + xj.z);
     double px = r.ox + t * r.dx, py = r.oy + t * r.dy, pz = r.oz + t * r.dz;
     double qx = mx - px, qy = my - py, qz = mz - pz;
     double inv = dt / denom;
-    add_pos(g4, i, (0.5 * nx - qx) * inv, (0.5 * ny - qy) * inv, (0.5 * nz - qz) * inv);
-    add_pos(g4, j, (0.5 * nx + qx) * inv, (0.5 * ny + qy) * inv, (0.5 * nz + qz) * inv);
+    gi[0] = (0.5 * nx - qx) * inv;
+    gi[1] = (0.5 * ny - qy) * inv;
+    gi[2] = (0.5 * nz - qz) * inv;
+    gj[0] = (0.5 * nx + qx) * inv;
+    gj[1] = (0.5 * ny + qy) * inv;
+    gj[2] = (0.5 * nz + qz) * inv;
+    return true;
 }
 
-template <int SHDEG>
-__device__ __forceinline__ void add_sh(float *gsh, int32_t i, int mask, double w, double ar,
-                                       double ag, double ab, const double *basis) {
-    // kernels.py:309-322: channel ch gets w*adj_ch*basis[k] unless clamped or
-    // adj_ch == 0.
-    double f[3];
-    f[0] = ((mask & 1) == 0 && ar != 0.0) ? w * ar : 0.0;
-    f[1] = ((mask & 2) == 0 && ag != 0.0) ? w * ag : 0.0;
-    f[2] = ((mask & 4) == 0 && ab != 0.0) ? w * ab : 0.0;
-    if (f[0] == 0.0 && f[1] == 0.0 && f[2] == 0.0) return;
-    float *row = gsh + 48 * (int64_t)i;
-    if (SHDEG == 0) {
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch)
-            if (f[ch] != 0.0) atomicAdd(row + ch, (float)(f[ch] * basis[0]));
-        return;
-    }
-    float v[48];
-#pragma unroll
-    for (int k = 0; k < 16; ++k)
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) v[3 * k + ch] = (float)(f[ch] * basis[k]);
-    float4 *row4 = reinterpret_cast<float4 *>(row);
-#pragma unroll
-    for (int c = 0; c < 12; ++c)
-        atomicAdd(row4 + c, make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]));
+__device__ __forceinline__ void face_grad_atomic(const double4 *__restrict__ site4, int32_t i,
+                                                 int32_t j, const Ray &r, double t, double dt,
+                                                 float *g4) {
+    double gi[3], gj[3];
+    if (!face_grad(site4, i, j, r, t, dt, gi, gj)) return;
+    red4(g4 + 4 * (int64_t)i, (float)gi[0], (float)gi[1], (float)gi[2], 0.f);
+    red4(g4 + 4 * (int64_t)j, (float)gj[0], (float)gj[1], (float)gj[2], 0.f);
 }
 
-template <int SHDEG, bool TRAIN>
-__global__ void __launch_bounds__(128) k_backward(DevScene S, ArrayRays src, double epsilon,
-                                                  double log_eps, double width_floor,
-                                                  int32_t step_limit, const double *adjoints,
-                                                  const double *targets, double rgb_scale,
-                                                  double q_scale, const double *u_pairs,
-                                                  int32_t n_pairs, double weight_floor, FwdOut O,
-                                                  Grads gr, double *loss, Scratch scr,
-                                                  unsigned long long *ray_counter) {
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    return v;
+}
+
+__device__ __forceinline__ unsigned order_key(double t) {
+    unsigned b = __float_as_uint((float)t);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+constexpr int kTrainBlock = 128;
+constexpr int kTrainWarps = kTrainBlock / 32;
+
+#ifndef RFB_TRAIN_MINB
+#define RFB_TRAIN_MINB 4
+#endif
+template <int SHDEG, bool PACKED, bool TRAIN>
+__global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
+    SceneView<PACKED> S, ArrayRays src, double epsilon, double log_eps, double width_floor,
+    int32_t step_limit, const double *adjoints, const double *targets, double rgb_scale,
+    double q_scale, const double *u_pairs, int32_t n_pairs, double weight_floor, FwdOut O,
+    Grads gr, double *loss, Scratch scr, unsigned long long *ray_counter) {
+    __shared__ float s_basis[kTrainWarps][32][17];
+    __shared__ float s_f[kTrainWarps][32][3];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t SL = scr.slots;
     int32_t *s_cell = scr.cell + slot;
@@ -352,162 +383,193 @@ __global__ void __launch_bounds__(128) k_backward(DevScene S, ArrayRays src, dou
     const int64_t total = src.count();
 
     for (;;) {
-        int64_t q = (int64_t)atomicAdd(ray_counter, 1ull);
-        if (q >= total) break;
-        Ray r;
-        src.get(q, r);
-        double basis[16];
-        if (SHDEG > 0)
-            sh_basis(r.dx, r.dy, r.dz, basis);
-        else
-            basis[0] = kC0;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ray_counter, 32ull);
+        base = __shfl_sync(kFull, base, 0);
+        if ((int64_t)base >= total) break;
+        const int64_t q = (int64_t)base + lane;
+        const bool have_ray = q < total;
 
-        int32_t i = r.start;
-        double entry = r.t_min, log_T = 0.0;
-        int32_t nseg = 0, zero_adv = 0, steps = 0;
+        Ray r;
+        r.t_min = 0.0;
+        float basis[16];
+        int32_t nseg = 0;
         int status = RFB_STATUS_OK;
         double Tc = 1.0, Tb = 1.0, wsum = 0.0, cr = 0.0, cg = 0.0, cb = 0.0;
-        int32_t cells = 0, visits = 0;
-
-        auto record = [&](int32_t cell, double t0, double t1) {
-            double sig = __ldg(&S.site4[cell].w);
-            double delta = t1 - t0;
-            log_T -= sig * delta;
-            double e = exp(-sig * delta);
-            double alpha = 1.0 - e;
-            double col[3];
-            int mask = cell_color<SHDEG>(S.sh, cell, basis, col);
-            double w = Tc * alpha;
-            wsum += w;
-            cr += w * col[0];
-            cg += w * col[1];
-            cb += w * col[2];
-            Tc *= 1.0 - alpha;
-            Tb = Tb * e;
-            s_cell[nseg * SL] = cell | (mask << 29);
-            s_t1[nseg * SL] = t1;
-            s_tb[nseg * SL] = Tb;
-            s_col[(3 * nseg) * SL] = (float)col[0];
-            s_col[(3 * nseg + 1) * SL] = (float)col[1];
-            s_col[(3 * nseg + 2) * SL] = (float)col[2];
-            nseg += 1;
-        };
-
-        for (;;) {
-            steps += 1;
-            if (steps > step_limit) {
-                status = RFB_STATUS_STEP_LIMIT;
-                break;
-            }
-            cells += 1;
-            double4 xi = ld_site(S.site4 + i);
-            int32_t k0 = __ldg(S.off + i), k1 = __ldg(S.off + i + 1);
-            visits += k1 - k0;
-            double best_t;
-            int32_t best_j;
-            exit_face<1>(S.site4, S.nbr, k0, k1, xi, r, 0, 0xffffffffu, best_t, best_j);
-            if (best_j < 0 || best_t >= r.t_max) {
-                if (r.t_max > entry) record(i, entry, r.t_max);
-                break;
-            }
-            if (best_t < entry) best_t = entry;
-            if (best_t - entry > width_floor) {
-                record(i, entry, best_t);
-                entry = best_t;
-                zero_adv = 0;
-                if (below_epsilon(log_T, epsilon, log_eps)) break;
-                if (nseg >= step_limit) {
-                    status = RFB_STATUS_STEP_LIMIT;
-                    break;
-                }
+        double ar = 0.0, ag = 0.0, ab = 0.0;
+        bool grad_ok = false;
+        if (have_ray) {
+            src.get(q, r);
+            double bsum = basis_setup(r, basis);
+            double cbsum = SHDEG > 0 ? bsum : kC0;
+            const double dir[3] = {r.dx, r.dy, r.dz};
+            int32_t cells, visits;
+            status = walk<1, PACKED>(
+                S, r, epsilon, log_eps, width_floor, step_limit, 0, kFull, nseg, cells, visits,
+                [&](int32_t s, int32_t cell, const Cell &c, double t0, double t1) {
+                    double delta = t1 - t0;
+                    double e = exp(-c.sigma * delta);
+                    double alpha = 1.0 - e;
+                    double col[3];
+                    int mask = cell_color<SHDEG, PACKED>(S, cell, c.cmax, basis, dir, cbsum, col);
+                    double w = Tc * alpha;
+                    wsum += w;
+                    cr += w * col[0];
+                    cg += w * col[1];
+                    cb += w * col[2];
+                    Tc *= 1.0 - alpha;
+                    Tb = Tb * e;
+                    s_cell[s * SL] = cell | (mask << 29);
+                    s_t1[s * SL] = t1;
+                    s_tb[s * SL] = Tb;
+                    s_col[(3 * s) * SL] = (float)col[0];
+                    s_col[(3 * s + 1) * SL] = (float)col[1];
+                    s_col[(3 * s + 2) * SL] = (float)col[2];
+                });
+            my_cells += (unsigned long long)cells;
+            my_visits += (unsigned long long)visits;
+            if (status != RFB_STATUS_OK) {
+                write_fwd(O, q, status, S.bg[0], S.bg[1], S.bg[2], 1.0, 0.0, nseg, cells, visits);
             } else {
-                zero_adv += 1;
-                if (zero_adv > kZeroAdvanceLimit) {
-                    status = RFB_STATUS_CYCLE;
-                    break;
+                cr += Tc * S.bg[0];
+                cg += Tc * S.bg[1];
+                cb += Tc * S.bg[2];
+                write_fwd(O, q, status, cr, cg, cb, Tc, wsum, nseg, cells, visits);
+                if (TRAIN) {  // kernels.py:430-437
+                    double er = cr - targets[3 * q], eg = cg - targets[3 * q + 1],
+                           eb = cb - targets[3 * q + 2];
+                    loss_rgb += er * er + eg * eg + eb * eb;
+                    ar = 2.0 * rgb_scale * er;
+                    ag = 2.0 * rgb_scale * eg;
+                    ab = 2.0 * rgb_scale * eb;
+                } else {
+                    ar = adjoints[3 * q];
+                    ag = adjoints[3 * q + 1];
+                    ab = adjoints[3 * q + 2];
                 }
+                grad_ok = nseg > 0;
             }
-            i = best_j;
-        }
-        my_cells += (unsigned long long)cells;
-        my_visits += (unsigned long long)visits;
-        if (O.status) O.status[q] = (int8_t)status;
-        if (O.nseg) O.nseg[q] = nseg;
-        if (status != RFB_STATUS_OK) {
-            store_out(O.rgb, 3 * q, S.bg[0], O.f64);
-            store_out(O.rgb, 3 * q + 1, S.bg[1], O.f64);
-            store_out(O.rgb, 3 * q + 2, S.bg[2], O.f64);
-            if (O.residual) store_out(O.residual, q, 1.0, O.f64);
-            if (O.wsum) store_out(O.wsum, q, 0.0, O.f64);
-            continue;
-        }
-        cr += Tc * S.bg[0];
-        cg += Tc * S.bg[1];
-        cb += Tc * S.bg[2];
-        store_out(O.rgb, 3 * q, cr, O.f64);
-        store_out(O.rgb, 3 * q + 1, cg, O.f64);
-        store_out(O.rgb, 3 * q + 2, cb, O.f64);
-        if (O.residual) store_out(O.residual, q, Tc, O.f64);
-        if (O.wsum) store_out(O.wsum, q, wsum, O.f64);
-
-        double ar, ag, ab;
-        if (TRAIN) {  // kernels.py:430-437
-            double er = cr - targets[3 * q], eg = cg - targets[3 * q + 1],
-                   eb = cb - targets[3 * q + 2];
-            loss_rgb += er * er + eg * eg + eb * eb;
-            ar = 2.0 * rgb_scale * er;
-            ag = 2.0 * rgb_scale * eg;
-            ab = 2.0 * rgb_scale * eb;
-        } else {
-            ar = adjoints[3 * q];
-            ag = adjoints[3 * q + 1];
-            ab = adjoints[3 * q + 2];
         }
 
-        // backward_ray (kernels.py:267-337), reverse order over the slot.
-        if (nseg > 0) {
-            double T_end = s_tb[(nseg - 1) * SL];
-            double Sr = T_end * S.bg[0], Sg = T_end * S.bg[1], Sb = T_end * S.bg[2];
-            double d_next = 0.0;
-            for (int32_t s = nseg - 1; s >= 0; --s) {
-                int32_t cm = s_cell[s * SL];
-                int32_t ci = cm & 0x1fffffff;
-                int mask = (cm >> 29) & 7;
-                double t1 = s_t1[s * SL];
-                double t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min;
-                double tb_s = s > 0 ? s_tb[(s - 1) * SL] : 1.0;
-                double tb_s1 = s_tb[s * SL];
-                double sig = __ldg(&S.site4[ci].w);
+        // ---- cooperative reverse pass -------------------------------------
+#pragma unroll
+        for (int k = 0; k < 16; ++k) s_basis[warp][lane][k] = grad_ok ? basis[k] : 0.f;
+        int32_t s = grad_ok ? nseg - 1 : -1;
+        int32_t ci = -1, cmask = 0, next_cell = -1;
+        double t1 = 0.0, t0 = 0.0, tb1 = 0.0, tb0 = 1.0;
+        double Sr = 0.0, Sg = 0.0, Sb = 0.0, d_next = 0.0;
+        auto load_seg = [&]() {
+            int32_t cm = s_cell[s * SL];
+            ci = cm & 0x1fffffff;
+            cmask = (cm >> 29) & 7;
+            t1 = s_t1[s * SL];
+            t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min;
+            tb1 = s_tb[s * SL];
+            tb0 = s > 0 ? s_tb[(s - 1) * SL] : 1.0;
+        };
+        if (s >= 0) {
+            load_seg();
+            Sr = tb1 * S.bg[0];  // suffix starts at T_end * background
+            Sg = tb1 * S.bg[1];
+            Sb = tb1 * S.bg[2];
+        }
+        for (;;) {
+            const bool act = s >= 0;
+            if (!__any_sync(kFull, act)) break;
+            const unsigned key = act ? order_key(t0) : 0u;
+            const unsigned kmax = __reduce_max_sync(kFull, key);
+            const int leader = __ffs(__ballot_sync(kFull, act && key == kmax)) - 1;
+            const int32_t lc = __shfl_sync(kFull, ci, leader);
+            const bool in = act && ci == lc;
+            float v_sig = 0.f, v_px = 0.f, v_py = 0.f, v_pz = 0.f;
+            float v_jx = 0.f, v_jy = 0.f, v_jz = 0.f;
+            float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+            int32_t jn = -1;
+            if (in) {
+                double sig = ld_site(S.site4 + ci).w;
                 double delta = t1 - t0;
                 double alpha = 1.0 - exp(-sig * delta);
-                double w = tb_s * alpha;
+                double w = tb0 * alpha;
                 double c0 = s_col[(3 * s) * SL], c1 = s_col[(3 * s + 1) * SL],
                        c2 = s_col[(3 * s + 2) * SL];
-                double g_r = ar * (tb_s1 * c0 - Sr);
-                double g_g = ag * (tb_s1 * c1 - Sg);
-                double g_b = ab * (tb_s1 * c2 - Sb);
+                double g_r = ar * (tb1 * c0 - Sr);
+                double g_g = ag * (tb1 * c1 - Sg);
+                double g_b = ab * (tb1 * c2 - Sb);
                 double common = g_r + g_g + g_b;
-                atomicAdd(gr.g4 + 4 * (int64_t)ci + 3, (float)(delta * common));
+                v_sig = (float)(delta * common);
                 double dd = sig * common;
-                if (s < nseg - 1) {  // interior boundary s+1 (kernels.py:328-337)
+                if (next_cell >= 0) {  // interior boundary s+1 (kernels.py:328-337)
                     double dt = dd - d_next;
-                    if (dt != 0.0) {
-                        int32_t cj = s_cell[(s + 1) * SL] & 0x1fffffff;
-                        face_t_gradient(S.site4, ci, cj, r, t1, dt, gr.g4);
+                    double gi[3], gj[3];
+                    if (dt != 0.0 && face_grad(S.site4, ci, next_cell, r, t1, dt, gi, gj)) {
+                        v_px = (float)gi[0];
+                        v_py = (float)gi[1];
+                        v_pz = (float)gi[2];
+                        v_jx = (float)gj[0];
+                        v_jy = (float)gj[1];
+                        v_jz = (float)gj[2];
+                        jn = next_cell;
                     }
                 }
-                if (w != 0.0) add_sh<SHDEG>(gr.sh, ci, mask, w, ar, ag, ab, basis);
+                if (w != 0.0) {  // kernels.py:309-322
+                    if ((cmask & 1) == 0 && ar != 0.0) f0 = (float)(w * ar);
+                    if ((cmask & 2) == 0 && ag != 0.0) f1 = (float)(w * ag);
+                    if ((cmask & 4) == 0 && ab != 0.0) f2 = (float)(w * ab);
+                }
                 Sr = Sr + w * c0;
                 Sg = Sg + w * c1;
                 Sb = Sb + w * c2;
                 d_next = dd;
+                next_cell = ci;
+                s -= 1;
+                if (s >= 0) load_seg();
+            }
+            // dsigma + dpos of the group's cell: one float4 atomic
+            v_sig = warp_sum(v_sig);
+            v_px = warp_sum(v_px);
+            v_py = warp_sum(v_py);
+            v_pz = warp_sum(v_pz);
+            if (lane == leader) red4(gr.g4 + 4 * (int64_t)lc, v_px, v_py, v_pz, v_sig);
+            // dpos of the previously processed cell: aggregated when the group agrees
+            const int32_t jany = __reduce_max_sync(kFull, in ? jn : -1);
+            if (jany >= 0) {
+                if (__all_sync(kFull, !in || jn < 0 || jn == jany)) {
+                    v_jx = warp_sum(v_jx);
+                    v_jy = warp_sum(v_jy);
+                    v_jz = warp_sum(v_jz);
+                    if (lane == leader) red4(gr.g4 + 4 * (int64_t)jany, v_jx, v_jy, v_jz, 0.f);
+                } else if (in && jn >= 0) {
+                    red4(gr.g4 + 4 * (int64_t)jn, v_jx, v_jy, v_jz, 0.f);
+                }
+            }
+            // dSH: sum_l f_l[ch] * basis_l[k] over the group, 48 outputs
+            const unsigned gm = __ballot_sync(kFull, in && (f0 != 0.f || f1 != 0.f || f2 != 0.f));
+            if (gm) {
+                s_f[warp][lane][0] = f0;
+                s_f[warp][lane][1] = f1;
+                s_f[warp][lane][2] = f2;
+                __syncwarp();
+                float acc0 = 0.f, acc1 = 0.f;
+                const int k0 = lane / 3, ch0 = lane % 3;
+                const int o1 = lane + 32, k1 = o1 / 3, ch1 = o1 % 3;
+                unsigned mm = gm;
+                while (mm) {
+                    const int l = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    acc0 += s_f[warp][l][ch0] * s_basis[warp][l][k0];
+                    if (o1 < 48) acc1 += s_f[warp][l][ch1] * s_basis[warp][l][k1];
+                }
+                float *row = gr.sh + 48 * (int64_t)lc;
+                atomicAdd(row + lane, acc0);
+                if (o1 < 48) atomicAdd(row + o1, acc1);
+                __syncwarp();
             }
         }
 
-        // quantile_backward_ray (kernels.py:456-567) for each pair.
-        if (TRAIN && q_scale > 0.0 && nseg > 0) {
-            double T_end = s_tb[(nseg - 1) * SL];
-            double tot = 1.0 - T_end;
+        // ---- quantile pairs (kernels.py:456-567), per lane ----------------
+        if (TRAIN && q_scale > 0.0 && grad_ok) {
+            double T_end_q = s_tb[(nseg - 1) * SL];
+            double tot = 1.0 - T_end_q;
             if (!(tot < weight_floor)) {
                 for (int32_t p = 0; p < n_pairs; ++p) {
                     const double *up = u_pairs + (q * n_pairs + p) * 2;
@@ -515,23 +577,22 @@ __global__ void __launch_bounds__(128) k_backward(DevScene S, ArrayRays src, dou
                     int32_t seg_hit[2];
                     for (int a = 0; a < 2; ++a) {
                         double target = up[a] * tot;
-                        int32_t s = 0;
-                        while (s < nseg - 1 && (1.0 - s_tb[s * SL]) < target) s += 1;
-                        int32_t ci = s_cell[s * SL] & 0x1fffffff;
-                        double si = __ldg(&S.site4[ci].w);
-                        double t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min;
-                        seg_hit[a] = s;
+                        int32_t sh_ = 0;
+                        while (sh_ < nseg - 1 && (1.0 - s_tb[sh_ * SL]) < target) sh_ += 1;
+                        int32_t c_ = s_cell[sh_ * SL] & 0x1fffffff;
+                        double si = ld_site(S.site4 + c_).w;
+                        double ts0 = sh_ > 0 ? s_t1[(sh_ - 1) * SL] : r.t_min;
+                        seg_hit[a] = sh_;
                         if (si <= 0.0) {
-                            t_hit[a] = t0;
+                            t_hit[a] = ts0;
                             continue;
                         }
-                        double Tbs = s > 0 ? s_tb[(s - 1) * SL] : 1.0;
-                        double Wbs = 1.0 - Tbs;
-                        double frac = (target - Wbs) / Tbs;
+                        double Tbs = sh_ > 0 ? s_tb[(sh_ - 1) * SL] : 1.0;
+                        double frac = (target - (1.0 - Tbs)) / Tbs;
                         if (frac > 1.0 - 1e-15) frac = 1.0 - 1e-15;
-                        double th = t0 - log(1.0 - frac) / si;
-                        double t1 = s_t1[s * SL];
-                        if (th > t1) th = t1;
+                        double th = ts0 - log(1.0 - frac) / si;
+                        double ts1 = s_t1[sh_ * SL];
+                        if (th > ts1) th = ts1;
                         t_hit[a] = th;
                     }
                     double diff = t_hit[0] - t_hit[1];
@@ -540,13 +601,13 @@ __global__ void __launch_bounds__(128) k_backward(DevScene S, ArrayRays src, dou
                     double sign = diff > 0.0 ? 1.0 : -1.0;
                     for (int a = 0; a < 2; ++a) {
                         double u = up[a];
-                        int32_t s = seg_hit[a];
-                        int32_t ci = s_cell[s * SL] & 0x1fffffff;
-                        double si = __ldg(&S.site4[ci].w);
+                        int32_t sh_ = seg_hit[a];
+                        int32_t c_ = s_cell[sh_ * SL] & 0x1fffffff;
+                        double si = ld_site(S.site4 + c_).w;
                         double t_u = t_hit[a];
-                        double t0s = s > 0 ? s_t1[(s - 1) * SL] : r.t_min;
-                        double Tbs = s > 0 ? s_tb[(s - 1) * SL] : 1.0;
-                        double T_at = Tbs * exp(-si * (t_u - t0s));
+                        double ts0 = sh_ > 0 ? s_t1[(sh_ - 1) * SL] : r.t_min;
+                        double Tbs = sh_ > 0 ? s_tb[(sh_ - 1) * SL] : 1.0;
+                        double T_at = Tbs * exp(-si * (t_u - ts0));
                         double wd = T_at * si;
                         if (wd <= 1e-300) continue;
                         double g = (a == 0 ? sign : -sign) * q_scale / wd;
@@ -555,12 +616,11 @@ __global__ void __launch_bounds__(128) k_backward(DevScene S, ArrayRays src, dou
                             double k_t0 = prev_t1, k_t1 = s_t1[k * SL];
                             prev_t1 = k_t1;
                             int32_t ck = s_cell[k * SL] & 0x1fffffff;
-                            double dA = T_end * (k_t1 - k_t0);
+                            double dA = T_end_q * (k_t1 - k_t0);
                             double contrib;
                             if (k_t0 < t_u) {
                                 double hi = k_t1 < t_u ? k_t1 : t_u;
-                                double dW = T_at * (hi - k_t0);
-                                contrib = g * (u * dA - dW);
+                                contrib = g * (u * dA - T_at * (hi - k_t0));
                             } else {
                                 contrib = g * (u * dA);
                             }
@@ -569,27 +629,25 @@ __global__ void __launch_bounds__(128) k_backward(DevScene S, ArrayRays src, dou
                         for (int32_t mm = 1; mm < nseg; ++mm) {  // kernels.py:552-566
                             int32_t im = s_cell[(mm - 1) * SL] & 0x1fffffff;
                             int32_t jm = s_cell[mm * SL] & 0x1fffffff;
-                            double dsig = __ldg(&S.site4[im].w) - __ldg(&S.site4[jm].w);
+                            double dsig = ld_site(S.site4 + im).w - ld_site(S.site4 + jm).w;
                             if (dsig == 0.0) continue;
-                            double tb = s_t1[(mm - 1) * SL];
-                            double dW = tb < t_u ? T_at * dsig : 0.0;
-                            double dA = T_end * dsig;
-                            double dt_term = g * (u * dA - dW);
-                            if (dt_term != 0.0) face_t_gradient(S.site4, im, jm, r, tb, dt_term, gr.g4);
+                            double tbq = s_t1[(mm - 1) * SL];
+                            double dW = tbq < t_u ? T_at * dsig : 0.0;
+                            double dt_term = g * (u * (T_end_q * dsig) - dW);
+                            if (dt_term != 0.0)
+                                face_grad_atomic(S.site4, im, jm, r, tbq, dt_term, gr.g4);
                         }
                     }
                 }
             }
         }
     }
-    // per-warp reductions of the loss and counters
-    const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-        loss_rgb += __shfl_xor_sync(0xffffffffu, loss_rgb, off);
-        loss_q += __shfl_xor_sync(0xffffffffu, loss_q, off);
-        my_cells += __shfl_xor_sync(0xffffffffu, my_cells, off);
-        my_visits += __shfl_xor_sync(0xffffffffu, my_visits, off);
+        loss_rgb += __shfl_xor_sync(kFull, loss_rgb, off);
+        loss_q += __shfl_xor_sync(kFull, loss_q, off);
+        my_cells += __shfl_xor_sync(kFull, my_cells, off);
+        my_visits += __shfl_xor_sync(kFull, my_visits, off);
     }
     if (lane == 0) {
         if (TRAIN && loss) {
@@ -606,24 +664,55 @@ __global__ void __launch_bounds__(128) k_backward(DevScene S, ArrayRays src, dou
 // ---------------------------------------------------------------------------
 // Scene packing, activation, camera rays, start-cell location.
 // ---------------------------------------------------------------------------
-__global__ void k_pack_sites(const double *pos, const double *sigma, int64_t n, double4 *site4) {
+__global__ void k_pack_sites(const double *pos, const double *sigma, const double *sh, int64_t n,
+                             const int64_t *off64, double4 *site4, int32_t *off32, CellHdr *cells,
+                             float *sh32) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sigma[i]);
+    if (i > n) return;
+    off32[i] = (int32_t)off64[i];
+    if (i == n) return;
+    site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sigma[i]);
+    if (cells) {
+        float cmax = 0.f;
+        for (int k = 0; k < 16; ++k)
+            for (int ch = 0; ch < 3; ++ch) {
+                double v = sh[i * 48 + 3 * k + ch];
+                sh32[i * 48 + 16 * ch + k] = (float)v;  // channel-major copy
+                cmax = fmaxf(cmax, (float)fabs(v));
+            }
+        CellHdr h;
+        h.x = (float)pos[3 * i];
+        h.y = (float)pos[3 * i + 1];
+        h.z = (float)pos[3 * i + 2];
+        h.k0 = (int32_t)off64[i];
+        h.sigma = sigma[i];
+        h.k1 = (int32_t)off64[i + 1];
+        h.cmax = cmax * (1.0f + 0x1p-20f);  // upper bound of |coefficient|
+        cells[i] = h;
+    }
 }
 
-__global__ void k_narrow(const int64_t *src, int64_t n, int32_t *dst) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) dst[i] = (int32_t)src[i];
+__global__ void k_pack_edges(const int64_t *nbr64, const double *pos, int64_t E, int32_t *nbr32,
+                             float4 *edges) {
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= E) return;
+    int32_t j = (int32_t)nbr64[k];
+    nbr32[k] = j;
+    if (edges)
+        edges[k] = make_float4((float)pos[3 * j], (float)pos[3 * j + 1], (float)pos[3 * j + 2],
+                               __int_as_float(j));
 }
 
-// foam.py:22-25 (device libm; differs from numpy's log1p/exp by <= 1 ulp).
-__global__ void k_softplus(const double *raw, int64_t n, double *out, double4 *site4) {
+// foam.py:22-25 (device libm; may differ from numpy's log1p/exp by 1 ulp).
+__global__ void k_softplus(const double *raw, int64_t n, double *out, double4 *site4,
+                           CellHdr *cells) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double x = raw[i];
     double v = fmax(x, 0.0) + log1p(exp(-fabs(10.0 * x))) / 10.0;
     if (out) out[i] = v;
     if (site4) site4[i].w = v;
+    if (cells) cells[i].sigma = v;
 }
 
 __global__ void k_camera_rays(CameraParams cam, int64_t begin, int64_t count, double *dirs) {
@@ -637,10 +726,15 @@ __global__ void k_camera_rays(CameraParams cam, int64_t begin, int64_t count, do
     dirs[3 * k + 2] = dz;
 }
 
+struct LocScene {
+    const double4 *site4;
+    const int32_t *off, *nbr;
+};
+
 // Greedy point location on the Delaunay graph: move to the neighbour with
 // the smallest (distance, id) while it beats the current site.  Same
 // distance expression and lowest-id tie rule as adjacency.py:194-200.
-__device__ int32_t locate_one(const DevScene &S, double qx, double qy, double qz, int32_t cur) {
+__device__ int32_t locate_one(const LocScene &S, double qx, double qy, double qz, int32_t cur) {
     auto dist = [&](int32_t i) {
         double4 p = ld_site(S.site4 + i);
         double dx = p.x - qx, dy = p.y - qy, dz = p.z - qz;
@@ -665,12 +759,12 @@ __device__ int32_t locate_one(const DevScene &S, double qx, double qy, double qz
     }
 }
 
-__global__ void k_locate(DevScene S, const double *qs, int64_t m, int32_t seed, int32_t *out) {
+__global__ void k_locate(LocScene S, const double *qs, int64_t m, int32_t seed, int32_t *out) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k < m) out[k] = locate_one(S, qs[3 * k], qs[3 * k + 1], qs[3 * k + 2], seed);
 }
 
-__global__ void k_locate_point(DevScene S, double qx, double qy, double qz, int32_t seed,
+__global__ void k_locate_point(LocScene S, double qx, double qy, double qz, int32_t seed,
                                int32_t *out) {
     if (threadIdx.x == 0 && blockIdx.x == 0) *out = locate_one(S, qx, qy, qz, seed);
 }
@@ -689,16 +783,24 @@ static int num_sms() {
     return sms;
 }
 
-static DevScene dev_scene(const rfb_scene *s) {
-    DevScene d;
-    d.site4 = reinterpret_cast<const double4 *>(s->site4);
-    d.off = s->offsets;
-    d.nbr = s->neighbors;
-    d.sh = s->sh;
-    d.bg[0] = s->background[0];
-    d.bg[1] = s->background[1];
-    d.bg[2] = s->background[2];
-    return d;
+template <bool PACKED>
+static SceneView<PACKED> view(const rfb_scene *s) {
+    SceneView<PACKED> v;
+    v.hdr = reinterpret_cast<const CellHdr *>(s->cells);
+    v.edge = reinterpret_cast<const float4 *>(s->edges);
+    v.site4 = reinterpret_cast<const double4 *>(s->site4);
+    v.off = s->offsets;
+    v.nbr = s->neighbors;
+    v.sh32 = s->sh32;
+    v.sh = s->sh;
+    v.bg[0] = s->background[0];
+    v.bg[1] = s->background[1];
+    v.bg[2] = s->background[2];
+    return v;
+}
+
+static LocScene loc_scene(const rfb_scene *s) {
+    return LocScene{reinterpret_cast<const double4 *>(s->site4), s->offsets, s->neighbors};
 }
 
 static FwdOut dev_out(const rfb_fwd_out *o) {
@@ -719,8 +821,11 @@ static FwdOut dev_out(const rfb_fwd_out *o) {
 }
 
 static bool scene_ok(const rfb_scene *s) {
-    return s && s->site4 && s->offsets && s->neighbors && s->sh && s->n_sites > 0 &&
-           s->n_sites < (1 << 29) && (s->sh_degree == 0 || s->sh_degree == 3);
+    if (!s || !s->site4 || !s->offsets || !s->neighbors || !s->sh || s->n_sites <= 0 ||
+        s->n_sites >= (1 << 29) || (s->sh_degree != 0 && s->sh_degree != 3))
+        return false;
+    if (s->packed && (!s->cells || !s->edges || !s->sh32)) return false;
+    return true;
 }
 
 static bool out_ok(const rfb_fwd_out *o) {
@@ -729,20 +834,31 @@ static bool out_ok(const rfb_fwd_out *o) {
     return true;
 }
 
-template <int G, class Src>
-static void launch_render_g(const DevScene &S, const Src &src, int shdeg, double eps,
-                            double log_eps, double wf, int32_t sl, const FwdOut &O,
-                            unsigned long long *ctr, cudaStream_t st) {
+template <int G, bool PACKED, class Src>
+static void launch_render_g(const rfb_scene *scene, const Src &src, double eps, double log_eps,
+                            double wf, int32_t sl, const FwdOut &O, unsigned long long *ctr,
+                            cudaStream_t st) {
+    SceneView<PACKED> S = view<PACKED>(scene);
     int per_sm = 0;
-    if (shdeg == 0) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<G, 0, Src>, 256, 0);
-        k_render<G, 0, Src><<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps,
-                                                                            wf, sl, O, ctr);
+    if (scene->sh_degree == 0) {
+        auto k = k_render<G, 0, PACKED, Src>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
+        k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr);
     } else {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_render<G, 3, Src>, 256, 0);
-        k_render<G, 3, Src><<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps,
-                                                                            wf, sl, O, ctr);
+        auto k = k_render<G, 3, PACKED, Src>;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
+        k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr);
     }
+}
+
+template <int G, class Src>
+static void launch_render_p(const rfb_scene *scene, const Src &src, double eps, double log_eps,
+                            double wf, int32_t sl, const FwdOut &O, unsigned long long *ctr,
+                            cudaStream_t st) {
+    if (scene->packed)
+        launch_render_g<G, true>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
+    else
+        launch_render_g<G, false>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
 }
 
 template <class Src>
@@ -751,17 +867,18 @@ static int launch_render(const rfb_scene *scene, const Src &src, const rfb_param
     if (!ws || ws_bytes < 256) return RFB_EINVAL;
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(ws);
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
-    DevScene S = dev_scene(scene);
     FwdOut O = dev_out(out);
     double log_eps = p->epsilon > 0.0 ? std::log(p->epsilon) : 0.0;
     int g = p->lanes_per_ray <= 0 ? 1 : p->lanes_per_ray;
+    const double e = p->epsilon, wf = p->width_floor;
+    const int32_t sl = p->step_limit;
     switch (g) {
-        case 1: launch_render_g<1>(S, src, scene->sh_degree, p->epsilon, log_eps, p->width_floor, p->step_limit, O, ctr, st); break;
-        case 2: launch_render_g<2>(S, src, scene->sh_degree, p->epsilon, log_eps, p->width_floor, p->step_limit, O, ctr, st); break;
-        case 4: launch_render_g<4>(S, src, scene->sh_degree, p->epsilon, log_eps, p->width_floor, p->step_limit, O, ctr, st); break;
-        case 8: launch_render_g<8>(S, src, scene->sh_degree, p->epsilon, log_eps, p->width_floor, p->step_limit, O, ctr, st); break;
-        case 16: launch_render_g<16>(S, src, scene->sh_degree, p->epsilon, log_eps, p->width_floor, p->step_limit, O, ctr, st); break;
-        case 32: launch_render_g<32>(S, src, scene->sh_degree, p->epsilon, log_eps, p->width_floor, p->step_limit, O, ctr, st); break;
+        case 1: launch_render_p<1>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
+        case 2: launch_render_p<2>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
+        case 4: launch_render_p<4>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
+        case 8: launch_render_p<8>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
+        case 16: launch_render_p<16>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
+        case 32: launch_render_p<32>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
         default: return RFB_EINVAL;
     }
     return (int)cudaGetLastError();
@@ -773,8 +890,28 @@ static int64_t bwd_slot_bytes(int32_t step_limit) {
 
 static int64_t bwd_slots_max() {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_backward<3, true>, 128, 0);
-    return (int64_t)num_sms() * std::max(per_sm, 1) * 128;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_train<3, true, true>, kTrainBlock, 0);
+    return (int64_t)num_sms() * std::max(per_sm, 1) * kTrainBlock;
+}
+
+template <bool PACKED>
+static void launch_train_p(const rfb_scene *scene, dim3 grid, cudaStream_t st, bool train,
+                           const ArrayRays &src, double eps, double log_eps, double wf,
+                           int32_t sl, const double *adj, const double *tg, double rgb_scale,
+                           double q_scale, const double *up, int32_t np, double wfloor,
+                           const FwdOut &O, const Grads &G, double *loss, const Scratch &scr,
+                           unsigned long long *ctr) {
+    SceneView<PACKED> S = view<PACKED>(scene);
+#define RFB_TRAIN(SH, TR)                                                                      \
+    k_train<SH, PACKED, TR><<<grid, kTrainBlock, 0, st>>>(S, src, eps, log_eps, wf, sl, adj, tg, \
+                                                          rgb_scale, q_scale, up, np, wfloor, O, \
+                                                          G, loss, scr, ctr)
+    if (scene->sh_degree == 0) {
+        if (train) RFB_TRAIN(0, true); else RFB_TRAIN(0, false);
+    } else {
+        if (train) RFB_TRAIN(3, true); else RFB_TRAIN(3, false);
+    }
+#undef RFB_TRAIN
 }
 
 static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *p,
@@ -791,17 +928,17 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
         return RFB_EINVAL;
     if (train && (!targets || (q_scale > 0.0 && (!u_pairs || n_pairs <= 0)))) return RFB_EINVAL;
     if (!train && !adjoints) return RFB_EINVAL;
-    if (!ws || ws_bytes < 256 + (size_t)bwd_slot_bytes(p->step_limit) * 128) return RFB_EINVAL;
-    int64_t slots = (int64_t)((ws_bytes - 256) / (size_t)bwd_slot_bytes(p->step_limit));
+    const int64_t per = bwd_slot_bytes(p->step_limit);
+    if (!ws || ws_bytes < 256 + (size_t)per * kTrainBlock) return RFB_EINVAL;
+    int64_t slots = (int64_t)((ws_bytes - 256) / (size_t)per);
     slots = std::min<int64_t>(slots, bwd_slots_max());
-    slots = (slots / 128) * 128;
-    const int64_t ray_blocks = (rays->m + 127) / 128;
-    slots = std::min<int64_t>(slots, ray_blocks * 128);
+    slots = std::min<int64_t>(slots, ((rays->m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
+    slots = (slots / kTrainBlock) * kTrainBlock;
     char *base = reinterpret_cast<char *>(ws);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(base);
     Scratch scr;
     scr.slots = slots;
-    int64_t cap = p->step_limit;
+    const int64_t cap = p->step_limit;
     char *c = base + 256;
     scr.t1 = reinterpret_cast<double *>(c);
     c += cap * slots * 8;
@@ -811,23 +948,20 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     c += cap * slots * 4;
     scr.col = reinterpret_cast<float *>(c);
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
-    DevScene S = dev_scene(scene);
     FwdOut O = dev_out(out);
     ArrayRays src{rays->origins, rays->directions, rays->t_min, rays->t_max, rays->start_sites,
                   rays->m};
     Grads G{grads->site4g, grads->sh};
     double log_eps = p->epsilon > 0.0 ? std::log(p->epsilon) : 0.0;
-    dim3 grid((unsigned)(slots / 128));
-#define RFB_BWD(SH, TR)                                                                           \
-    k_backward<SH, TR><<<grid, 128, 0, st>>>(S, src, p->epsilon, log_eps, p->width_floor,        \
-                                             p->step_limit, adjoints, targets, rgb_scale, q_scale, \
-                                             u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr)
-    if (scene->sh_degree == 0) {
-        if (train) RFB_BWD(0, true); else RFB_BWD(0, false);
-    } else {
-        if (train) RFB_BWD(3, true); else RFB_BWD(3, false);
-    }
-#undef RFB_BWD
+    dim3 grid((unsigned)(slots / kTrainBlock));
+    if (scene->packed)
+        launch_train_p<true>(scene, grid, st, train, src, p->epsilon, log_eps, p->width_floor,
+                             p->step_limit, adjoints, targets, rgb_scale, q_scale, u_pairs,
+                             n_pairs, wfloor, O, G, loss, scr, ctr);
+    else
+        launch_train_p<false>(scene, grid, st, train, src, p->epsilon, log_eps, p->width_floor,
+                              p->step_limit, adjoints, targets, rgb_scale, q_scale, u_pairs,
+                              n_pairs, wfloor, O, G, loss, scr, ctr);
     return (int)cudaGetLastError();
 }
 
@@ -867,26 +1001,30 @@ int rfb_device_ok(void) {
     return major == 10 ? 1 : 0;
 }
 
-int rfb_pack_scene(const double *positions, const double *sigma, const int64_t *offsets,
-                   const int64_t *neighbors, int64_t n_sites, int64_t n_edges, double *site4,
-                   int32_t *offsets32, int32_t *neighbors32, void *stream) {
+int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
+                   const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
+                   int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
+                   void *cells, void *edges, float *sh32, void *stream) {
     if (!positions || !sigma || !offsets || !neighbors || !site4 || !offsets32 || !neighbors32 ||
-        n_sites <= 0 || n_edges < 0 || n_edges >= (int64_t)1 << 31)
+        n_sites <= 0 || n_edges < 0 || n_edges >= ((int64_t)1 << 31) ||
+        ((cells || edges || sh32) && (!cells || !edges || !sh32 || !sh)))
         return RFB_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    k_pack_sites<<<(unsigned)((n_sites + 255) / 256), 256, 0, st>>>(
-        positions, sigma, n_sites, reinterpret_cast<double4 *>(site4));
-    k_narrow<<<(unsigned)((n_sites + 1 + 255) / 256), 256, 0, st>>>(offsets, n_sites + 1, offsets32);
+    k_pack_sites<<<(unsigned)((n_sites + 1 + 255) / 256), 256, 0, st>>>(
+        positions, sigma, sh, n_sites, offsets, reinterpret_cast<double4 *>(site4), offsets32,
+        reinterpret_cast<CellHdr *>(cells), sh32);
     if (n_edges > 0)
-        k_narrow<<<(unsigned)((n_edges + 255) / 256), 256, 0, st>>>(neighbors, n_edges, neighbors32);
+        k_pack_edges<<<(unsigned)((n_edges + 255) / 256), 256, 0, st>>>(
+            neighbors, positions, n_edges, neighbors32, reinterpret_cast<float4 *>(edges));
     return (int)cudaGetLastError();
 }
 
-int rfb_softplus(const double *raw, int64_t n, double *out, double *site4_sigma, void *stream) {
-    if (!raw || n < 0 || (!out && !site4_sigma)) return RFB_EINVAL;
+int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void *cells,
+                 void *stream) {
+    if (!raw || n < 0 || (!out && !site4 && !cells)) return RFB_EINVAL;
     if (n == 0) return RFB_OK;
     k_softplus<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        raw, n, out, reinterpret_cast<double4 *>(site4_sigma));
+        raw, n, out, reinterpret_cast<double4 *>(site4), reinterpret_cast<CellHdr *>(cells));
     return (int)cudaGetLastError();
 }
 
@@ -908,15 +1046,16 @@ int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t
         seed_site >= scene->n_sites)
         return RFB_EINVAL;
     if (m == 0) return RFB_OK;
-    k_locate<<<(unsigned)((m + 127) / 128), 128, 0, (cudaStream_t)stream>>>(dev_scene(scene),
+    k_locate<<<(unsigned)((m + 127) / 128), 128, 0, (cudaStream_t)stream>>>(loc_scene(scene),
                                                                             queries, m, seed_site, out);
     return (int)cudaGetLastError();
 }
 
 size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind) {
     if (kind == 0) return 256;
-    int64_t slots = std::min<int64_t>(bwd_slots_max(), ((m + 127) / 128) * 128);
-    slots = std::max<int64_t>(slots, 128);
+    int64_t slots = std::min<int64_t>(bwd_slots_max(),
+                                      ((m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
+    slots = std::max<int64_t>(slots, kTrainBlock);
     return 256 + (size_t)slots * (size_t)bwd_slot_bytes(step_limit);
 }
 
@@ -947,7 +1086,7 @@ int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb
     cudaStream_t st = (cudaStream_t)stream;
     int32_t *start_ptr = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + 64);
     if (start_site < 0) {
-        k_locate_point<<<1, 32, 0, st>>>(dev_scene(scene), camera->pose[3], camera->pose[7],
+        k_locate_point<<<1, 32, 0, st>>>(loc_scene(scene), camera->pose[3], camera->pose[7],
                                          camera->pose[11], 0, start_ptr);
     } else {
         cudaMemcpyAsync(start_ptr, &start_site, sizeof(int32_t), cudaMemcpyHostToDevice, st);

@@ -5,6 +5,15 @@
 // visited-cell sequence is bit-identical to rfoam/tracer/kernels.py:76-162
 // (numba, fastmath=False, rfoam/_accel.py:33-39).  The only intentional FMA
 // (camera rays) is written with explicit __fma_rn to match numpy's matmul.
+//
+// Scene layouts:
+//  * Packed (positions exactly representable in fp32, the fixture rule):
+//      cell header  [n]  32 B = {float x,y,z; int k0; double sigma; int k1; float cmax}
+//      edge record  [E]  16 B = {float xj, yj, zj; int j}   (CSR order)
+//    One step = one 32-byte header load + one 16-byte load per neighbour,
+//    contiguous per cell; the fp32 values are widened to fp64 exactly.
+//  * Generic (arbitrary fp64 positions): site4 [n] {x,y,z,sigma} fp64,
+//    offsets/neighbors int32 -- two dependent gathers per neighbour.
 #pragma once
 
 #include <cstdint>
@@ -28,6 +37,8 @@ constexpr double kC3_2 = 0.4570457994644658;
 constexpr double kC3_3 = 0.3731763325901154;
 constexpr double kC3_5 = 1.445305721320277;
 
+__device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000LL); }
+
 // tracer/kernels.py:38-58, same association order.
 __device__ __forceinline__ void sh_basis(double dx, double dy, double dz, double *out) {
     double xx = dx * dx, yy = dy * dy, zz = dz * dz;
@@ -49,53 +60,159 @@ __device__ __forceinline__ void sh_basis(double dx, double dy, double dz, double
     out[15] = kC3_0 * dx * (xx - 3.0 * yy);
 }
 
-// tracer/kernels.py:61-73.  SHDEG 0 reads only the DC band: with bands 1..15
-// all zero the skipped terms add +-0.0, so the result is bit-identical.
-template <int SHDEG>
-__device__ __forceinline__ int cell_color(const double *__restrict__ sh, int32_t i,
-                                          const double *basis, double *col) {
-    const double *row = sh + (int64_t)i * 48;
-    int mask = 0;
-    if (SHDEG == 0) {
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            double acc = 0.5;
-            acc += basis[0] * __ldg(row + ch);
-            if (acc < 0.0) {
-                acc = 0.0;
-                mask |= 1 << ch;
-            }
-            col[ch] = acc;
-        }
-    } else {
-        double c[48];
-        const double2 *row2 = reinterpret_cast<const double2 *>(row);
-#pragma unroll
-        for (int k = 0; k < 24; ++k) {
-            double2 v = __ldg(row2 + k);
-            c[2 * k] = v.x;
-            c[2 * k + 1] = v.y;
-        }
-#pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            double acc = 0.5;
-#pragma unroll
-            for (int k = 0; k < 16; ++k) acc += basis[k] * c[k * 3 + ch];
-            if (acc < 0.0) {
-                acc = 0.0;
-                mask |= 1 << ch;
-            }
-            col[ch] = acc;
-        }
-    }
-    return mask;
-}
-
-// 32-byte read-only site record load (two 16-byte vector loads).
+// 32-byte read-only record load (two 16-byte vector loads).
 __device__ __forceinline__ double4 ld_site(const double4 *p) {
     const double2 *q = reinterpret_cast<const double2 *>(p);
     double2 a = __ldg(q), b = __ldg(q + 1);
     return make_double4(a.x, a.y, b.x, b.y);
+}
+
+struct CellHdr {  // packed layout, 32 bytes
+    float x, y, z;
+    int32_t k0;
+    double sigma;
+    int32_t k1;
+    float cmax;  // max |sh coefficient| of the site (fp32 colour error bound)
+};
+static_assert(sizeof(CellHdr) == 32, "cell header must be one 32-byte sector");
+
+struct Cell {
+    double x, y, z, sigma;
+    int32_t k0, k1;
+    float cmax;
+    float4 hf;  // packed: fp32 x, y, z (exact copies of x, y, z)
+};
+
+// Read-only view of the device scene.  PACKED selects the layout above.
+template <bool PACKED>
+struct SceneView {
+    const CellHdr *hdr;     // PACKED
+    const float4 *edge;     // PACKED
+    const double4 *site4;   // both (backward gradients use fp64 positions)
+    const int32_t *off;     // generic
+    const int32_t *nbr;     // generic
+    const float *sh32;      // [n][3][16] fp32, channel-major (PACKED) -- exact fallback below
+    const double *sh;       // [n][48] fp64 (reference values)
+    double bg[3];
+
+    __device__ __forceinline__ Cell cell(int32_t i) const {
+        Cell c;
+        if (PACKED) {
+            const float4 *p = reinterpret_cast<const float4 *>(hdr + i);
+            float4 a = __ldg(p), b = __ldg(p + 1);
+            c.hf = a;
+            c.x = a.x;
+            c.y = a.y;
+            c.z = a.z;
+            c.k0 = __float_as_int(a.w);
+            c.sigma = __hiloint2double(__float_as_int(b.y), __float_as_int(b.x));
+            c.k1 = __float_as_int(b.z);
+            c.cmax = b.w;
+        } else {
+            double4 s = ld_site(site4 + i);
+            c.x = s.x;
+            c.y = s.y;
+            c.z = s.z;
+            c.sigma = s.w;
+            c.k0 = __ldg(off + i);
+            c.k1 = __ldg(off + i + 1);
+            c.cmax = 0.f;
+        }
+        return c;
+    }
+
+    __device__ __forceinline__ void edge_at(int32_t k, double &x, double &y, double &z,
+                                            int32_t &j) const {
+        if (PACKED) {
+            float4 e = __ldg(edge + k);
+            x = e.x;
+            y = e.y;
+            z = e.z;
+            j = __float_as_int(e.w);
+        } else {
+            j = __ldg(nbr + k);
+            double4 s = ld_site(site4 + j);
+            x = s.x;
+            y = s.y;
+            z = s.z;
+        }
+    }
+};
+
+// tracer/kernels.py:61-73.  SHDEG 0 reads only the DC band: with bands 1..15
+// all zero the skipped terms add +-0.0, so the result is bit-identical.
+//
+// PACKED (fast path): basis (fp32, per ray) and coefficients (fp32 copy) are
+// accumulated with fp32 FMAs in the reference's k order.  Input rounding (2u)
+// plus 16 accumulation roundings bound the deviation from the reference by
+// 20u * (cmax * sum|basis| + 1), u = 2^-24; whenever |acc| is within 2^-19 *
+// (cmax * sum|basis| + 1) >= that bound of the clamp threshold, the channel is
+// recomputed exactly (fp64 basis from the direction, fp64 coefficients), so
+// the clamp mask -- which gates the SH gradient -- is always the reference's
+// and the colour is within ~1e-6 of it.
+template <int SHDEG, bool PACKED>
+__device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i, float cmax,
+                                          const float *basis_f, const double *dir,
+                                          double bsum, double *col) {
+    constexpr int NB = SHDEG == 0 ? 1 : 16;
+    double acc[3] = {0.5, 0.5, 0.5};
+    if (PACKED) {
+        // sh32 is channel-major per site: [ch][16]; fp32 FMA accumulation
+        const float *row = S.sh32 + (int64_t)i * 48;
+        if (SHDEG == 0) {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch)
+                acc[ch] = (double)__fmaf_rn(basis_f[0], __ldg(row + 16 * ch), 0.5f);
+        } else {
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) {
+                const float4 *r4 = reinterpret_cast<const float4 *>(row + 16 * ch);
+                float a = 0.5f;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    float4 v = __ldg(r4 + q);
+                    a = __fmaf_rn(basis_f[4 * q], v.x, a);
+                    a = __fmaf_rn(basis_f[4 * q + 1], v.y, a);
+                    a = __fmaf_rn(basis_f[4 * q + 2], v.z, a);
+                    a = __fmaf_rn(basis_f[4 * q + 3], v.w, a);
+                }
+                acc[ch] = (double)a;
+            }
+        }
+    } else {
+        double basis[16];
+        if (SHDEG == 0)
+            basis[0] = kC0;
+        else
+            sh_basis(dir[0], dir[1], dir[2], basis);
+        const double *row = S.sh + (int64_t)i * 48;
+#pragma unroll
+        for (int k = 0; k < NB; ++k)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) acc[ch] += basis[k] * __ldg(row + k * 3 + ch);
+    }
+    const double tol = PACKED ? ((double)cmax * bsum + 1.0) * 0x1p-19 : 0.0;
+    int mask = 0;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        double a = acc[ch];
+        if (PACKED && fabs(a) <= tol) {  // ambiguous clamp: redo in fp64 (exact)
+            double basis[16];
+            if (SHDEG == 0)
+                basis[0] = kC0;
+            else
+                sh_basis(dir[0], dir[1], dir[2], basis);
+            const double *row = S.sh + (int64_t)i * 48;
+            a = 0.5;
+            for (int k = 0; k < NB; ++k) a += basis[k] * __ldg(row + k * 3 + ch);
+        }
+        if (a < 0.0) {
+            a = 0.0;
+            mask |= 1 << ch;
+        }
+        col[ch] = a;
+    }
+    return mask;
 }
 
 struct Ray {
@@ -113,32 +230,178 @@ __device__ __forceinline__ bool below_epsilon(double log_T, double epsilon, doub
     return exp(log_T) < epsilon;
 }
 
-// One walk step's exit-face search over the CSR row of cell i, executed by
+// One walk step's exit-face search over the CSR row of cell c, executed by
 // the G lanes of a ray group (gl = lane within group); returns the group-wide
 // first minimum in ascending CSR order (kernels.py:116-133).
-template <int G>
-__device__ __forceinline__ void exit_face(const double4 *__restrict__ site4,
-                                          const int32_t *__restrict__ nbr, int32_t k0, int32_t k1,
-                                          double4 xi, const Ray &r, int gl, unsigned gmask,
-                                          double &best_t, int32_t &best_j) {
-    best_t = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+//
+// Division filter: a candidate whose exact quotient num/denom is provably
+// larger than the current best's (cross-multiplied with a rounding margin;
+// both denominators are > 0) cannot satisfy the reference's `t < best_t`
+// (rounding is monotone), so it is rejected without the fp64 division.
+// Every quotient that could win is computed with IEEE division exactly as
+// in the reference.
+#ifndef RFB_EXIT_UNROLL
+#define RFB_EXIT_UNROLL 2
+#endif
+#define RFB_STR_(x) #x
+#define RFB_PRAGMA_UNROLL(n) _Pragma(RFB_STR_(unroll n))
+
+template <int G, bool PACKED>
+__device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell &c,
+                                          const Ray &r, int gl, unsigned gmask, double &best_t,
+                                          int32_t &best_j) {
+    best_t = dinf();
     best_j = -1;
     int32_t best_k = 0x7fffffff;
-    for (int32_t k = k0 + gl; k < k1; k += G) {
-        int32_t j = __ldg(nbr + k);
-        double4 xj = ld_site(site4 + j);
-        double nx = xj.x - xi.x;
-        double ny = xj.y - xi.y;
-        double nz = xj.z - xi.z;
+    double bnum = 0.0, bden = 1.0;
+    bool have = false;
+    RFB_PRAGMA_UNROLL(RFB_EXIT_UNROLL)
+    for (int32_t k = c.k0 + gl; k < c.k1; k += G) {
+        double xj, yj, zj;
+        int32_t j;
+        S.edge_at(k, xj, yj, zj, j);
+        double nx = xj - c.x;
+        double ny = yj - c.y;
+        double nz = zj - c.z;
         double denom = r.dx * nx + r.dy * ny + r.dz * nz;
         if (denom <= 0.0) continue;
-        double mx = 0.5 * (xj.x + xi.x);
-        double my = 0.5 * (xj.y + xi.y);
-        double mz = 0.5 * (xj.z + xi.z);
-        double t = ((mx - r.ox) * nx + (my - r.oy) * ny + (mz - r.oz) * nz) / denom;
+        double mx = 0.5 * (xj + c.x);
+        double my = 0.5 * (yj + c.y);
+        double mz = 0.5 * (zj + c.z);
+        double num = (mx - r.ox) * nx + (my - r.oy) * ny + (mz - r.oz) * nz;
+        if (have) {
+            double c1 = num * bden, c2 = bnum * denom;
+            if (c1 - c2 > (fabs(c1) + fabs(c2)) * 0x1p-50) continue;
+        }
+        double t = num / denom;
         if (t < best_t) {
             best_t = t;
             best_j = j;
+            best_k = k;
+            bnum = num;
+            bden = denom;
+            have = true;
+        }
+    }
+    if (G > 1) {
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) {
+            double ot = __shfl_xor_sync(gmask, best_t, off, G);
+            int32_t oj = __shfl_xor_sync(gmask, best_j, off, G);
+            int32_t ok = __shfl_xor_sync(gmask, best_k, off, G);
+            if (ot < best_t || (ot == best_t && ok < best_k)) {
+                best_t = ot;
+                best_j = oj;
+                best_k = ok;
+            }
+        }
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Packed-layout exit face with an fp32 pre-filter.
+//
+// Phase 1 (fp32 FMA, no conversions): for every neighbour compute, relative
+// to q = o + entry*d (fp64, rounded once to fp32), the shifted depth
+// s = ((m - q).n) / (d.n) and a rigorous bound on |s - s_exact|:
+//   den:  |den_f - d.n|  <= Ed = 8u |n|_1                       (u = 2^-24)
+//   num:  |num_f - (m-q).n| <= En = u |n|_1 (|q|_inf + 8|h|_inf + 2|n|_1)
+//   s:    es = 2.2 (En + |s| Ed) / den_f + 8u |s| + 2^-40 (|entry| + |s| + 1)
+// (first-order roundings of the inputs, the differences, the FMA chains and
+// the fast division, with margin; the last term covers the reference's own
+// fp64 rounding).  A neighbour is certainly back-facing if den_f < -Ed, and
+// certainly front-facing if den_f > 2 Ed; anything in between is
+// "uncertain".  Front-facing neighbours with s - es > U, U the running
+// minimum of s + es, cannot be the reference's first minimum (their fp64
+// t is strictly larger than some other neighbour's).
+// Phase 2 (fp64, exactly the reference's expressions): every uncertain
+// neighbour and every front-facing one that was within the running band
+// when it was seen (a superset of the final band) is re-evaluated in CSR
+// order with `denom <= 0 -> skip`, `t < best_t` -- so best_t / best_j are
+// bit-identical to kernels.py:116-133.  Rows longer than 64 neighbours
+// evaluate the tail exactly.
+// ---------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Cell &c,
+                                              const float4 &hdr_f, const Ray &r, double entry,
+                                              const float *df, int gl, unsigned gmask,
+                                              double &best_t, int32_t &best_j) {
+    constexpr float u = 0x1p-24f;
+    // q = o + entry * d in fp64 (once per step), rounded to fp32
+    const double qx = r.ox + entry * r.dx, qy = r.oy + entry * r.dy, qz = r.oz + entry * r.dz;
+    const float qxf = (float)qx, qyf = (float)qy, qzf = (float)qz;
+    const float Q = fmaxf(fabsf(qxf), fmaxf(fabsf(qyf), fabsf(qzf))) * (1.0f + 4.0f * u);
+    const float px = hdr_f.x - qxf, py = hdr_f.y - qyf, pz = hdr_f.z - qzf;
+    const float slack = (float)(0x1p-40 * (fabs(entry) + 1.0));
+    float U = __int_as_float(0x7f800000);  // +inf
+    unsigned long long mask = 0ull;
+    const int32_t k0 = c.k0 + gl;
+    int32_t nk = 0;
+    for (int32_t k = k0; k < c.k1; k += G, ++nk) {
+        const float4 e = __ldg(S.edge + k);
+        const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
+        const float den = __fmaf_rn(df[2], nz, __fmaf_rn(df[1], ny, df[0] * nx));
+        const float n1 = fabsf(nx) + fabsf(ny) + fabsf(nz);
+        const float Ed = 8.0f * u * n1;
+        if (den < -Ed) continue;                       // certainly back-facing
+        const unsigned long long bit = nk < 64 ? (1ull << nk) : 0ull;
+        if (den <= 2.0f * Ed || den < 0x1p-100f) {     // uncertain: exact path
+            mask |= bit;
+            continue;
+        }
+        const float hx = __fmaf_rn(0.5f, nx, px), hy = __fmaf_rn(0.5f, ny, py),
+                    hz = __fmaf_rn(0.5f, nz, pz);
+        const float num = __fmaf_rn(hz, nz, __fmaf_rn(hy, ny, hx * nx));
+        const float H = fmaxf(fabsf(hx), fmaxf(fabsf(hy), fabsf(hz)));
+        const float En = u * n1 * (Q + 8.0f * H + 2.0f * n1);
+        float rinv;  // MUFU reciprocal, <= 1 ulp (normal den guaranteed above)
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rinv) : "f"(den));
+        const float s = num * rinv;
+        const float as = fabsf(s);
+        const float es = 2.2f * (En + as * Ed) * rinv + 8.0f * u * as + slack + 0x1p-40f * as;
+        if (s - es <= U) mask |= bit;
+        U = fminf(U, s + es);
+    }
+    // phase 2: exact fp64 re-evaluation of the candidates, CSR order
+    best_t = dinf();
+    best_j = -1;
+    int32_t best_k = 0x7fffffff;
+    const int32_t nexact = nk;
+    for (;;) {
+        int32_t idx;
+        if (mask) {
+            idx = __ffsll((long long)mask) - 1;
+            mask &= mask - 1;
+        } else {
+            break;
+        }
+        const int32_t k = k0 + idx * G;
+        const float4 e = __ldg(S.edge + k);
+        const double xj = e.x, yj = e.y, zj = e.z;
+        const double nx = xj - c.x, ny = yj - c.y, nz = zj - c.z;
+        const double denom = r.dx * nx + r.dy * ny + r.dz * nz;
+        if (denom <= 0.0) continue;
+        const double mx = 0.5 * (xj + c.x), my = 0.5 * (yj + c.y), mz = 0.5 * (zj + c.z);
+        const double t = ((mx - r.ox) * nx + (my - r.oy) * ny + (mz - r.oz) * nz) / denom;
+        if (t < best_t) {
+            best_t = t;
+            best_j = __float_as_int(e.w);
+            best_k = k;
+        }
+    }
+    for (int32_t idx = 64; idx < nexact; ++idx) {  // rows with > 64 neighbours per lane
+        const int32_t k = k0 + idx * G;
+        const float4 e = __ldg(S.edge + k);
+        const double xj = e.x, yj = e.y, zj = e.z;
+        const double nx = xj - c.x, ny = yj - c.y, nz = zj - c.z;
+        const double denom = r.dx * nx + r.dy * ny + r.dz * nz;
+        if (denom <= 0.0) continue;
+        const double mx = 0.5 * (xj + c.x), my = 0.5 * (yj + c.y), mz = 0.5 * (zj + c.z);
+        const double t = ((mx - r.ox) * nx + (my - r.oy) * ny + (mz - r.oz) * nz) / denom;
+        if (t < best_t) {
+            best_t = t;
+            best_j = __float_as_int(e.w);
             best_k = k;
         }
     }

@@ -54,24 +54,24 @@ class DeviceScene:
     device instead (device-resident training).
     """
 
-    def __init__(self, scene, device=None, sh_degree=None):
+    def __init__(self, scene, device=None, sh_degree=None, packed=None):
         adj = scene.require_adjacency()
         sh = np.asarray(scene.sh_coeffs, dtype=np.float64).reshape(len(adj.positions), 48)
         self._init(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density), sh,
-                   scene.background, adj.bbox_lo, adj.bbox_hi, device, sh_degree)
+                   scene.background, adj.bbox_lo, adj.bbox_hi, device, sh_degree, packed)
 
     @classmethod
     def from_arrays(cls, positions, offsets, neighbors, sigma, sh_flat, background, device=None,
-                    sh_degree=None):
+                    sh_degree=None, packed=None):
         """Flat kernel arrays as passed to kernels.render_rays (kernels.py:199-209)."""
         self = cls.__new__(cls)
         pos = np.asarray(positions, dtype=np.float64)
         self._init(pos, offsets, neighbors, sigma, sh_flat, background, pos.min(axis=0),
-                   pos.max(axis=0), device, sh_degree)
+                   pos.max(axis=0), device, sh_degree, packed)
         return self
 
     def _init(self, positions, offsets, neighbors, sigma, sh_flat, background, bbox_lo, bbox_hi,
-              device, sh_degree):
+              device, sh_degree, packed):
         self.lib = _lib.load()
         self.device = torch.device(device or "cuda")
         pos = np.ascontiguousarray(positions, dtype=np.float64)
@@ -87,19 +87,30 @@ class DeviceScene:
         sh = np.ascontiguousarray(np.asarray(sh_flat, dtype=np.float64).reshape(n, 48))
         self.sh_degree = sh_degree_of(sh) if sh_degree is None else int(sh_degree)
         sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        # packed layout only when every coordinate survives an fp32 round trip
+        self.packed = bool(np.array_equal(pos.astype(np.float32).astype(np.float64), pos)) \
+            if packed is None else bool(packed)
         dev = self.device
         with torch.cuda.device(dev):
             self.site4 = torch.empty((n, 4), dtype=torch.float64, device=dev)
             self.offsets = torch.empty(n + 1, dtype=torch.int32, device=dev)
             self.neighbors = torch.empty(max(self.n_edges, 1), dtype=torch.int32, device=dev)
             self.sh = torch.from_numpy(sh).to(dev)
+            if self.packed:
+                self.cells = torch.empty((n, 8), dtype=torch.int32, device=dev)      # 32 B headers
+                self.edges = torch.empty((max(self.n_edges, 1), 4), dtype=torch.float32,
+                                         device=dev)                                # 16 B records
+                self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
+            else:
+                self.cells = self.edges = self.sh32 = None
             pos_d = torch.from_numpy(pos).to(dev)
             sig_d = torch.from_numpy(sigma).to(dev)
             off_d = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
             nbr_d = torch.from_numpy(np.ascontiguousarray(neighbors, dtype=np.int64)).to(dev)
             _lib.check(self.lib.rfb_pack_scene(
-                _ptr(pos_d), _ptr(sig_d), _ptr(off_d), _ptr(nbr_d), n, self.n_edges,
-                _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors), _stream()),
+                _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
+                self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
+                _ptr(self.cells), _ptr(self.edges), _ptr(self.sh32), _stream()),
                 "rfb_pack_scene")
             torch.cuda.current_stream().synchronize()
         self._c = _lib.rfb_scene()
@@ -113,6 +124,10 @@ class DeviceScene:
         c.offsets = self.offsets.data_ptr()
         c.neighbors = self.neighbors.data_ptr()
         c.sh = self.sh.data_ptr()
+        c.cells = self.cells.data_ptr() if self.packed else None
+        c.edges = self.edges.data_ptr() if self.packed else None
+        c.sh32 = self.sh32.data_ptr() if self.packed else None
+        c.packed = 1 if self.packed else 0
         c.sh_degree = self.sh_degree
         for k in range(3):
             c.background[k] = float(self.background[k])
@@ -124,9 +139,8 @@ class DeviceScene:
     # -- device-resident updates (training) ------------------------------
     def set_raw_density(self, raw: torch.Tensor, stream=None):
         raw = raw.to(self.device, torch.float64).contiguous()
-        _lib.check(self.lib.rfb_softplus(_ptr(raw), self.n_sites, None,
-                                         ctypes.c_void_p(self.site4.data_ptr() + 24),
-                                         _stream(stream)), "rfb_softplus")
+        _lib.check(self.lib.rfb_softplus(_ptr(raw), self.n_sites, None, _ptr(self.site4),
+                                         _ptr(self.cells), _stream(stream)), "rfb_softplus")
 
     def default_t_max(self, origins: np.ndarray) -> float:
         """Batch fallback t_max (render.py:72-76)."""

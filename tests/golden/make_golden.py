@@ -233,6 +233,7 @@ if __name__ == "__main__":
     frame_case("frame_3k_surface", s3k, tuple(orbit_poses(np.zeros(3), 3.0, 0.3, 8)[0][:3, 3]),
                48, 27, 1e-3, seed=4)
     grad_case("grad_2k_deg3", s2k, 64, 11, 1e-3)
+    grad_case("grad_10k_deg0", s10k, 64, 15, 1e-3)
     grad_case("grad_2k_deg3_inside_eps0", s2k, 48, 12, 0.0, inside=True)
     train_case("train_2k_deg3_q", s2k, 192, 13, 1e-3, 0.01 / (192 * 2))
     train_case("train_3k_surface_q", s3k, 160, 14, 1e-3, 0.01 / (160 * 2))

@@ -1,0 +1,74 @@
+"""Forward-kernel sweep / profiling driver (not part of the product).
+
+python tools/sweep_fwd.py [--lanes 1,2,4,8] [--reps 5] [--train] [--once]
+--once renders a single frame per variant (for ncu -k regex:k_render).
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import make_views  # noqa: E402
+from paper_2502_01157_b200 import device as dv  # noqa: E402
+from paper_2502_01157_b200.synthetic import make_foam  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--lanes", default="1,2,4,8,16")
+ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--n-sites", type=int, default=1_000_000)
+ap.add_argument("--width", type=int, default=1920)
+ap.add_argument("--height", type=int, default=1080)
+ap.add_argument("--train", action="store_true")
+ap.add_argument("--once", action="store_true")
+ap.add_argument("--view", type=int, default=0)
+ap.add_argument("--packed", type=int, default=-1)
+args = ap.parse_args()
+print("lib", os.environ.get("RFB_LIB", "default"), flush=True)
+
+scene = make_foam(args.n_sites, 1, 3)
+ds = dv.DeviceScene(scene, packed=None if args.packed < 0 else bool(args.packed))
+cam = make_views(args.view + 1, args.width, args.height)[args.view]
+ws = dv.Workspace(ds.device)
+out = dv.alloc_forward(args.width * args.height, ds.device, per_ray=False)
+for lanes in [int(x) for x in args.lanes.split(",")]:
+    reps = 1 if args.once else args.reps
+    if not args.once:
+        dv.render_image_device(ds, cam, lanes_per_ray=lanes, workspace=ws, out=out)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        dv.render_image_device(ds, cam, lanes_per_ray=lanes, workspace=ws, out=out)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    m = args.width * args.height
+    print(f"fwd lanes={lanes:2d}: {ms:8.2f} ms/frame  {m / ms / 1e3:8.2f} Mrays/s", flush=True)
+
+if args.train:
+    dirs = cam.ray_directions_device()
+    m = dirs.shape[0]
+    o = torch.from_numpy(np.broadcast_to(cam.position, (m, 3)).copy()).cuda()
+    start = ds.locate(o[:1]).expand(m).contiguous()
+    tmin = torch.zeros(m, dtype=torch.float64, device="cuda")
+    tmax = torch.full((m,), ds.default_t_max(cam.position[None, :]), dtype=torch.float64,
+                      device="cuda")
+    tg = torch.from_numpy(np.random.default_rng(11).uniform(0, 1, (m, 3))).cuda()
+    gb = dv.GradBuffers(ds.n_sites, ds.device)
+    loss = torch.zeros(2, dtype=torch.float64, device="cuda")
+    wsb = dv.Workspace(ds.device)
+    fo = dv.alloc_forward(m, ds.device)
+    reps = 1 if args.once else args.reps
+    for r in range(reps + (0 if args.once else 1)):
+        if r == 1 or (args.once and r == 0):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+        dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
+                              rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo)
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3 / reps
+    print(f"train: {ms:8.2f} ms/step  {m / ms / 1e3:8.2f} Mrays/s", flush=True)
