@@ -53,15 +53,16 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 2
+#define RFB_ABI_VERSION 4
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
  *  packed (packed != 0, positions exactly representable in fp32): per-site
  *   32-byte cell headers {float x,y,z; int k0; double sigma; int k1;
- *   float cmax} and per-edge 16-byte records {float xj,yj,zj; int j} in CSR
- *   order, plus fp32 SH (sh32) with the fp64 table kept for the exact clamp
- *   fallback.  The generic arrays are always present (backward, locate). */
+ *   float n1max} and per-edge 16-byte records {float xj,yj,zj; int j} in CSR
+ *   order, per-edge int2 {k0, k1} of the target site (edge_meta), plus
+ *   fp32 SH (sh32) with the fp64 table kept for the exact clamp fallback.
+ *   The generic arrays are always present (backward, locate). */
 typedef struct rfb_scene {
     int64_t n_sites;
     int64_t n_edges;
@@ -71,10 +72,13 @@ typedef struct rfb_scene {
     const double *sh;         /* [n_sites][48], index k*3 + ch (render.py:53) */
     const void *cells;        /* packed: [n_sites] 32-byte headers (nullable) */
     const void *edges;        /* packed: [n_edges] 16-byte records (nullable) */
+    const void *edge_meta;    /* packed: [n_edges] int2 {k0, k1} of the edge's target site */
     const float *sh32;        /* packed: [n_sites][3][16] fp32 channel-major copy of sh (nullable) */
     int32_t packed;           /* 1: use cells/edges/sh32 for the walk */
+    float sh_absmax;          /* packed: >= max |sh| over the scene (fp32 colour bound) */
     int32_t sh_degree;        /* 0: read the DC band only (exact when bands 1..15 are
                                  all zero), 3: all 16 bands */
+    int32_t pad_;
     double background[3];     /* (host value) */
 } rfb_scene;
 
@@ -144,7 +148,7 @@ int rfb_device_ok(void);                /* 1 when an sm_100 device is current */
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
-                   void *cells, void *edges, float *sh32, void *stream);
+                   void *cells, void *edges, void *edge_meta, float *sh32, void *stream);
 
 /* sigma = softplus_10(raw) for device-resident training, written to out
  * (nullable), site4[:,3] (nullable) and the packed headers (nullable). */

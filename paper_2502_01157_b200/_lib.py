@@ -29,9 +29,12 @@ class rfb_scene(ctypes.Structure):
         ("sh", ctypes.c_void_p),
         ("cells", ctypes.c_void_p),
         ("edges", ctypes.c_void_p),
+        ("edge_meta", ctypes.c_void_p),
         ("sh32", ctypes.c_void_p),
         ("packed", ctypes.c_int32),
+        ("sh_absmax", ctypes.c_float),
         ("sh_degree", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
         ("background", ctypes.c_double * 3),
     ]
 
@@ -100,7 +103,7 @@ SIGNATURES = {
     "rfb_abi_version": (ctypes.c_int, []),
     "rfb_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rfb_device_ok": (ctypes.c_int, []),
-    "rfb_pack_scene": (ctypes.c_int, [VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP, VP, VP]),
+    "rfb_pack_scene": (ctypes.c_int, [VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP, VP, VP, VP]),
     "rfb_softplus": (ctypes.c_int, [VP, I64, VP, VP, VP, VP]),
     "rfb_camera_rays": (ctypes.c_int, [P(rfb_camera), I64, I64, VP, VP]),
     "rfb_locate": (ctypes.c_int, [P(rfb_scene), VP, I64, I32, VP, VP]),
@@ -139,7 +142,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rfb_abi_version() != 2:
+        if lib.rfb_abi_version() != 4:
             raise ExtensionMissing("librfb.so ABI version mismatch; rebuild")
         if path is None:
             _lib = lib

@@ -18,6 +18,9 @@ constexpr unsigned kFull = 0xffffffffu;
 #define RFB_F32_FILTER 1
 #endif
 constexpr bool kUseF32Filter = RFB_F32_FILTER != 0;
+#ifndef RFB_CHAIN
+#define RFB_CHAIN 0
+#endif
 
 // ---------------------------------------------------------------------------
 // Ray sources: explicit arrays (render.py:57-125) or a pinhole camera over a
@@ -147,15 +150,24 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const Ray &r, do
     nseg = 0;
     cells = 0;
     visits = 0;
+    // PACKED: after the first step the next cell's position comes from the
+    // chosen edge record and its CSR row from the (speculatively loaded)
+    // edge meta, so only sigma/cmax are fetched per step, off the critical
+    // path.
+    constexpr bool kChain = PACKED && kUseF32Filter && RFB_CHAIN;
+    Cell c = S.cell(i);
     for (;;) {
         steps += 1;
         if (steps > step_limit) return RFB_STATUS_STEP_LIMIT;
         cells += 1;
-        Cell c = S.cell(i);
+        if (!kChain && steps > 1) c = S.cell(i);
         visits += c.k1 - c.k0;
         double best_t;
-        int32_t best_j;
-        if constexpr (PACKED && kUseF32Filter)
+        int32_t best_j, best_k = -1;
+        int2 meta = make_int2(0, 0);
+        if constexpr (kChain)
+            exit_face_f32<G>(S, c, c.hf, r, entry, df, gl, gmask, best_t, best_j, &best_k, &meta);
+        else if constexpr (PACKED && kUseF32Filter)
             exit_face_f32<G>(S, c, c.hf, r, entry, df, gl, gmask, best_t, best_j);
         else
             exit_face<G, PACKED>(S, c, r, gl, gmask, best_t, best_j);
@@ -181,6 +193,18 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const Ray &r, do
             if (zero_adv > kZeroAdvanceLimit) return RFB_STATUS_CYCLE;
         }
         i = best_j;
+        if constexpr (kChain) {
+            const float4 e = __ldg(S.edge + best_k);  // L1 hit: read in this step
+            const float4 h2 = __ldg(reinterpret_cast<const float4 *>(S.hdr + i) + 1);
+            c.hf = e;
+            c.x = e.x;
+            c.y = e.y;
+            c.z = e.z;
+            c.k0 = meta.x;
+            c.k1 = meta.y;
+            c.sigma = __hiloint2double(__float_as_int(h2.y), __float_as_int(h2.x));
+            c.n1max = h2.w;
+        }
     }
 }
 
@@ -248,7 +272,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 double delta = t1 - t0;
                 double alpha = 1.0 - exp(-c.sigma * delta);
                 double col[3];
-                cell_color<SHDEG, PACKED>(S, cell, c.cmax, basis, dir, bsum, col);
+                cell_color<SHDEG, PACKED>(S, cell, basis, dir, bsum, col);
                 double w = T * alpha;
                 wsum += w;
                 cr += w * col[0];
@@ -411,7 +435,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                     double e = exp(-c.sigma * delta);
                     double alpha = 1.0 - e;
                     double col[3];
-                    int mask = cell_color<SHDEG, PACKED>(S, cell, c.cmax, basis, dir, cbsum, col);
+                    int mask = cell_color<SHDEG, PACKED>(S, cell, basis, dir, cbsum, col);
                     double w = Tc * alpha;
                     wsum += w;
                     cr += w * col[0];
@@ -665,42 +689,48 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
 // Scene packing, activation, camera rays, start-cell location.
 // ---------------------------------------------------------------------------
 __global__ void k_pack_sites(const double *pos, const double *sigma, const double *sh, int64_t n,
-                             const int64_t *off64, double4 *site4, int32_t *off32, CellHdr *cells,
-                             float *sh32) {
+                             const int64_t *off64, const int64_t *nbr64, double4 *site4,
+                             int32_t *off32, CellHdr *cells, float *sh32) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n) return;
     off32[i] = (int32_t)off64[i];
     if (i == n) return;
     site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sigma[i]);
     if (cells) {
-        float cmax = 0.f;
         for (int k = 0; k < 16; ++k)
-            for (int ch = 0; ch < 3; ++ch) {
-                double v = sh[i * 48 + 3 * k + ch];
-                sh32[i * 48 + 16 * ch + k] = (float)v;  // channel-major copy
-                cmax = fmaxf(cmax, (float)fabs(v));
-            }
+            for (int ch = 0; ch < 3; ++ch)
+                sh32[i * 48 + 16 * ch + k] = (float)sh[i * 48 + 3 * k + ch];  // channel-major
+        const float xi = (float)pos[3 * i], yi = (float)pos[3 * i + 1], zi = (float)pos[3 * i + 2];
+        float n1max = 0.f;
+        for (int64_t k = off64[i]; k < off64[i + 1]; ++k) {  // same fp32 ops as exit_face_f32
+            const int64_t j = nbr64[k];
+            const float nx = (float)pos[3 * j] - xi, ny = (float)pos[3 * j + 1] - yi,
+                        nz = (float)pos[3 * j + 2] - zi;
+            n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
+        }
         CellHdr h;
-        h.x = (float)pos[3 * i];
-        h.y = (float)pos[3 * i + 1];
-        h.z = (float)pos[3 * i + 2];
+        h.x = xi;
+        h.y = yi;
+        h.z = zi;
         h.k0 = (int32_t)off64[i];
         h.sigma = sigma[i];
         h.k1 = (int32_t)off64[i + 1];
-        h.cmax = cmax * (1.0f + 0x1p-20f);  // upper bound of |coefficient|
+        h.n1max = n1max * (1.0f + 0x1p-20f);
         cells[i] = h;
     }
 }
 
-__global__ void k_pack_edges(const int64_t *nbr64, const double *pos, int64_t E, int32_t *nbr32,
-                             float4 *edges) {
+__global__ void k_pack_edges(const int64_t *nbr64, const int64_t *off64, const double *pos,
+                             int64_t E, int32_t *nbr32, float4 *edges, int2 *emeta) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= E) return;
     int32_t j = (int32_t)nbr64[k];
     nbr32[k] = j;
-    if (edges)
+    if (edges) {
         edges[k] = make_float4((float)pos[3 * j], (float)pos[3 * j + 1], (float)pos[3 * j + 2],
                                __int_as_float(j));
+        emeta[k] = make_int2((int32_t)off64[j], (int32_t)off64[j + 1]);
+    }
 }
 
 // foam.py:22-25 (device libm; may differ from numpy's log1p/exp by 1 ulp).
@@ -788,11 +818,13 @@ static SceneView<PACKED> view(const rfb_scene *s) {
     SceneView<PACKED> v;
     v.hdr = reinterpret_cast<const CellHdr *>(s->cells);
     v.edge = reinterpret_cast<const float4 *>(s->edges);
+    v.emeta = reinterpret_cast<const int2 *>(s->edge_meta);
     v.site4 = reinterpret_cast<const double4 *>(s->site4);
     v.off = s->offsets;
     v.nbr = s->neighbors;
     v.sh32 = s->sh32;
     v.sh = s->sh;
+    v.sh_absmax = s->sh_absmax;
     v.bg[0] = s->background[0];
     v.bg[1] = s->background[1];
     v.bg[2] = s->background[2];
@@ -824,7 +856,7 @@ static bool scene_ok(const rfb_scene *s) {
     if (!s || !s->site4 || !s->offsets || !s->neighbors || !s->sh || s->n_sites <= 0 ||
         s->n_sites >= (1 << 29) || (s->sh_degree != 0 && s->sh_degree != 3))
         return false;
-    if (s->packed && (!s->cells || !s->edges || !s->sh32)) return false;
+    if (s->packed && (!s->cells || !s->edges || !s->edge_meta || !s->sh32)) return false;
     return true;
 }
 
@@ -1004,18 +1036,19 @@ int rfb_device_ok(void) {
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
-                   void *cells, void *edges, float *sh32, void *stream) {
+                   void *cells, void *edges, void *edge_meta, float *sh32, void *stream) {
     if (!positions || !sigma || !offsets || !neighbors || !site4 || !offsets32 || !neighbors32 ||
         n_sites <= 0 || n_edges < 0 || n_edges >= ((int64_t)1 << 31) ||
-        ((cells || edges || sh32) && (!cells || !edges || !sh32 || !sh)))
+        ((cells || edges || edge_meta || sh32) && (!cells || !edges || !edge_meta || !sh32 || !sh)))
         return RFB_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     k_pack_sites<<<(unsigned)((n_sites + 1 + 255) / 256), 256, 0, st>>>(
-        positions, sigma, sh, n_sites, offsets, reinterpret_cast<double4 *>(site4), offsets32,
-        reinterpret_cast<CellHdr *>(cells), sh32);
+        positions, sigma, sh, n_sites, offsets, neighbors, reinterpret_cast<double4 *>(site4),
+        offsets32, reinterpret_cast<CellHdr *>(cells), sh32);
     if (n_edges > 0)
         k_pack_edges<<<(unsigned)((n_edges + 255) / 256), 256, 0, st>>>(
-            neighbors, positions, n_edges, neighbors32, reinterpret_cast<float4 *>(edges));
+            neighbors, offsets, positions, n_edges, neighbors32, reinterpret_cast<float4 *>(edges),
+            reinterpret_cast<int2 *>(edge_meta));
     return (int)cudaGetLastError();
 }
 

@@ -72,14 +72,14 @@ struct CellHdr {  // packed layout, 32 bytes
     int32_t k0;
     double sigma;
     int32_t k1;
-    float cmax;  // max |sh coefficient| of the site (fp32 colour error bound)
+    float n1max;  // >= max over the row of |x_j - x_i|_1 as the kernel computes it in fp32
 };
 static_assert(sizeof(CellHdr) == 32, "cell header must be one 32-byte sector");
 
 struct Cell {
     double x, y, z, sigma;
     int32_t k0, k1;
-    float cmax;
+    float n1max;
     float4 hf;  // packed: fp32 x, y, z (exact copies of x, y, z)
 };
 
@@ -88,11 +88,13 @@ template <bool PACKED>
 struct SceneView {
     const CellHdr *hdr;     // PACKED
     const float4 *edge;     // PACKED
+    const int2 *emeta;      // PACKED: [E] {k0_j, k1_j} of the edge's target site
     const double4 *site4;   // both (backward gradients use fp64 positions)
     const int32_t *off;     // generic
     const int32_t *nbr;     // generic
     const float *sh32;      // [n][3][16] fp32, channel-major (PACKED) -- exact fallback below
     const double *sh;       // [n][48] fp64 (reference values)
+    float sh_absmax;        // max |sh coefficient| over the scene (colour rounding bound)
     double bg[3];
 
     __device__ __forceinline__ Cell cell(int32_t i) const {
@@ -107,7 +109,7 @@ struct SceneView {
             c.k0 = __float_as_int(a.w);
             c.sigma = __hiloint2double(__float_as_int(b.y), __float_as_int(b.x));
             c.k1 = __float_as_int(b.z);
-            c.cmax = b.w;
+            c.n1max = b.w;
         } else {
             double4 s = ld_site(site4 + i);
             c.x = s.x;
@@ -116,7 +118,7 @@ struct SceneView {
             c.sigma = s.w;
             c.k0 = __ldg(off + i);
             c.k1 = __ldg(off + i + 1);
-            c.cmax = 0.f;
+            c.n1max = 0.f;
         }
         return c;
     }
@@ -151,9 +153,10 @@ struct SceneView {
 // the clamp mask -- which gates the SH gradient -- is always the reference's
 // and the colour is within ~1e-6 of it.
 template <int SHDEG, bool PACKED>
-__device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i, float cmax,
+__device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
                                           const float *basis_f, const double *dir,
                                           double bsum, double *col) {
+    const float cmax = S.sh_absmax;
     constexpr int NB = SHDEG == 0 ? 1 : 16;
     double acc[3] = {0.5, 0.5, 0.5};
     if (PACKED) {
@@ -322,11 +325,27 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 // bit-identical to kernels.py:116-133.  Rows longer than 64 neighbours
 // evaluate the tail exactly.
 // ---------------------------------------------------------------------------
+#ifndef RFB_MASK32
+#define RFB_MASK32 1
+#endif
+#ifndef RFB_FAST_BOUND
+#define RFB_FAST_BOUND 1
+#endif
+#if RFB_MASK32
+typedef unsigned int cand_mask_t;
+constexpr int kMaskBits = 32;
+#else
+typedef unsigned long long cand_mask_t;
+constexpr int kMaskBits = 64;
+#endif
+
 template <int G>
 __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Cell &c,
                                               const float4 &hdr_f, const Ray &r, double entry,
                                               const float *df, int gl, unsigned gmask,
-                                              double &best_t, int32_t &best_j) {
+                                              double &best_t, int32_t &best_j,
+                                              int32_t *best_k_out = nullptr,
+                                              int2 *meta_out = nullptr) {
     constexpr float u = 0x1p-24f;
     // q = o + entry * d in fp64 (once per step), rounded to fp32
     const double qx = r.ox + entry * r.dx, qy = r.oy + entry * r.dy, qz = r.oz + entry * r.dz;
@@ -334,18 +353,31 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
     const float Q = fmaxf(fabsf(qxf), fmaxf(fabsf(qyf), fabsf(qzf))) * (1.0f + 4.0f * u);
     const float px = hdr_f.x - qxf, py = hdr_f.y - qyf, pz = hdr_f.z - qzf;
     const float slack = (float)(0x1p-40 * (fabs(entry) + 1.0));
+#if RFB_FAST_BOUND
+    const float N = c.n1max;
+    const float Ed = 8.0f * u * N;
+    const float P = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
+    const float Hm = (P + 0.5f * N) * (1.0f + 4.0f * u);
+    const float K1 = 2.2f * u * N * (Q + 8.0f * Hm + 2.0f * N);
+    const float K2 = 2.2f * Ed;
+    constexpr float K3 = 8.0f * u + 0x1p-40f;
+#endif
     float U = __int_as_float(0x7f800000);  // +inf
-    unsigned long long mask = 0ull;
+    float smin = U;
+    int32_t kguess = -1;
+    cand_mask_t mask = 0;
     const int32_t k0 = c.k0 + gl;
     int32_t nk = 0;
     for (int32_t k = k0; k < c.k1; k += G, ++nk) {
         const float4 e = __ldg(S.edge + k);
         const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
         const float den = __fmaf_rn(df[2], nz, __fmaf_rn(df[1], ny, df[0] * nx));
+#if !RFB_FAST_BOUND
         const float n1 = fabsf(nx) + fabsf(ny) + fabsf(nz);
         const float Ed = 8.0f * u * n1;
+#endif
         if (den < -Ed) continue;                       // certainly back-facing
-        const unsigned long long bit = nk < 64 ? (1ull << nk) : 0ull;
+        const cand_mask_t bit = nk < kMaskBits ? ((cand_mask_t)1 << nk) : (cand_mask_t)0;
         if (den <= 2.0f * Ed || den < 0x1p-100f) {     // uncertain: exact path
             mask |= bit;
             continue;
@@ -353,16 +385,29 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
         const float hx = __fmaf_rn(0.5f, nx, px), hy = __fmaf_rn(0.5f, ny, py),
                     hz = __fmaf_rn(0.5f, nz, pz);
         const float num = __fmaf_rn(hz, nz, __fmaf_rn(hy, ny, hx * nx));
-        const float H = fmaxf(fabsf(hx), fmaxf(fabsf(hy), fabsf(hz)));
-        const float En = u * n1 * (Q + 8.0f * H + 2.0f * n1);
         float rinv;  // MUFU reciprocal, <= 1 ulp (normal den guaranteed above)
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rinv) : "f"(den));
         const float s = num * rinv;
         const float as = fabsf(s);
+#if RFB_FAST_BOUND
+        // per-cell constants: |n|_1 <= N, |h|_inf <= P + N/2
+        const float es = __fmaf_rn(K3, as, __fmaf_rn(__fmaf_rn(K2, as, K1), rinv, slack));
+#else
+        const float H = fmaxf(fabsf(hx), fmaxf(fabsf(hy), fabsf(hz)));
+        const float En = u * n1 * (Q + 8.0f * H + 2.0f * n1);
         const float es = 2.2f * (En + as * Ed) * rinv + 8.0f * u * as + slack + 0x1p-40f * as;
+#endif
         if (s - es <= U) mask |= bit;
         U = fminf(U, s + es);
+        if (s < smin) {
+            smin = s;
+            kguess = k;
+        }
     }
+    // speculative load of the likely exit neighbour's CSR row bounds: it is
+    // in flight while phase 2 runs (G == 1 only)
+    int2 meta_g = make_int2(0, 0);
+    if (G == 1 && meta_out && kguess >= 0) meta_g = __ldg(S.emeta + kguess);
     // phase 2: exact fp64 re-evaluation of the candidates, CSR order
     best_t = dinf();
     best_j = -1;
@@ -371,7 +416,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
     for (;;) {
         int32_t idx;
         if (mask) {
-            idx = __ffsll((long long)mask) - 1;
+            idx = (kMaskBits == 32 ? __ffs((int)mask) : __ffsll((long long)mask)) - 1;
             mask &= mask - 1;
         } else {
             break;
@@ -390,7 +435,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
             best_k = k;
         }
     }
-    for (int32_t idx = 64; idx < nexact; ++idx) {  // rows with > 64 neighbours per lane
+    for (int32_t idx = kMaskBits; idx < nexact; ++idx) {  // rows longer than the mask
         const int32_t k = k0 + idx * G;
         const float4 e = __ldg(S.edge + k);
         const double xj = e.x, yj = e.y, zj = e.z;
@@ -418,6 +463,9 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
             }
         }
     }
+    if (best_k_out) *best_k_out = best_k;
+    if (meta_out && best_j >= 0)
+        *meta_out = (G == 1 && best_k == kguess) ? meta_g : __ldg(S.emeta + best_k);
 }
 
 }  // namespace rfb

@@ -86,6 +86,8 @@ class DeviceScene:
         self.background = np.asarray(background, dtype=np.float64).copy()
         sh = np.ascontiguousarray(np.asarray(sh_flat, dtype=np.float64).reshape(n, 48))
         self.sh_degree = sh_degree_of(sh) if sh_degree is None else int(sh_degree)
+        # fp32 upper bound of max |coefficient| (colour rounding bound, packed layout)
+        self.sh_absmax = float(np.float32(np.abs(sh).max() if sh.size else 0.0) * np.float32(1.0001))
         sigma = np.ascontiguousarray(sigma, dtype=np.float64)
         # packed layout only when every coordinate survives an fp32 round trip
         self.packed = bool(np.array_equal(pos.astype(np.float32).astype(np.float64), pos)) \
@@ -100,9 +102,11 @@ class DeviceScene:
                 self.cells = torch.empty((n, 8), dtype=torch.int32, device=dev)      # 32 B headers
                 self.edges = torch.empty((max(self.n_edges, 1), 4), dtype=torch.float32,
                                          device=dev)                                # 16 B records
+                self.edge_meta = torch.empty((max(self.n_edges, 1), 2), dtype=torch.int32,
+                                             device=dev)                            # {k0, k1}
                 self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
             else:
-                self.cells = self.edges = self.sh32 = None
+                self.cells = self.edges = self.edge_meta = self.sh32 = None
             pos_d = torch.from_numpy(pos).to(dev)
             sig_d = torch.from_numpy(sigma).to(dev)
             off_d = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
@@ -110,7 +114,8 @@ class DeviceScene:
             _lib.check(self.lib.rfb_pack_scene(
                 _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
                 self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
-                _ptr(self.cells), _ptr(self.edges), _ptr(self.sh32), _stream()),
+                _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_meta), _ptr(self.sh32),
+                _stream()),
                 "rfb_pack_scene")
             torch.cuda.current_stream().synchronize()
         self._c = _lib.rfb_scene()
@@ -126,8 +131,10 @@ class DeviceScene:
         c.sh = self.sh.data_ptr()
         c.cells = self.cells.data_ptr() if self.packed else None
         c.edges = self.edges.data_ptr() if self.packed else None
+        c.edge_meta = self.edge_meta.data_ptr() if self.packed else None
         c.sh32 = self.sh32.data_ptr() if self.packed else None
         c.packed = 1 if self.packed else 0
+        c.sh_absmax = self.sh_absmax
         c.sh_degree = self.sh_degree
         for k in range(3):
             c.background[k] = float(self.background[k])
