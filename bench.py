@@ -402,7 +402,7 @@ def main():
                    "scene_build_s": round(build_s, 1)},
         "fwd_bwd": fb,
         "e2e": e2e,
-        "gpu_launches": 2 * args.steps * len(views),
+        "gpu_launches": 3 * args.steps * len(views),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": "k_render (walk + SH + composite)",

@@ -794,9 +794,57 @@ __global__ void k_locate(LocScene S, const double *qs, int64_t m, int32_t seed, 
     if (k < m) out[k] = locate_one(S, qs[3 * k], qs[3 * k + 1], qs[3 * k + 2], seed);
 }
 
-__global__ void k_locate_point(LocScene S, double qx, double qy, double qz, int32_t seed,
-                               int32_t *out) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) *out = locate_one(S, qx, qy, qz, seed);
+// Exact nearest site of one query point by a full-device scan (shared-origin
+// cameras: one query per frame, render.py:78-82): pass 1 takes the minimum
+// squared distance (non-negative doubles order like their bit patterns),
+// pass 2 the lowest id attaining it -- the reference's tie rule, with no
+// dependence on the CSR (so a stale adjacency cannot change the answer).
+__device__ __forceinline__ double qdist(const double4 *site4, int64_t i, double qx, double qy,
+                                        double qz) {
+    double4 p = ld_site(site4 + i);
+    double dx = p.x - qx, dy = p.y - qy, dz = p.z - qz;
+    return dx * dx + dy * dy + dz * dz;
+}
+
+__global__ void k_nearest_dist(const double4 *site4, int64_t n, double qx, double qy, double qz,
+                               unsigned long long *best) {
+    unsigned long long m = ~0ull;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        unsigned long long b = __double_as_longlong(qdist(site4, i, qx, qy, qz));
+        m = b < m ? b : m;
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+        unsigned long long o = __shfl_xor_sync(0xffffffffu, m, off);
+        m = o < m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMin(best, m);
+}
+
+__global__ void k_nearest_id(const double4 *site4, int64_t n, double qx, double qy, double qz,
+                             const unsigned long long *best, int32_t *out) {
+    const unsigned long long b = *best;
+    int32_t m = 0x7fffffff;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if ((unsigned long long)__double_as_longlong(qdist(site4, i, qx, qy, qz)) == b) {
+            m = (int32_t)i;
+            break;  // grid-stride order: the first hit of this thread is its lowest id
+        }
+    }
+    m = __reduce_min_sync(0xffffffffu, (unsigned)m);
+    if ((threadIdx.x & 31) == 0) atomicMin(out, m);
+}
+
+static void nearest_point(const rfb_scene *s, double qx, double qy, double qz, void *tmp8,
+                          int32_t *out, cudaStream_t st) {
+    unsigned long long *best = reinterpret_cast<unsigned long long *>(tmp8);
+    const double4 *site4 = reinterpret_cast<const double4 *>(s->site4);
+    const unsigned grid = (unsigned)std::min<int64_t>((s->n_sites + 255) / 256, 148 * 8);
+    cudaMemsetAsync(best, 0xff, sizeof(unsigned long long), st);
+    cudaMemsetAsync(out, 0x7f, sizeof(int32_t), st);
+    k_nearest_dist<<<grid, 256, 0, st>>>(site4, s->n_sites, qx, qy, qz, best);
+    k_nearest_id<<<grid, 256, 0, st>>>(site4, s->n_sites, qx, qy, qz, best, out);
 }
 
 // ---------------------------------------------------------------------------
@@ -1119,8 +1167,8 @@ int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb
     cudaStream_t st = (cudaStream_t)stream;
     int32_t *start_ptr = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + 64);
     if (start_site < 0) {
-        k_locate_point<<<1, 32, 0, st>>>(loc_scene(scene), camera->pose[3], camera->pose[7],
-                                         camera->pose[11], 0, start_ptr);
+        nearest_point(scene, camera->pose[3], camera->pose[7], camera->pose[11],
+                      reinterpret_cast<char *>(workspace) + 128, start_ptr, st);
     } else {
         cudaMemcpyAsync(start_ptr, &start_site, sizeof(int32_t), cudaMemcpyHostToDevice, st);
     }

@@ -199,13 +199,18 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
                     out[1].reshape(camera.height, camera.width))
         return img
     H, W = camera.height, camera.width
+    fc = _frame_cache(ds, W, H, weight_check)
     torch.cuda.synchronize(ds.device)
     t0 = time.perf_counter()
     res = dv.render_image_device(ds, camera, epsilon=epsilon, step_limit=step_limit, f64=True,
-                                 lanes_per_ray=lanes_per_ray)
-    torch.cuda.synchronize(ds.device)
+                                 lanes_per_ray=lanes_per_ray, workspace=fc["ws"], out=fc["out"])
+    fc["h_rgb"].copy_(res.rgb, non_blocking=True)
+    if weight_check:
+        fc["h_wsum"].copy_(res.wsum, non_blocking=True)
+        fc["h_resid"].copy_(res.residual, non_blocking=True)
+    torch.cuda.current_stream(ds.device).synchronize()
     dt = time.perf_counter() - t0
-    img = res.rgb.cpu().numpy().reshape(H, W, 3)
+    img = fc["h_rgb"].numpy().reshape(H, W, 3).copy()
     if stats is not None:
         cnt = res.counters.cpu().numpy()
         status = res.status.cpu().numpy()
@@ -213,8 +218,28 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
                                 neighbor_visits=int(cnt[1]), grid_queries=1,
                                 failed_rays=int((status != STATUS_OK).sum()), seconds=dt))
     if weight_check:
-        return (img, res.wsum.cpu().numpy().reshape(H, W), res.residual.cpu().numpy().reshape(H, W))
+        return (img, fc["h_wsum"].numpy().reshape(H, W).copy(),
+                fc["h_resid"].numpy().reshape(H, W).copy())
     return img
+
+
+def _frame_cache(ds, W, H, weight_check):
+    """Per-(scene, resolution) device outputs, workspace and pinned host
+    buffers, so the public render_image call does no allocation after the
+    first frame."""
+    cache = ds.__dict__.setdefault("_frame_cache", {})
+    key = (W, H)
+    fc = cache.get(key)
+    if fc is None:
+        fc = {"ws": dv.Workspace(ds.device),
+              "out": dv.alloc_forward(W * H, ds.device, f64=True, per_ray=False),
+              "h_rgb": torch.empty((W * H, 3), dtype=torch.float64, pin_memory=True)}
+        cache[key] = fc
+    if weight_check and "h_wsum" not in fc:
+        fc["h_wsum"] = torch.empty(W * H, dtype=torch.float64, pin_memory=True)
+        fc["h_resid"] = torch.empty(W * H, dtype=torch.float64, pin_memory=True)
+    fc["out"].counters.zero_()
+    return fc
 
 
 def render_rays_with_gradients(scene, origins, directions, adjoints, t_min=None, t_max=None,

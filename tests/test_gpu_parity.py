@@ -208,3 +208,47 @@ def test_empty_and_step_limit(cuda_ok):
     np.testing.assert_array_equal(res.rgb.cpu().numpy()[ref["status"] == 2],
                                   np.broadcast_to(g["background"], ((ref["status"] == 2).sum(), 3)))
     np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
+
+
+def test_flat_kernels_drop_in(cuda_ok):
+    """paper_2502_01157_b200.kernels.train_batch with the reference's exact
+    positional signature and per-worker buffers (kernels.py:372-385)."""
+    from paper_2502_01157_b200 import kernels as K
+    from paper_2502_01157_b200.scene import softplus
+
+    g = load_golden("train_2k_deg3_q")
+    n = len(g["positions"])
+    m = len(g["origins"])
+    W = int(g["workers"])
+    out_rgb = np.empty((m, 3))
+    out_status = np.empty(m, dtype=np.int8)
+    d_sigma_w, d_sh_w, d_pos_w = np.zeros((W, n)), np.zeros((W, n, 48)), np.zeros((W, n, 3))
+    loss_w = np.zeros((W, 2))
+    counters = np.zeros((W, 2), dtype=np.int64)
+    sc = np.empty((W, 4096), dtype=np.int64)
+    K.train_batch(g["positions"], g["offsets"].astype(np.int64), g["neighbors"].astype(np.int64),
+                  softplus(g["raw_density"]), g["sh"], g["background"], g["origins"], g["dirs"],
+                  np.zeros(m), g["t_max"], g["start"], g["targets"], float(g["epsilon"]), 4096,
+                  1e-12 * float(np.linalg.norm(g["positions"].max(0) - g["positions"].min(0))),
+                  float(g["rgb_scale"]), float(g["quantile_scale"]), g["u_pairs"], 1e-4, W,
+                  out_rgb, out_status, d_sigma_w, d_sh_w, d_pos_w, loss_w, counters, sc, sc, sc)
+    assert np.abs(out_rgb - g["out_rgb"]).max() <= IMG_TOL
+    np.testing.assert_array_equal(counters.sum(0), g["counters"].sum(0))
+    assert rel_err(d_sigma_w.sum(0), g["d_sigma_w"].sum(0)) <= GRAD_RTOL
+    assert rel_err(d_sh_w.sum(0), g["d_sh_w"].sum(0)) <= GRAD_RTOL
+    assert rel_err(d_pos_w.sum(0), g["d_pos_w"].sum(0)) <= GRAD_RTOL
+    np.testing.assert_allclose(loss_w.sum(0), g["loss_w"].sum(0), rtol=1e-6)
+    # render_rays drop-in on a frame
+    f = load_golden("frame_2k_deg3")
+    sa, origins, dirs, start, t_max = frame_rays(f)
+    mm = len(dirs)
+    rgb = np.empty((mm, 3))
+    res = np.empty(mm)
+    st = np.empty(mm, dtype=np.int8)
+    ws = np.empty(mm)
+    cnt = np.zeros((8, 2), dtype=np.int64)
+    K.render_rays(sa.positions, sa.offsets, sa.neighbors, sa.sigma, sa.sh, sa.background, origins,
+                  dirs, np.zeros(mm), np.full(mm, t_max), np.full(mm, start), 1e-3, 4096,
+                  sa.width_floor, 8, rgb, res, st, ws, cnt)
+    assert np.abs(rgb.reshape(f["img"].shape) - f["img"]).max() <= IMG_TOL
+    assert cnt.sum(0)[0] == f["stats"][1] and cnt.sum(0)[1] == f["stats"][2]

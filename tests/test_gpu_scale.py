@@ -1,0 +1,113 @@
+"""Larger-scene parity (100k-site foam, Qhull CSR built in-test) and
+size-independent properties: every ray of a frame against the oracle
+(status, counters, segment counts bit-exact; image 1e-4), weight
+conservation, tile-sharded assembly == single render (bitwise), and
+training gradients against the oracle's fp64 train_batch (1e-3 rel)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def scene100k():
+    from paper_2502_01157_b200.synthetic import make_foam
+
+    return make_foam(100_000, 21, 3)
+
+
+def _sa(scene):
+    from paper_2502_01157_b200.scene import softplus
+
+    adj = scene.adjacency
+    return orc.SceneArrays(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density),
+                           scene.sh_coeffs.reshape(-1, 48), scene.background)
+
+
+def _cam(W, H, k=0):
+    from bench import make_views
+
+    return make_views(k + 1, W, H)[k]
+
+
+@pytest.mark.parametrize("view,eps", [(0, 1e-3), (3, 0.0)])
+def test_frame_100k_all_rays(cuda_ok, scene100k, view, eps):
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = 160, 96
+    cam = _cam(W, H, view)
+    ds = dv.DeviceScene(scene100k)
+    res = dv.render_image_device(ds, cam, epsilon=eps, f64=True, per_ray=True)
+    torch.cuda.synchronize()
+    sa = _sa(scene100k)
+    dirs = cam.ray_directions()
+    o = cam.position
+    start = int(orc.nearest_sites(sa.positions, o[None, :])[0])
+    t_max = float(np.linalg.norm(o - sa.center) + 2.0 * sa.diagonal + 1.0)
+    ref = orc.render_rays(sa, np.broadcast_to(o, (W * H, 3)), dirs, 0.0, t_max, start, epsilon=eps)
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
+    np.testing.assert_array_equal(res.nseg.cpu().numpy(), ref["nseg"])
+    assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= 1e-4
+    # conservation: sum of weights + residual transmittance == 1
+    tot = res.wsum.cpu().numpy() + res.residual.cpu().numpy()
+    assert np.abs(tot - 1.0).max() <= 1e-6
+
+
+def test_tile_sharded_assembly_bitwise(cuda_ok, scene100k):
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200.distributed import tile_assignment
+
+    W, H = 200, 120
+    cam = _cam(W, H, 1)
+    ds = dv.DeviceScene(scene100k)
+    full = dv.render_image_device(ds, cam).rgb.clone()
+    acc = torch.zeros_like(full)
+    for r in range(3):
+        tiles = torch.from_numpy(tile_assignment(W, H, r, 3)).cuda()
+        part = dv.alloc_forward(W * H, ds.device, per_ray=False)
+        part.rgb.zero_()
+        dv.render_image_device(ds, cam, tile_ids=tiles, out=part)
+        acc += part.rgb
+    torch.cuda.synchronize()
+    assert torch.equal(acc, full)
+
+
+def test_train_100k_gradients(cuda_ok, scene100k):
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = 96, 64
+    cam = _cam(W, H, 2)
+    dirs = cam.ray_directions()
+    m = len(dirs)
+    o = np.broadcast_to(cam.position, (m, 3)).copy()
+    sa = _sa(scene100k)
+    start = int(orc.nearest_sites(sa.positions, cam.position[None, :])[0])
+    t_max = np.full(m, np.linalg.norm(cam.position - sa.center) + 2.0 * sa.diagonal + 1.0)
+    rng = np.random.default_rng(3)
+    targets = rng.uniform(0, 1, (m, 3))
+    u = rng.random((m, 2, 2))
+    qs = 0.01 / (m * 2)
+    ref = orc.train_batch(sa, o, dirs, np.zeros(m), t_max, np.full(m, start), targets,
+                          1.0 / (3 * m), qs, u, 1e-4, n_workers=4, threads=8)
+    ds = dv.DeviceScene(scene100k)
+    gb = dv.GradBuffers(ds.n_sites, ds.device)
+    loss = torch.zeros(2, dtype=torch.float64, device="cuda")
+    d = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)  # noqa
+    dv.train_batch_device(ds, d(o), d(dirs), d(np.zeros(m)), d(t_max),
+                          d(np.full(m, start), torch.int32), d(targets), gb, loss,
+                          rgb_scale=1.0 / (3 * m), quantile_scale=qs, u_pairs=d(u))
+    torch.cuda.synchronize()
+    g4 = gb.g4.double().cpu().numpy()
+
+    def rel(a, b):
+        return np.abs(a - b).max() / np.abs(b).max()
+
+    assert rel(g4[:, 3], ref["d_sigma_w"].sum(0)) <= 1e-3
+    assert rel(g4[:, :3], ref["d_pos_w"].sum(0)) <= 1e-3
+    assert rel(gb.sh.double().cpu().numpy(), ref["d_sh_w"].sum(0)) <= 1e-3
+    np.testing.assert_allclose(loss.cpu().numpy(), ref["loss_w"].sum(0), rtol=1e-5)

@@ -1,0 +1,112 @@
+"""Host-side logic (no GPU): scene containers, activations, camera math, the
+synthetic fixture generator and the distributed tile/ray partitioning."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_scene_arrays, load_golden
+from oracle import oracle as orc
+from paper_2502_01157_b200 import distributed as D
+from paper_2502_01157_b200.camera import (PINHOLE, CameraModel, camera_rays, look_at,
+                                          orbit_poses)
+from paper_2502_01157_b200.errors import OutOfBounds, ShapeMismatch
+from paper_2502_01157_b200.scene import (AdjacencyGraph, FoamScene, GradientBuffer, softplus,
+                                         softplus_grad)
+from paper_2502_01157_b200.synthetic import delaunay_csr, random_positions
+
+
+def test_softplus_matches_reference_bits():
+    g = load_golden("kat")
+    np.testing.assert_array_equal(softplus(g["softplus_in"]), g["softplus_out"])
+    np.testing.assert_array_equal(softplus_grad(g["softplus_in"]), g["softplus_grad_out"])
+    assert softplus(0.0) == pytest.approx(0.0693147, abs=1e-7)
+    assert float(softplus(-10.0)) == pytest.approx(3.72e-45, rel=1e-2)  # code value
+
+
+def test_scene_validation():
+    with pytest.raises(ShapeMismatch):
+        FoamScene(np.zeros((3, 3)), np.zeros(2), np.zeros((3, 16, 3)))
+    with pytest.raises(ShapeMismatch):
+        FoamScene(np.zeros((3, 3)), np.zeros(3), np.zeros((3, 9, 3)))
+    gb = GradientBuffer(4)
+    gb.d_sh += 1.0
+    assert gb.all_finite()
+    gb.zero()
+    assert not gb.d_sh.any()
+
+
+def test_adjacency_from_lists_and_nearest():
+    pos = np.array([[0.0, 0, 0], [2.0, 0, 0], [0, 2.0, 0]])
+    adj = AdjacencyGraph.from_lists(pos, [[1, 2], [], []])
+    assert adj.neighbor_list(0).tolist() == [1, 2]
+    assert adj.neighbor_list(1).tolist() == [0]
+    assert adj.degree(2) == 1
+    # tie at the midpoint of sites 0 and 1: lowest id wins (adjacency.py:198)
+    assert adj.nearest_site([1.0, 0.0, 0.0]) == 0
+    g = load_golden("frame_2k_deg3")
+    sa = golden_scene_arrays(g)
+    adj = AdjacencyGraph(g["positions"], g["offsets"], g["neighbors"])
+    q = np.random.default_rng(0).uniform(-1.5, 1.5, (200, 3))
+    ref = orc.nearest_sites(sa.positions, q)
+    assert [adj.nearest_site(x) for x in q] == ref.tolist()
+
+
+@pytest.mark.parametrize("name", ["frame_2k_deg3", "frame_3k_surface"])
+def test_camera_matches_reference(name):
+    g = load_golden(name)
+    cam = CameraModel(PINHOLE, int(g["width"]), int(g["height"]), float(g["focal"]), g["pose"])
+    np.testing.assert_array_equal(cam.ray_directions(), g["dirs"])
+    o, d = camera_rays(cam, (0, 0))
+    np.testing.assert_array_equal(d, g["dirs"][0])
+    with pytest.raises(OutOfBounds):
+        camera_rays(cam, (int(g["height"]), 0))
+
+
+def test_look_at_and_orbit():
+    pose = look_at((0, 0, 3), (0, 0, 0))
+    np.testing.assert_allclose(pose[:3, 2], [0, 0, 1])
+    poses = orbit_poses(np.zeros(3), 3.0, 0.3, 8)
+    assert len(poses) == 8
+    for p in poses:
+        np.testing.assert_allclose(np.linalg.norm(p[:3, 3]), 3.0)
+        np.testing.assert_allclose(p[:3, :3] @ p[:3, :3].T, np.eye(3), atol=1e-12)
+
+
+def test_synthetic_positions_fp32_exact_and_csr_symmetric():
+    pos = random_positions(500, 3)
+    np.testing.assert_array_equal(pos.astype(np.float32).astype(np.float64), pos)
+    off, nbr, hull = delaunay_csr(pos)
+    assert off[-1] == len(nbr)
+    pairs = set()
+    for i in range(len(pos)):
+        row = nbr[off[i]:off[i + 1]]
+        assert np.all(np.diff(row) > 0), "ascending neighbour ids per site"
+        pairs.update((i, int(j)) for j in row)
+    assert all((j, i) in pairs for i, j in pairs), "symmetric"
+    assert hull.any()
+
+
+def test_golden_csr_is_reference_delaunay():
+    # make_golden.py asserted Qhull == rfoam.geometry.delaunay.build at 2k/3k;
+    # the committed CSR must still be the Qhull CSR of the committed sites.
+    g = load_golden("frame_2k_deg3")
+    off, nbr, _ = delaunay_csr(g["positions"])
+    np.testing.assert_array_equal(off, g["offsets"])
+    np.testing.assert_array_equal(nbr, g["neighbors"])
+
+
+@pytest.mark.parametrize("W,H,world", [(1920, 1080, 1), (1920, 1080, 2), (1920, 1080, 8),
+                                       (130, 70, 3), (3840, 2160, 4)])
+def test_tile_assignment_partitions_frame(W, H, world):
+    cover = np.zeros((H, W), dtype=np.int32)
+    for r in range(world):
+        tiles = D.tile_assignment(W, H, r, world)
+        cover += D.tile_pixel_mask(W, H, tiles)
+    assert (cover == 1).all()
+
+
+def test_shard_rays_partition():
+    for m, w in [(10, 3), (65536, 8), (7, 8)]:
+        ranges = [D.shard_rays(m, r, w) for r in range(w)]
+        covered = np.concatenate([np.arange(lo, hi) for lo, hi in ranges])
+        np.testing.assert_array_equal(covered, np.arange(m))
