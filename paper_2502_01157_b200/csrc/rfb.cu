@@ -229,7 +229,7 @@ __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
 // time from a global counter (persistent grid).
 // ---------------------------------------------------------------------------
 #ifndef RFB_FWD_MINB
-#define RFB_FWD_MINB 2
+#define RFB_FWD_MINB 4
 #endif
 template <int G, int SHDEG, bool PACKED, class Src>
 __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> S, Src src, double epsilon,
@@ -385,7 +385,7 @@ constexpr int kTrainBlock = 128;
 constexpr int kTrainWarps = kTrainBlock / 32;
 
 #ifndef RFB_TRAIN_MINB
-#define RFB_TRAIN_MINB 4
+#define RFB_TRAIN_MINB 8
 #endif
 template <int SHDEG, bool PACKED, bool TRAIN>
 __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
@@ -512,8 +512,10 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             if (in) {
                 double sig = ld_site(S.site4 + ci).w;
                 double delta = t1 - t0;
-                double alpha = 1.0 - exp(-sig * delta);
-                double w = tb0 * alpha;
+                // w = T_before[s] * alpha (kernels.py:300-301); with T_before[s+1] =
+                // T_before[s] * exp(-sigma*delta) from the forward pass this is
+                // T_before[s] - T_before[s+1] (equal up to rounding, no fp64 exp)
+                double w = tb0 - tb1;
                 double c0 = s_col[(3 * s) * SL], c1 = s_col[(3 * s + 1) * SL],
                        c2 = s_col[(3 * s + 2) * SL];
                 double g_r = ar * (tb1 * c0 - Sr);
