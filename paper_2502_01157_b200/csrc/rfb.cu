@@ -33,15 +33,15 @@ struct ArrayRays {
     __device__ __forceinline__ int64_t count() const { return m; }
     // returns the output index (ray id / pixel) or -1 for a padding slot
     __device__ __forceinline__ int64_t get(int64_t q, Ray &r) const {
-        r.ox = origins[3 * q];
-        r.oy = origins[3 * q + 1];
-        r.oz = origins[3 * q + 2];
-        r.dx = directions[3 * q];
-        r.dy = directions[3 * q + 1];
-        r.dz = directions[3 * q + 2];
-        r.t_min = t_min[q];
-        r.t_max = t_max[q];
-        r.start = start[q];
+        r.ox_ = origins[3 * q];
+        r.oy_ = origins[3 * q + 1];
+        r.oz_ = origins[3 * q + 2];
+        r.dx_ = directions[3 * q];
+        r.dy_ = directions[3 * q + 1];
+        r.dz_ = directions[3 * q + 2];
+        r.t_min_ = t_min[q];
+        r.t_max_ = t_max[q];
+        r.start_ = start[q];
         return q;
     }
 };
@@ -87,13 +87,13 @@ struct TileRays {
         int32_t px = (tile % tiles_x) * tile_w + (sub % subs_x) * 8 + (l & 7);
         int32_t py = (tile / tiles_x) * tile_h + (sub / subs_x) * 4 + (l >> 3);
         if (px >= cam.width || py >= cam.height) return -1;
-        r.ox = cam.o[0];
-        r.oy = cam.o[1];
-        r.oz = cam.o[2];
-        pinhole_dir(cam, py, px, r.dx, r.dy, r.dz);
-        r.t_min = t_min;
-        r.t_max = t_max;
-        r.start = *start_ptr;
+        r.ox_ = cam.o[0];
+        r.oy_ = cam.o[1];
+        r.oz_ = cam.o[2];
+        pinhole_dir(cam, py, px, r.dx_, r.dy_, r.dz_);
+        r.t_min_ = t_min;
+        r.t_max_ = t_max;
+        r.start_ = *start_ptr;
         return (int64_t)py * cam.width + px;
     }
 };
@@ -138,15 +138,16 @@ __device__ __forceinline__ void write_fwd(const FwdOut &O, int64_t q, int status
 // group.  rec(index, cell, header, t0, t1) is called for every recorded
 // segment, in order.  Returns the status code.
 // ---------------------------------------------------------------------------
-template <int G, bool PACKED, class Rec>
-__device__ __forceinline__ int walk(const SceneView<PACKED> &S, const Ray &r, double epsilon,
+template <int G, bool PACKED, class RayT, class Rec>
+__device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, int32_t start,
+                                    double epsilon,
                                     double log_eps, double width_floor, int32_t step_limit,
                                     int gl, unsigned gmask, int32_t &nseg, int32_t &cells,
                                     int32_t &visits, Rec &&rec) {
-    int32_t i = r.start;
-    double entry = r.t_min, log_T = 0.0;
+    int32_t i = start;
+    double entry = r.t_min(), log_T = 0.0;
     int32_t zero_adv = 0, steps = 0;
-    const float df[3] = {(float)r.dx, (float)r.dy, (float)r.dz};
+    const float df[3] = {(float)r.dx(), (float)r.dy(), (float)r.dz()};
     nseg = 0;
     cells = 0;
     visits = 0;
@@ -171,10 +172,10 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const Ray &r, do
             exit_face_f32<G>(S, c, c.hf, r, entry, df, gl, gmask, best_t, best_j);
         else
             exit_face<G, PACKED>(S, c, r, gl, gmask, best_t, best_j);
-        if (best_j < 0 || best_t >= r.t_max) {  // hull exit or far plane
-            if (r.t_max > entry) {
-                log_T -= c.sigma * (r.t_max - entry);
-                rec(nseg, i, c, entry, r.t_max);
+        if (best_j < 0 || best_t >= r.t_max()) {  // hull exit or far plane
+            if (r.t_max() > entry) {
+                log_T -= c.sigma * (r.t_max() - entry);
+                rec(nseg, i, c, entry, r.t_max());
                 nseg += 1;
             }
             return RFB_STATUS_OK;
@@ -212,7 +213,7 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const Ray &r, do
 // colour rounding bound.
 __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
     double basis[16];
-    sh_basis(r.dx, r.dy, r.dz, basis);
+    sh_basis(r.dx(), r.dy(), r.dz(), basis);
     double bsum = 0.0;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
@@ -229,7 +230,7 @@ __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
 // time from a global counter (persistent grid).
 // ---------------------------------------------------------------------------
 #ifndef RFB_FWD_MINB
-#define RFB_FWD_MINB 4
+#define RFB_FWD_MINB 5
 #endif
 template <int G, int SHDEG, bool PACKED, class Src>
 __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> S, Src src, double epsilon,
@@ -237,6 +238,8 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                                                 int32_t step_limit, FwdOut O,
                                                 unsigned long long *ray_counter) {
     constexpr int RPW = 32 / G;
+    __shared__ float s_basis[16 * 256];
+    __shared__ double s_ray[8 * 256];
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
@@ -250,34 +253,50 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
         if ((int64_t)base >= total) break;
         int64_t q = (int64_t)base + lane / G;
         if (q >= total) continue;
-        Ray r;
-        int64_t oidx = src.get(q, r);
-        if (oidx < 0) continue;
-
-        float basis[16];
+        int64_t oidx;
+        int32_t start;
+        // the ray's fp64 constants and fp32 SH basis live in shared memory
+        // (field-major, conflict-free) to keep registers for the walk: the
+        // kernel is occupancy-bound
+        RaySmem<256> r{s_ray + threadIdx.x};
+        float *basis = s_basis + threadIdx.x;
         double bsum;
-        if (SHDEG > 0) {
-            bsum = basis_setup(r, basis);
-        } else {
-            basis[0] = (float)kC0;
-            bsum = kC0;
+        {
+            Ray rr;
+            oidx = src.get(q, rr);
+            if (oidx < 0) continue;
+            start = rr.start_;
+            r.store(rr);
+            if (SHDEG > 0) {
+                float bf[16];
+                bsum = basis_setup(rr, bf);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) basis[k * 256] = bf[k];
+            } else {
+                basis[0] = (float)kC0;
+                bsum = kC0;
+            }
         }
-        const double dir[3] = {r.dx, r.dy, r.dz};
-        double T = 1.0, wsum = 0.0, cr = 0.0, cg = 0.0, cb = 0.0;
+        // colour accumulation in fp32 (image tolerance 1e-4); transmittance and
+        // the weight sum stay fp64 so sum(w) + T == 1 to ~1e-14; the walk's own
+        // log-transmittance test is fp64 as in the reference.
+        double T = 1.0, wsum = 0.0;
+        float cr = 0.f, cg = 0.f, cb = 0.f;
         const bool dump = O.seg_cap > 0;
         int32_t nseg, cells, visits;
         int status = walk<G, PACKED>(
-            S, r, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells, visits,
+            S, r, start, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells, visits,
             [&](int32_t s, int32_t cell, const Cell &c, double t0, double t1) {
                 double delta = t1 - t0;
-                double alpha = 1.0 - exp(-c.sigma * delta);
+                const double alpha = (double)(-expm1f(-(float)(c.sigma * delta)));
                 double col[3];
-                cell_color<SHDEG, PACKED>(S, cell, basis, dir, bsum, col);
-                double w = T * alpha;
+                cell_color<SHDEG, PACKED, 256>(S, cell, basis, r, bsum, col);
+                const double w = T * alpha;
                 wsum += w;
-                cr += w * col[0];
-                cg += w * col[1];
-                cb += w * col[2];
+                const float wf = (float)w;
+                cr += wf * (float)col[0];
+                cg += wf * (float)col[1];
+                cb += wf * (float)col[2];
                 T *= 1.0 - alpha;
                 if (dump && s < O.seg_cap && gl == 0) {
                     int64_t o = oidx * O.seg_cap + s;
@@ -341,15 +360,16 @@ __device__ __forceinline__ void red4(float *p, float a, float b, float c, float 
 }
 
 // kernels.py:340-369 -> contributions to x_i (gi) and x_j (gj).
+template <class RayT>
 __device__ __forceinline__ bool face_grad(const double4 *__restrict__ site4, int32_t i,
-                                          int32_t j, const Ray &r, double t, double dt,
+                                          int32_t j, const RayT &r, double t, double dt,
                                           double *gi, double *gj) {
     double4 xi = ld_site(site4 + i), xj = ld_site(site4 + j);
     double nx = xj.x - xi.x, ny = xj.y - xi.y, nz = xj.z - xi.z;
-    double denom = r.dx * nx + r.dy * ny + r.dz * nz;
+    double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
     if (denom == 0.0) return false;
     double mx = 0.5 * (xi.x + xj.x), my = 0.5 * (xi.y + xj.y), mz = 0.5 * (xi.z + xj.z);
-    double px = r.ox + t * r.dx, py = r.oy + t * r.dy, pz = r.oz + t * r.dz;
+    double px = r.ox() + t * r.dx(), py = r.oy() + t * r.dy(), pz = r.oz() + t * r.dz();
     double qx = mx - px, qy = my - py, qz = mz - pz;
     double inv = dt / denom;
     gi[0] = (0.5 * nx - qx) * inv;
@@ -361,8 +381,9 @@ __device__ __forceinline__ bool face_grad(const double4 *__restrict__ site4, int
     return true;
 }
 
+template <class RayT>
 __device__ __forceinline__ void face_grad_atomic(const double4 *__restrict__ site4, int32_t i,
-                                                 int32_t j, const Ray &r, double t, double dt,
+                                                 int32_t j, const RayT &r, double t, double dt,
                                                  float *g4) {
     double gi[3], gj[3];
     if (!face_grad(site4, i, j, r, t, dt, gi, gj)) return;
@@ -415,7 +436,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         const bool have_ray = q < total;
 
         Ray r;
-        r.t_min = 0.0;
+        r.t_min_ = 0.0;
         float basis[16];
         int32_t nseg = 0;
         int status = RFB_STATUS_OK;
@@ -426,16 +447,16 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             src.get(q, r);
             double bsum = basis_setup(r, basis);
             double cbsum = SHDEG > 0 ? bsum : kC0;
-            const double dir[3] = {r.dx, r.dy, r.dz};
             int32_t cells, visits;
             status = walk<1, PACKED>(
-                S, r, epsilon, log_eps, width_floor, step_limit, 0, kFull, nseg, cells, visits,
+                S, r, r.start_, epsilon, log_eps, width_floor, step_limit, 0, kFull, nseg, cells,
+                visits,
                 [&](int32_t s, int32_t cell, const Cell &c, double t0, double t1) {
                     double delta = t1 - t0;
                     double e = exp(-c.sigma * delta);
                     double alpha = 1.0 - e;
                     double col[3];
-                    int mask = cell_color<SHDEG, PACKED>(S, cell, basis, dir, cbsum, col);
+                    int mask = cell_color<SHDEG, PACKED>(S, cell, basis, r, cbsum, col);
                     double w = Tc * alpha;
                     wsum += w;
                     cr += w * col[0];
@@ -487,7 +508,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             ci = cm & 0x1fffffff;
             cmask = (cm >> 29) & 7;
             t1 = s_t1[s * SL];
-            t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min;
+            t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min();
             tb1 = s_tb[s * SL];
             tb0 = s > 0 ? s_tb[(s - 1) * SL] : 1.0;
         };
@@ -607,7 +628,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                         while (sh_ < nseg - 1 && (1.0 - s_tb[sh_ * SL]) < target) sh_ += 1;
                         int32_t c_ = s_cell[sh_ * SL] & 0x1fffffff;
                         double si = ld_site(S.site4 + c_).w;
-                        double ts0 = sh_ > 0 ? s_t1[(sh_ - 1) * SL] : r.t_min;
+                        double ts0 = sh_ > 0 ? s_t1[(sh_ - 1) * SL] : r.t_min();
                         seg_hit[a] = sh_;
                         if (si <= 0.0) {
                             t_hit[a] = ts0;
@@ -631,13 +652,13 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                         int32_t c_ = s_cell[sh_ * SL] & 0x1fffffff;
                         double si = ld_site(S.site4 + c_).w;
                         double t_u = t_hit[a];
-                        double ts0 = sh_ > 0 ? s_t1[(sh_ - 1) * SL] : r.t_min;
+                        double ts0 = sh_ > 0 ? s_t1[(sh_ - 1) * SL] : r.t_min();
                         double Tbs = sh_ > 0 ? s_tb[(sh_ - 1) * SL] : 1.0;
                         double T_at = Tbs * exp(-si * (t_u - ts0));
                         double wd = T_at * si;
                         if (wd <= 1e-300) continue;
                         double g = (a == 0 ? sign : -sign) * q_scale / wd;
-                        double prev_t1 = r.t_min;
+                        double prev_t1 = r.t_min();
                         for (int32_t k = 0; k < nseg; ++k) {  // kernels.py:534-548
                             double k_t0 = prev_t1, k_t1 = s_t1[k * SL];
                             prev_t1 = k_t1;

@@ -152,9 +152,9 @@ struct SceneView {
 // recomputed exactly (fp64 basis from the direction, fp64 coefficients), so
 // the clamp mask -- which gates the SH gradient -- is always the reference's
 // and the colour is within ~1e-6 of it.
-template <int SHDEG, bool PACKED>
+template <int SHDEG, bool PACKED, int BSTRIDE = 1, class RayT>
 __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
-                                          const float *basis_f, const double *dir,
+                                          const float *basis_f, const RayT &ray,
                                           double bsum, double *col) {
     const float cmax = S.sh_absmax;
     constexpr int NB = SHDEG == 0 ? 1 : 16;
@@ -174,10 +174,10 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     float4 v = __ldg(r4 + q);
-                    a = __fmaf_rn(basis_f[4 * q], v.x, a);
-                    a = __fmaf_rn(basis_f[4 * q + 1], v.y, a);
-                    a = __fmaf_rn(basis_f[4 * q + 2], v.z, a);
-                    a = __fmaf_rn(basis_f[4 * q + 3], v.w, a);
+                    a = __fmaf_rn(basis_f[(4 * q) * BSTRIDE], v.x, a);
+                    a = __fmaf_rn(basis_f[(4 * q + 1) * BSTRIDE], v.y, a);
+                    a = __fmaf_rn(basis_f[(4 * q + 2) * BSTRIDE], v.z, a);
+                    a = __fmaf_rn(basis_f[(4 * q + 3) * BSTRIDE], v.w, a);
                 }
                 acc[ch] = (double)a;
             }
@@ -187,7 +187,7 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
         if (SHDEG == 0)
             basis[0] = kC0;
         else
-            sh_basis(dir[0], dir[1], dir[2], basis);
+            sh_basis(ray.dx(), ray.dy(), ray.dz(), basis);
         const double *row = S.sh + (int64_t)i * 48;
 #pragma unroll
         for (int k = 0; k < NB; ++k)
@@ -204,7 +204,7 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
             if (SHDEG == 0)
                 basis[0] = kC0;
             else
-                sh_basis(dir[0], dir[1], dir[2], basis);
+                sh_basis(ray.dx(), ray.dy(), ray.dz(), basis);
             const double *row = S.sh + (int64_t)i * 48;
             a = 0.5;
             for (int k = 0; k < NB; ++k) a += basis[k] * __ldg(row + k * 3 + ch);
@@ -218,9 +218,44 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
     return mask;
 }
 
+// A ray in registers (writable by the ray sources) ...
 struct Ray {
-    double ox, oy, oz, dx, dy, dz, t_min, t_max;
-    int32_t start;
+    double ox_, oy_, oz_, dx_, dy_, dz_, t_min_, t_max_;
+    int32_t start_;
+    __device__ __forceinline__ double ox() const { return ox_; }
+    __device__ __forceinline__ double oy() const { return oy_; }
+    __device__ __forceinline__ double oz() const { return oz_; }
+    __device__ __forceinline__ double dx() const { return dx_; }
+    __device__ __forceinline__ double dy() const { return dy_; }
+    __device__ __forceinline__ double dz() const { return dz_; }
+    __device__ __forceinline__ double t_min() const { return t_min_; }
+    __device__ __forceinline__ double t_max() const { return t_max_; }
+    __device__ __forceinline__ int32_t start() const { return start_; }
+};
+
+// ... or parked in shared memory, field-major [8][NT] (conflict-free), so the
+// fp64 ray constants do not occupy registers across the walk.
+template <int NT>
+struct RaySmem {
+    double *p;  // &s_ray[0][threadIdx.x]
+    __device__ __forceinline__ double ox() const { return p[0 * NT]; }
+    __device__ __forceinline__ double oy() const { return p[1 * NT]; }
+    __device__ __forceinline__ double oz() const { return p[2 * NT]; }
+    __device__ __forceinline__ double dx() const { return p[3 * NT]; }
+    __device__ __forceinline__ double dy() const { return p[4 * NT]; }
+    __device__ __forceinline__ double dz() const { return p[5 * NT]; }
+    __device__ __forceinline__ double t_min() const { return p[6 * NT]; }
+    __device__ __forceinline__ double t_max() const { return p[7 * NT]; }
+    __device__ __forceinline__ void store(const Ray &r) {
+        p[0 * NT] = r.ox_;
+        p[1 * NT] = r.oy_;
+        p[2 * NT] = r.oz_;
+        p[3 * NT] = r.dx_;
+        p[4 * NT] = r.dy_;
+        p[5 * NT] = r.dz_;
+        p[6 * NT] = r.t_min_;
+        p[7 * NT] = r.t_max_;
+    }
 };
 
 // log(eps) test with a guard band: exp() is only evaluated when log_T is
@@ -249,9 +284,9 @@ __device__ __forceinline__ bool below_epsilon(double log_T, double epsilon, doub
 #define RFB_STR_(x) #x
 #define RFB_PRAGMA_UNROLL(n) _Pragma(RFB_STR_(unroll n))
 
-template <int G, bool PACKED>
+template <int G, bool PACKED, class RayT>
 __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell &c,
-                                          const Ray &r, int gl, unsigned gmask, double &best_t,
+                                          const RayT &r, int gl, unsigned gmask, double &best_t,
                                           int32_t &best_j) {
     best_t = dinf();
     best_j = -1;
@@ -266,12 +301,12 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
         double nx = xj - c.x;
         double ny = yj - c.y;
         double nz = zj - c.z;
-        double denom = r.dx * nx + r.dy * ny + r.dz * nz;
+        double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
         if (denom <= 0.0) continue;
         double mx = 0.5 * (xj + c.x);
         double my = 0.5 * (yj + c.y);
         double mz = 0.5 * (zj + c.z);
-        double num = (mx - r.ox) * nx + (my - r.oy) * ny + (mz - r.oz) * nz;
+        double num = (mx - r.ox()) * nx + (my - r.oy()) * ny + (mz - r.oz()) * nz;
         if (have) {
             double c1 = num * bden, c2 = bnum * denom;
             if (c1 - c2 > (fabs(c1) + fabs(c2)) * 0x1p-50) continue;
@@ -339,16 +374,16 @@ typedef unsigned long long cand_mask_t;
 constexpr int kMaskBits = 64;
 #endif
 
-template <int G>
+template <int G, class RayT>
 __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Cell &c,
-                                              const float4 &hdr_f, const Ray &r, double entry,
+                                              const float4 &hdr_f, const RayT &r, double entry,
                                               const float *df, int gl, unsigned gmask,
                                               double &best_t, int32_t &best_j,
                                               int32_t *best_k_out = nullptr,
                                               int2 *meta_out = nullptr) {
     constexpr float u = 0x1p-24f;
     // q = o + entry * d in fp64 (once per step), rounded to fp32
-    const double qx = r.ox + entry * r.dx, qy = r.oy + entry * r.dy, qz = r.oz + entry * r.dz;
+    const double qx = r.ox() + entry * r.dx(), qy = r.oy() + entry * r.dy(), qz = r.oz() + entry * r.dz();
     const float qxf = (float)qx, qyf = (float)qy, qzf = (float)qz;
     const float Q = fmaxf(fabsf(qxf), fmaxf(fabsf(qyf), fabsf(qzf))) * (1.0f + 4.0f * u);
     const float px = hdr_f.x - qxf, py = hdr_f.y - qyf, pz = hdr_f.z - qzf;
@@ -425,10 +460,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
         const float4 e = __ldg(S.edge + k);
         const double xj = e.x, yj = e.y, zj = e.z;
         const double nx = xj - c.x, ny = yj - c.y, nz = zj - c.z;
-        const double denom = r.dx * nx + r.dy * ny + r.dz * nz;
+        const double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
         if (denom <= 0.0) continue;
         const double mx = 0.5 * (xj + c.x), my = 0.5 * (yj + c.y), mz = 0.5 * (zj + c.z);
-        const double t = ((mx - r.ox) * nx + (my - r.oy) * ny + (mz - r.oz) * nz) / denom;
+        const double t = ((mx - r.ox()) * nx + (my - r.oy()) * ny + (mz - r.oz()) * nz) / denom;
         if (t < best_t) {
             best_t = t;
             best_j = __float_as_int(e.w);
@@ -440,10 +475,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
         const float4 e = __ldg(S.edge + k);
         const double xj = e.x, yj = e.y, zj = e.z;
         const double nx = xj - c.x, ny = yj - c.y, nz = zj - c.z;
-        const double denom = r.dx * nx + r.dy * ny + r.dz * nz;
+        const double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
         if (denom <= 0.0) continue;
         const double mx = 0.5 * (xj + c.x), my = 0.5 * (yj + c.y), mz = 0.5 * (zj + c.z);
-        const double t = ((mx - r.ox) * nx + (my - r.oy) * ny + (mz - r.oz) * nz) / denom;
+        const double t = ((mx - r.ox()) * nx + (my - r.oy()) * ny + (mz - r.oz()) * nz) / denom;
         if (t < best_t) {
             best_t = t;
             best_j = __float_as_int(e.w);

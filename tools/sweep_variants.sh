@@ -1,5 +1,5 @@
 #!/bin/bash
 # Run the forward/train sweep for the default library and every build/variants/*.so
 cd "$(dirname "$0")/.."
-python tools/sweep_fwd.py --lanes 1 --train "$@"
-for f in build/variants/*.so; do RFB_LIB=$f python tools/sweep_fwd.py --lanes 1 --train "$@"; done
+python tools/sweep_fwd.py --lanes 1 ${SWEEP_TRAIN---train} "$@"
+for f in build/variants/*.so; do RFB_LIB=$f python tools/sweep_fwd.py --lanes 1 ${SWEEP_TRAIN---train} "$@"; done
