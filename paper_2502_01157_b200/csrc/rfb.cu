@@ -406,7 +406,7 @@ constexpr int kTrainBlock = 128;
 constexpr int kTrainWarps = kTrainBlock / 32;
 
 #ifndef RFB_TRAIN_MINB
-#define RFB_TRAIN_MINB 8
+#define RFB_TRAIN_MINB 6
 #endif
 template <int SHDEG, bool PACKED, bool TRAIN>
 __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
@@ -414,8 +414,11 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
     int32_t step_limit, const double *adjoints, const double *targets, double rgb_scale,
     double q_scale, const double *u_pairs, int32_t n_pairs, double weight_floor, FwdOut O,
     Grads gr, double *loss, Scratch scr, unsigned long long *ray_counter) {
+    // per lane: 16 basis values + a constant 1 (column 16) used by the plain sums
     __shared__ float s_basis[kTrainWarps][32][17];
-    __shared__ float s_f[kTrainWarps][32][3];
+    // per lane per reverse iteration: f_r, f_g, f_b, dpos_i xyz, dsigma_i, dpos_j xyz
+    __shared__ float s_f[kTrainWarps][32][11];
+    __shared__ double s_ray[8 * kTrainBlock];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t SL = scr.slots;
@@ -424,8 +427,15 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
     double *s_tb = scr.tb + slot;
     float *s_col = scr.col + slot;
     double loss_rgb = 0.0, loss_q = 0.0;
-    unsigned long long my_cells = 0, my_visits = 0;
+    unsigned int my_cells = 0, my_visits = 0;
     const int64_t total = src.count();
+    float *bas = &s_basis[warp][lane][0];
+    bas[16] = 1.0f;
+    // reverse-pass output o (two per lane): o < 48 -> dSH[k][ch] = sum f[ch] * basis[k];
+    // 48..51 -> (dpos_i xyz, dsigma_i); 52..54 -> dpos_j xyz
+    const int o0 = lane, o1 = lane + 32;
+    const int k0 = o0 / 3, c0i = o0 % 3;
+    const int k1 = o1 < 48 ? o1 / 3 : 16, c1i = o1 < 48 ? o1 % 3 : 3 + (o1 - 48);
 
     for (;;) {
         unsigned long long base = 0;
@@ -435,88 +445,94 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         const int64_t q = (int64_t)base + lane;
         const bool have_ray = q < total;
 
-        Ray r;
-        r.t_min_ = 0.0;
-        float basis[16];
+        RaySmem<kTrainBlock> r{s_ray + threadIdx.x};
         int32_t nseg = 0;
         int status = RFB_STATUS_OK;
-        double Tc = 1.0, Tb = 1.0, wsum = 0.0, cr = 0.0, cg = 0.0, cb = 0.0;
-        double ar = 0.0, ag = 0.0, ab = 0.0;
+        float ar = 0.f, ag = 0.f, ab = 0.f;
         bool grad_ok = false;
         if (have_ray) {
-            src.get(q, r);
-            double bsum = basis_setup(r, basis);
-            double cbsum = SHDEG > 0 ? bsum : kC0;
+            double cbsum;
+            int32_t start;
+            {
+                Ray rr;
+                src.get(q, rr);
+                r.store(rr);
+                start = rr.start_;
+                double bsum = basis_setup(rr, bas);
+                cbsum = SHDEG > 0 ? bsum : kC0;
+            }
+            double Tb = 1.0, wsum = 0.0;
+            float cr = 0.f, cg = 0.f, cb = 0.f;
             int32_t cells, visits;
             status = walk<1, PACKED>(
-                S, r, r.start_, epsilon, log_eps, width_floor, step_limit, 0, kFull, nseg, cells,
+                S, r, start, epsilon, log_eps, width_floor, step_limit, 0, kFull, nseg, cells,
                 visits,
                 [&](int32_t s, int32_t cell, const Cell &c, double t0, double t1) {
-                    double delta = t1 - t0;
-                    double e = exp(-c.sigma * delta);
-                    double alpha = 1.0 - e;
+                    const double e = exp(-c.sigma * (t1 - t0));
                     double col[3];
-                    int mask = cell_color<SHDEG, PACKED>(S, cell, basis, r, cbsum, col);
-                    double w = Tc * alpha;
+                    const int mask = cell_color<SHDEG, PACKED>(S, cell, bas, r, cbsum, col);
+                    const double Tn = Tb * e;  // T_before[s+1] (kernels.py:275)
+                    const double w = Tb - Tn;  // T_before[s] * alpha
                     wsum += w;
-                    cr += w * col[0];
-                    cg += w * col[1];
-                    cb += w * col[2];
-                    Tc *= 1.0 - alpha;
-                    Tb = Tb * e;
+                    const float wf = (float)w;
+                    cr += wf * (float)col[0];
+                    cg += wf * (float)col[1];
+                    cb += wf * (float)col[2];
+                    Tb = Tn;
                     s_cell[s * SL] = cell | (mask << 29);
                     s_t1[s * SL] = t1;
-                    s_tb[s * SL] = Tb;
+                    s_tb[s * SL] = Tn;
                     s_col[(3 * s) * SL] = (float)col[0];
                     s_col[(3 * s + 1) * SL] = (float)col[1];
                     s_col[(3 * s + 2) * SL] = (float)col[2];
                 });
-            my_cells += (unsigned long long)cells;
-            my_visits += (unsigned long long)visits;
+            my_cells += (unsigned)cells;
+            my_visits += (unsigned)visits;
             if (status != RFB_STATUS_OK) {
                 write_fwd(O, q, status, S.bg[0], S.bg[1], S.bg[2], 1.0, 0.0, nseg, cells, visits);
             } else {
-                cr += Tc * S.bg[0];
-                cg += Tc * S.bg[1];
-                cb += Tc * S.bg[2];
-                write_fwd(O, q, status, cr, cg, cb, Tc, wsum, nseg, cells, visits);
+                const double R = cr + Tb * S.bg[0], G = cg + Tb * S.bg[1], B = cb + Tb * S.bg[2];
+                write_fwd(O, q, status, R, G, B, Tb, wsum, nseg, cells, visits);
                 if (TRAIN) {  // kernels.py:430-437
-                    double er = cr - targets[3 * q], eg = cg - targets[3 * q + 1],
-                           eb = cb - targets[3 * q + 2];
+                    double er = R - targets[3 * q], eg = G - targets[3 * q + 1],
+                           eb = B - targets[3 * q + 2];
                     loss_rgb += er * er + eg * eg + eb * eb;
-                    ar = 2.0 * rgb_scale * er;
-                    ag = 2.0 * rgb_scale * eg;
-                    ab = 2.0 * rgb_scale * eb;
+                    ar = (float)(2.0 * rgb_scale * er);
+                    ag = (float)(2.0 * rgb_scale * eg);
+                    ab = (float)(2.0 * rgb_scale * eb);
                 } else {
-                    ar = adjoints[3 * q];
-                    ag = adjoints[3 * q + 1];
-                    ab = adjoints[3 * q + 2];
+                    ar = (float)adjoints[3 * q];
+                    ag = (float)adjoints[3 * q + 1];
+                    ab = (float)adjoints[3 * q + 2];
                 }
                 grad_ok = nseg > 0;
             }
         }
 
-        // ---- cooperative reverse pass -------------------------------------
-#pragma unroll
-        for (int k = 0; k < 16; ++k) s_basis[warp][lane][k] = grad_ok ? basis[k] : 0.f;
+        // ---- cooperative reverse pass (kernels.py:267-337) -------------------
+        // Each iteration: the farthest pending segment's cell is processed by
+        // every lane currently in it; the group's 55 gradient values (48 dSH,
+        // dpos+dsigma of the cell, dpos of the previously processed cell) are
+        // reduced through shared memory and land with coalesced atomics.
         int32_t s = grad_ok ? nseg - 1 : -1;
         int32_t ci = -1, cmask = 0, next_cell = -1;
-        double t1 = 0.0, t0 = 0.0, tb1 = 0.0, tb0 = 1.0;
-        double Sr = 0.0, Sg = 0.0, Sb = 0.0, d_next = 0.0;
+        double t1 = 0.0, t0 = 0.0;
+        float tb1 = 0.f, tb0 = 1.f;
+        float Sr = 0.f, Sg = 0.f, Sb = 0.f, d_next = 0.f;
         auto load_seg = [&]() {
-            int32_t cm = s_cell[s * SL];
+            const int32_t cm = s_cell[s * SL];
             ci = cm & 0x1fffffff;
             cmask = (cm >> 29) & 7;
             t1 = s_t1[s * SL];
             t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min();
-            tb1 = s_tb[s * SL];
-            tb0 = s > 0 ? s_tb[(s - 1) * SL] : 1.0;
+            tb1 = (float)s_tb[s * SL];
+            tb0 = s > 0 ? (float)s_tb[(s - 1) * SL] : 1.f;
         };
         if (s >= 0) {
             load_seg();
-            Sr = tb1 * S.bg[0];  // suffix starts at T_end * background
-            Sg = tb1 * S.bg[1];
-            Sb = tb1 * S.bg[2];
+            Sr = tb1 * (float)S.bg[0];  // suffix starts at T_end * background
+            Sg = tb1 * (float)S.bg[1];
+            Sb = tb1 * (float)S.bg[2];
         }
         for (;;) {
             const bool act = s >= 0;
@@ -526,91 +542,79 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             const int leader = __ffs(__ballot_sync(kFull, act && key == kmax)) - 1;
             const int32_t lc = __shfl_sync(kFull, ci, leader);
             const bool in = act && ci == lc;
-            float v_sig = 0.f, v_px = 0.f, v_py = 0.f, v_pz = 0.f;
-            float v_jx = 0.f, v_jy = 0.f, v_jz = 0.f;
-            float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+            float v[11];
+#pragma unroll
+            for (int k = 0; k < 11; ++k) v[k] = 0.f;
             int32_t jn = -1;
             if (in) {
-                double sig = ld_site(S.site4 + ci).w;
-                double delta = t1 - t0;
-                // w = T_before[s] * alpha (kernels.py:300-301); with T_before[s+1] =
-                // T_before[s] * exp(-sigma*delta) from the forward pass this is
-                // T_before[s] - T_before[s+1] (equal up to rounding, no fp64 exp)
-                double w = tb0 - tb1;
-                double c0 = s_col[(3 * s) * SL], c1 = s_col[(3 * s + 1) * SL],
-                       c2 = s_col[(3 * s + 2) * SL];
-                double g_r = ar * (tb1 * c0 - Sr);
-                double g_g = ag * (tb1 * c1 - Sg);
-                double g_b = ab * (tb1 * c2 - Sb);
-                double common = g_r + g_g + g_b;
-                v_sig = (float)(delta * common);
-                double dd = sig * common;
+                const float sig = (float)ld_site(S.site4 + ci).w;
+                const float delta = (float)(t1 - t0);
+                const float w = tb0 - tb1;
+                const float c0 = s_col[(3 * s) * SL], c1 = s_col[(3 * s + 1) * SL],
+                            c2 = s_col[(3 * s + 2) * SL];
+                const float common =
+                    ar * (tb1 * c0 - Sr) + ag * (tb1 * c1 - Sg) + ab * (tb1 * c2 - Sb);
+                v[6] = delta * common;
+                const float dd = sig * common;
                 if (next_cell >= 0) {  // interior boundary s+1 (kernels.py:328-337)
-                    double dt = dd - d_next;
+                    const float dt = dd - d_next;
                     double gi[3], gj[3];
-                    if (dt != 0.0 && face_grad(S.site4, ci, next_cell, r, t1, dt, gi, gj)) {
-                        v_px = (float)gi[0];
-                        v_py = (float)gi[1];
-                        v_pz = (float)gi[2];
-                        v_jx = (float)gj[0];
-                        v_jy = (float)gj[1];
-                        v_jz = (float)gj[2];
+                    if (dt != 0.f && face_grad(S.site4, ci, next_cell, r, t1, (double)dt, gi, gj)) {
+                        v[3] = (float)gi[0];
+                        v[4] = (float)gi[1];
+                        v[5] = (float)gi[2];
+                        v[7] = (float)gj[0];
+                        v[8] = (float)gj[1];
+                        v[9] = (float)gj[2];
                         jn = next_cell;
                     }
                 }
-                if (w != 0.0) {  // kernels.py:309-322
-                    if ((cmask & 1) == 0 && ar != 0.0) f0 = (float)(w * ar);
-                    if ((cmask & 2) == 0 && ag != 0.0) f1 = (float)(w * ag);
-                    if ((cmask & 4) == 0 && ab != 0.0) f2 = (float)(w * ab);
+                if (w != 0.f) {  // kernels.py:309-322
+                    if ((cmask & 1) == 0 && ar != 0.f) v[0] = w * ar;
+                    if ((cmask & 2) == 0 && ag != 0.f) v[1] = w * ag;
+                    if ((cmask & 4) == 0 && ab != 0.f) v[2] = w * ab;
                 }
-                Sr = Sr + w * c0;
-                Sg = Sg + w * c1;
-                Sb = Sb + w * c2;
+                Sr += w * c0;
+                Sg += w * c1;
+                Sb += w * c2;
                 d_next = dd;
                 next_cell = ci;
                 s -= 1;
                 if (s >= 0) load_seg();
             }
-            // dsigma + dpos of the group's cell: one float4 atomic
-            v_sig = warp_sum(v_sig);
-            v_px = warp_sum(v_px);
-            v_py = warp_sum(v_py);
-            v_pz = warp_sum(v_pz);
-            if (lane == leader) red4(gr.g4 + 4 * (int64_t)lc, v_px, v_py, v_pz, v_sig);
-            // dpos of the previously processed cell: aggregated when the group agrees
+            // previous cell: aggregated when the whole group agrees on it
             const int32_t jany = __reduce_max_sync(kFull, in ? jn : -1);
-            if (jany >= 0) {
-                if (__all_sync(kFull, !in || jn < 0 || jn == jany)) {
-                    v_jx = warp_sum(v_jx);
-                    v_jy = warp_sum(v_jy);
-                    v_jz = warp_sum(v_jz);
-                    if (lane == leader) red4(gr.g4 + 4 * (int64_t)jany, v_jx, v_jy, v_jz, 0.f);
-                } else if (in && jn >= 0) {
-                    red4(gr.g4 + 4 * (int64_t)jn, v_jx, v_jy, v_jz, 0.f);
-                }
+            const bool juni = __all_sync(kFull, !in || jn < 0 || jn == jany);
+            if (!juni && in && jn >= 0) {  // rare: scatter this lane's share directly
+                float *pj = gr.g4 + 4 * (int64_t)jn;
+                atomicAdd(pj, v[7]);
+                atomicAdd(pj + 1, v[8]);
+                atomicAdd(pj + 2, v[9]);
+                v[7] = v[8] = v[9] = 0.f;
             }
-            // dSH: sum_l f_l[ch] * basis_l[k] over the group, 48 outputs
-            const unsigned gm = __ballot_sync(kFull, in && (f0 != 0.f || f1 != 0.f || f2 != 0.f));
-            if (gm) {
-                s_f[warp][lane][0] = f0;
-                s_f[warp][lane][1] = f1;
-                s_f[warp][lane][2] = f2;
-                __syncwarp();
-                float acc0 = 0.f, acc1 = 0.f;
-                const int k0 = lane / 3, ch0 = lane % 3;
-                const int o1 = lane + 32, k1 = o1 / 3, ch1 = o1 % 3;
-                unsigned mm = gm;
-                while (mm) {
-                    const int l = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    acc0 += s_f[warp][l][ch0] * s_basis[warp][l][k0];
-                    if (o1 < 48) acc1 += s_f[warp][l][ch1] * s_basis[warp][l][k1];
-                }
-                float *row = gr.sh + 48 * (int64_t)lc;
-                atomicAdd(row + lane, acc0);
-                if (o1 < 48) atomicAdd(row + o1, acc1);
-                __syncwarp();
+            float *fr = &s_f[warp][lane][0];
+#pragma unroll
+            for (int k = 0; k < 10; ++k) fr[k] = v[k];
+            const unsigned gm = __ballot_sync(kFull, in);
+            __syncwarp();
+            float acc0 = 0.f, acc1 = 0.f;
+            unsigned mm = gm;
+            while (mm) {
+                const int l = __ffs(mm) - 1;
+                mm &= mm - 1;
+                acc0 += s_f[warp][l][c0i] * s_basis[warp][l][k0];
+                acc1 += s_f[warp][l][c1i] * s_basis[warp][l][k1];
             }
+            float *row = gr.sh + 48 * (int64_t)lc;
+            atomicAdd(row + o0, acc0);  // dSH, 32 contiguous floats
+            if (o1 < 48) {
+                atomicAdd(row + o1, acc1);  // dSH, 16 contiguous floats
+            } else if (o1 < 52) {
+                atomicAdd(gr.g4 + 4 * (int64_t)lc + (o1 - 48), acc1);  // dpos_i, dsigma_i
+            } else if (o1 < 55 && jany >= 0 && juni) {
+                atomicAdd(gr.g4 + 4 * (int64_t)jany + (o1 - 52), acc1);  // dpos_j
+            }
+            __syncwarp();
         }
 
         // ---- quantile pairs (kernels.py:456-567), per lane ----------------
@@ -689,12 +693,13 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             }
         }
     }
+    unsigned long long tc = my_cells, tv = my_visits;
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         loss_rgb += __shfl_xor_sync(kFull, loss_rgb, off);
         loss_q += __shfl_xor_sync(kFull, loss_q, off);
-        my_cells += __shfl_xor_sync(kFull, my_cells, off);
-        my_visits += __shfl_xor_sync(kFull, my_visits, off);
+        tc += __shfl_xor_sync(kFull, tc, off);
+        tv += __shfl_xor_sync(kFull, tv, off);
     }
     if (lane == 0) {
         if (TRAIN && loss) {
@@ -702,8 +707,8 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             atomicAdd(loss + 1, loss_q);
         }
         if (O.counters) {
-            atomicAdd(O.counters, my_cells);
-            atomicAdd(O.counters + 1, my_visits);
+            atomicAdd(O.counters, tc);
+            atomicAdd(O.counters + 1, tv);
         }
     }
 }
