@@ -72,7 +72,7 @@ typedef struct rfb_scene {
     const double *sh;         /* [n_sites][48], index k*3 + ch (render.py:53) */
     const void *cells;        /* packed: [n_sites] 32-byte headers (nullable) */
     const void *edges;        /* packed: [n_edges] 16-byte records (nullable) */
-    const void *edge_meta;    /* packed: [n_edges] int2 {k0, k1} of the edge's target site */
+    const void *edge_meta;    /* packed, optional: [n_edges] int2 {k0, k1} of the edge's target */
     const float *sh32;        /* packed: [n_sites][3][16] fp32 channel-major copy of sh (nullable) */
     int32_t packed;           /* 1: use cells/edges/sh32 for the walk */
     float sh_absmax;          /* packed: >= max |sh| over the scene (fp32 colour bound) */

@@ -18,9 +18,6 @@ constexpr unsigned kFull = 0xffffffffu;
 #define RFB_F32_FILTER 1
 #endif
 constexpr bool kUseF32Filter = RFB_F32_FILTER != 0;
-#ifndef RFB_CHAIN
-#define RFB_CHAIN 0
-#endif
 
 // ---------------------------------------------------------------------------
 // Ray sources: explicit arrays (render.py:57-125) or a pinhole camera over a
@@ -150,67 +147,58 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
     const float df[3] = {(float)r.dx(), (float)r.dy(), (float)r.dz()};
     nseg = 0;
     cells = 0;
-    visits = 0;
-    // PACKED: after the first step the next cell's position comes from the
-    // chosen edge record and its CSR row from the (speculatively loaded)
-    // edge meta, so only sigma/cmax are fetched per step, off the critical
-    // path.
-    constexpr bool kChain = PACKED && kUseF32Filter && RFB_CHAIN;
-    Cell c = S.cell(i);
+    visits = 0;  // cells stepped == steps taken (kernels.py:111), set on return
     for (;;) {
         steps += 1;
-        if (steps > step_limit) return RFB_STATUS_STEP_LIMIT;
-        cells += 1;
-        if (!kChain && steps > 1) c = S.cell(i);
+        if (steps > step_limit) {
+            cells = step_limit;
+            return RFB_STATUS_STEP_LIMIT;
+        }
+        const Cell c = S.cell(i);
         visits += c.k1 - c.k0;
         double best_t;
-        int32_t best_j, best_k = -1;
-        int2 meta = make_int2(0, 0);
-        if constexpr (kChain)
-            exit_face_f32<G>(S, c, c.hf, r, entry, df, gl, gmask, best_t, best_j, &best_k, &meta);
-        else if constexpr (PACKED && kUseF32Filter)
+        int32_t best_j;
+        if constexpr (PACKED && kUseF32Filter)
             exit_face_f32<G>(S, c, c.hf, r, entry, df, gl, gmask, best_t, best_j);
         else
             exit_face<G, PACKED>(S, c, r, gl, gmask, best_t, best_j);
         if (best_j < 0 || best_t >= r.t_max()) {  // hull exit or far plane
             if (r.t_max() > entry) {
-                log_T -= c.sigma * (r.t_max() - entry);
-                rec(nseg, i, c, entry, r.t_max());
+                const double sig = S.sigma_of(i, c);
+                log_T -= sig * (r.t_max() - entry);
+                rec(nseg, i, sig, entry, r.t_max());
                 nseg += 1;
             }
+            cells = steps;
             return RFB_STATUS_OK;
         }
         if (best_t < entry) best_t = entry;
         if (best_t - entry > width_floor) {
-            log_T -= c.sigma * (best_t - entry);
-            rec(nseg, i, c, entry, best_t);
+            const double sig = S.sigma_of(i, c);
+            log_T -= sig * (best_t - entry);
+            rec(nseg, i, sig, entry, best_t);
             nseg += 1;
             entry = best_t;
             zero_adv = 0;
-            if (below_epsilon(log_T, epsilon, log_eps)) return RFB_STATUS_OK;
-            if (nseg >= step_limit) return RFB_STATUS_STEP_LIMIT;
+            if (below_epsilon(log_T, epsilon, log_eps)) {
+                cells = steps;
+                return RFB_STATUS_OK;
+            }
+            if (nseg >= step_limit) {
+                cells = steps;
+                return RFB_STATUS_STEP_LIMIT;
+            }
         } else {
             zero_adv += 1;
-            if (zero_adv > kZeroAdvanceLimit) return RFB_STATUS_CYCLE;
+            if (zero_adv > kZeroAdvanceLimit) {
+                cells = steps;
+                return RFB_STATUS_CYCLE;
+            }
         }
         i = best_j;
-        if constexpr (kChain) {
-            const float4 e = __ldg(S.edge + best_k);  // L1 hit: read in this step
-            const float4 h2 = __ldg(reinterpret_cast<const float4 *>(S.hdr + i) + 1);
-            c.hf = e;
-            c.x = e.x;
-            c.y = e.y;
-            c.z = e.z;
-            c.k0 = meta.x;
-            c.k1 = meta.y;
-            c.sigma = __hiloint2double(__float_as_int(h2.y), __float_as_int(h2.x));
-            c.n1max = h2.w;
-        }
     }
 }
 
-// fp32 copy of the ray's 16 SH basis values and sum |basis| (fp64) for the
-// colour rounding bound.
 __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
     double basis[16];
     sh_basis(r.dx(), r.dy(), r.dz(), basis);
@@ -230,7 +218,7 @@ __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
 // time from a global counter (persistent grid).
 // ---------------------------------------------------------------------------
 #ifndef RFB_FWD_MINB
-#define RFB_FWD_MINB 5
+#define RFB_FWD_MINB 4
 #endif
 template <int G, int SHDEG, bool PACKED, class Src>
 __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> S, Src src, double epsilon,
@@ -244,7 +232,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
     const int gl = lane & (G - 1);
     const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const int64_t total = src.count();
-    unsigned long long my_cells = 0, my_visits = 0;
+    unsigned int my_cells = 0, my_visits = 0;
 
     for (;;) {
         unsigned long long base = 0;
@@ -286,9 +274,9 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
         int32_t nseg, cells, visits;
         int status = walk<G, PACKED>(
             S, r, start, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells, visits,
-            [&](int32_t s, int32_t cell, const Cell &c, double t0, double t1) {
+            [&](int32_t s, int32_t cell, double sigma, double t0, double t1) {
                 double delta = t1 - t0;
-                const double alpha = (double)(-expm1f(-(float)(c.sigma * delta)));
+                const double alpha = (double)(-expm1f(-(float)(sigma * delta)));
                 double col[3];
                 cell_color<SHDEG, PACKED, 256>(S, cell, basis, r, bsum, col);
                 const double w = T * alpha;
@@ -306,8 +294,8 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 }
             });
         if (gl == 0) {
-            my_cells += (unsigned long long)cells;
-            my_visits += (unsigned long long)visits;
+            my_cells += (unsigned)cells;
+            my_visits += (unsigned)visits;
             if (status != RFB_STATUS_OK)  // kernels.py:230-236
                 write_fwd(O, oidx, status, S.bg[0], S.bg[1], S.bg[2], 1.0, 0.0, nseg, cells,
                           visits);
@@ -317,14 +305,15 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
         }
     }
     if (O.counters) {
+        unsigned long long tc = my_cells, tv = my_visits;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) {
-            my_cells += __shfl_xor_sync(kFull, my_cells, off);
-            my_visits += __shfl_xor_sync(kFull, my_visits, off);
+            tc += __shfl_xor_sync(kFull, tc, off);
+            tv += __shfl_xor_sync(kFull, tv, off);
         }
         if (lane == 0) {
-            atomicAdd(O.counters, my_cells);
-            atomicAdd(O.counters + 1, my_visits);
+            atomicAdd(O.counters, tc);
+            atomicAdd(O.counters + 1, tv);
         }
     }
 }
@@ -467,8 +456,8 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             status = walk<1, PACKED>(
                 S, r, start, epsilon, log_eps, width_floor, step_limit, 0, kFull, nseg, cells,
                 visits,
-                [&](int32_t s, int32_t cell, const Cell &c, double t0, double t1) {
-                    const double e = exp(-c.sigma * (t1 - t0));
+                [&](int32_t s, int32_t cell, double sigma, double t0, double t1) {
+                    const double e = exp(-sigma * (t1 - t0));
                     double col[3];
                     const int mask = cell_color<SHDEG, PACKED>(S, cell, bas, r, cbsum, col);
                     const double Tn = Tb * e;  // T_before[s+1] (kernels.py:275)
@@ -757,7 +746,7 @@ __global__ void k_pack_edges(const int64_t *nbr64, const int64_t *off64, const d
     if (edges) {
         edges[k] = make_float4((float)pos[3 * j], (float)pos[3 * j + 1], (float)pos[3 * j + 2],
                                __int_as_float(j));
-        emeta[k] = make_int2((int32_t)off64[j], (int32_t)off64[j + 1]);
+        if (emeta) emeta[k] = make_int2((int32_t)off64[j], (int32_t)off64[j + 1]);
     }
 }
 
@@ -932,7 +921,7 @@ static bool scene_ok(const rfb_scene *s) {
     if (!s || !s->site4 || !s->offsets || !s->neighbors || !s->sh || s->n_sites <= 0 ||
         s->n_sites >= (1 << 29) || (s->sh_degree != 0 && s->sh_degree != 3))
         return false;
-    if (s->packed && (!s->cells || !s->edges || !s->edge_meta || !s->sh32)) return false;
+    if (s->packed && (!s->cells || !s->edges || !s->sh32)) return false;
     return true;
 }
 
@@ -1115,7 +1104,7 @@ int rfb_pack_scene(const double *positions, const double *sigma, const double *s
                    void *cells, void *edges, void *edge_meta, float *sh32, void *stream) {
     if (!positions || !sigma || !offsets || !neighbors || !site4 || !offsets32 || !neighbors32 ||
         n_sites <= 0 || n_edges < 0 || n_edges >= ((int64_t)1 << 31) ||
-        ((cells || edges || edge_meta || sh32) && (!cells || !edges || !edge_meta || !sh32 || !sh)))
+        ((cells || edges || sh32) && (!cells || !edges || !sh32 || !sh)))
         return RFB_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     k_pack_sites<<<(unsigned)((n_sites + 1 + 255) / 256), 256, 0, st>>>(

@@ -97,19 +97,20 @@ struct SceneView {
     float sh_absmax;        // max |sh coefficient| over the scene (colour rounding bound)
     double bg[3];
 
+    // Per-step cell record.  PACKED: only the fp32 header fields (the walk
+    // widens x,y,z exactly where the fp64 path needs them and fetches sigma
+    // when a segment is recorded) -- fewer live registers across the
+    // neighbour loop.
     __device__ __forceinline__ Cell cell(int32_t i) const {
         Cell c;
         if (PACKED) {
             const float4 *p = reinterpret_cast<const float4 *>(hdr + i);
-            float4 a = __ldg(p), b = __ldg(p + 1);
+            float4 a = __ldg(p);
             c.hf = a;
-            c.x = a.x;
-            c.y = a.y;
-            c.z = a.z;
             c.k0 = __float_as_int(a.w);
-            c.sigma = __hiloint2double(__float_as_int(b.y), __float_as_int(b.x));
-            c.k1 = __float_as_int(b.z);
-            c.n1max = b.w;
+            const float2 b = __ldg(reinterpret_cast<const float2 *>(p + 1) + 1);
+            c.k1 = __float_as_int(b.x);
+            c.n1max = b.y;
         } else {
             double4 s = ld_site(site4 + i);
             c.x = s.x;
@@ -121,6 +122,11 @@ struct SceneView {
             c.n1max = 0.f;
         }
         return c;
+    }
+
+    __device__ __forceinline__ double sigma_of(int32_t i, const Cell &c) const {
+        if (PACKED) return __ldg(&hdr[i].sigma);
+        return c.sigma;
     }
 
     __device__ __forceinline__ void edge_at(int32_t k, double &x, double &y, double &z,
@@ -152,6 +158,17 @@ struct SceneView {
 // recomputed exactly (fp64 basis from the direction, fp64 coefficients), so
 // the clamp mask -- which gates the SH gradient -- is always the reference's
 // and the colour is within ~1e-6 of it.
+// Reference-exact channel value (kernels.py:66-68) from the fp64 table;
+// out of line so its registers do not count against the walk.
+__device__ __noinline__ double exact_channel(const double *row, int ch, int nb, double dx,
+                                             double dy, double dz) {
+    double basis[16];
+    sh_basis(dx, dy, dz, basis);
+    double a = 0.5;
+    for (int k = 0; k < nb; ++k) a += basis[k] * __ldg(row + k * 3 + ch);
+    return a;
+}
+
 template <int SHDEG, bool PACKED, int BSTRIDE = 1, class RayT>
 __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
                                           const float *basis_f, const RayT &ray,
@@ -167,8 +184,8 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
             for (int ch = 0; ch < 3; ++ch)
                 acc[ch] = (double)__fmaf_rn(basis_f[0], __ldg(row + 16 * ch), 0.5f);
         } else {
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) {
+#pragma unroll 1
+            for (int ch = 0; ch < 3; ++ch) {  // one channel (4 x 16 B) in flight: registers
                 const float4 *r4 = reinterpret_cast<const float4 *>(row + 16 * ch);
                 float a = 0.5f;
 #pragma unroll
@@ -199,16 +216,8 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
         double a = acc[ch];
-        if (PACKED && fabs(a) <= tol) {  // ambiguous clamp: redo in fp64 (exact)
-            double basis[16];
-            if (SHDEG == 0)
-                basis[0] = kC0;
-            else
-                sh_basis(ray.dx(), ray.dy(), ray.dz(), basis);
-            const double *row = S.sh + (int64_t)i * 48;
-            a = 0.5;
-            for (int k = 0; k < NB; ++k) a += basis[k] * __ldg(row + k * 3 + ch);
-        }
+        if (PACKED && fabs(a) <= tol)  // ambiguous clamp: redo in fp64 (exact)
+            a = exact_channel(S.sh + (int64_t)i * 48, ch, NB, ray.dx(), ray.dy(), ray.dz());
         if (a < 0.0) {
             a = 0.0;
             mask |= 1 << ch;
@@ -366,6 +375,9 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #ifndef RFB_FAST_BOUND
 #define RFB_FAST_BOUND 1
 #endif
+#ifndef RFB_F32_UNROLL
+#define RFB_F32_UNROLL 4
+#endif
 #if RFB_MASK32
 typedef unsigned int cand_mask_t;
 constexpr int kMaskBits = 32;
@@ -378,9 +390,7 @@ template <int G, class RayT>
 __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Cell &c,
                                               const float4 &hdr_f, const RayT &r, double entry,
                                               const float *df, int gl, unsigned gmask,
-                                              double &best_t, int32_t &best_j,
-                                              int32_t *best_k_out = nullptr,
-                                              int2 *meta_out = nullptr) {
+                                              double &best_t, int32_t &best_j) {
     constexpr float u = 0x1p-24f;
     // q = o + entry * d in fp64 (once per step), rounded to fp32
     const double qx = r.ox() + entry * r.dx(), qy = r.oy() + entry * r.dy(), qz = r.oz() + entry * r.dz();
@@ -398,11 +408,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
     constexpr float K3 = 8.0f * u + 0x1p-40f;
 #endif
     float U = __int_as_float(0x7f800000);  // +inf
-    float smin = U;
-    int32_t kguess = -1;
     cand_mask_t mask = 0;
     const int32_t k0 = c.k0 + gl;
     int32_t nk = 0;
+    RFB_PRAGMA_UNROLL(RFB_F32_UNROLL)
     for (int32_t k = k0; k < c.k1; k += G, ++nk) {
         const float4 e = __ldg(S.edge + k);
         const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
@@ -434,15 +443,8 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
 #endif
         if (s - es <= U) mask |= bit;
         U = fminf(U, s + es);
-        if (s < smin) {
-            smin = s;
-            kguess = k;
-        }
     }
-    // speculative load of the likely exit neighbour's CSR row bounds: it is
-    // in flight while phase 2 runs (G == 1 only)
-    int2 meta_g = make_int2(0, 0);
-    if (G == 1 && meta_out && kguess >= 0) meta_g = __ldg(S.emeta + kguess);
+    const double cx = hdr_f.x, cy = hdr_f.y, cz = hdr_f.z;  // exact widening
     // phase 2: exact fp64 re-evaluation of the candidates, CSR order
     best_t = dinf();
     best_j = -1;
@@ -459,10 +461,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
         const int32_t k = k0 + idx * G;
         const float4 e = __ldg(S.edge + k);
         const double xj = e.x, yj = e.y, zj = e.z;
-        const double nx = xj - c.x, ny = yj - c.y, nz = zj - c.z;
+        const double nx = xj - cx, ny = yj - cy, nz = zj - cz;
         const double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
         if (denom <= 0.0) continue;
-        const double mx = 0.5 * (xj + c.x), my = 0.5 * (yj + c.y), mz = 0.5 * (zj + c.z);
+        const double mx = 0.5 * (xj + cx), my = 0.5 * (yj + cy), mz = 0.5 * (zj + cz);
         const double t = ((mx - r.ox()) * nx + (my - r.oy()) * ny + (mz - r.oz()) * nz) / denom;
         if (t < best_t) {
             best_t = t;
@@ -474,10 +476,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
         const int32_t k = k0 + idx * G;
         const float4 e = __ldg(S.edge + k);
         const double xj = e.x, yj = e.y, zj = e.z;
-        const double nx = xj - c.x, ny = yj - c.y, nz = zj - c.z;
+        const double nx = xj - cx, ny = yj - cy, nz = zj - cz;
         const double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
         if (denom <= 0.0) continue;
-        const double mx = 0.5 * (xj + c.x), my = 0.5 * (yj + c.y), mz = 0.5 * (zj + c.z);
+        const double mx = 0.5 * (xj + cx), my = 0.5 * (yj + cy), mz = 0.5 * (zj + cz);
         const double t = ((mx - r.ox()) * nx + (my - r.oy()) * ny + (mz - r.oz()) * nz) / denom;
         if (t < best_t) {
             best_t = t;
@@ -498,9 +500,6 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
             }
         }
     }
-    if (best_k_out) *best_k_out = best_k;
-    if (meta_out && best_j >= 0)
-        *meta_out = (G == 1 && best_k == kguess) ? meta_g : __ldg(S.emeta + best_k);
 }
 
 }  // namespace rfb

@@ -102,8 +102,7 @@ class DeviceScene:
                 self.cells = torch.empty((n, 8), dtype=torch.int32, device=dev)      # 32 B headers
                 self.edges = torch.empty((max(self.n_edges, 1), 4), dtype=torch.float32,
                                          device=dev)                                # 16 B records
-                self.edge_meta = torch.empty((max(self.n_edges, 1), 2), dtype=torch.int32,
-                                             device=dev)                            # {k0, k1}
+                self.edge_meta = None  # optional {k0, k1} per edge (unused by the walk)
                 self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
             else:
                 self.cells = self.edges = self.edge_meta = self.sh32 = None
@@ -131,7 +130,7 @@ class DeviceScene:
         c.sh = self.sh.data_ptr()
         c.cells = self.cells.data_ptr() if self.packed else None
         c.edges = self.edges.data_ptr() if self.packed else None
-        c.edge_meta = self.edge_meta.data_ptr() if self.packed else None
+        c.edge_meta = None
         c.sh32 = self.sh32.data_ptr() if self.packed else None
         c.packed = 1 if self.packed else 0
         c.sh_absmax = self.sh_absmax
