@@ -14,6 +14,15 @@
 namespace rfb {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kBlockTile = 1024;  // rays claimed per block at a time (one 32x32 tile)
+#ifndef RFB_BLOCK_TILES
+#define RFB_BLOCK_TILES 0
+#endif
+#ifndef RFB_OTF_BASIS
+#define RFB_OTF_BASIS 0
+#endif
+constexpr bool kBlockTiles = RFB_BLOCK_TILES != 0;
+constexpr bool kOtfBasis = RFB_OTF_BASIS != 0;
 #ifndef RFB_F32_FILTER
 #define RFB_F32_FILTER 1
 #endif
@@ -226,8 +235,19 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                                                 int32_t step_limit, FwdOut O,
                                                 unsigned long long *ray_counter) {
     constexpr int RPW = 32 / G;
-    __shared__ float s_basis[16 * 256];
-    __shared__ double s_ray[8 * 256];
+    // per thread: the ray's fp64 constants + sum|basis| (field-major, conflict-free)
+    __shared__ double s_ray[9 * 256];
+    __shared__ float s_basis[kOtfBasis ? 1 : 16 * 256];  // [k][thread] when not on the fly
+    // block-level work claiming: the block takes kBlockTile consecutive rays
+    // (one 32x32 image tile for rfb_render_image) at a time and its warps
+    // split it, so co-resident warps walk the same cells and share L1.
+    __shared__ int s_lock, s_used;
+    __shared__ unsigned long long s_tile;
+    if (threadIdx.x == 0) {
+        s_lock = 0;
+        s_used = kBlockTile;
+    }
+    __syncthreads();
     const int lane = threadIdx.x & 31;
     const int gl = lane & (G - 1);
     const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
@@ -236,7 +256,24 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
 
     for (;;) {
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(ray_counter, (unsigned long long)RPW);
+        if (!kBlockTiles) {
+            if (lane == 0) base = atomicAdd(ray_counter, (unsigned long long)RPW);
+        } else if (lane == 0) {
+            while (atomicCAS(&s_lock, 0, 1) != 0) {
+            }
+            __threadfence_block();
+            int used = *(volatile int *)&s_used;
+            unsigned long long tile = *(volatile unsigned long long *)&s_tile;
+            if (used + RPW > kBlockTile) {
+                tile = atomicAdd(ray_counter, (unsigned long long)kBlockTile);
+                used = 0;
+                *(volatile unsigned long long *)&s_tile = tile;
+            }
+            base = tile + (unsigned long long)used;
+            *(volatile int *)&s_used = used + RPW;
+            __threadfence_block();
+            atomicExch(&s_lock, 0);
+        }
         base = __shfl_sync(kFull, base, 0);
         if ((int64_t)base >= total) break;
         int64_t q = (int64_t)base + lane / G;
@@ -247,8 +284,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
         // (field-major, conflict-free) to keep registers for the walk: the
         // kernel is occupancy-bound
         RaySmem<256> r{s_ray + threadIdx.x};
-        float *basis = s_basis + threadIdx.x;
-        double bsum;
+        double *bsum_p = s_ray + 8 * 256 + threadIdx.x;
         {
             Ray rr;
             oidx = src.get(q, rr);
@@ -257,12 +293,14 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
             r.store(rr);
             if (SHDEG > 0) {
                 float bf[16];
-                bsum = basis_setup(rr, bf);
+                *bsum_p = basis_setup(rr, bf);
+                if constexpr (!kOtfBasis) {
 #pragma unroll
-                for (int k = 0; k < 16; ++k) basis[k * 256] = bf[k];
+                    for (int k = 0; k < 16; ++k) s_basis[k * 256 + threadIdx.x] = bf[k];
+                }
             } else {
-                basis[0] = (float)kC0;
-                bsum = kC0;
+                *bsum_p = kC0;
+                if constexpr (!kOtfBasis) s_basis[threadIdx.x] = (float)kC0;
             }
         }
         // colour accumulation in fp32 (image tolerance 1e-4); transmittance and
@@ -278,7 +316,16 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 double delta = t1 - t0;
                 const double alpha = (double)(-expm1f(-(float)(sigma * delta)));
                 double col[3];
-                cell_color<SHDEG, PACKED, 256>(S, cell, basis, r, bsum, col);
+                if constexpr (kOtfBasis) {
+                    float bf[16];  // on-the-fly fp32 basis (registers only during colour)
+                    if (SHDEG > 0)
+                        sh_basis_f32((float)r.dx(), (float)r.dy(), (float)r.dz(), bf);
+                    else
+                        bf[0] = (float)kC0;
+                    cell_color<SHDEG, PACKED, 1, true>(S, cell, bf, r, *bsum_p, col);
+                } else {
+                    cell_color<SHDEG, PACKED, 256>(S, cell, s_basis + threadIdx.x, r, *bsum_p, col);
+                }
                 const double w = T * alpha;
                 wsum += w;
                 const float wf = (float)w;
