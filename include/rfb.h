@@ -17,7 +17,7 @@
  *                        activation for device-resident training; the parity
  *                        shim uploads the host numpy value instead)
  *   rfb_camera_rays     tracer/camera.py:66-92      CameraModel.ray_directions()
- *                        (pinhole branch, lines 80-83/91-92)
+ *                        (pinhole and fisheye)
  *   rfb_locate          geometry/adjacency.py:85-100 nearest_site()
  *                        (greedy walk on the CSR; same distance expression
  *                        and lowest-id tie rule as _grid_nearest 140-203)
@@ -31,6 +31,8 @@
  *                        (backward_ray 250-337 + face_t_gradient 340-369)
  *   rfb_train_batch     tracer/kernels.py:372-453   train_batch()
  *                        (+ quantile_backward_ray 456-567)
+ *   rfb_post_grad_adam  optim/train.py:195-209 + optim/adam.py:15-31
+ *   rfb_refresh_scene   diffrender/render.py:49-54 after a device-side update
  *
  * Per-ray status semantics are the reference's (tracer/kernels.py:11-21):
  * 0 ok, 2 step limit, 3 cycle; failed rays render the background with
@@ -53,7 +55,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 4
+#define RFB_ABI_VERSION 5
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
@@ -126,7 +128,7 @@ typedef struct rfb_grads {
     float *sh;      /* [n][48] */
 } rfb_grads;
 
-/* Pinhole camera (camera.py:20-60). pose is row-major world-from-camera. */
+/* Camera (camera.py:20-92). pose is row-major world-from-camera. */
 typedef struct rfb_camera {
     double pose[16]; /* (host value) */
     int32_t width;
@@ -134,6 +136,8 @@ typedef struct rfb_camera {
     double focal;
     double cx;
     double cy;
+    int32_t kind;    /* 0 pinhole, 1 fisheye (equidistant, theta = r) */
+    int32_t pad_;
 } rfb_camera;
 
 int rfb_abi_version(void);
@@ -154,6 +158,26 @@ int rfb_pack_scene(const double *positions, const double *sigma, const double *s
  * (nullable), site4[:,3] (nullable) and the packed headers (nullable). */
 int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void *cells,
                  void *stream);
+
+/* Fused gradient post-processing + Adam after the gradient all-reduce
+ * (optim/train.py:195-209 + optim/adam.py:15-31).  grads_flat is the [n*52]
+ * fp32 buffer of rfb_grads; positions [n][3], raw_density [n], sh [n][48] are
+ * the fp64 parameters updated in place; adam_state holds m_pos, v_pos (3n
+ * each), m_raw, v_raw (n each), m_sh, v_sh (48n each).  hyper (host) is
+ * 3 x {lr, beta1, beta2, eps, 1-beta1^step, 1-beta2^step} for positions,
+ * densities and SH.  sh_warmup zeroes the SH bands 1..15 gradient;
+ * update_positions = 0 skips positions (lr_pos == 0 tail). */
+int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positions,
+                       double *raw_density, double *sh, double *adam_state, double clip,
+                       int32_t sh_warmup, int32_t update_positions, const double *hyper,
+                       void *stream);
+
+/* After a parameter update: site4 = {positions, softplus(raw)}, packed
+ * headers' sigma and the fp32 SH copy are refreshed from scene->sh.  (The
+ * packed edge records hold positions: a scene whose positions moved must be
+ * re-packed, or used with packed = 0.) */
+int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const double *raw_density,
+                      void *stream);
 
 /* dirs [pix_count][3] f64 for row-major pixels pix_begin .. pix_begin+count-1. */
 int rfb_camera_rays(const rfb_camera *camera, int64_t pix_begin, int64_t pix_count,

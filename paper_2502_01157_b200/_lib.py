@@ -88,6 +88,8 @@ class rfb_camera(ctypes.Structure):
         ("focal", ctypes.c_double),
         ("cx", ctypes.c_double),
         ("cy", ctypes.c_double),
+        ("kind", ctypes.c_int32),
+        ("pad_", ctypes.c_int32),
     ]
 
 
@@ -106,6 +108,8 @@ SIGNATURES = {
     "rfb_pack_scene": (ctypes.c_int, [VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP, VP, VP, VP]),
     "rfb_softplus": (ctypes.c_int, [VP, I64, VP, VP, VP, VP]),
     "rfb_camera_rays": (ctypes.c_int, [P(rfb_camera), I64, I64, VP, VP]),
+    "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP]),
+    "rfb_refresh_scene": (ctypes.c_int, [P(rfb_scene), VP, VP, VP]),
     "rfb_locate": (ctypes.c_int, [P(rfb_scene), VP, I64, I32, VP, VP]),
     "rfb_render_rays": (ctypes.c_int, [P(rfb_scene), P(rfb_rays), P(rfb_params), P(rfb_fwd_out),
                                        VP, SZ, VP]),
@@ -142,7 +146,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rfb_abi_version() != 4:
+        if lib.rfb_abi_version() != 5:
             raise ExtensionMissing("librfb.so ABI version mismatch; rebuild")
         if path is None:
             _lib = lib

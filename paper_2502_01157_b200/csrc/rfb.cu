@@ -57,18 +57,30 @@ struct CameraParams {
     double o[3];  // pose[:3,3]
     double focal, cx, cy;
     int32_t width, height;
+    int32_t kind;  // 0 pinhole, 1 fisheye (camera.py:16-17)
 };
 
-// camera.py:78-92 pinhole branch; the fma order reproduces numpy's
-// `d_cam @ R.T` bit-for-bit (tests/test_gpu_parity.py).
+// camera.py:78-92.  Pinhole: the fma order reproduces numpy's `d_cam @ R.T`
+// bit-for-bit (tests/test_gpu_parity.py).  Fisheye (equidistant, theta = r):
+// same matmul order; its sin/cos/hypot are the device's (<= 2 ulp), so the
+// directions agree with numpy to ~1e-16 rather than bit-for-bit.
 __device__ __forceinline__ void pinhole_dir(const CameraParams &c, int64_t row, int64_t col,
                                             double &dx, double &dy, double &dz) {
     double u = ((double)col + 0.5 - c.cx) / c.focal;
     double v = -((double)row + 0.5 - c.cy) / c.focal;
+    double a = u, b = v, z = -1.0;
+    if (c.kind == 1) {
+        const double r = hypot(u, v);
+        double sn, cs;
+        sincos(r, &sn, &cs);
+        a = r > 0.0 ? sn * u / r : 0.0;
+        b = r > 0.0 ? sn * v / r : 0.0;
+        z = -cs;
+    }
     double w[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k)
-        w[k] = __fma_rn(-1.0, c.R[3 * k + 2], __fma_rn(v, c.R[3 * k + 1], u * c.R[3 * k]));
+        w[k] = __fma_rn(z, c.R[3 * k + 2], __fma_rn(b, c.R[3 * k + 1], a * c.R[3 * k]));
     double nrm = sqrt((w[0] * w[0] + w[1] * w[1]) + w[2] * w[2]);
     dx = w[0] / nrm;
     dy = w[1] / nrm;
@@ -912,6 +924,72 @@ static void nearest_point(const rfb_scene *s, double qx, double qy, double qz, v
 }
 
 // ---------------------------------------------------------------------------
+// Gradient post-processing + Adam (optim/train.py:195-209, optim/adam.py:15-31)
+// One fused elementwise pass over the flat gradient buffer after the
+// all-reduce: d_raw = dsigma * sigmoid(10 raw), SH warm-up mask (bands 1..15
+// zeroed), clip to +-clip, then Adam with bias correction on the fp64
+// parameters, in the reference's operation order (bias corrections are host
+// scalars, like numpy's beta ** step).
+// ---------------------------------------------------------------------------
+struct AdamArgs {
+    double lr, b1, b2, eps, bc1, bc2;  // bc = 1 - beta ** step
+};
+
+__device__ __forceinline__ void adam1(double &p, double g, double &m, double &v,
+                                      const AdamArgs &a) {
+    m = m * a.b1;
+    m = m + (1.0 - a.b1) * g;
+    v = v * a.b2;
+    v = v + (1.0 - a.b2) * g * g;
+    const double m_hat = m / a.bc1;
+    const double v_hat = v / a.bc2;
+    p = p - a.lr * m_hat / (sqrt(v_hat) + a.eps);
+}
+
+__device__ __forceinline__ double clipd(double x, double c) { return fmin(fmax(x, -c), c); }
+
+__global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double *pos,
+                            double *raw, double *sh, double *m_pos, double *v_pos, double *m_raw,
+                            double *v_raw, double *m_sh, double *v_sh, double clip, int sh_warmup,
+                            int update_pos, AdamArgs a_pos, AdamArgs a_raw, AdamArgs a_sh) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n * 52) return;
+    if (t < n * 48) {  // SH coefficient t = i*48 + k*3 + ch
+        double g = (double)gsh[t];
+        if (sh_warmup && (t % 48) >= 3) g = 0.0;  // train.py:197-198
+        adam1(sh[t], clipd(g, clip), m_sh[t], v_sh[t], a_sh);
+        return;
+    }
+    const int64_t u = t - n * 48;
+    if (u < n) {  // raw density: d_raw = dsigma * softplus_grad(raw) (render.py:220)
+        const double x = raw[u];
+        const double d_raw = (double)g4[4 * u + 3] * (1.0 / (1.0 + exp(-10.0 * x)));
+        adam1(raw[u], clipd(d_raw, clip), m_raw[u], v_raw[u], a_raw);
+        return;
+    }
+    const int64_t w = u - n;  // position component w = i*3 + c
+    if (update_pos && w < 3 * n) {
+        const int64_t i = w / 3, c = w % 3;
+        adam1(pos[w], clipd((double)g4[4 * i + c], clip), m_pos[w], v_pos[w], a_pos);
+    }
+}
+
+// Refresh the kernel arrays from updated parameters (render.py:49-54 on
+// device): site4 = {pos, softplus(raw)}, packed headers' sigma, sh32.
+__global__ void k_refresh_scene(int64_t n, const double *pos, const double *raw,
+                                const double *sh, double4 *site4, CellHdr *cells, float *sh32) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double x = raw[i];
+    const double sig = fmax(x, 0.0) + log1p(exp(-fabs(10.0 * x))) / 10.0;
+    site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sig);
+    if (cells) cells[i].sigma = sig;
+    if (sh32)
+        for (int k = 0; k < 16; ++k)
+            for (int ch = 0; ch < 3; ++ch) sh32[i * 48 + 16 * ch + k] = (float)sh[i * 48 + 3 * k + ch];
+}
+
+// ---------------------------------------------------------------------------
 // Host helpers
 // ---------------------------------------------------------------------------
 static int num_sms() {
@@ -1120,6 +1198,7 @@ static CameraParams cam_params(const rfb_camera *c) {
     p.cy = c->cy;
     p.width = c->width;
     p.height = c->height;
+    p.kind = c->kind;
     return p;
 }
 
@@ -1173,10 +1252,41 @@ int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void 
     return (int)cudaGetLastError();
 }
 
+int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positions,
+                       double *raw_density, double *sh, double *adam_state, double clip,
+                       int32_t sh_warmup, int32_t update_positions, const double *hyper,
+                       void *stream) {
+    if (n_sites <= 0 || !grads_flat || !positions || !raw_density || !sh || !adam_state ||
+        !hyper || !(clip > 0.0))
+        return RFB_EINVAL;
+    const int64_t n = n_sites;
+    double *m_pos = adam_state, *v_pos = m_pos + 3 * n, *m_raw = v_pos + 3 * n,
+           *v_raw = m_raw + n, *m_sh = v_raw + n, *v_sh = m_sh + 48 * n;
+    AdamArgs a[3];
+    for (int k = 0; k < 3; ++k) {
+        const double *h = hyper + 6 * k;
+        a[k] = AdamArgs{h[0], h[1], h[2], h[3], h[4], h[5]};
+    }
+    const int64_t total = n * 52;
+    k_post_adam<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        n, grads_flat, grads_flat + 4 * n, positions, raw_density, sh, m_pos, v_pos, m_raw, v_raw,
+        m_sh, v_sh, clip, sh_warmup, update_positions, a[0], a[1], a[2]);
+    return (int)cudaGetLastError();
+}
+
+int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const double *raw_density,
+                      void *stream) {
+    if (!scene_ok(scene) || !positions || !raw_density) return RFB_EINVAL;
+    k_refresh_scene<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        scene->n_sites, positions, raw_density, scene->sh, (double4 *)scene->site4,
+        (CellHdr *)scene->cells, (float *)scene->sh32);
+    return (int)cudaGetLastError();
+}
+
 int rfb_camera_rays(const rfb_camera *camera, int64_t pix_begin, int64_t pix_count, double *dirs,
                     void *stream) {
     if (!camera || !dirs || pix_begin < 0 || pix_count < 0 || camera->width < 1 ||
-        camera->height < 1 || !(camera->focal > 0.0) ||
+        camera->height < 1 || !(camera->focal > 0.0) || camera->kind < 0 || camera->kind > 1 ||
         pix_begin + pix_count > (int64_t)camera->width * camera->height)
         return RFB_EINVAL;
     if (pix_count == 0) return RFB_OK;
@@ -1224,8 +1334,8 @@ int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb
                      void *workspace, size_t workspace_bytes, void *stream) {
     if (!scene_ok(scene) || !camera || !params || !out_ok(out) || params->step_limit <= 0 ||
         !tile_ids || n_tiles < 0 || tile_w < 8 || tile_h < 4 || tile_w % 8 || tile_h % 4 ||
-        camera->width < 1 || camera->height < 1 || !(camera->focal > 0.0) ||
-        start_site >= scene->n_sites || !workspace || workspace_bytes < 256)
+        camera->width < 1 || camera->height < 1 || !(camera->focal > 0.0) || camera->kind < 0 ||
+        camera->kind > 1 || start_site >= scene->n_sites || !workspace || workspace_bytes < 256)
         return RFB_EINVAL;
     if (n_tiles == 0) return RFB_OK;
     cudaStream_t st = (cudaStream_t)stream;

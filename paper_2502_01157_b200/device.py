@@ -260,6 +260,7 @@ def camera_struct(camera) -> _lib.rfb_camera:
     c.focal = float(camera.focal)
     c.cx = float(camera.cx)
     c.cy = float(camera.cy)
+    c.kind = 1 if getattr(camera, "kind", "pinhole") == "fisheye" else 0
     return c
 
 

@@ -188,16 +188,6 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
     device in one pass (rfb_render_image).
     """
     ds = _device_scene(scene, device_scene)
-    if camera.kind != "pinhole":
-        dirs = camera.ray_directions()
-        origins = np.broadcast_to(camera.position, (len(dirs), 3)).copy()
-        out = render_ray_batch(scene, origins, dirs, epsilon=epsilon, step_limit=step_limit,
-                               stats=stats, return_wsum=weight_check, device_scene=ds)
-        img = out[0].reshape(camera.height, camera.width, 3)
-        if weight_check:
-            return (img, out[3].reshape(camera.height, camera.width),
-                    out[1].reshape(camera.height, camera.width))
-        return img
     H, W = camera.height, camera.width
     fc = _frame_cache(ds, W, H, weight_check)
     torch.cuda.synchronize(ds.device)

@@ -36,7 +36,7 @@ from rfoam.diffrender.render import (RenderStats, render_image, render_ray_batch
 from rfoam.foam import FoamScene  # noqa: E402
 from rfoam.geometry import AdjacencyGraph, build  # noqa: E402
 from rfoam.tracer import kernels  # noqa: E402
-from rfoam.tracer.camera import PINHOLE, CameraModel, look_at, orbit_poses  # noqa: E402
+from rfoam.tracer.camera import FISHEYE, PINHOLE, CameraModel, look_at, orbit_poses  # noqa: E402
 from rfoam.tracer.rays import WIDTH_FLOOR_SCALE, Ray, intersect_face, trace  # noqa: E402
 
 from paper_2502_01157_b200.synthetic import delaunay_csr, random_positions  # noqa: E402
@@ -99,8 +99,8 @@ def traces_for(scene, origins, dirs, idx, epsilon, step_limit=4096):
                 tr_status=np.asarray(status, dtype=np.int8))
 
 
-def frame_case(name, scene, eye, W, H, epsilon, n_trace=96, seed=0, angle=0.9):
-    cam = CameraModel.from_angle_x(PINHOLE, W, H, angle, look_at(eye, (0.0, 0.0, 0.0)))
+def frame_case(name, scene, eye, W, H, epsilon, n_trace=96, seed=0, angle=0.9, kind=PINHOLE):
+    cam = CameraModel.from_angle_x(kind, W, H, angle, look_at(eye, (0.0, 0.0, 0.0)))
     stats = RenderStats()
     img, wsum, resid = render_image(scene, cam, epsilon=epsilon, workers=1, stats=stats,
                                     weight_check=True)
@@ -112,6 +112,7 @@ def frame_case(name, scene, eye, W, H, epsilon, n_trace=96, seed=0, angle=0.9):
     idx = np.sort(rng.choice(len(dirs), size=min(n_trace, len(dirs)), replace=False))
     d = dict(scene_dict(scene))
     d.update(pose=cam.pose, width=W, height=H, focal=cam.focal, epsilon=epsilon, dirs=dirs,
+             kind=np.array(kind),
              img=img, wsum=wsum, residual=resid, status=status,
              stats=np.array([stats.rays, stats.cells_stepped, stats.neighbor_visits,
                              stats.failed_rays], dtype=np.int64))
@@ -221,12 +222,70 @@ def kat_case():
     print("kat", {k: v for k, v in out.items() if np.size(v) < 4})
 
 
+def adam_case():
+    """train.py:195-209 post-processing + adam.py:15-31 for two iterations
+    (second with the SH warm-up mask off and positions frozen), on
+    fp32-representable gradients so the device's fp32 buffer holds them
+    exactly."""
+    from rfoam.optim.adam import AdamState, adam_step
+
+    rng = np.random.default_rng(21)
+    n = 300
+    pos = rng.uniform(-1, 1, (n, 3))
+    raw = rng.normal(0, 1, n)
+    sh = rng.normal(0, 0.3, (n, 16, 3))
+    out = dict(pos0=pos.copy(), raw0=raw.copy(), sh0=sh.copy())
+    st = [AdamState(pos.shape), AdamState(raw.shape), AdamState(sh.shape)]
+    clip = 1e3
+    for it, (lrs, warm) in enumerate([((2e-4, 1e-1, 5e-3), True), ((0.0, 5e-2, 2e-3), False)]):
+        g_pos = (rng.normal(0, 1, (n, 3)) * 10).astype(np.float32).astype(np.float64)
+        g_sig = (rng.normal(0, 1, n) * 2).astype(np.float32).astype(np.float64)
+        g_sh = rng.normal(0, 1, (n, 16, 3)).astype(np.float32).astype(np.float64)
+        g_pos[0, 0] = 5e3  # exercises the clip
+        g_sh[1, 2, 1] = -2e3
+        out[f"g_pos{it}"], out[f"g_sig{it}"], out[f"g_sh{it}"] = g_pos, g_sig, g_sh
+        out[f"lrs{it}"] = np.array(lrs)
+        out[f"warm{it}"] = np.array(warm)
+        d_raw = g_sig * rfoam_foam.softplus_grad(raw)
+        d_sh = g_sh.copy()
+        if warm:
+            d_sh[:, 1:, :] = 0.0
+        d_pos = g_pos.copy()
+        np.clip(d_raw, -clip, clip, out=d_raw)
+        np.clip(d_sh, -clip, clip, out=d_sh)
+        np.clip(d_pos, -clip, clip, out=d_pos)
+        if lrs[0] > 0.0:
+            adam_step(pos, d_pos, st[0], lrs[0])
+        adam_step(raw, d_raw, st[1], lrs[1])
+        adam_step(sh, d_sh, st[2], lrs[2])
+        out[f"pos{it + 1}"], out[f"raw{it + 1}"], out[f"sh{it + 1}"] = pos.copy(), raw.copy(), sh.copy()
+    np.savez_compressed(os.path.join(HERE, "adam.npz"), **out)
+    print("adam", {k: v.shape for k, v in out.items() if k.startswith("pos")})
+
+
+def checkpoint_case():
+    """A reference-written RFOAM1 file (io/checkpoint.py:18-27)."""
+    from rfoam.io.checkpoint import save_checkpoint
+
+    sc = ref_scene(300, 31, 3, check_delaunay=False)
+    save_checkpoint(sc, os.path.join(HERE, "scene300.rfoam"))
+    np.savez_compressed(os.path.join(HERE, "scene300_expect.npz"),
+                        positions=sc.positions.astype(np.float32).astype(np.float64),
+                        raw=sc.raw_density.astype(np.float32).astype(np.float64),
+                        sh=sc.sh_coeffs.astype(np.float32).astype(np.float64),
+                        background=sc.background.astype(np.float32).astype(np.float64))
+
+
 if __name__ == "__main__":
+    checkpoint_case()
+    adam_case()
     kat_case()
     s2k = ref_scene(2000, 7, 3)
     frame_case("frame_2k_deg3", s2k, (0.0, 0.0, 3.0), 64, 48, 1e-3, seed=1)
     frame_case("frame_2k_deg3_eps0_orbit", s2k, tuple(orbit_poses(np.zeros(3), 3.0, 0.3, 8)[3][:3, 3]),
                40, 32, 0.0, seed=2)
+    frame_case("frame_2k_deg3_fisheye", s2k, (0.3, 0.2, 2.6), 48, 36, 1e-3, seed=5,
+               angle=1.4, kind=FISHEYE)
     s10k = ref_scene(10000, 0, 0, check_delaunay=False)
     frame_case("frame_10k_deg0", s10k, (0.0, 0.0, 3.0), 32, 32, 1e-3, seed=3)
     s3k = ref_scene(3000, 2, 3, kind="surface")

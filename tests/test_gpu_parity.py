@@ -18,6 +18,7 @@ from oracle import oracle as orc
 pytestmark = pytest.mark.gpu
 
 FRAMES = ["frame_2k_deg3", "frame_2k_deg3_eps0_orbit", "frame_10k_deg0", "frame_3k_surface"]
+ALL_FRAMES = FRAMES + ["frame_2k_deg3_fisheye"]
 IMG_TOL = 1e-4
 GRAD_RTOL = 1e-3
 
@@ -84,14 +85,15 @@ def test_render_rays_bit_exact_walk(cuda_ok, name, lanes, packed):
         np.testing.assert_array_equal(t1[q, :L], b[:L])
 
 
-@pytest.mark.parametrize("name", FRAMES)
+@pytest.mark.parametrize("name", ALL_FRAMES)
 def test_render_image_matches_reference(cuda_ok, name):
     from paper_2502_01157_b200 import render
     from paper_2502_01157_b200.camera import PINHOLE, CameraModel
     from paper_2502_01157_b200.render import RenderStats
 
     g = load_golden(name)
-    cam = CameraModel(PINHOLE, int(g["width"]), int(g["height"]), float(g["focal"]), g["pose"])
+    cam = CameraModel(str(g["kind"]), int(g["width"]), int(g["height"]), float(g["focal"]),
+                      g["pose"])
     stats = RenderStats()
     img, wsum, resid = render.render_image(golden_scene(g), cam, epsilon=float(g["epsilon"]),
                                            stats=stats, weight_check=True)
@@ -125,6 +127,11 @@ def test_camera_rays_device_bit_exact(cuda_ok):
     cam = CameraModel(PINHOLE, int(g["width"]), int(g["height"]), float(g["focal"]), g["pose"])
     d = cam.ray_directions_device().cpu().numpy()
     np.testing.assert_array_equal(d, g["dirs"])
+    # fisheye: device sin/cos/hypot, so ~1 ulp instead of bits
+    f = load_golden("frame_2k_deg3_fisheye")
+    cam = CameraModel("fisheye", int(f["width"]), int(f["height"]), float(f["focal"]), f["pose"])
+    d = cam.ray_directions_device().cpu().numpy()
+    assert np.abs(d - f["dirs"]).max() <= 4e-16
 
 
 def test_locate_matches_exact_nearest(cuda_ok):
@@ -252,3 +259,31 @@ def test_flat_kernels_drop_in(cuda_ok):
                   sa.width_floor, 8, rgb, res, st, ws, cnt)
     assert np.abs(rgb.reshape(f["img"].shape) - f["img"]).max() <= IMG_TOL
     assert cnt.sum(0)[0] == f["stats"][1] and cnt.sum(0)[1] == f["stats"][2]
+
+
+def test_checkpoint_to_device_render(cuda_ok):
+    """a reference-written RFOAM1 checkpoint rendered on the
+    device matches the oracle on the same loaded scene."""
+    import os
+
+    from conftest import GOLDEN
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200.camera import PINHOLE, CameraModel, look_at
+    from paper_2502_01157_b200.checkpoint import load_device_scene
+    from paper_2502_01157_b200.scene import softplus
+
+    scene, ds = load_device_scene(os.path.join(GOLDEN, "scene300.rfoam"))
+    assert ds.packed
+    cam = CameraModel.from_angle_x(PINHOLE, 40, 30, 0.9, look_at((0.2, 0.1, 2.8), (0, 0, 0)))
+    res = dv.render_image_device(ds, cam, f64=True, per_ray=True)
+    torch.cuda.synchronize()
+    adj = scene.adjacency
+    sa = orc.SceneArrays(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density),
+                         scene.sh_coeffs.reshape(-1, 48), scene.background)
+    o = cam.position
+    start = int(orc.nearest_sites(sa.positions, o[None, :])[0])
+    t_max = float(np.linalg.norm(o - sa.center) + 2.0 * sa.diagonal + 1.0)
+    ref = orc.render_rays(sa, np.broadcast_to(o, (1200, 3)), cam.ray_directions(), 0.0, t_max,
+                          start)
+    np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
+    assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= IMG_TOL

@@ -110,3 +110,37 @@ def test_shard_rays_partition():
         ranges = [D.shard_rays(m, r, w) for r in range(w)]
         covered = np.concatenate([np.arange(lo, hi) for lo, hi in ranges])
         np.testing.assert_array_equal(covered, np.arange(m))
+
+
+def test_rfoam1_checkpoint_roundtrip(tmp_path):
+    """Reads the reference-written file; writes byte-identical files; rejects
+    corrupt ones (io/checkpoint.py:30-60)."""
+    import os
+
+    from conftest import GOLDEN
+    from paper_2502_01157_b200.checkpoint import (CorruptCheckpoint, load_checkpoint,
+                                                  save_checkpoint)
+
+    path = os.path.join(GOLDEN, "scene300.rfoam")
+    e = load_golden("scene300_expect")
+    sc = load_checkpoint(path, rebuild=True)
+    np.testing.assert_array_equal(sc.positions, e["positions"])
+    np.testing.assert_array_equal(sc.raw_density, e["raw"])
+    np.testing.assert_array_equal(sc.sh_coeffs, e["sh"])
+    np.testing.assert_array_equal(sc.background, e["background"])
+    assert sc.adjacency.offsets[-1] == len(sc.adjacency.neighbors)
+    out = tmp_path / "copy.rfoam"
+    save_checkpoint(sc, out)
+    assert out.read_bytes() == open(path, "rb").read()
+    bad = tmp_path / "bad.rfoam"
+    bad.write_bytes(b"RFOAM2" + out.read_bytes()[6:])
+    with pytest.raises(CorruptCheckpoint):
+        load_checkpoint(bad)
+    bad.write_bytes(out.read_bytes()[:-4])
+    with pytest.raises(CorruptCheckpoint):
+        load_checkpoint(bad)
+    blob = bytearray(out.read_bytes())
+    blob[10:14] = np.array([np.nan], dtype="<f4").tobytes()
+    bad.write_bytes(bytes(blob))
+    with pytest.raises(CorruptCheckpoint):
+        load_checkpoint(bad)
