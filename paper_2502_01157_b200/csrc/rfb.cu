@@ -478,6 +478,8 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
     unsigned int my_cells = 0, my_visits = 0;
     const int64_t total = src.count();
     float *bas = &s_basis[warp][lane][0];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) bas[k] = 0.f;  // rows of idle lanes stay finite (x 0 below)
     bas[16] = 1.0f;
     // reverse-pass output o (two per lane): o < 48 -> dSH[k][ch] = sum f[ch] * basis[k];
     // 48..51 -> (dpos_i xyz, dsigma_i); 52..54 -> dpos_j xyz
@@ -562,6 +564,9 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         // every lane currently in it; the group's 55 gradient values (48 dSH,
         // dpos+dsigma of the cell, dpos of the previously processed cell) are
         // reduced through shared memory and land with coalesced atomics.
+#ifdef RFB_NO_REVERSE  // profiling knob: walk + record only
+        grad_ok = false;
+#endif
         int32_t s = grad_ok ? nseg - 1 : -1;
         int32_t ci = -1, cmask = 0, next_cell = -1;
         double t1 = 0.0, t0 = 0.0;
@@ -585,6 +590,9 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         for (;;) {
             const bool act = s >= 0;
             if (!__any_sync(kFull, act)) break;
+#ifdef RFB_COUNT_ITERS  // profiling knob: O.counters[1] += reverse iterations (per warp)
+            if (lane == 0) atomicAdd(O.counters + 1, 1ull);
+#endif
             const unsigned key = act ? order_key(t0) : 0u;
             const unsigned kmax = __reduce_max_sync(kFull, key);
             const int leader = __ffs(__ballot_sync(kFull, act && key == kmax)) - 1;
@@ -643,15 +651,24 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             float *fr = &s_f[warp][lane][0];
 #pragma unroll
             for (int k = 0; k < 10; ++k) fr[k] = v[k];
-            const unsigned gm = __ballot_sync(kFull, in);
             __syncwarp();
+            // lanes outside the group wrote zeros, so a fixed 32-term sum is the
+            // group sum; unrolled, its shared-memory loads issue back to back
+            // instead of one dependent ffs/load/fma chain per member
+            // (skipping lane quartets with no member: a cell's lanes are a compact
+            // pixel patch, so few quartets are active)
+            const unsigned gm = __ballot_sync(kFull, in);
             float acc0 = 0.f, acc1 = 0.f;
-            unsigned mm = gm;
-            while (mm) {
-                const int l = __ffs(mm) - 1;
-                mm &= mm - 1;
-                acc0 += s_f[warp][l][c0i] * s_basis[warp][l][k0];
-                acc1 += s_f[warp][l][c1i] * s_basis[warp][l][k1];
+#pragma unroll
+            for (int qd = 0; qd < 8; ++qd) {
+                if ((gm >> (4 * qd)) & 0xfu) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int l = 4 * qd + e;
+                        acc0 = __fmaf_rn(s_f[warp][l][c0i], s_basis[warp][l][k0], acc0);
+                        acc1 = __fmaf_rn(s_f[warp][l][c1i], s_basis[warp][l][k1], acc1);
+                    }
+                }
             }
             float *row = gr.sh + 48 * (int64_t)lc;
             atomicAdd(row + o0, acc0);  // dSH, 32 contiguous floats
