@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
@@ -33,6 +34,7 @@ constexpr bool kUseF32Filter = RFB_F32_FILTER != 0;
 // tile list (render.py:128-149 + camera.py:66-92).
 // ---------------------------------------------------------------------------
 struct ArrayRays {
+    static constexpr bool kUniform = false;  // per-ray origins / ranges
     const double *origins, *directions, *t_min, *t_max;
     const int32_t *start;
     int64_t m;
@@ -88,6 +90,7 @@ __device__ __forceinline__ void pinhole_dir(const CameraParams &c, int64_t row, 
 }
 
 struct TileRays {
+    static constexpr bool kUniform = true;  // one camera origin / range for all rays
     CameraParams cam;
     const int32_t *tile_ids;
     int64_t n_tiles;
@@ -95,6 +98,13 @@ struct TileRays {
     double t_min, t_max;
     const int32_t *start_ptr;  // device scalar (located start cell)
     __device__ __forceinline__ int64_t count() const { return n_tiles * tile_w * tile_h; }
+    __device__ __forceinline__ void uniform(double *u) const {
+        u[0] = cam.o[0];
+        u[1] = cam.o[1];
+        u[2] = cam.o[2];
+        u[3] = t_min;
+        u[4] = t_max;
+    }
     // 8x4 sub-tiles inside each tile keep a warp's 32 rays on a compact patch.
     __device__ __forceinline__ int64_t get(int64_t q, Ray &r) const {
         int64_t per = (int64_t)tile_w * tile_h;
@@ -247,8 +257,11 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                                                 int32_t step_limit, FwdOut O,
                                                 unsigned long long *ray_counter) {
     constexpr int RPW = 32 / G;
-    // per thread: the ray's fp64 constants + sum|basis| (field-major, conflict-free)
-    __shared__ double s_ray[9 * 256];
+    // per thread: the ray's fp64 constants + sum|basis| (field-major, conflict-free);
+    // shared-origin sources keep only the direction per thread
+    constexpr int kRayFields = Src::kUniform ? 4 : 9;
+    __shared__ double s_ray[kRayFields * 256];
+    __shared__ double s_uni[5];
     __shared__ float s_basis[kOtfBasis ? 1 : 16 * 256];  // [k][thread] when not on the fly
     // block-level work claiming: the block takes kBlockTile consecutive rays
     // (one 32x32 image tile for rfb_render_image) at a time and its warps
@@ -258,6 +271,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
     if (threadIdx.x == 0) {
         s_lock = 0;
         s_used = kBlockTile;
+        if constexpr (Src::kUniform) src.uniform(s_uni);
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -295,8 +309,11 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
         // the ray's fp64 constants and fp32 SH basis live in shared memory
         // (field-major, conflict-free) to keep registers for the walk: the
         // kernel is occupancy-bound
-        RaySmem<256> r{s_ray + threadIdx.x};
-        double *bsum_p = s_ray + 8 * 256 + threadIdx.x;
+        using RayS = typename std::conditional<Src::kUniform, RaySmemU<256>, RaySmem<256>>::type;
+        RayS r;
+        r.p = s_ray + threadIdx.x;
+        if constexpr (Src::kUniform) r.u = s_uni;
+        double *bsum_p = s_ray + (kRayFields - 1) * 256 + threadIdx.x;
         {
             Ray rr;
             oidx = src.get(q, rr);

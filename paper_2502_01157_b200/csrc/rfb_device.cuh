@@ -270,6 +270,27 @@ struct Ray {
     __device__ __forceinline__ int32_t start() const { return start_; }
 };
 
+// ... or, for a shared-origin camera, only the direction per thread ([3][NT])
+// with origin / t_min / t_max in one block-uniform shared copy.
+template <int NT>
+struct RaySmemU {
+    double *p;        // &s_dir[0][threadIdx.x]
+    const double *u;  // block-uniform {ox, oy, oz, t_min, t_max}
+    __device__ __forceinline__ double ox() const { return u[0]; }
+    __device__ __forceinline__ double oy() const { return u[1]; }
+    __device__ __forceinline__ double oz() const { return u[2]; }
+    __device__ __forceinline__ double dx() const { return p[0 * NT]; }
+    __device__ __forceinline__ double dy() const { return p[1 * NT]; }
+    __device__ __forceinline__ double dz() const { return p[2 * NT]; }
+    __device__ __forceinline__ double t_min() const { return u[3]; }
+    __device__ __forceinline__ double t_max() const { return u[4]; }
+    __device__ __forceinline__ void store(const Ray &r) {
+        p[0 * NT] = r.dx_;
+        p[1 * NT] = r.dy_;
+        p[2 * NT] = r.dz_;
+    }
+};
+
 // ... or parked in shared memory, field-major [8][NT] (conflict-free), so the
 // fp64 ray constants do not occupy registers across the walk.
 template <int NT>
