@@ -292,7 +292,10 @@ def main():
     fb = None
     if not args.no_fwd_bwd:
         cam = views[rank]
-        dirs = cam.ray_directions_device(device=dev)
+        # the view's rays in tile order (4x8 warp patches): the same ray set,
+        # scheduled coherently (dv.tile_order); targets follow the permutation
+        perm = torch.from_numpy(dv.tile_order(W, H)).to(dev)
+        dirs = cam.ray_directions_device(device=dev)[perm].contiguous()
         m = dirs.shape[0]
         origins = torch.from_numpy(np.broadcast_to(cam.position, (m, 3)).copy()).to(dev)
         start = ds.locate(origins[:1]).expand(m).contiguous()
@@ -300,7 +303,7 @@ def main():
         t_max = torch.full((m,), ds.default_t_max(cam.position[None, :]), dtype=torch.float64,
                            device=dev)
         rng = np.random.default_rng(11)
-        targets = torch.from_numpy(rng.uniform(0.0, 1.0, (m, 3))).to(dev)
+        targets = torch.from_numpy(rng.uniform(0.0, 1.0, (m, 3))).to(dev)[perm].contiguous()
         gb = dv.GradBuffers(ds.n_sites, dev)
         loss = torch.zeros(2, dtype=torch.float64, device=dev)
         out_fb = dv.alloc_forward(m, dev, per_ray=True)

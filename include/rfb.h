@@ -55,7 +55,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 5
+#define RFB_ABI_VERSION 6
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
@@ -101,6 +101,8 @@ typedef struct rfb_rays {
     const double *t_min;       /* [m] */
     const double *t_max;       /* [m] */
     const int32_t *start_sites;/* [m] */
+    const int32_t *order;      /* [m] nullable: processing order, a permutation of 0..m-1
+                                  (coherence only; outputs stay indexed by ray id) */
 } rfb_rays;
 
 /* Forward outputs.  rgb/residual/wsum are float32 unless f64_outputs != 0,
@@ -190,7 +192,7 @@ int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t
 int rfb_render_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,
                     const rfb_fwd_out *out, void *workspace, size_t workspace_bytes, void *stream);
 
-/* Renders the listed tile_w x tile_h pixel tiles (tile id = ty * tiles_x + tx,
+/* Renders the listed tile_w x tile_h pixel tiles (multiples of 32) (tile id = ty * tiles_x + tx,
  * tiles_x = ceil(W / tile_w)) of the frame; outputs are full-frame [H*W]
  * arrays indexed by pixel (row-major), untouched outside the listed tiles.
  * start_site < 0: locate the camera position's nearest site on device from

@@ -56,6 +56,7 @@ class rfb_rays(ctypes.Structure):
         ("t_min", ctypes.c_void_p),
         ("t_max", ctypes.c_void_p),
         ("start_sites", ctypes.c_void_p),
+        ("order", ctypes.c_void_p),
     ]
 
 
@@ -146,7 +147,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rfb_abi_version() != 5:
+        if lib.rfb_abi_version() != 6:
             raise ExtensionMissing("librfb.so ABI version mismatch; rebuild")
         if path is None:
             _lib = lib

@@ -15,6 +15,9 @@
 namespace rfb {
 
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef RFB_SUBTILE_W
+#define RFB_SUBTILE_W 4  // a warp's 32 rays cover a 4 x 8 pixel patch (measured best)
+#endif
 constexpr int kBlockTile = 1024;  // rays claimed per block at a time (one 32x32 tile)
 #ifndef RFB_BLOCK_TILES
 #define RFB_BLOCK_TILES 0
@@ -38,9 +41,14 @@ struct ArrayRays {
     const double *origins, *directions, *t_min, *t_max;
     const int32_t *start;
     int64_t m;
+    const int32_t *order;  // optional processing order (a permutation of 0..m-1)
     __device__ __forceinline__ int64_t count() const { return m; }
+    __device__ __forceinline__ int64_t index(int64_t slot) const {
+        return order ? (int64_t)order[slot] : slot;
+    }
     // returns the output index (ray id / pixel) or -1 for a padding slot
-    __device__ __forceinline__ int64_t get(int64_t q, Ray &r) const {
+    __device__ __forceinline__ int64_t get(int64_t slot, Ray &r) const {
+        const int64_t q = index(slot);
         r.ox_ = origins[3 * q];
         r.oy_ = origins[3 * q + 1];
         r.oz_ = origins[3 * q + 2];
@@ -111,9 +119,10 @@ struct TileRays {
         int32_t tile = tile_ids[q / per];
         int32_t p = (int32_t)(q % per);
         int32_t sub = p >> 5, l = p & 31;
-        int32_t subs_x = tile_w >> 3;
-        int32_t px = (tile % tiles_x) * tile_w + (sub % subs_x) * 8 + (l & 7);
-        int32_t py = (tile / tiles_x) * tile_h + (sub / subs_x) * 4 + (l >> 3);
+        constexpr int SW = RFB_SUBTILE_W, SH = 32 / RFB_SUBTILE_W;  // warp patch SW x SH
+        int32_t subs_x = tile_w / SW;
+        int32_t px = (tile % tiles_x) * tile_w + (sub % subs_x) * SW + (l % SW);
+        int32_t py = (tile / tiles_x) * tile_h + (sub / subs_x) * SH + (l / SW);
         if (px >= cam.width || py >= cam.height) return -1;
         r.ox_ = cam.o[0];
         r.oy_ = cam.o[1];
@@ -509,8 +518,9 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         if (lane == 0) base = atomicAdd(ray_counter, 32ull);
         base = __shfl_sync(kFull, base, 0);
         if ((int64_t)base >= total) break;
-        const int64_t q = (int64_t)base + lane;
-        const bool have_ray = q < total;
+        const int64_t qs = (int64_t)base + lane;
+        const bool have_ray = qs < total;
+        const int64_t q = have_ray ? src.index(qs) : 0;  // ray id (optional order)
 
         RaySmem<kTrainBlock> r{s_ray + threadIdx.x};
         int32_t nseg = 0;
@@ -522,7 +532,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             int32_t start;
             {
                 Ray rr;
-                src.get(q, rr);
+                src.get(qs, rr);
                 r.store(rr);
                 start = rr.start_;
                 double bsum = basis_setup(rr, bas);
@@ -1206,7 +1216,7 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
     FwdOut O = dev_out(out);
     ArrayRays src{rays->origins, rays->directions, rays->t_min, rays->t_max, rays->start_sites,
-                  rays->m};
+                  rays->m, rays->order};
     Grads G{grads->site4g, grads->sh};
     double log_eps = p->epsilon > 0.0 ? std::log(p->epsilon) : 0.0;
     dim3 grid((unsigned)(slots / kTrainBlock));
@@ -1357,7 +1367,7 @@ int rfb_render_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_para
     if (!rays->origins || !rays->directions || !rays->t_min || !rays->t_max || !rays->start_sites)
         return RFB_EINVAL;
     ArrayRays src{rays->origins, rays->directions, rays->t_min, rays->t_max, rays->start_sites,
-                  rays->m};
+                  rays->m, rays->order};
     return launch_render(scene, src, params, out, workspace, workspace_bytes,
                          (cudaStream_t)stream);
 }
@@ -1367,7 +1377,7 @@ int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb
                      int64_t n_tiles, int32_t tile_w, int32_t tile_h, const rfb_fwd_out *out,
                      void *workspace, size_t workspace_bytes, void *stream) {
     if (!scene_ok(scene) || !camera || !params || !out_ok(out) || params->step_limit <= 0 ||
-        !tile_ids || n_tiles < 0 || tile_w < 8 || tile_h < 4 || tile_w % 8 || tile_h % 4 ||
+        !tile_ids || n_tiles < 0 || tile_w < 32 || tile_h < 32 || tile_w % 32 || tile_h % 32 ||
         camera->width < 1 || camera->height < 1 || !(camera->focal > 0.0) || camera->kind < 0 ||
         camera->kind > 1 || start_site >= scene->n_sites || !workspace || workspace_bytes < 256)
         return RFB_EINVAL;

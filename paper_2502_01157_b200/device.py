@@ -239,7 +239,7 @@ def fwd_struct(r: ForwardResult) -> _lib.rfb_fwd_out:
     return o
 
 
-def rays_struct(origins, directions, t_min, t_max, start) -> _lib.rfb_rays:
+def rays_struct(origins, directions, t_min, t_max, start, order=None) -> _lib.rfb_rays:
     r = _lib.rfb_rays()
     r.m = origins.shape[0]
     r.origins = origins.data_ptr()
@@ -247,7 +247,16 @@ def rays_struct(origins, directions, t_min, t_max, start) -> _lib.rfb_rays:
     r.t_min = t_min.data_ptr()
     r.t_max = t_max.data_ptr()
     r.start_sites = start.data_ptr()
+    r.order = order.data_ptr() if order is not None else None
     return r
+
+
+def _order32(order, m, device):
+    if order is None:
+        return None
+    o = order.to(device=device, dtype=torch.int32).contiguous()
+    assert o.numel() == m, "order must be a permutation of the m rays"
+    return o
 
 
 def camera_struct(camera) -> _lib.rfb_camera:
@@ -268,13 +277,16 @@ def render_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
                        per_ray=True, seg_capacity=0, lanes_per_ray=DEFAULT_LANES,
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
-                       stream=None) -> ForwardResult:
-    """rfb_render_rays on device tensors (kernels.py:199-247)."""
+                       order=None, stream=None) -> ForwardResult:
+    """rfb_render_rays on device tensors (kernels.py:199-247).  ``order``: an
+    optional processing permutation (e.g. coherent_order) -- outputs stay
+    indexed by ray."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=per_ray, seg_capacity=seg_capacity)
     ws = (workspace or Workspace(ds.device)).get(256)
     p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
-    rays = rays_struct(origins, directions, t_min, t_max, start)
+    order = _order32(order, m, ds.device)
+    rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)
     _lib.check(ds.lib.rfb_render_rays(ds.c, ctypes.byref(rays), ctypes.byref(p), ctypes.byref(o),
                                       _ptr(ws), ws.numel(), _stream(stream)), "rfb_render_rays")
@@ -348,13 +360,14 @@ def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, sta
                          grads: GradBuffers, *, epsilon=DEFAULT_EPSILON,
                          step_limit=DEFAULT_STEP_LIMIT, f64=False,
                          workspace: Workspace | None = None, out: ForwardResult | None = None,
-                         stream=None) -> ForwardResult:
+                         order=None, stream=None) -> ForwardResult:
     """rfb_backward_rays (render.py:152-221 generic adjoint)."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
     p = make_params(epsilon, ds.width_floor, step_limit, 1)
-    rays = rays_struct(origins, directions, t_min, t_max, start)
+    order = _order32(order, m, ds.device)
+    rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)
     g = grads.struct()
     adj = adjoints.to(ds.device, torch.float64).contiguous()
@@ -369,13 +382,14 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        quantile_scale: float = 0.0, u_pairs=None, weight_floor: float = 1e-4,
                        epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
-                       stream=None) -> ForwardResult:
+                       order=None, stream=None) -> ForwardResult:
     """rfb_train_batch (kernels.py:372-453).  ``loss`` float64 [2] accumulates."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
     p = make_params(epsilon, ds.width_floor, step_limit, 1)
-    rays = rays_struct(origins, directions, t_min, t_max, start)
+    order = _order32(order, m, ds.device)
+    rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)
     g = grads.struct()
     n_pairs = 0
@@ -389,3 +403,55 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                                       _ptr(loss), _ptr(ws), ws.numel(), _stream(stream)),
                "rfb_train_batch")
     return res
+
+
+def tile_order(width: int, height: int, tile_w: int = 32, tile_h: int = 32, sub_w: int = 4):
+    """Permutation of row-major pixel indices into the order rfb_render_image
+    walks them (32x32 tiles, each split into sub_w x (32/sub_w) warp patches),
+    so a batch of rays covering a view hands each warp a compact pixel patch
+    (coherent cells: L1 reuse in the walk, large cell groups in the reverse
+    pass).  Returns int64 numpy indices; losses/gradients are order-free."""
+    sub_h = 32 // sub_w
+    tx = (width + tile_w - 1) // tile_w
+    ty = (height + tile_h - 1) // tile_h
+    out = []
+    for t in range(tx * ty):
+        x0, y0 = (t % tx) * tile_w, (t // tx) * tile_h
+        for s in range((tile_w // sub_w) * (tile_h // sub_h)):
+            sx = x0 + (s % (tile_w // sub_w)) * sub_w
+            sy = y0 + (s // (tile_w // sub_w)) * sub_h
+            yy, xx = np.meshgrid(np.arange(sy, sy + sub_h), np.arange(sx, sx + sub_w), indexing="ij")
+            keep = (xx < width) & (yy < height)
+            out.append((yy * width + xx)[keep])
+    return np.concatenate(out).astype(np.int64)
+
+
+def _spread10(x: torch.Tensor) -> torch.Tensor:
+    """Interleave zeros between the low 16 bits (Morton helper)."""
+    x = x & 0xFFFF
+    x = (x | (x << 8)) & 0x00FF00FF
+    x = (x | (x << 4)) & 0x0F0F0F0F
+    x = (x | (x << 2)) & 0x33333333
+    x = (x | (x << 1)) & 0x55555555
+    return x
+
+
+def coherent_order(origins: torch.Tensor, directions: torch.Tensor, bits: int = 10):
+    """Device-side ray sort for large or incoherent batches (e.g. random
+    training pixels, train.py:135-140): key = (origin id, Morton code of the
+    octahedral direction cell), so 32 consecutive rays share a compact patch
+    of directions.  Returns an int32 permutation for the ``order`` argument;
+    it changes only scheduling (outputs stay indexed by ray; gradient sums
+    are order-free up to fp32 summation order)."""
+    d = directions
+    n1 = d.abs().sum(dim=1, keepdim=True)
+    p = d[:, :2] / n1
+    neg = d[:, 2] < 0
+    px = torch.where(neg, (1 - p[:, 1].abs()) * torch.sign(p[:, 0]), p[:, 0])
+    py = torch.where(neg, (1 - p[:, 0].abs()) * torch.sign(p[:, 1]), p[:, 1])
+    q = (1 << bits) - 1
+    ix = ((px * 0.5 + 0.5) * q).clamp(0, q).long()
+    iy = ((py * 0.5 + 0.5) * q).clamp(0, q).long()
+    _, oid = torch.unique(origins, dim=0, return_inverse=True)
+    key = (oid << (2 * bits)) | _spread10(ix) | (_spread10(iy) << 1)
+    return torch.argsort(key).to(torch.int32)

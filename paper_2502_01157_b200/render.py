@@ -161,9 +161,12 @@ def render_ray_batch(scene, origins, directions, t_min=None, t_max=None, start_s
         grid_queries = 0
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
+    # large batches are scheduled in a coherent order (device Morton sort of
+    # directions); results are written per ray, so the order is invisible
+    order = dv.coherent_order(o_d, d_d) if m >= 16384 else None
     res = dv.render_rays_device(ds, o_d, d_d, tmin_d, tmax_d, start_d, epsilon=epsilon,
                                 step_limit=step_limit, f64=True, per_ray=False,
-                                lanes_per_ray=lanes_per_ray)
+                                lanes_per_ray=lanes_per_ray, order=order)
     torch.cuda.synchronize(dev)
     dt = time.perf_counter() - t0
     rgb = res.rgb.cpu().numpy()

@@ -111,3 +111,40 @@ def test_train_100k_gradients(cuda_ok, scene100k):
     assert rel(g4[:, :3], ref["d_pos_w"].sum(0)) <= 1e-3
     assert rel(gb.sh.double().cpu().numpy(), ref["d_sh_w"].sum(0)) <= 1e-3
     np.testing.assert_allclose(loss.cpu().numpy(), ref["loss_w"].sum(0), rtol=1e-5)
+
+
+def test_processing_order_is_invisible(cuda_ok, scene100k):
+    """rfb_rays.order (coherent scheduling) changes nothing per ray: forward
+    outputs bitwise equal; training rgb/status equal and gradients equal up to
+    fp32 summation order."""
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = 128, 96
+    cam = _cam(W, H, 2)
+    ds = dv.DeviceScene(scene100k)
+    dirs = cam.ray_directions_device()
+    m = dirs.shape[0]
+    o = torch.from_numpy(np.broadcast_to(cam.position, (m, 3)).copy()).cuda()
+    start = ds.locate(o[:1]).expand(m).contiguous()
+    tmin = torch.zeros(m, dtype=torch.float64, device="cuda")
+    tmax = torch.full((m,), ds.default_t_max(cam.position[None, :]), dtype=torch.float64,
+                      device="cuda")
+    a = dv.render_rays_device(ds, o, dirs, tmin, tmax, start, f64=True)
+    for order in (dv.coherent_order(o, dirs), torch.randperm(m, device="cuda")):
+        b = dv.render_rays_device(ds, o, dirs, tmin, tmax, start, f64=True, order=order)
+        torch.cuda.synchronize()
+        assert torch.equal(a.rgb, b.rgb) and torch.equal(a.status, b.status)
+        assert torch.equal(a.ray_counters, b.ray_counters)
+    tg = torch.rand((m, 3), dtype=torch.float64, device="cuda")
+    outs = []
+    for order in (None, dv.coherent_order(o, dirs)):
+        gb = dv.GradBuffers(ds.n_sites, ds.device)
+        loss = torch.zeros(2, dtype=torch.float64, device="cuda")
+        r = dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
+                                  rgb_scale=1.0 / (3 * m), f64=True, order=order)
+        torch.cuda.synchronize()
+        outs.append((r.rgb.clone(), gb.flat.clone(), loss.clone()))
+    assert torch.equal(outs[0][0], outs[1][0])
+    g0, g1 = outs[0][1].double(), outs[1][1].double()
+    assert float((g0 - g1).abs().max() / g0.abs().max()) <= 1e-4
+    assert torch.allclose(outs[0][2], outs[1][2], rtol=1e-12)

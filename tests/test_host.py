@@ -144,3 +144,14 @@ def test_rfoam1_checkpoint_roundtrip(tmp_path):
     bad.write_bytes(bytes(blob))
     with pytest.raises(CorruptCheckpoint):
         load_checkpoint(bad)
+
+
+def test_tile_order_is_permutation():
+    from paper_2502_01157_b200.device import tile_order
+
+    for W, H in [(130, 70), (1920, 1080), (32, 32)]:
+        o = tile_order(W, H)
+        np.testing.assert_array_equal(np.sort(o), np.arange(W * H))
+    o = tile_order(64, 32)
+    # first warp = a 4 x 8 pixel patch
+    np.testing.assert_array_equal(o[:8], [0, 1, 2, 3, 64, 65, 66, 67])

@@ -50,7 +50,8 @@ for lanes in [int(x) for x in args.lanes.split(",")]:
     print(f"fwd lanes={lanes:2d}: {ms:8.2f} ms/frame  {m / ms / 1e3:8.2f} Mrays/s", flush=True)
 
 if args.train:
-    dirs = cam.ray_directions_device()
+    perm = torch.from_numpy(dv.tile_order(args.width, args.height)).cuda()
+    dirs = cam.ray_directions_device()[perm].contiguous()
     m = dirs.shape[0]
     o = torch.from_numpy(np.broadcast_to(cam.position, (m, 3)).copy()).cuda()
     start = ds.locate(o[:1]).expand(m).contiguous()
