@@ -425,7 +425,7 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #define RFB_FAST_BOUND 1
 #endif
 #ifndef RFB_F32_UNROLL
-#define RFB_F32_UNROLL 4
+#define RFB_F32_UNROLL 2
 #endif
 #if RFB_MASK32
 typedef unsigned int cand_mask_t;
