@@ -63,7 +63,23 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-row-stride", type=int, default=8)
-    return ap.parse_args()
+    ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5],
+                    help="2: config 2 forward + config 3 fwd+bwd (1M, 1080p; default); "
+                         "4: 3M-site surface foam, one 4K frame tile-sharded over the ranks; "
+                         "5: 3M surface foam, 8 orbit views at 1080p fwd+bwd split over the "
+                         "ranks + NCCL gradient all-reduce")
+    args = ap.parse_args()
+    args.kind = "uniform"
+    if args.config in (4, 5):
+        args.kind = "surface"
+        if args.n_sites == 1_000_000:
+            args.n_sites = 3_000_000
+        if args.seed == 1:
+            args.seed = 2
+    if args.config == 4 and (args.width, args.height) == (1920, 1080):
+        args.width, args.height = 3840, 2160
+        args.cpu_row_stride = max(args.cpu_row_stride, 32)
+    return args
 
 
 def peaks():
@@ -138,6 +154,14 @@ def make_views(n_views, W, H):
             for k in range(n_views)]
 
 
+def orbit_views(W, H, count=8):
+    """orbit_poses(centre 0, r=3, elev 0.3, 8)."""
+    from paper_2502_01157_b200.camera import PINHOLE, CameraModel, orbit_poses
+
+    return [CameraModel.from_angle_x(PINHOLE, W, H, 0.9, p)
+            for p in orbit_poses(np.zeros(3), 3.0, 0.3, count)]
+
+
 def algorithmic_bytes(C, V, N, m, sh_bytes):
     """B_f = 24C + 16V + S_b N + 12 per ray (totals here)."""
     return 24.0 * C + 16.0 * V + sh_bytes * N + 12.0 * m
@@ -163,17 +187,19 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline_measure(args, steps=1, warmup=0, scene=None):
+def cpu_baseline_measure(args, steps=1, warmup=0, scene=None, cam=None):
     from oracle import oracle as orc
     from paper_2502_01157_b200.scene import softplus
     from paper_2502_01157_b200.synthetic import make_foam
 
     if scene is None:
-        scene = make_foam(args.n_sites, args.seed, 3)
+        scene = make_foam(args.n_sites, args.seed, 3, kind=getattr(args, "kind", "uniform"))
     adj = scene.adjacency
     sa = orc.SceneArrays(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density),
                          scene.sh_coeffs.reshape(-1, 48), scene.background)
-    cam = make_views(1, args.width, args.height)[0]
+    if cam is None:
+        cam = (make_views(1, args.width, args.height)[0] if getattr(args, "config", 2) == 2
+               else orbit_views(args.width, args.height, 8)[0])
     rows = np.arange(0, args.height, args.cpu_row_stride)
     rr, cc = np.meshgrid(rows, np.arange(args.width), indexing="ij")
     dirs = cam.ray_directions(rr.reshape(-1), cc.reshape(-1))
@@ -192,7 +218,7 @@ def cpu_baseline_measure(args, steps=1, warmup=0, scene=None):
         times.append(time.perf_counter() - t0)
     dt = float(np.mean(times))
     return {"value": m / dt, "ms_per_step": dt * 1e3, "cores": threads,
-            "sample": f"every {args.cpu_row_stride}th row of the 1920x1080 frame "
+            "sample": f"every {args.cpu_row_stride}th row of the {args.width}x{args.height} frame "
                       f"({m} rays/step, {len(times)} steps, C oracle port, {threads} threads)"}
 
 
@@ -225,10 +251,21 @@ def main():
     W, H = args.width, args.height
     lanes = args.lanes if args.lanes > 0 else dv.DEFAULT_LANES
     t_build = time.perf_counter()
-    scene = make_foam(args.n_sites, args.seed, 3, verbose=(rank == 0))
+    scene = make_foam(args.n_sites, args.seed, 3, kind=args.kind, verbose=(rank == 0))
     ds = dv.DeviceScene(scene, device=dev)
     build_s = time.perf_counter() - t_build
-    views = make_views(world, W, H)
+    scaling = "weak"
+    if args.config == 2:
+        views = make_views(world, W, H)  # one view per rank per step, tile-sharded
+        train_views = [views[rank]]
+    elif args.config == 4:
+        views = orbit_views(W, H, 8)[:1]  # one 4K frame per step, tile-sharded
+        train_views = []
+        scaling = "strong"
+    else:
+        views = orbit_views(W, H, 8)[:1]  # (forward probe only)
+        train_views = orbit_views(W, H, 8)[rank::world]
+        scaling = "strong"
     tx, ty = dv.tile_grid(W, H, 32, 32)
     all_tiles = np.arange(tx * ty, dtype=np.int32)
     my_tiles = torch.from_numpy(all_tiles[rank::world].copy()).to(dev)
@@ -257,7 +294,9 @@ def main():
     bytes_per_frame = algorithmic_bytes(C_tot, V_tot, N_tot, m0, sh_bytes)
 
     # -- forward timing ------------------------------------------------------------
-    for _ in range(args.warmup):
+    if args.config == 5:
+        args.steps_fwd = 0
+    for _ in range(args.warmup if args.config != 5 else 0):
         fwd_step()
     torch.cuda.synchronize()
     barrier()
@@ -273,7 +312,8 @@ def main():
     ev0.record(stream)
     for s in range(args.steps):
         kev[s][0].record(stream)
-        fwd_step()
+        if args.config != 5:
+            fwd_step()
         kev[s][1].record(stream)
     ev1.record(stream)
     torch.cuda.synchronize()
@@ -286,35 +326,40 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     fwd_ms = float(t.item())
     rays_total = args.steps * W * H * len(views)
-    fwd_value = rays_total / (fwd_ms / 1e3)
+    fwd_value = rays_total / max(fwd_ms / 1e3, 1e-12)
 
     # -- fwd+bwd timing (config 3) -------------------------------------------------
     fb = None
-    if not args.no_fwd_bwd:
-        cam = views[rank]
-        # the view's rays in tile order (4x8 warp patches): the same ray set,
-        # scheduled coherently (dv.tile_order); targets follow the permutation
+    if not args.no_fwd_bwd and train_views:
+        # each training view's rays in tile order (4x8 warp patches): the same
+        # ray set, scheduled coherently (dv.tile_order); targets follow it
         perm = torch.from_numpy(dv.tile_order(W, H)).to(dev)
-        dirs = cam.ray_directions_device(device=dev)[perm].contiguous()
-        m = dirs.shape[0]
-        origins = torch.from_numpy(np.broadcast_to(cam.position, (m, 3)).copy()).to(dev)
-        start = ds.locate(origins[:1]).expand(m).contiguous()
-        t_min = torch.zeros(m, dtype=torch.float64, device=dev)
-        t_max = torch.full((m,), ds.default_t_max(cam.position[None, :]), dtype=torch.float64,
-                           device=dev)
         rng = np.random.default_rng(11)
-        targets = torch.from_numpy(rng.uniform(0.0, 1.0, (m, 3))).to(dev)[perm].contiguous()
+        batches = []
+        for cam in train_views:
+            dirs = cam.ray_directions_device(device=dev)[perm].contiguous()
+            m = dirs.shape[0]
+            origins = torch.from_numpy(np.broadcast_to(cam.position, (m, 3)).copy()).to(dev)
+            start = ds.locate(origins[:1]).expand(m).contiguous()
+            t_min = torch.zeros(m, dtype=torch.float64, device=dev)
+            t_max = torch.full((m,), ds.default_t_max(cam.position[None, :]), dtype=torch.float64,
+                               device=dev)
+            targets = torch.from_numpy(rng.uniform(0.0, 1.0, (m, 3))).to(dev)[perm].contiguous()
+            batches.append((origins, dirs, t_min, t_max, start, targets))
+        m = W * H
+        n_train_views = len(train_views) * world if args.config == 2 else 8
         gb = dv.GradBuffers(ds.n_sites, dev)
         loss = torch.zeros(2, dtype=torch.float64, device=dev)
         out_fb = dv.alloc_forward(m, dev, per_ray=True)
-        rgb_scale = 1.0 / (3.0 * m * world)
+        rgb_scale = 1.0 / (3.0 * m * n_train_views)  # global ray count (train.py:168)
         wsb = dv.Workspace(dev)
 
         def fb_step():
             gb.zero_()
             loss.zero_()
-            dv.train_batch_device(ds, origins, dirs, t_min, t_max, start, targets, gb, loss,
-                                  rgb_scale=rgb_scale, workspace=wsb, out=out_fb)
+            for (origins, dirs, t_min, t_max, start, targets) in batches:
+                dv.train_batch_device(ds, origins, dirs, t_min, t_max, start, targets, gb, loss,
+                                      rgb_scale=rgb_scale, workspace=wsb, out=out_fb)
             if world > 1:
                 dist.all_reduce(gb.flat)
                 dist.all_reduce(loss)
@@ -342,12 +387,24 @@ def main():
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         fb_ms = float(t.item())
-        fb = {"value": args.steps * m * world / (fb_ms / 1e3), "unit": UNIT,
+        fb_C = int(out_fb.ray_counters[:, 0].sum().item())
+        fb_V = int(out_fb.ray_counters[:, 1].sum().item())
+        fb_N = int(out_fb.nseg.to(torch.int64).sum().item())
+        fb_bytes = algorithmic_bytes(fb_C, fb_V, fb_N, m, 192 if ds.sh_degree == 3 else 12) \
+            + 12.0 * m + 2.0 * fb_N * (4 + (192 if ds.sh_degree == 3 else 12)) \
+            + 2.0 * max(fb_N - m, 0) * 24  # B_fb, last view's counters
+        fb = {"value": args.steps * m * n_train_views / (fb_ms / 1e3), "unit": UNIT,
               "ms_per_step": fb_ms / args.steps,
-              "workload": "config 3: 1080p forward+backward (L2 adjoint, quantile off), "
-                          "per-site fp32 gradients" + (", NCCL all-reduce" if world > 1 else ""),
+              "workload": ("config 3: 1080p forward+backward (L2 adjoint, quantile off), "
+                           "per-site fp32 gradients" if args.config == 2 else
+                           "config 5: 3M-site surface foam, 8 orbit views at 1080p "
+                           "forward+backward split over the ranks")
+                          + (", NCCL all-reduce" if world > 1 else ""),
+              "views_per_step": n_train_views,
+              "algorithmic_bytes_per_view": fb_bytes,
+              "achieved_GBps": fb_bytes * n_train_views / world / (fb_ms / args.steps / 1e3) / 1e9,
               "cells_per_ray": int(out_fb.ray_counters[:, 0].sum().item()) / m,
-              "loss_rgb": float(loss[0].item()) / (3.0 * m * world),
+              "loss_rgb": float(loss[0].item()) / (3.0 * m * n_train_views),
               "clocks": clocks_fb}
 
     # -- e2e through the public API (rank 0 view, host image out) -----------------
@@ -373,7 +430,7 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
-            cb = cpu_baseline_measure(args, steps=1, warmup=1, scene=scene)
+            cb = cpu_baseline_measure(args, steps=1, warmup=1, scene=scene, cam=views[0])
             cpu = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": "port",
                    "sample": cb["sample"]}
         except Exception as e:  # noqa: BLE001
@@ -381,7 +438,7 @@ def main():
                    "sample": f"failed: {e}"}
 
     peak, peak_kind = peaks()
-    achieved = bytes_per_frame * len(views) / world / (kernel_ms / 1e3) / 1e9
+    achieved = bytes_per_frame * len(views) / world / max(kernel_ms / 1e3, 1e-12) / 1e9
     traffic = None
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
@@ -390,13 +447,28 @@ def main():
                 traffic = json.load(f).get("k_render_dram_bytes_per_launch")
         except Exception:
             traffic = None
+    workload = {
+        2: "config 2: 1M-site foam (seed 1), SH deg 3, 1920x1080 forward render per view, "
+           "camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
+        4: "config 4: 3M-site surface foam (seed 2), SH deg 3, one 3840x2160 frame per step "
+           "from orbit pose 0, 32x32 tiles interleaved over the ranks",
+        5: "config 5: 3M-site surface foam (seed 2), 8 orbit views at 1920x1080 forward+backward "
+           "per step split over the ranks, NCCL all-reduce of the [n,52] gradients",
+    }[args.config]
+    value = fwd_value
+    ms_step = fwd_ms / args.steps
+    if args.config == 5 and fb is not None:
+        value = fb["value"]
+        ms_step = fb["ms_per_step"]
+        achieved = fb["achieved_GBps"]
+        bytes_per_frame = fb["algorithmic_bytes_per_view"]
+        kernel_ms = fb["ms_per_step"] / max(len(train_views), 1)
     out = {
-        "metric": METRIC, "value": fwd_value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": fwd_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (SURVEY.md §8d foam generator; random-init scene, no dataset)",
-        "config": {"workload": "config 2: 1M-site foam (seed 1), SH deg 3, 1920x1080 forward "
-                               "render per view, camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
+        "config": {"workload": workload,
                    "n_sites": args.n_sites, "n_edges": ds.n_edges, "views_per_step": len(views),
                    "tiles": "32x32 interleaved over ranks", "lanes_per_ray": lanes,
                    "l2": "inputs larger than L2 (scene 482 MB vs 126 MB L2); no flush",
@@ -405,10 +477,12 @@ def main():
                    "scene_build_s": round(build_s, 1)},
         "fwd_bwd": fb,
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps * len(views),
+        "gpu_launches": (3 * args.steps * len(views) if args.config != 5
+                         else args.steps * len(train_views)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_render (walk + SH + composite)",
+                     "kernel": "k_render (walk + SH + composite)" if args.config != 5 else
+                               "k_train (walk + composite + reverse pass)",
                      "algorithmic_bytes_per_launch": bytes_per_frame,
                      "launch_ms": kernel_ms},
         "cpu_baseline": cpu,
