@@ -424,8 +424,11 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #ifndef RFB_FAST_BOUND
 #define RFB_FAST_BOUND 1
 #endif
+#ifndef RFB_BRANCHFREE
+#define RFB_BRANCHFREE 1
+#endif
 #ifndef RFB_F32_UNROLL
-#define RFB_F32_UNROLL 2
+#define RFB_F32_UNROLL 4
 #endif
 #if RFB_MASK32
 typedef unsigned int cand_mask_t;
@@ -469,6 +472,25 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
         const float n1 = fabsf(nx) + fabsf(ny) + fabsf(nz);
         const float Ed = 8.0f * u * n1;
 #endif
+#if RFB_BRANCHFREE && RFB_FAST_BOUND
+        // predicated form: every lane evaluates the same instruction stream
+        // (no per-neighbour divergence); back-facing values are computed and
+        // discarded.  Same decisions as the branchy form below.
+        const cand_mask_t bit = nk < kMaskBits ? ((cand_mask_t)1 << nk) : (cand_mask_t)0;
+        const bool back = den < -Ed;
+        const bool sure = den > 2.0f * Ed && den >= 0x1p-100f;
+        const float hx = __fmaf_rn(0.5f, nx, px), hy = __fmaf_rn(0.5f, ny, py),
+                    hz = __fmaf_rn(0.5f, nz, pz);
+        const float num = __fmaf_rn(hz, nz, __fmaf_rn(hy, ny, hx * nx));
+        float rinv;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rinv) : "f"(sure ? den : 1.0f));
+        const float s = num * rinv;
+        const float as = fabsf(s);
+        const float es = __fmaf_rn(K3, as, __fmaf_rn(__fmaf_rn(K2, as, K1), rinv, slack));
+        const bool cand = !back && (!sure || s - es <= U);
+        mask |= cand ? bit : (cand_mask_t)0;
+        U = sure ? fminf(U, s + es) : U;
+#else
         if (den < -Ed) continue;                       // certainly back-facing
         const cand_mask_t bit = nk < kMaskBits ? ((cand_mask_t)1 << nk) : (cand_mask_t)0;
         if (den <= 2.0f * Ed || den < 0x1p-100f) {     // uncertain: exact path
@@ -492,6 +514,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
 #endif
         if (s - es <= U) mask |= bit;
         U = fminf(U, s + es);
+#endif
     }
     const double cx = hdr_f.x, cy = hdr_f.y, cz = hdr_f.z;  // exact widening
     // phase 2: exact fp64 re-evaluation of the candidates, CSR order
