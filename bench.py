@@ -60,6 +60,9 @@ def parse():
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--lanes", type=int, default=0, help="lanes per ray (0 = library default)")
     ap.add_argument("--no-fwd-bwd", action="store_true")
+    ap.add_argument("--quantile", action="store_true",
+                    help="fwd+bwd with the quantile regulariser on (lambda 0.01, P=2 pairs, "
+                         "u_pairs from rng(12); optim/config.py:34-36)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-row-stride", type=int, default=8)
@@ -345,21 +348,25 @@ def main():
             t_max = torch.full((m,), ds.default_t_max(cam.position[None, :]), dtype=torch.float64,
                                device=dev)
             targets = torch.from_numpy(rng.uniform(0.0, 1.0, (m, 3))).to(dev)[perm].contiguous()
-            batches.append((origins, dirs, t_min, t_max, start, targets))
+            u_pairs = (torch.from_numpy(np.random.default_rng(12).uniform(0.0, 1.0, (m, 2, 2)))
+                       .to(dev)[perm].contiguous() if args.quantile else None)
+            batches.append((origins, dirs, t_min, t_max, start, targets, u_pairs))
         m = W * H
         n_train_views = len(train_views) * world if args.config == 2 else 8
         gb = dv.GradBuffers(ds.n_sites, dev)
         loss = torch.zeros(2, dtype=torch.float64, device=dev)
         out_fb = dv.alloc_forward(m, dev, per_ray=True)
         rgb_scale = 1.0 / (3.0 * m * n_train_views)  # global ray count (train.py:168)
+        q_scale = 0.01 / (m * n_train_views * 2) if args.quantile else 0.0  # lambda / (m P)
         wsb = dv.Workspace(dev)
 
         def fb_step():
             gb.zero_()
             loss.zero_()
-            for (origins, dirs, t_min, t_max, start, targets) in batches:
+            for (origins, dirs, t_min, t_max, start, targets, u_pairs) in batches:
                 dv.train_batch_device(ds, origins, dirs, t_min, t_max, start, targets, gb, loss,
-                                      rgb_scale=rgb_scale, workspace=wsb, out=out_fb)
+                                      rgb_scale=rgb_scale, quantile_scale=q_scale,
+                                      u_pairs=u_pairs, workspace=wsb, out=out_fb)
             if world > 1:
                 dist.all_reduce(gb.flat)
                 dist.all_reduce(loss)
@@ -395,10 +402,12 @@ def main():
             + 2.0 * max(fb_N - m, 0) * 24  # B_fb, last view's counters
         fb = {"value": args.steps * m * n_train_views / (fb_ms / 1e3), "unit": UNIT,
               "ms_per_step": fb_ms / args.steps,
-              "workload": ("config 3: 1080p forward+backward (L2 adjoint, quantile off), "
-                           "per-site fp32 gradients" if args.config == 2 else
+              "workload": ("config 3: 1080p forward+backward, per-site fp32 gradients"
+                           if args.config == 2 else
                            "config 5: 3M-site surface foam, 8 orbit views at 1080p "
                            "forward+backward split over the ranks")
+                          + (", L2 adjoint + quantile regulariser (lambda 0.01, P=2)"
+                             if args.quantile else ", L2 adjoint, quantile off")
                           + (", NCCL all-reduce" if world > 1 else ""),
               "views_per_step": n_train_views,
               "algorithmic_bytes_per_view": fb_bytes,

@@ -482,7 +482,44 @@ constexpr int kTrainWarps = kTrainBlock / 32;
 #ifndef RFB_TRAIN_MINB
 #define RFB_TRAIN_MINB 6
 #endif
-template <int SHDEG, bool PACKED, bool TRAIN>
+// Quantile pairs folded into the cooperative reverse pass (the first
+// kQFusedPairs pairs; any further pairs take the per-lane scatter path).
+constexpr int kQFusedPairs = 2;
+constexpr int kQSamples = 2 * kQFusedPairs;
+
+// kernels.py:456-527: locate sample u of one ray's weight CDF -> (t_u, its
+// segment, T(t_u)). `tot` = 1 - T_end.
+struct QHit {
+    double t, T_at, sigma;
+    int32_t seg;
+};
+template <class RayT>
+__device__ __forceinline__ QHit quantile_hit(const double4 *__restrict__ site4, const int32_t *cellp,
+                                             const double *t1p, const double *tbp, int64_t SL,
+                                             int32_t nseg, const RayT &r, double u, double tot) {
+    const double target = u * tot;
+    int32_t sh = 0;
+    while (sh < nseg - 1 && (1.0 - tbp[sh * SL]) < target) sh += 1;
+    QHit h;
+    h.seg = sh;
+    h.sigma = ld_site(site4 + (cellp[sh * SL] & 0x1fffffff)).w;
+    const double ts0 = sh > 0 ? t1p[(sh - 1) * SL] : r.t_min();
+    const double Tbs = sh > 0 ? tbp[(sh - 1) * SL] : 1.0;
+    if (h.sigma <= 0.0) {
+        h.t = ts0;
+    } else {
+        double frac = (target - (1.0 - Tbs)) / Tbs;
+        if (frac > 1.0 - 1e-15) frac = 1.0 - 1e-15;
+        double th = ts0 - log(1.0 - frac) / h.sigma;
+        const double ts1 = t1p[sh * SL];
+        if (th > ts1) th = ts1;
+        h.t = th;
+    }
+    h.T_at = Tbs * exp(-h.sigma * (h.t - ts0));
+    return h;
+}
+
+template <int SHDEG, bool PACKED, bool TRAIN, bool QUANT>
 __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
     SceneView<PACKED> S, ArrayRays src, double epsilon, double log_eps, double width_floor,
     int32_t step_limit, const double *adjoints, const double *targets, double rgb_scale,
@@ -493,6 +530,9 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
     // per lane per reverse iteration: f_r, f_g, f_b, dpos_i xyz, dsigma_i, dpos_j xyz
     __shared__ float s_f[kTrainWarps][32][11];
     __shared__ double s_ray[8 * kTrainBlock];
+    // fused quantile samples, per thread: t_u[a], g_a * T(t_u)[a]
+    __shared__ double s_qt[QUANT ? kQSamples : 1][kTrainBlock];
+    __shared__ double s_qg[QUANT ? kQSamples : 1][kTrainBlock];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t SL = scr.slots;
@@ -586,6 +626,49 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             }
         }
 
+        // ---- quantile samples (kernels.py:456-567), located per lane ---------
+        // The loss gradient of each sample is linear in per-segment and
+        // per-boundary terms (kernels.py:534-566), so the reverse pass below
+        // adds them to the L2 terms of the same segment / boundary: dsigma +=
+        // qA*dt - sum_{t0<t_u} gT*(min(t1,t_u)-t0) and boundary dt +=
+        // (sigma_i - sigma_j) * (qA - sum_{t1<t_u} gT), with qA = sum g*u*T_end.
+        double qA = 0.0;
+        if (QUANT) {
+#pragma unroll
+            for (int a = 0; a < kQSamples; ++a) {
+                s_qt[a][threadIdx.x] = -INFINITY;
+                s_qg[a][threadIdx.x] = 0.0;
+            }
+            if (grad_ok) {
+                const double T_end_q = s_tb[(nseg - 1) * SL];
+                const double tot = 1.0 - T_end_q;
+                const int np = n_pairs < kQFusedPairs ? n_pairs : kQFusedPairs;
+                if (!(tot < weight_floor)) {
+                    for (int32_t p = 0; p < np; ++p) {
+                        const double *up = u_pairs + (q * n_pairs + p) * 2;
+                        const QHit h0 = quantile_hit(S.site4, s_cell, s_t1, s_tb, SL, nseg, r,
+                                                     up[0], tot);
+                        const QHit h1 = quantile_hit(S.site4, s_cell, s_t1, s_tb, SL, nseg, r,
+                                                     up[1], tot);
+                        const double diff = h0.t - h1.t;
+                        loss_q += fabs(diff);
+                        if (diff == 0.0) continue;
+                        const double sign = diff > 0.0 ? 1.0 : -1.0;
+#pragma unroll
+                        for (int a = 0; a < 2; ++a) {
+                            const QHit &h = a == 0 ? h0 : h1;
+                            const double wd = h.T_at * h.sigma;
+                            if (wd <= 1e-300) continue;
+                            const double g = (a == 0 ? sign : -sign) * q_scale / wd;
+                            qA += g * (up[a] * T_end_q);
+                            s_qt[2 * p + a][threadIdx.x] = h.t;
+                            s_qg[2 * p + a][threadIdx.x] = g * h.T_at;
+                        }
+                    }
+                }
+            }
+        }
+
         // ---- cooperative reverse pass (kernels.py:267-337) -------------------
         // Each iteration: the farthest pending segment's cell is processed by
         // every lane currently in it; the group's 55 gradient values (48 dSH,
@@ -599,6 +682,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         double t1 = 0.0, t0 = 0.0;
         float tb1 = 0.f, tb0 = 1.f;
         float Sr = 0.f, Sg = 0.f, Sb = 0.f, d_next = 0.f;
+        double sig_next = 0.0;  // sigma of next_cell (quantile boundary terms)
         auto load_seg = [&]() {
             const int32_t cm = s_cell[s * SL];
             ci = cm & 0x1fffffff;
@@ -630,7 +714,8 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             for (int k = 0; k < 11; ++k) v[k] = 0.f;
             int32_t jn = -1;
             if (in) {
-                const float sig = (float)ld_site(S.site4 + ci).w;
+                const double sig_d = ld_site(S.site4 + ci).w;
+                const float sig = (float)sig_d;
                 const float delta = (float)(t1 - t0);
                 const float w = tb0 - tb1;
                 const float c0 = s_col[(3 * s) * SL], c1 = s_col[(3 * s + 1) * SL],
@@ -639,10 +724,26 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                     ar * (tb1 * c0 - Sr) + ag * (tb1 * c1 - Sg) + ab * (tb1 * c2 - Sb);
                 v[6] = delta * common;
                 const float dd = sig * common;
+                double qdt = 0.0;
+                if (QUANT) {  // kernels.py:534-566 for this segment and boundary s+1
+                    double dq = qA * (t1 - t0), bq = qA;
+#pragma unroll
+                    for (int a = 0; a < kQSamples; ++a) {
+                        const double tu = s_qt[a][threadIdx.x];
+                        if (t0 < tu) {
+                            const double gT = s_qg[a][threadIdx.x];
+                            dq -= gT * ((t1 < tu ? t1 : tu) - t0);
+                            if (t1 < tu) bq -= gT;
+                        }
+                    }
+                    v[6] += (float)dq;
+                    qdt = (sig_d - sig_next) * bq;
+                    sig_next = sig_d;
+                }
                 if (next_cell >= 0) {  // interior boundary s+1 (kernels.py:328-337)
-                    const float dt = dd - d_next;
+                    const double dt = (double)(dd - d_next) + qdt;
                     double gi[3], gj[3];
-                    if (dt != 0.f && face_grad(S.site4, ci, next_cell, r, t1, (double)dt, gi, gj)) {
+                    if (dt != 0.0 && face_grad(S.site4, ci, next_cell, r, t1, dt, gi, gj)) {
                         v[3] = (float)gi[0];
                         v[4] = (float)gi[1];
                         v[5] = (float)gi[2];
@@ -709,60 +810,34 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             __syncwarp();
         }
 
-        // ---- quantile pairs (kernels.py:456-567), per lane ----------------
-        if (TRAIN && q_scale > 0.0 && grad_ok) {
+        // ---- quantile pairs beyond the fused ones: per-lane scatter --------
+        if (QUANT && n_pairs > kQFusedPairs && grad_ok) {
             double T_end_q = s_tb[(nseg - 1) * SL];
             double tot = 1.0 - T_end_q;
             if (!(tot < weight_floor)) {
-                for (int32_t p = 0; p < n_pairs; ++p) {
+                for (int32_t p = kQFusedPairs; p < n_pairs; ++p) {
                     const double *up = u_pairs + (q * n_pairs + p) * 2;
-                    double t_hit[2];
-                    int32_t seg_hit[2];
-                    for (int a = 0; a < 2; ++a) {
-                        double target = up[a] * tot;
-                        int32_t sh_ = 0;
-                        while (sh_ < nseg - 1 && (1.0 - s_tb[sh_ * SL]) < target) sh_ += 1;
-                        int32_t c_ = s_cell[sh_ * SL] & 0x1fffffff;
-                        double si = ld_site(S.site4 + c_).w;
-                        double ts0 = sh_ > 0 ? s_t1[(sh_ - 1) * SL] : r.t_min();
-                        seg_hit[a] = sh_;
-                        if (si <= 0.0) {
-                            t_hit[a] = ts0;
-                            continue;
-                        }
-                        double Tbs = sh_ > 0 ? s_tb[(sh_ - 1) * SL] : 1.0;
-                        double frac = (target - (1.0 - Tbs)) / Tbs;
-                        if (frac > 1.0 - 1e-15) frac = 1.0 - 1e-15;
-                        double th = ts0 - log(1.0 - frac) / si;
-                        double ts1 = s_t1[sh_ * SL];
-                        if (th > ts1) th = ts1;
-                        t_hit[a] = th;
-                    }
-                    double diff = t_hit[0] - t_hit[1];
+                    const QHit hh[2] = {
+                        quantile_hit(S.site4, s_cell, s_t1, s_tb, SL, nseg, r, up[0], tot),
+                        quantile_hit(S.site4, s_cell, s_t1, s_tb, SL, nseg, r, up[1], tot)};
+                    const double diff = hh[0].t - hh[1].t;
                     loss_q += fabs(diff);
                     if (diff == 0.0) continue;
-                    double sign = diff > 0.0 ? 1.0 : -1.0;
+                    const double sign = diff > 0.0 ? 1.0 : -1.0;
                     for (int a = 0; a < 2; ++a) {
-                        double u = up[a];
-                        int32_t sh_ = seg_hit[a];
-                        int32_t c_ = s_cell[sh_ * SL] & 0x1fffffff;
-                        double si = ld_site(S.site4 + c_).w;
-                        double t_u = t_hit[a];
-                        double ts0 = sh_ > 0 ? s_t1[(sh_ - 1) * SL] : r.t_min();
-                        double Tbs = sh_ > 0 ? s_tb[(sh_ - 1) * SL] : 1.0;
-                        double T_at = Tbs * exp(-si * (t_u - ts0));
-                        double wd = T_at * si;
+                        const double u = up[a], t_u = hh[a].t, T_at = hh[a].T_at;
+                        const double wd = T_at * hh[a].sigma;
                         if (wd <= 1e-300) continue;
-                        double g = (a == 0 ? sign : -sign) * q_scale / wd;
+                        const double g = (a == 0 ? sign : -sign) * q_scale / wd;
                         double prev_t1 = r.t_min();
                         for (int32_t k = 0; k < nseg; ++k) {  // kernels.py:534-548
-                            double k_t0 = prev_t1, k_t1 = s_t1[k * SL];
+                            const double k_t0 = prev_t1, k_t1 = s_t1[k * SL];
                             prev_t1 = k_t1;
-                            int32_t ck = s_cell[k * SL] & 0x1fffffff;
-                            double dA = T_end_q * (k_t1 - k_t0);
+                            const int32_t ck = s_cell[k * SL] & 0x1fffffff;
+                            const double dA = T_end_q * (k_t1 - k_t0);
                             double contrib;
                             if (k_t0 < t_u) {
-                                double hi = k_t1 < t_u ? k_t1 : t_u;
+                                const double hi = k_t1 < t_u ? k_t1 : t_u;
                                 contrib = g * (u * dA - T_at * (hi - k_t0));
                             } else {
                                 contrib = g * (u * dA);
@@ -770,13 +845,13 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                             atomicAdd(gr.g4 + 4 * (int64_t)ck + 3, (float)contrib);
                         }
                         for (int32_t mm = 1; mm < nseg; ++mm) {  // kernels.py:552-566
-                            int32_t im = s_cell[(mm - 1) * SL] & 0x1fffffff;
-                            int32_t jm = s_cell[mm * SL] & 0x1fffffff;
-                            double dsig = ld_site(S.site4 + im).w - ld_site(S.site4 + jm).w;
+                            const int32_t im = s_cell[(mm - 1) * SL] & 0x1fffffff;
+                            const int32_t jm = s_cell[mm * SL] & 0x1fffffff;
+                            const double dsig = ld_site(S.site4 + im).w - ld_site(S.site4 + jm).w;
                             if (dsig == 0.0) continue;
-                            double tbq = s_t1[(mm - 1) * SL];
-                            double dW = tbq < t_u ? T_at * dsig : 0.0;
-                            double dt_term = g * (u * (T_end_q * dsig) - dW);
+                            const double tbq = s_t1[(mm - 1) * SL];
+                            const double dW = tbq < t_u ? T_at * dsig : 0.0;
+                            const double dt_term = g * (u * (T_end_q * dsig) - dW);
                             if (dt_term != 0.0)
                                 face_grad_atomic(S.site4, im, jm, r, tbq, dt_term, gr.g4);
                         }
@@ -1156,7 +1231,7 @@ static int64_t bwd_slot_bytes(int32_t step_limit) {
 
 static int64_t bwd_slots_max() {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_train<3, true, true>, kTrainBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_train<3, true, true, true>, kTrainBlock, 0);
     return (int64_t)num_sms() * std::max(per_sm, 1) * kTrainBlock;
 }
 
@@ -1168,14 +1243,19 @@ static void launch_train_p(const rfb_scene *scene, dim3 grid, cudaStream_t st, b
                            const FwdOut &O, const Grads &G, double *loss, const Scratch &scr,
                            unsigned long long *ctr) {
     SceneView<PACKED> S = view<PACKED>(scene);
-#define RFB_TRAIN(SH, TR)                                                                      \
-    k_train<SH, PACKED, TR><<<grid, kTrainBlock, 0, st>>>(S, src, eps, log_eps, wf, sl, adj, tg, \
-                                                          rgb_scale, q_scale, up, np, wfloor, O, \
-                                                          G, loss, scr, ctr)
+#define RFB_TRAIN(SH, TR, QU)                                                                 \
+    k_train<SH, PACKED, TR, QU><<<grid, kTrainBlock, 0, st>>>(                                  \
+        S, src, eps, log_eps, wf, sl, adj, tg, rgb_scale, q_scale, up, np, wfloor, O, G, loss, \
+        scr, ctr)
+    const bool quant = train && q_scale > 0.0;
     if (scene->sh_degree == 0) {
-        if (train) RFB_TRAIN(0, true); else RFB_TRAIN(0, false);
+        if (quant) RFB_TRAIN(0, true, true);
+        else if (train) RFB_TRAIN(0, true, false);
+        else RFB_TRAIN(0, false, false);
     } else {
-        if (train) RFB_TRAIN(3, true); else RFB_TRAIN(3, false);
+        if (quant) RFB_TRAIN(3, true, true);
+        else if (train) RFB_TRAIN(3, true, false);
+        else RFB_TRAIN(3, false, false);
     }
 #undef RFB_TRAIN
 }

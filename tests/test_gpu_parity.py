@@ -287,3 +287,36 @@ def test_checkpoint_to_device_render(cuda_ok):
                           start)
     np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
     assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= IMG_TOL
+
+
+@pytest.mark.parametrize("rgb_scale", [None, 0.0])
+@pytest.mark.parametrize("n_pairs", [1, 2, 3])
+def test_train_batch_quantile_pairs_vs_oracle(cuda_ok, n_pairs, rgb_scale):
+    """Pair counts other than the default P=2: the first two pairs are fused
+    into the reverse pass, any further pairs take the per-lane scatter path;
+    both must agree with kernels.py:456-567 (oracle).  rgb_scale=0 isolates
+    the quantile gradient."""
+    from paper_2502_01157_b200 import device as dv
+
+    g = load_golden("train_2k_deg3_q")
+    sa = golden_scene_arrays(g)
+    m = len(g["origins"])
+    rs = float(g["rgb_scale"]) if rgb_scale is None else rgb_scale
+    up = np.random.default_rng(40 + n_pairs).uniform(0, 1, (m, n_pairs, 2))
+    qs = 0.05 / (m * n_pairs)
+    ref = orc.train_batch(sa, g["origins"], g["dirs"], np.zeros(m), g["t_max"], g["start"],
+                          g["targets"], rs, qs, up, 1e-4,
+                          epsilon=float(g["epsilon"]), threads=8)
+    ds = dv.DeviceScene(golden_scene(g))
+    gb = dv.GradBuffers(ds.n_sites, ds.device)
+    loss = torch.zeros(2, dtype=torch.float64, device="cuda")
+    dv.train_batch_device(ds, _dev(g["origins"]), _dev(g["dirs"]), _dev(np.zeros(m)),
+                          _dev(g["t_max"]), _dev(g["start"], torch.int32), _dev(g["targets"]),
+                          gb, loss, rgb_scale=rs, quantile_scale=qs,
+                          u_pairs=_dev(up), weight_floor=1e-4, epsilon=float(g["epsilon"]))
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(loss.cpu().numpy(), ref["loss_w"].sum(axis=0), rtol=1e-6)
+    g4 = gb.g4.double().cpu().numpy()
+    assert rel_err(g4[:, 3], ref["d_sigma_w"].sum(axis=0)) <= GRAD_RTOL
+    assert rel_err(g4[:, :3], ref["d_pos_w"].sum(axis=0)) <= GRAD_RTOL
+    assert rel_err(gb.sh.double().cpu().numpy(), ref["d_sh_w"].sum(axis=0)) <= GRAD_RTOL

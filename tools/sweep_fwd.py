@@ -26,6 +26,7 @@ ap.add_argument("--train", action="store_true")
 ap.add_argument("--once", action="store_true")
 ap.add_argument("--view", type=int, default=0)
 ap.add_argument("--packed", type=int, default=-1)
+ap.add_argument("--quantile", action="store_true")
 args = ap.parse_args()
 print("lib", os.environ.get("RFB_LIB", "default"), flush=True)
 
@@ -68,8 +69,14 @@ if args.train:
         if r == 1 or (args.once and r == 0):
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-        dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
-                              rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo)
+        if args.quantile:
+            up = torch.rand((m, 2, 2), dtype=torch.float64, device="cuda")
+            dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
+                                  rgb_scale=1.0 / (3 * m), quantile_scale=0.01 / (2 * m),
+                                  u_pairs=up, workspace=wsb, out=fo)
+        else:
+            dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
+                                  rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo)
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / reps
     print(f"train: {ms:8.2f} ms/step  {m / ms / 1e3:8.2f} Mrays/s", flush=True)
