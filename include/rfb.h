@@ -55,7 +55,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 6
+#define RFB_ABI_VERSION 7
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
@@ -73,9 +73,12 @@ typedef struct rfb_scene {
     const int32_t *neighbors; /* [n_edges] ascending per site */
     const double *sh;         /* [n_sites][48], index k*3 + ch (render.py:53) */
     const void *cells;        /* packed: [n_sites] 32-byte headers (nullable) */
-    const void *edges;        /* packed: [n_edges] 16-byte records (nullable) */
+    const void *edges;        /* packed: [n_edges + 1] 16-byte records (nullable); the walk
+                                 reads 32-byte aligned pairs, so the record after the last
+                                 one must be readable (its value is ignored) */
     const void *edge_meta;    /* packed, optional: [n_edges] int2 {k0, k1} of the edge's target */
-    const float *sh32;        /* packed: [n_sites][3][16] fp32 channel-major copy of sh (nullable) */
+    const float *sh32;        /* packed: [n_sites][3][16] fp32 channel-major copy of sh (nullable)
+                                 cells, edges and sh32 must be 32-byte aligned (EINVAL) */
     int32_t packed;           /* 1: use cells/edges/sh32 for the walk */
     float sh_absmax;          /* packed: >= max |sh| over the scene (fp32 colour bound) */
     int32_t sh_degree;        /* 0: read the DC band only (exact when bands 1..15 are

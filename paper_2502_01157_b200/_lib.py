@@ -147,7 +147,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rfb_abi_version() != 6:
+        if lib.rfb_abi_version() != 7:
             raise ExtensionMissing("librfb.so ABI version mismatch; rebuild")
         if path is None:
             _lib = lib

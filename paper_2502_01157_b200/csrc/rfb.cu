@@ -1166,6 +1166,9 @@ static bool scene_ok(const rfb_scene *s) {
         s->n_sites >= (1 << 29) || (s->sh_degree != 0 && s->sh_degree != 3))
         return false;
     if (s->packed && (!s->cells || !s->edges || !s->sh32)) return false;
+    if (s->packed && ((reinterpret_cast<uintptr_t>(s->cells) | reinterpret_cast<uintptr_t>(s->edges) |
+                       reinterpret_cast<uintptr_t>(s->sh32)) & 31u))
+        return false;  // 256-bit loads
     return true;
 }
 

@@ -21,6 +21,10 @@
 
 #include "../../include/rfb.h"
 
+#ifndef RFB_LDG256
+#define RFB_LDG256 1  // 256-bit loads for edge pairs and SH rows (packed layout)
+#endif
+
 namespace rfb {
 
 constexpr int kZeroAdvanceLimit = 32;  // tracer/kernels.py:23
@@ -84,6 +88,15 @@ struct Cell {
 };
 
 // Read-only view of the device scene.  PACKED selects the layout above.
+// 256-bit read-only global load (LDG.E.ENL2.256 on sm_100a): one request
+// for 32 contiguous, 32-byte aligned bytes.
+__device__ __forceinline__ void ldg256(const void *p, float4 &a, float4 &b) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+          "=f"(b.w)
+        : "l"(p));
+}
+
 template <bool PACKED>
 struct SceneView {
     const CellHdr *hdr;     // PACKED
@@ -214,9 +227,18 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
             for (int ch = 0; ch < 3; ++ch) {  // one channel (4 x 16 B) in flight: registers
                 const float4 *r4 = reinterpret_cast<const float4 *>(row + 16 * ch);
                 float a = 0.5f;
+#if RFB_LDG256
+                float4 vv[4];
+                ldg256(r4, vv[0], vv[1]);  // rows are 192 B: 32-byte aligned
+                ldg256(r4 + 2, vv[2], vv[3]);
+#endif
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    float4 v = __ldg(r4 + q);
+#if RFB_LDG256
+                    const float4 v = vv[q];
+#else
+                    const float4 v = __ldg(r4 + q);
+#endif
                     a = __fmaf_rn(basis_f[(4 * q) * BSTRIDE], v.x, a);
                     a = __fmaf_rn(basis_f[(4 * q + 1) * BSTRIDE], v.y, a);
                     a = __fmaf_rn(basis_f[(4 * q + 2) * BSTRIDE], v.z, a);
@@ -430,6 +452,9 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #ifndef RFB_F32_UNROLL
 #define RFB_F32_UNROLL 4
 #endif
+#ifndef RFB_PAIR_UNROLL
+#define RFB_PAIR_UNROLL 2  // edge pairs per unrolled phase-1 iteration (LDG.256 path)
+#endif
 #if RFB_MASK32
 typedef unsigned int cand_mask_t;
 constexpr int kMaskBits = 32;
@@ -463,6 +488,41 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
     cand_mask_t mask = 0;
     const int32_t k0 = c.k0 + gl;
     int32_t nk = 0;
+#if RFB_LDG256 && RFB_BRANCHFREE && RFB_FAST_BOUND
+    if (G == 1) {
+        // Edge records are read as 32-byte aligned pairs starting at k0 & ~1
+        // (one LDG.256 per two neighbours); slots outside [k0, k1) -- the
+        // previous row's last edge, the next row's first, or the record
+        // after the array -- are predicated off.
+        auto visit = [&](const float4 &e, int32_t idx, bool valid) {
+            const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
+            const float den = __fmaf_rn(df[2], nz, __fmaf_rn(df[1], ny, df[0] * nx));
+            const cand_mask_t bit =
+                (valid && idx < kMaskBits) ? ((cand_mask_t)1 << idx) : (cand_mask_t)0;
+            const bool back = !valid || den < -Ed;
+            const bool sure = valid && den > 2.0f * Ed && den >= 0x1p-100f;
+            const float hx = __fmaf_rn(0.5f, nx, px), hy = __fmaf_rn(0.5f, ny, py),
+                        hz = __fmaf_rn(0.5f, nz, pz);
+            const float num = __fmaf_rn(hz, nz, __fmaf_rn(hy, ny, hx * nx));
+            float rinv;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rinv) : "f"(sure ? den : 1.0f));
+            const float s = num * rinv;
+            const float as = fabsf(s);
+            const float es = __fmaf_rn(K3, as, __fmaf_rn(__fmaf_rn(K2, as, K1), rinv, slack));
+            const bool cand = !back && (!sure || s - es <= U);
+            mask |= cand ? bit : (cand_mask_t)0;
+            U = sure ? fminf(U, s + es) : U;
+        };
+        RFB_PRAGMA_UNROLL(RFB_PAIR_UNROLL)
+        for (int32_t kp = c.k0 & ~1; kp < c.k1; kp += 2) {
+            float4 e0, e1;
+            ldg256(S.edge + kp, e0, e1);
+            visit(e0, kp - k0, kp >= k0);
+            visit(e1, kp + 1 - k0, kp + 1 < c.k1);
+        }
+        nk = c.k1 - k0;
+    } else
+#endif
     RFB_PRAGMA_UNROLL(RFB_F32_UNROLL)
     for (int32_t k = k0; k < c.k1; k += G, ++nk) {
         const float4 e = __ldg(S.edge + k);

@@ -100,8 +100,8 @@ class DeviceScene:
             self.sh = torch.from_numpy(sh).to(dev)
             if self.packed:
                 self.cells = torch.empty((n, 8), dtype=torch.int32, device=dev)      # 32 B headers
-                self.edges = torch.empty((max(self.n_edges, 1), 4), dtype=torch.float32,
-                                         device=dev)                                # 16 B records
+                # 16 B records + one readable pad record (the walk loads aligned pairs)
+                self.edges = torch.zeros((self.n_edges + 1, 4), dtype=torch.float32, device=dev)
                 self.edge_meta = None  # optional {k0, k1} per edge (unused by the walk)
                 self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
             else:
