@@ -502,7 +502,7 @@ __device__ __forceinline__ QHit quantile_hit(const double4 *__restrict__ site4, 
     while (sh < nseg - 1 && (1.0 - tbp[sh * SL]) < target) sh += 1;
     QHit h;
     h.seg = sh;
-    h.sigma = ld_site(site4 + (cellp[sh * SL] & 0x1fffffff)).w;
+    h.sigma = ld_sigma(site4 + (cellp[sh * SL] & 0x1fffffff));
     const double ts0 = sh > 0 ? t1p[(sh - 1) * SL] : r.t_min();
     const double Tbs = sh > 0 ? tbp[(sh - 1) * SL] : 1.0;
     if (h.sigma <= 0.0) {
@@ -714,7 +714,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             for (int k = 0; k < 11; ++k) v[k] = 0.f;
             int32_t jn = -1;
             if (in) {
-                const double sig_d = ld_site(S.site4 + ci).w;
+                const double sig_d = ld_sigma(S.site4 + ci);
                 const float sig = (float)sig_d;
                 const float delta = (float)(t1 - t0);
                 const float w = tb0 - tb1;
@@ -764,7 +764,15 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 d_next = dd;
                 next_cell = ci;
                 s -= 1;
-                if (s >= 0) load_seg();
+                if (s >= 0) {  // segment s's end is segment s+1's start: reuse it
+                    const int32_t cm = s_cell[s * SL];
+                    ci = cm & 0x1fffffff;
+                    cmask = (cm >> 29) & 7;
+                    t1 = t0;
+                    tb1 = tb0;
+                    t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min();
+                    tb0 = s > 0 ? (float)s_tb[(s - 1) * SL] : 1.f;
+                }
             }
             // previous cell: aggregated when the whole group agrees on it
             const int32_t jany = __reduce_max_sync(kFull, in ? jn : -1);
@@ -847,7 +855,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                         for (int32_t mm = 1; mm < nseg; ++mm) {  // kernels.py:552-566
                             const int32_t im = s_cell[(mm - 1) * SL] & 0x1fffffff;
                             const int32_t jm = s_cell[mm * SL] & 0x1fffffff;
-                            const double dsig = ld_site(S.site4 + im).w - ld_site(S.site4 + jm).w;
+                            const double dsig = ld_sigma(S.site4 + im) - ld_sigma(S.site4 + jm);
                             if (dsig == 0.0) continue;
                             const double tbq = s_t1[(mm - 1) * SL];
                             const double dW = tbq < t_u ? T_at * dsig : 0.0;

@@ -24,6 +24,9 @@
 #ifndef RFB_LDG256
 #define RFB_LDG256 1  // 256-bit loads for edge pairs and SH rows (packed layout)
 #endif
+#ifndef RFB_HDR256
+#define RFB_HDR256 0  // one 256-bit load per cell header
+#endif
 
 namespace rfb {
 
@@ -66,9 +69,21 @@ __device__ __forceinline__ void sh_basis(double dx, double dy, double dz, double
 
 // 32-byte read-only record load (two 16-byte vector loads).
 __device__ __forceinline__ double4 ld_site(const double4 *p) {
+#if RFB_LDG256
+    double4 v;  // one 256-bit request (site4 rows are 32-byte aligned)
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+        : "l"(p));
+    return v;
+#else
     const double2 *q = reinterpret_cast<const double2 *>(p);
     double2 a = __ldg(q), b = __ldg(q + 1);
     return make_double4(a.x, a.y, b.x, b.y);
+#endif
+}
+// sigma only (site4[i].w)
+__device__ __forceinline__ double ld_sigma(const double4 *p) {
+    return __ldg(reinterpret_cast<const double *>(p) + 3);
 }
 
 struct CellHdr {  // packed layout, 32 bytes
@@ -118,10 +133,16 @@ struct SceneView {
         Cell c;
         if (PACKED) {
             const float4 *p = reinterpret_cast<const float4 *>(hdr + i);
+#if RFB_HDR256
+            float4 a, b4;
+            ldg256(p, a, b4);  // whole 32-byte header in one request (sigma unused here)
+            const float2 b = make_float2(b4.z, b4.w);
+#else
             float4 a = __ldg(p);
+            const float2 b = __ldg(reinterpret_cast<const float2 *>(p + 1) + 1);
+#endif
             c.hf = a;
             c.k0 = __float_as_int(a.w);
-            const float2 b = __ldg(reinterpret_cast<const float2 *>(p + 1) + 1);
             c.k1 = __float_as_int(b.x);
             c.n1max = b.y;
         } else {
