@@ -18,6 +18,8 @@
  *                        shim uploads the host numpy value instead)
  *   rfb_camera_rays     tracer/camera.py:66-92      CameraModel.ray_directions()
  *                        (pinhole and fisheye)
+ *   rfb_effect_rays     tracer/rays.py:123-176      EffectPlane/reflect/refract/
+ *                        apply_effect, batched
  *   rfb_locate          geometry/adjacency.py:85-100 nearest_site()
  *                        (greedy walk on the CSR; same distance expression
  *                        and lowest-id tie rule as _grid_nearest 140-203)
@@ -187,6 +189,18 @@ int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const dou
 /* dirs [pix_count][3] f64 for row-major pixels pix_begin .. pix_begin+count-1. */
 int rfb_camera_rays(const rfb_camera *camera, int64_t pix_begin, int64_t pix_count,
                     double *dirs, void *stream);
+
+/* Effect rays (tracer/rays.py:123-176 EffectPlane / reflect / refract /
+ * apply_effect): ray q continues from origins[q] + t_at[q] * directions[q]
+ * with the mirrored (kind RFB_EFFECT_MIRROR) or refracted (RFB_EFFECT_REFRACT,
+ * relative index eta, total internal reflection -> mirror, back side -> flipped
+ * normal and 1/eta) unit direction.  normal (host, 3 doubles) need not be
+ * unit length.  New rays start at t_min = 0 with the old t_max. */
+#define RFB_EFFECT_MIRROR 0
+#define RFB_EFFECT_REFRACT 1
+int rfb_effect_rays(const double *origins, const double *directions, const double *t_at,
+                    int64_t m, const double *normal, int32_t kind, double eta,
+                    double *out_origins, double *out_directions, void *stream);
 
 /* out[q] = nearest site to queries[q] (greedy CSR walk from seed_site). */
 int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t seed_site,

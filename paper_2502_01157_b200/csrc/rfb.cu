@@ -959,6 +959,61 @@ __global__ void k_camera_rays(CameraParams cam, int64_t begin, int64_t count, do
     dirs[3 * k + 2] = dz;
 }
 
+// rays.py:139-176: continue rays across an effect plane (mirror / Snell
+// refraction with total internal reflection falling back to the mirror).
+__device__ __forceinline__ void reflect_dir(double dx, double dy, double dz, double nx, double ny,
+                                            double nz, double *o) {
+    const double dn = dx * nx + dy * ny + dz * nz;
+    o[0] = dx - 2.0 * dn * nx;
+    o[1] = dy - 2.0 * dn * ny;
+    o[2] = dz - 2.0 * dn * nz;
+}
+
+__global__ void k_effect_rays(const double *origins, const double *dirs, const double *t_at,
+                              int64_t m, double nx, double ny, double nz, int32_t kind, double eta,
+                              double *out_o, double *out_d) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const double dx = dirs[3 * i], dy = dirs[3 * i + 1], dz = dirs[3 * i + 2];
+    const double t = t_at[i];
+    double o[3];
+    if (kind == 0) {
+        reflect_dir(dx, dy, dz, nx, ny, nz, o);
+    } else {
+        double cos_i = -(dx * nx + dy * ny + dz * nz);
+        double ex = eta;
+        if (cos_i < 0.0) {  // back side: flip the normal, invert the ratio (rays.py:153-155)
+            nx = -nx;
+            ny = -ny;
+            nz = -nz;
+            ex = 1.0 / eta;
+            cos_i = -(dx * nx + dy * ny + dz * nz);
+        }
+        const double ratio = 1.0 / ex;
+        const double sin2_t = ratio * ratio * (1.0 - cos_i * cos_i);
+        if (sin2_t > 1.0) {
+            reflect_dir(dx, dy, dz, nx, ny, nz, o);
+        } else {
+            const double cos_t = sqrt(1.0 - sin2_t);
+            const double c = ratio * cos_i - cos_t;
+            o[0] = ratio * dx + c * nx;
+            o[1] = ratio * dy + c * ny;
+            o[2] = ratio * dz + c * nz;
+            const double l = sqrt(o[0] * o[0] + o[1] * o[1] + o[2] * o[2]);
+            o[0] /= l;
+            o[1] /= l;
+            o[2] /= l;
+        }
+    }
+    const double l = sqrt(o[0] * o[0] + o[1] * o[1] + o[2] * o[2]);  // apply_effect renormalises
+    out_d[3 * i] = o[0] / l;
+    out_d[3 * i + 1] = o[1] / l;
+    out_d[3 * i + 2] = o[2] / l;
+    out_o[3 * i] = origins[3 * i] + t * dx;
+    out_o[3 * i + 1] = origins[3 * i + 1] + t * dy;
+    out_o[3 * i + 2] = origins[3 * i + 2] + t * dz;
+}
+
 struct LocScene {
     const double4 *site4;
     const int32_t *off, *nbr;
@@ -1427,6 +1482,20 @@ int rfb_camera_rays(const rfb_camera *camera, int64_t pix_begin, int64_t pix_cou
     if (pix_count == 0) return RFB_OK;
     k_camera_rays<<<(unsigned)((pix_count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         cam_params(camera), pix_begin, pix_count, dirs);
+    return (int)cudaGetLastError();
+}
+
+int rfb_effect_rays(const double *origins, const double *directions, const double *t_at,
+                    int64_t m, const double *normal, int32_t kind, double eta,
+                    double *out_origins, double *out_directions, void *stream) {
+    if (m < 0 || !normal || (kind != RFB_EFFECT_MIRROR && kind != RFB_EFFECT_REFRACT)) return RFB_EINVAL;
+    if (m == 0) return RFB_OK;
+    if (!origins || !directions || !t_at || !out_origins || !out_directions) return RFB_EINVAL;
+    const double l = std::sqrt(normal[0] * normal[0] + normal[1] * normal[1] + normal[2] * normal[2]);
+    if (!(l > 0.0)) return RFB_EINVAL;  // EffectPlane normalises (rays.py:135)
+    k_effect_rays<<<(unsigned)((m + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        origins, directions, t_at, m, normal[0] / l, normal[1] / l, normal[2] / l, kind, eta,
+        out_origins, out_directions);
     return (int)cudaGetLastError();
 }
 

@@ -162,6 +162,30 @@ class DeviceScene:
         return out
 
 
+EFFECT_KINDS = {"mirror": 0, "reflect": 0, "refract": 1}
+
+
+def effect_rays_device(origins, directions, t_at, normal, effect="mirror", eta=1.5, stream=None):
+    """Batched apply_effect (rays.py:166-176) on the device: every ray
+    continues from origin + t_at * direction across one effect plane with
+    normal `normal`.  Returns (origins', directions') fp64 [m, 3]; the new rays
+    start at t_min = 0 with the old t_max."""
+    if effect not in EFFECT_KINDS:
+        raise ValueError(f"unknown effect {effect!r}")
+    lib = _lib.load()
+    o = origins.to(torch.float64).contiguous()
+    d = directions.to(o.device, torch.float64).contiguous()
+    m = o.shape[0]
+    t = torch.as_tensor(t_at, dtype=torch.float64, device=o.device).expand(m).contiguous()
+    n = (ctypes.c_double * 3)(*[float(v) for v in np.asarray(normal, dtype=np.float64)])
+    oo = torch.empty_like(o)
+    od = torch.empty_like(d)
+    _lib.check(lib.rfb_effect_rays(_ptr(o), _ptr(d), _ptr(t), m, n, EFFECT_KINDS[effect],
+                                   float(eta), _ptr(oo), _ptr(od), _stream(stream)),
+               "rfb_effect_rays")
+    return oo, od
+
+
 def make_params(epsilon=DEFAULT_EPSILON, width_floor=0.0, step_limit=DEFAULT_STEP_LIMIT,
                 lanes_per_ray=DEFAULT_LANES):
     p = _lib.rfb_params()

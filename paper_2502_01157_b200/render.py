@@ -11,6 +11,9 @@ kernel arrays on every call too, render.py:49-54).
   render_image                render.py:128-149
   render_rays_with_gradients  render.py:152-221
   trace                       rays.py:81-115
+  intersect_face              rays.py:60-78
+  EffectPlane, reflect, refract, apply_effect   rays.py:123-176 (single ray,
+                              host; effect_rays() is the batched device form)
   RenderStats                 render.py:27-46
 """
 
@@ -98,6 +101,82 @@ class RaySegments:
     def midpoints(self, ray):
         mid = 0.5 * (self.t_entry + self.t_exit)
         return ray.origin[None, :] + mid[:, None] * ray.direction[None, :]
+
+
+def intersect_face(ray, x, x_prime):
+    """rays.py:60-78: depth of the bisector-plane crossing between sites x and
+    x' and whether the face is a candidate exit of x's cell."""
+    x = np.asarray(x, dtype=np.float64)
+    xp = np.asarray(x_prime, dtype=np.float64)
+    if np.array_equal(x, xp):
+        raise ValueError("sites coincide; no bisector plane")
+    n = xp - x
+    denom = float(ray.direction @ n)
+    if denom == 0.0:
+        return np.inf, False
+    return float((0.5 * (x + xp) - ray.origin) @ n) / denom, denom > 0.0
+
+
+@dataclass
+class EffectPlane:
+    """rays.py:123-136: a tagged interface for mirror / refraction effects."""
+    point: np.ndarray
+    normal: np.ndarray
+    kind: str = "mirror"
+    eta: float = 1.5
+
+    def __post_init__(self):
+        self.point = np.asarray(self.point, dtype=np.float64)
+        self.normal = np.asarray(self.normal, dtype=np.float64)
+        self.normal = self.normal / np.linalg.norm(self.normal)
+        if self.kind not in ("mirror", "refract"):
+            raise ValueError(f"unknown effect kind {self.kind!r}")
+
+
+def reflect(direction, normal):
+    """rays.py:139-142."""
+    d = np.asarray(direction, dtype=np.float64)
+    n = np.asarray(normal, dtype=np.float64)
+    return d - 2.0 * float(d @ n) * n
+
+
+def refract(direction, normal, eta):
+    """rays.py:145-163: Snell refraction into a medium of relative index eta;
+    the back side flips the normal and inverts the ratio, total internal
+    reflection falls back to the mirror direction."""
+    d = np.asarray(direction, dtype=np.float64)
+    n = np.asarray(normal, dtype=np.float64)
+    cos_i = float(-d @ n)
+    if cos_i < 0.0:
+        n, eta = -n, 1.0 / eta
+        cos_i = float(-d @ n)
+    ratio = 1.0 / eta
+    sin2_t = ratio * ratio * (1.0 - cos_i * cos_i)
+    if sin2_t > 1.0:
+        return reflect(d, n)
+    out = ratio * d + (ratio * cos_i - np.sqrt(1.0 - sin2_t)) * n
+    return out / np.linalg.norm(out)
+
+
+def apply_effect(ray, normal, effect, eta=1.5, at_t=0.0):
+    """rays.py:166-176: continue `ray` across an effect interface at depth at_t."""
+    if effect in ("reflect", "mirror"):
+        d = reflect(ray.direction, normal)
+    elif effect == "refract":
+        d = refract(ray.direction, normal, eta)
+    else:
+        raise ValueError(f"unknown effect {effect!r}")
+    return Ray(ray.at(at_t), d / np.linalg.norm(d), 0.0, ray.t_max)
+
+
+def effect_rays(origins, directions, t_at, normal, effect="mirror", eta=1.5):
+    """Batched apply_effect for host arrays through librfb (rfb_effect_rays):
+    (m,3) origins/directions, (m,) or scalar t_at -> new (origins, directions)."""
+    o = torch.from_numpy(np.ascontiguousarray(origins, dtype=np.float64).reshape(-1, 3)).cuda()
+    d = torch.from_numpy(np.ascontiguousarray(directions, dtype=np.float64).reshape(-1, 3)).cuda()
+    oo, od = dv.effect_rays_device(o, d, torch.as_tensor(t_at, dtype=torch.float64).cuda(),
+                                   normal, effect, eta)
+    return oo.cpu().numpy(), od.cpu().numpy()
 
 
 def _default_t_max(adj, ray):

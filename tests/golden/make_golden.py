@@ -276,7 +276,45 @@ def checkpoint_case():
                         background=sc.background.astype(np.float32).astype(np.float64))
 
 
+def effects_case():
+    """rays.py:60-176: intersect_face, reflect, refract (incl. back side and
+    total internal reflection) and apply_effect on random unit vectors."""
+    from rfoam.tracer.rays import EffectPlane, apply_effect, reflect, refract
+
+    rng = np.random.default_rng(77)
+    m = 64
+    d = rng.normal(size=(m, 3))
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    o = rng.uniform(-1, 1, (m, 3))
+    nr = rng.normal(size=(m, 3))
+    nrm = np.stack([EffectPlane(np.zeros(3), v).normal for v in nr])
+    eta = np.where(np.arange(m) % 2 == 0, 1.5, 1.0 / 1.5)
+    t_at = rng.uniform(0, 2, m)
+    out = {"d": d, "o": o, "normal": nrm, "eta": eta, "t_at": t_at}
+    out["reflect"] = np.stack([reflect(d[i], nrm[i]) for i in range(m)])
+    out["refract"] = np.stack([refract(d[i], nrm[i], eta[i]) for i in range(m)])
+    for kind in ("mirror", "refract"):
+        rs = [apply_effect(Ray(o[i], d[i], 0.0, 9.0), nrm[i], kind, eta[i], t_at[i])
+              for i in range(m)]
+        out[f"{kind}_o"] = np.stack([r.origin for r in rs])
+        out[f"{kind}_d"] = np.stack([r.direction for r in rs])
+    xs, xps = rng.uniform(-1, 1, (m, 3)), rng.uniform(-1, 1, (m, 3))
+    xps[0] = xs[0] + np.cross(d[0], [0.0, 0.0, 1.0])  # face parallel to the ray
+    f = [intersect_face(Ray(o[i], d[i]), xs[i], xps[i]) for i in range(m)]
+    out.update(x=xs, xp=xps, face_t=np.array([v[0] for v in f]),
+               face_front=np.array([v[1] for v in f]))
+    tir = sum(1 for i in range(m) if np.allclose(out["refract"][i], out["reflect"][i] /
+                                                 np.linalg.norm(out["reflect"][i])))
+    np.savez_compressed(os.path.join(HERE, "effects.npz"), **out)
+    print("effects", m, "tir/mirror-equal", tir)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate only the named cases, e.g. `effects`
+        for name in sys.argv[1:]:
+            globals()[f"{name}_case"]()
+        sys.exit(0)
+    effects_case()
     checkpoint_case()
     adam_case()
     kat_case()

@@ -320,3 +320,25 @@ def test_train_batch_quantile_pairs_vs_oracle(cuda_ok, n_pairs, rgb_scale):
     assert rel_err(g4[:, 3], ref["d_sigma_w"].sum(axis=0)) <= GRAD_RTOL
     assert rel_err(g4[:, :3], ref["d_pos_w"].sum(axis=0)) <= GRAD_RTOL
     assert rel_err(gb.sh.double().cpu().numpy(), ref["d_sh_w"].sum(axis=0)) <= GRAD_RTOL
+
+
+@pytest.mark.parametrize("kind", ["mirror", "refract"])
+def test_effect_rays_device(cuda_ok, kind):
+    """rfb_effect_rays (batched apply_effect, rays.py:166-176) vs the
+    reference's per-ray outputs, one plane per launch."""
+    from paper_2502_01157_b200 import device as dv
+
+    g = load_golden("effects")
+    for i in range(0, len(g["d"]), 7):
+        sel = [i]
+        oo, od = dv.effect_rays_device(_dev(g["o"][sel]), _dev(g["d"][sel]), _dev(g["t_at"][sel]),
+                                       g["normal"][i], kind, float(g["eta"][i]))
+        np.testing.assert_allclose(oo.cpu().numpy()[0], g[f"{kind}_o"][i], rtol=0, atol=1e-15)
+        np.testing.assert_allclose(od.cpu().numpy()[0], g[f"{kind}_d"][i], rtol=0, atol=1e-14)
+    # a batch sharing one plane
+    n = g["normal"][3]
+    oo, od = dv.effect_rays_device(_dev(g["o"]), _dev(g["d"]), _dev(g["t_at"]), n, kind, 1.5)
+    from paper_2502_01157_b200 import render as rd
+    for i in range(len(g["d"])):
+        r = rd.apply_effect(rd.Ray(g["o"][i], g["d"][i], 0.0, 9.0), n, kind, 1.5, g["t_at"][i])
+        np.testing.assert_allclose(od.cpu().numpy()[i], r.direction, rtol=0, atol=1e-14)

@@ -155,3 +155,28 @@ def test_tile_order_is_permutation():
     o = tile_order(64, 32)
     # first warp = a 4 x 8 pixel patch
     np.testing.assert_array_equal(o[:8], [0, 1, 2, 3, 64, 65, 66, 67])
+
+
+def test_effect_rays_host_match_reference():
+    """render.reflect / refract / apply_effect / intersect_face against the
+    reference's own outputs (tests/golden/effects.npz, rays.py:60-176)."""
+    from paper_2502_01157_b200 import render as rd
+
+    g = load_golden("effects")
+    m = len(g["d"])
+    for i in range(m):
+        np.testing.assert_array_equal(rd.reflect(g["d"][i], g["normal"][i]), g["reflect"][i])
+        np.testing.assert_allclose(rd.refract(g["d"][i], g["normal"][i], g["eta"][i]),
+                                   g["refract"][i], rtol=0, atol=1e-15)
+        for kind in ("mirror", "refract"):
+            r = rd.apply_effect(rd.Ray(g["o"][i], g["d"][i], 0.0, 9.0), g["normal"][i], kind,
+                                g["eta"][i], g["t_at"][i])
+            np.testing.assert_array_equal(r.origin, g[f"{kind}_o"][i])
+            np.testing.assert_allclose(r.direction, g[f"{kind}_d"][i], rtol=0, atol=1e-15)
+            assert r.t_min == 0.0 and r.t_max == 9.0
+        t, front = rd.intersect_face(rd.Ray(g["o"][i], g["d"][i]), g["x"][i], g["xp"][i])
+        assert t == g["face_t"][i] and front == g["face_front"][i]
+    with pytest.raises(ValueError):
+        rd.EffectPlane(np.zeros(3), np.ones(3), kind="lens")
+    with pytest.raises(ValueError):
+        rd.intersect_face(rd.Ray(np.zeros(3), np.array([0.0, 0.0, 1.0])), np.ones(3), np.ones(3))
