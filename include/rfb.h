@@ -20,6 +20,9 @@
  *                        (pinhole and fisheye)
  *   rfb_effect_rays     tracer/rays.py:123-176      EffectPlane/reflect/refract/
  *                        apply_effect, batched
+ *   rfb_build_adjacency geometry/delaunay.py:445-520 build() +
+ *                        adjacency.py:46-64 from_triangulation() (Voronoi
+ *                        cell clipping on the GPU; rfb_adjacency.cu)
  *   rfb_locate          geometry/adjacency.py:85-100 nearest_site()
  *                        (greedy walk on the CSR; same distance expression
  *                        and lowest-id tie rule as _grid_nearest 140-203)
@@ -52,6 +55,8 @@ extern "C" {
 
 #define RFB_OK 0
 #define RFB_EINVAL (-1)
+#define RFB_ECAPACITY (-2)   /* a caller-sized buffer / row capacity is too small */
+#define RFB_EDEGENERATE (-3) /* non-finite, duplicate or degenerate input points */
 
 #define RFB_STATUS_OK 0
 #define RFB_STATUS_STEP_LIMIT 2
@@ -201,6 +206,28 @@ int rfb_camera_rays(const rfb_camera *camera, int64_t pix_begin, int64_t pix_cou
 int rfb_effect_rays(const double *origins, const double *directions, const double *t_at,
                     int64_t m, const double *normal, int32_t kind, double eta,
                     double *out_origins, double *out_directions, void *stream);
+
+/* Delaunay adjacency on the device (geometry/delaunay.py:445-520 build +
+ * geometry/adjacency.py:46-64 from_triangulation): per-site Voronoi cell
+ * clipping, one warp per site.  positions [n][3] f64 (device).  Writes
+ * offsets [n+1] (int64, device) and, when neighbors is non-NULL and
+ * neighbor_capacity >= the edge count, the ascending symmetric neighbour
+ * lists (int64) and hull flags (uint8, nullable).  stats (host, 8 int64):
+ * [0] directed edge count E, [1] reverse edges added by the symmetrisation,
+ * [2] sites that needed the ring scan, [3] max cell vertices, [4] max
+ * planes.  With neighbors == NULL the call is a size query: allocate E and
+ * finish with rfb_adjacency_emit on the same workspace.  max_degree <= 128
+ * is the per-site row capacity (RFB_ECAPACITY beyond).  Synchronises the
+ * stream.  RFB_EDEGENERATE: non-finite input or two sites within
+ * 1e-7 x the bounding-box diagonal (delaunay.py:436-467). */
+size_t rfb_adjacency_workspace_bytes(int64_t n_sites, int32_t max_degree);
+int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_degree,
+                        int64_t *offsets, int64_t *neighbors, int64_t neighbor_capacity,
+                        uint8_t *hull, int64_t *stats, void *workspace, size_t workspace_bytes,
+                        void *stream);
+int rfb_adjacency_emit(int64_t n_sites, int32_t max_degree, const int64_t *offsets,
+                       int64_t *neighbors, uint8_t *hull, const void *workspace,
+                       size_t workspace_bytes, void *stream);
 
 /* out[q] = nearest site to queries[q] (greedy CSR walk from seed_site). */
 int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t seed_site,

@@ -16,7 +16,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librfb.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("rfb.cu", "rfb_device.cuh")] + [
+CU_FILES = [os.path.join(CSRC, f) for f in ("rfb.cu", "rfb_adjacency.cu")]
+SOURCES = CU_FILES + [os.path.join(CSRC, "rfb_device.cuh")] + [
     os.path.join(REPO, "include", "rfb.h")
 ]
 
@@ -43,7 +44,7 @@ def _stale(target: str, deps) -> bool:
 
 def build_extension(force: bool = False, verbose: bool = False) -> str:
     if force or _stale(LIB, SOURCES):
-        cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", os.path.join(CSRC, "rfb.cu")]
+        cmd = [_nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *CU_FILES]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -112,6 +112,10 @@ SIGNATURES = {
     "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP]),
     "rfb_refresh_scene": (ctypes.c_int, [P(rfb_scene), VP, VP, VP]),
     "rfb_locate": (ctypes.c_int, [P(rfb_scene), VP, I64, I32, VP, VP]),
+    "rfb_adjacency_workspace_bytes": (SZ, [I64, I32]),
+    "rfb_build_adjacency": (ctypes.c_int, [VP, I64, I32, VP, VP, I64, VP, P(ctypes.c_int64), VP,
+                                           SZ, VP]),
+    "rfb_adjacency_emit": (ctypes.c_int, [I64, I32, VP, VP, VP, VP, SZ, VP]),
     "rfb_effect_rays": (ctypes.c_int, [VP, VP, VP, I64, P(ctypes.c_double), I32, ctypes.c_double,
                                        VP, VP, VP]),
     "rfb_render_rays": (ctypes.c_int, [P(rfb_scene), P(rfb_rays), P(rfb_params), P(rfb_fwd_out),

@@ -1403,6 +1403,8 @@ int rfb_abi_version(void) { return RFB_ABI_VERSION; }
 const char *rfb_error_string(int code) {
     if (code == RFB_OK) return "ok";
     if (code == RFB_EINVAL) return "invalid argument";
+    if (code == RFB_ECAPACITY) return "capacity exceeded";
+    if (code == RFB_EDEGENERATE) return "degenerate input";
     return cudaGetErrorString((cudaError_t)code);
 }
 

@@ -28,3 +28,11 @@ class DeviceError(FoamError):
 
 class ExtensionMissing(FoamError):
     """The sm_100a extension (librfb.so) is not built or cannot be loaded."""
+
+
+class DegenerateInput(FoamError):
+    """Point set the Delaunay builder cannot triangulate (rfoam/errors.py:8)."""
+
+
+class DuplicatePoints(FoamError):
+    """Two sites within the duplicate tolerance (rfoam/errors.py:12)."""

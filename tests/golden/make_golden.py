@@ -276,6 +276,28 @@ def checkpoint_case():
                         background=sc.background.astype(np.float32).astype(np.float64))
 
 
+def adjacency_case():
+    """geometry/delaunay.py build + adjacency.py from_triangulation on three
+    point sets (uniform, surface shell, anisotropic Gaussian cluster):
+    offsets, neighbors and hull flags, for the device builder."""
+    out = {}
+    rng = np.random.default_rng(99)
+    sets = {
+        "uniform2k": random_positions(2000, 7),
+        "surface3k": random_positions(3000, 2, "surface"),
+        "gauss1500": (rng.normal(size=(1500, 3)) * [1.0, 0.3, 2.0]).astype(np.float32)
+        .astype(np.float64),
+    }
+    for name, pos in sets.items():
+        adj = AdjacencyGraph.from_triangulation(build(pos))
+        out[f"{name}_positions"] = pos
+        out[f"{name}_offsets"] = adj.offsets
+        out[f"{name}_neighbors"] = adj.neighbors.astype(np.int32)
+        out[f"{name}_hull"] = adj.hull
+        print(name, len(adj.neighbors), int(adj.hull.sum()))
+    np.savez_compressed(os.path.join(HERE, "adjacency.npz"), **out)
+
+
 def effects_case():
     """rays.py:60-176: intersect_face, reflect, refract (incl. back side and
     total internal reflection) and apply_effect on random unit vectors."""
@@ -314,6 +336,7 @@ if __name__ == "__main__":
         for name in sys.argv[1:]:
             globals()[f"{name}_case"]()
         sys.exit(0)
+    adjacency_case()
     effects_case()
     checkpoint_case()
     adam_case()
