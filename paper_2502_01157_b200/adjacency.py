@@ -56,6 +56,9 @@ def build_device(positions: torch.Tensor, max_degree: int = MAX_DEGREE, stream=N
                 raise DegenerateInput("non-finite coordinates")
             raise DuplicatePoints("sites within duplicate tolerance "
                                   f"{1e-7 * _diag(pos):g}")
+        if code == -2:
+            raise DeviceError(f"rfb_build_adjacency: capacity exceeded (flags {int(stats[7])}, "
+                              f"max vertices {int(stats[3])}, max planes {int(stats[4])})")
         _lib.check(code, "rfb_build_adjacency")
         E = int(stats[0])
         neighbors = torch.empty(max(E, 1), dtype=torch.int64, device=dev)

@@ -41,8 +41,11 @@ namespace rfb_adj {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kWarps = 2;          // sites (warps) per block
-constexpr int kMaxPlanes = 128;    // planes per cell, box included (8-bit ids)
-constexpr int kMaxVerts = 256;     // polytope vertices (dual triangles)
+constexpr int kMaxPlanes = 128;    // pass-1 planes per cell, box included (8-bit ids)
+#ifndef RFB_ADJ_MAX_VERTS
+#define RFB_ADJ_MAX_VERTS 256
+#endif
+constexpr int kMaxVerts = RFB_ADJ_MAX_VERTS;  // polytope vertices (dual triangles)
 #ifndef RFB_ADJ_SPIRAL_G
 #define RFB_ADJ_SPIRAL_G 5
 #endif
@@ -51,16 +54,23 @@ constexpr int kSpiralN = (2 * kSpiralG + 1) * (2 * kSpiralG + 1) * (2 * kSpiralG
 
 enum : int { kErrNone = 0, kErrOverflow = 1, kErrDuplicate = 2, kErrDegenerate = 4 };
 
-struct WarpCell {
-    double nx[kMaxPlanes], ny[kMaxPlanes], nz[kMaxPlanes], no[kMaxPlanes];
-    double vx[kMaxVerts], vy[kMaxVerts], vz[kMaxVerts];
-    int32_t pid[kMaxPlanes];  // site id, or -1 for the box planes
-    uint32_t tri[kMaxVerts];  // a | b << 8 | c << 16
-    uint16_t edge[3 * kMaxVerts];
-    uint32_t rmask[kMaxVerts / 32];
-    uint8_t used[kMaxPlanes];
-    uint8_t pmap[kMaxPlanes];
+// One cell under construction (shared memory).  Pass 1 uses the small
+// buffer; cells that outgrow it (transiently long cells at the boundary of a
+// dense region) restart in pass 2 with the large one.
+template <int MP, int MV>
+struct CellBuf {
+    static constexpr int kPlanes = MP, kVerts = MV;
+    double nx[MP], ny[MP], nz[MP], no[MP];
+    double vx[MV], vy[MV], vz[MV];
+    int32_t pid[MP];       // site id, or -1 for the box planes
+    uint32_t tri[MV];      // a | b << 8 | c << 16
+    uint16_t edge[3 * MV];
+    uint32_t rmask[MV / 32];
+    uint8_t used[MP];
+    uint8_t pmap[MP];
 };
+using WarpCell = CellBuf<kMaxPlanes, kMaxVerts>;
+using BigCell = CellBuf<255, 1024>;
 
 struct Grid {
     double lo[3];
@@ -106,7 +116,8 @@ __device__ __forceinline__ int cell_index(const Grid &g, int ix, int iy, int iz)
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // vertex = intersection of planes a, b, c (local coordinates)
-__device__ __forceinline__ bool vertex_of(const WarpCell &C, int a, int b, int c, double pnx,
+template <class Cell>
+__device__ __forceinline__ bool vertex_of(const Cell &C, int a, int b, int c, double pnx,
                                           double pny, double pnz, double po, double &x, double &y,
                                           double &z) {
     // c may be the plane being added (passed in registers, c < 0)
@@ -136,7 +147,8 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 // Drop planes no triangle references (full-scan cells clip many transient planes).
-__device__ void compact_planes(WarpCell &C, int lane, int nv, int &np) {
+template <class Cell>
+__device__ void compact_planes(Cell &C, int lane, int nv, int &np) {
     for (int p = lane; p < np; p += 32) C.used[p] = 0;
     __syncwarp();
     for (int v = lane; v < nv; v += 32) {
@@ -176,7 +188,8 @@ __device__ void compact_planes(WarpCell &C, int lane, int nv, int &np) {
 
 // Clip the cell by n.x <= o (plane of site j).  Returns false on overflow /
 // degeneracy (err set).
-__device__ bool clip(WarpCell &C, int lane, double pnx, double pny, double pnz, double po,
+template <class Cell>
+__device__ bool clip(Cell &C, int lane, double pnx, double pny, double pnz, double po,
                      int32_t j, CellState &S) {
     int &nv = S.nv, &np = S.np, &err = S.err;
     int nrem = 0;
@@ -190,8 +203,8 @@ __device__ bool clip(WarpCell &C, int lane, double pnx, double pny, double pnz, 
     }
     if (nrem == 0) return true;
     __syncwarp();
-    if (np == kMaxPlanes) compact_planes(C, lane, nv, np);
-    if (np == kMaxPlanes) {
+    if (np == Cell::kPlanes) compact_planes(C, lane, nv, np);
+    if (np == Cell::kPlanes) {
         err |= kErrOverflow;
         return false;
     }
@@ -255,7 +268,7 @@ __device__ bool clip(WarpCell &C, int lane, double pnx, double pny, double pnz, 
         const unsigned bm = __ballot_sync(kFull, bnd);
         if (bnd) {
             const int d = nvn + __popc(bm & lanemask_lt());
-            if (d < kMaxVerts) {
+            if (d < Cell::kVerts) {
                 const int u = ed & 255, w = ed >> 8;
                 double x, y, z;
                 if (!vertex_of(C, u, w, -1, pnx, pny, pnz, po, x, y, z)) bad = true;
@@ -266,7 +279,7 @@ __device__ bool clip(WarpCell &C, int lane, double pnx, double pny, double pnz, 
         nvn += __popc(bm);
     }
     if (__any_sync(kFull, bad)) err |= kErrDegenerate;
-    if (nvn > kMaxVerts) {
+    if (nvn > Cell::kVerts) {
         err |= kErrOverflow;
         return false;
     }
@@ -303,7 +316,8 @@ __device__ __forceinline__ bool may_cut(const CellState &S, double dx, double dy
     return sup * (1.0 + 1e-12) > 0.5 * d2;
 }
 
-__device__ __forceinline__ void offer_cells(const Args &A, WarpCell &C, int lane, int cell,
+template <class Cell>
+__device__ __forceinline__ void offer_cells(const Args &A, Cell &C, int lane, int cell,
                                             double sx, double sy, double sz, int32_t self,
                                             CellState &S, int phase) {
     int c0 = 0, c1 = 0;
@@ -347,7 +361,8 @@ __device__ __forceinline__ void offer_cells(const Args &A, WarpCell &C, int lane
     }
 }
 
-__device__ void init_cell(WarpCell &C, int lane, double B, CellState &S) {
+template <class Cell>
+__device__ void init_cell(Cell &C, int lane, double B, CellState &S) {
     // box: planes 0..5 = +x, -x, +y, -y, +z, -z at distance B
     if (lane < 6) {
         const double sgn = (lane & 1) ? -1.0 : 1.0;
@@ -377,7 +392,8 @@ __device__ void init_cell(WarpCell &C, int lane, double B, CellState &S) {
 
 // Clip by the sites of the spiral table's cells, nearest first, until the
 // security radius is reached.  Returns true when the cell is final.
-__device__ bool spiral_phase(const Args &A, WarpCell &C, int lane, const double4 &s, int32_t self,
+template <class Cell>
+__device__ bool spiral_phase(const Args &A, Cell &C, int lane, const double4 &s, int32_t self,
                              int ix, int iy, int iz, CellState &S) {
     const Grid &g = A.g;
     const double h2 = g.h * g.h;
@@ -396,7 +412,8 @@ __device__ bool spiral_phase(const Args &A, WarpCell &C, int lane, const double4
 }
 
 // neighbours: planes with at least one final vertex, ascending site id
-__device__ void emit_site(const Args &A, WarpCell &C, int lane, int32_t self, const CellState &S) {
+template <class Cell>
+__device__ void emit_site(const Args &A, Cell &C, int lane, int32_t self, const CellState &S) {
     const int nv = S.nv, np = S.np;
     int err = S.err;
     for (int p = lane; p < np; p += 32) C.used[p] = 0;
@@ -457,9 +474,10 @@ __global__ void __launch_bounds__(32 * kWarps) k_voronoi(Args A) {
         init_cell(C, lane, A.box, S);
         int ix, iy, iz;
         site_cell(A.g, s, ix, iy, iz);
-        if (spiral_phase(A, C, lane, s, self, ix, iy, iz, S) || S.err) {
+        const bool done = spiral_phase(A, C, lane, s, self, ix, iy, iz, S);
+        if ((done && S.err == 0) || (S.err & ~kErrOverflow)) {
             emit_site(A, C, lane, self, S);
-        } else if (lane == 0) {
+        } else if (lane == 0) {  // not final after the spiral, or outgrew the buffer
             const int q = atomicAdd(A.flags + 1, 1);
             A.tail[q] = (int32_t)k;
         }
@@ -467,22 +485,91 @@ __global__ void __launch_bounds__(32 * kWarps) k_voronoi(Args A) {
     }
 }
 
-// Pass 2: one block per queued site.  Warp 0 rebuilds the spiral cell, then
-// the whole block scans the grid cells of the vertex balls' bounding box
-// (every site that can still cut the cell lies in some ball B(v, |v|)):
-// each thread tests its candidates exactly against the current vertices
-// (p.v > |p|^2/2, the clip test), survivors are queued in shared memory
-// and warp 0 clips by them in order.
+// Grid-cell bounds of the union of the vertex balls B(v, |v|) (warp 0).
+template <class Cell>
+__device__ void ball_box(const Cell &C, int lane, const CellState &S, const double4 &s,
+                         const Grid &g, int *box) {
+    double bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int v = lane; v < S.nv; v += 32) {
+        const double x = C.vx[v], y = C.vy[v], z = C.vz[v];
+        const double r = sqrt(x * x + y * y + z * z) * (1.0 + 1e-12);
+        bl[0] = fmin(bl[0], x - r); bh[0] = fmax(bh[0], x + r);
+        bl[1] = fmin(bl[1], y - r); bh[1] = fmax(bh[1], y + r);
+        bl[2] = fmin(bl[2], z - r); bh[2] = fmax(bh[2], z + r);
+    }
+    const double sc[3] = {s.x, s.y, s.z};
+    for (int q = 0; q < 3; ++q) {
+        const double lo = -warp_max(-bl[q]) + sc[q], hi = warp_max(bh[q]) + sc[q];
+        const double f0 = floor((lo - g.lo[q]) / g.h), f1 = floor((hi - g.lo[q]) / g.h);
+        if (lane == 0) {
+            box[q] = f0 < 0.0 ? 0 : (f0 > g.dim[q] - 1 ? g.dim[q] - 1 : (int)f0);
+            box[3 + q] = f1 < 0.0 ? 0 : (f1 > g.dim[q] - 1 ? g.dim[q] - 1 : (int)f1);
+        }
+    }
+}
+
+// The part of Chebyshev ring r around (ix, iy, iz) inside the inclusive
+// cell box `box` (lo xyz, hi xyz), as up to six face rectangles.
+struct RingBox {
+    int start[7];
+    int fix[6];      // coordinate on the face's fixed axis
+    int lo1[6], n1[6], lo2[6];
+    __device__ int total() const { return start[6]; }
+    __device__ void cell(int t, int &cx, int &cy, int &cz) const {
+        int f = 0;
+        while (t >= start[f + 1]) ++f;
+        const int u = t - start[f], a = lo1[f] + u % n1[f], b = lo2[f] + u / n1[f];
+        if (f < 2) { cx = fix[f]; cy = a; cz = b; }
+        else if (f < 4) { cx = a; cy = fix[f]; cz = b; }
+        else { cx = a; cy = b; cz = fix[f]; }
+    }
+};
+
+__device__ __forceinline__ RingBox ring_box(int r, int ix, int iy, int iz, const int *box) {
+    RingBox R;
+    const int c[3] = {ix, iy, iz};
+    int n = 0;
+    for (int f = 0; f < 6; ++f) {
+        const int ax = f >> 1, sgn = (f & 1) ? -1 : 1;
+        const int fixv = c[ax] + sgn * r;
+        // the two free axes; faces of lower axes own the shared edges
+        const int a1 = ax == 0 ? 1 : 0, a2 = ax == 2 ? 1 : 2;
+        const int s1 = a1 < ax ? r - 1 : r, s2 = a2 < ax ? r - 1 : r;
+        const int l1 = max(c[a1] - s1, box[a1]), h1 = min(c[a1] + s1, box[3 + a1]);
+        const int l2 = max(c[a2] - s2, box[a2]), h2 = min(c[a2] + s2, box[3 + a2]);
+        const bool ok = fixv >= box[ax] && fixv <= box[3 + ax] && h1 >= l1 && h2 >= l2;
+        R.start[f] = n;
+        R.fix[f] = fixv;
+        R.lo1[f] = l1;
+        R.lo2[f] = l2;
+        R.n1[f] = ok ? h1 - l1 + 1 : 1;
+        n += ok ? (h1 - l1 + 1) * (h2 - l2 + 1) : 0;
+    }
+    R.start[6] = n;
+    return R;
+}
+
+// Pass 2: one block per queued site.  Warp 0 rebuilds the cell (spiral)
+// in the large buffer; if it is not final the whole block scans Chebyshev
+// rings of grid cells outward, restricted to the grid-cell box of the
+// vertex balls B(v, |v|) (every site that can still cut the cell lies in
+// one of them).  Each thread tests its candidates exactly against the
+// current vertices (p.v > |p|^2/2, the clip test); survivors are queued in
+// shared memory and warp 0 clips by them.  After every ring the box and the
+// security radius are refreshed, so a long cell that gets capped stops
+// scanning early; unbounded (hull) cells scan to the grid's edge.
 constexpr int kTailThreads = 256;
 constexpr int kTailQueue = 512;
 
 __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t count) {
-    __shared__ WarpCell C;
+    __shared__ BigCell C;
     __shared__ CellState SS;
+    __shared__ bool fin;
     __shared__ int32_t queue[kTailQueue];
     __shared__ int qn, box[6];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const Grid &g = A.g;
+    const int rmax = max(max(g.dim[0], g.dim[1]), g.dim[2]);
     for (int32_t item = blockIdx.x; item < count; item += gridDim.x) {
         const int64_t k = A.tail[item];
         const double4 s = A.pos[k];
@@ -492,66 +579,58 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
         if (warp == 0) {
             CellState S;
             init_cell(C, lane, A.box, S);
-            spiral_phase(A, C, lane, s, self, ix, iy, iz, S);
-            double bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
-            for (int v = lane; v < S.nv; v += 32) {
-                const double x = C.vx[v], y = C.vy[v], z = C.vz[v];
-                const double r = sqrt(x * x + y * y + z * z) * (1.0 + 1e-12);
-                bl[0] = fmin(bl[0], x - r); bh[0] = fmax(bh[0], x + r);
-                bl[1] = fmin(bl[1], y - r); bh[1] = fmax(bh[1], y + r);
-                bl[2] = fmin(bl[2], z - r); bh[2] = fmax(bh[2], z + r);
-            }
-            const double sc[3] = {s.x, s.y, s.z};
-            for (int q = 0; q < 3; ++q) {
-                const double lo = -warp_max(-bl[q]) + sc[q], hi = warp_max(bh[q]) + sc[q];
-                const double f0 = floor((lo - g.lo[q]) / g.h), f1 = floor((hi - g.lo[q]) / g.h);
-                if (lane == 0) {
-                    box[q] = f0 < 0.0 ? 0 : (f0 > g.dim[q] - 1 ? g.dim[q] - 1 : (int)f0);
-                    box[3 + q] = f1 < 0.0 ? 0 : (f1 > g.dim[q] - 1 ? g.dim[q] - 1 : (int)f1);
-                }
-            }
+            const bool done = spiral_phase(A, C, lane, s, self, ix, iy, iz, S);
+            ball_box(C, lane, S, s, g, box);
             if (lane == 0) {
+                fin = done || S.err != 0;
                 SS = S;
                 qn = 0;
             }
         }
         __syncthreads();
-        const int ex = box[3] - box[0] + 1, ey = box[4] - box[1] + 1, ez = box[5] - box[2] + 1;
-        const int64_t total = (int64_t)ex * ey * ez;
-        for (int64_t t0 = 0; t0 < total && SS.err == 0; t0 += kTailThreads) {
-            const int64_t t = t0 + tid;
-            if (t < total) {
-                const int cx = box[0] + (int)(t % ex), cy = box[1] + (int)((t / ex) % ey),
-                          cz = box[2] + (int)(t / ((int64_t)ex * ey));
-                if (max(max(abs(cx - ix), abs(cy - iy)), abs(cz - iz)) > kSpiralG) {
-                    const int cell = cell_index(g, cx, cy, cz);
-                    const int c0 = __ldg(A.cstart + cell), c1 = __ldg(A.cstart + cell + 1);
-                    for (int q = c0; q < c1; ++q) {
-                        const double4 p = A.pos[q];
-                        const double dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
-                        const double d2 = dx * dx + dy * dy + dz * dz;
-                        if (d2 <= A.dup2) {
-                            atomicOr(A.flags, kErrDuplicate);
-                            continue;
-                        }
-                        if (!may_cut(SS, dx, dy, dz, d2)) continue;
-                        const double o = 0.5 * d2;
-                        bool cut = false;
-                        for (int v = 0; v < SS.nv && !cut; ++v)
-                            cut = dx * C.vx[v] + dy * C.vy[v] + dz * C.vz[v] > o;
-                        if (cut) {
-                            const int slot = atomicAdd(&qn, 1);
-                            if (slot < kTailQueue) queue[slot] = q;
+        for (int r = kSpiralG + 1; r <= rmax && !fin; ++r) {
+            // stop: remaining sites are >= (r-1) h away, beyond the security radius,
+            // or the ring lies outside the ball box
+            const double lb = (double)(r - 1) * g.h;
+            if (lb * lb >= 4.0 * SS.R2 * (1.0 + 1e-12)) break;
+            if (max(max(ix - box[0], box[3] - ix), max(max(iy - box[1], box[4] - iy),
+                                                       max(iz - box[2], box[5] - iz))) < r)
+                break;
+            const RingBox RB = ring_box(r, ix, iy, iz, box);
+            const int total = RB.total();
+            for (int t0 = 0; t0 < total && SS.err == 0; t0 += kTailThreads) {
+                const int t = t0 + tid;
+                if (t < total) {
+                    int cx, cy, cz;
+                    RB.cell(t, cx, cy, cz);
+                    {
+                        const int cell = cell_index(g, cx, cy, cz);
+                        const int c0 = __ldg(A.cstart + cell), c1 = __ldg(A.cstart + cell + 1);
+                        for (int q = c0; q < c1; ++q) {
+                            const double4 p = A.pos[q];
+                            const double dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
+                            const double d2 = dx * dx + dy * dy + dz * dz;
+                            if (d2 <= A.dup2) {
+                                atomicOr(A.flags, kErrDuplicate);
+                                continue;
+                            }
+                            if (!may_cut(SS, dx, dy, dz, d2)) continue;
+                            const double o = 0.5 * d2;
+                            bool cut = false;
+                            for (int v = 0; v < SS.nv && !cut; ++v)
+                                cut = dx * C.vx[v] + dy * C.vy[v] + dz * C.vz[v] > o;
+                            if (cut) {
+                                const int slot = atomicAdd(&qn, 1);
+                                if (slot < kTailQueue) queue[slot] = q;
+                            }
                         }
                     }
                 }
-            }
-            __syncthreads();
-            const int nq = qn;
-            if (nq > kTailQueue) {  // queue overflow: this batch again after clipping
-                if (warp == 0) {
+                __syncthreads();
+                const int nq = qn;
+                if (nq > 0 && warp == 0) {
                     CellState S = SS;
-                    for (int i = 0; i < kTailQueue && S.err == 0; ++i) {
+                    for (int i = 0; i < min(nq, kTailQueue) && S.err == 0; ++i) {
                         const int q = queue[i];
                         const double4 p = A.pos[q];
                         const double dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
@@ -565,24 +644,9 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                     }
                 }
                 __syncthreads();
-                t0 -= kTailThreads;
-                continue;
+                if (nq > kTailQueue) t0 -= kTailThreads;  // overflowed: this batch again
             }
-            if (nq > 0 && warp == 0) {
-                CellState S = SS;
-                for (int i = 0; i < nq && S.err == 0; ++i) {
-                    const int q = queue[i];
-                    const double4 p = A.pos[q];
-                    const double dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
-                    const double d2 = dx * dx + dy * dy + dz * dz;
-                    if (may_cut(S, dx, dy, dz, d2))
-                        clip(C, lane, dx, dy, dz, 0.5 * d2, __ldg(A.ids + q), S);
-                }
-                if (lane == 0) {
-                    SS = S;
-                    qn = 0;
-                }
-            }
+            if (warp == 0) ball_box(C, lane, SS, s, g, box);
             __syncthreads();
         }
         if (warp == 0) {
@@ -911,6 +975,7 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
     stats[4] = hflags[3];  // max planes
     stats[5] = *reinterpret_cast<int64_t *>(hflags + 8);   // clip tests, spiral (profile)
     stats[6] = *reinterpret_cast<int64_t *>(hflags + 10);  // clip tests, rings (profile)
+    stats[7] = hflags[0];  // error flags (1 overflow, 2 duplicate, 4 degenerate)
     if (hflags[0] & kErrDuplicate) return RFB_EDEGENERATE;
     if (hflags[0] & kErrOverflow) return RFB_ECAPACITY;
     if (hflags[0] & kErrDegenerate) return RFB_EDEGENERATE;

@@ -14,10 +14,12 @@ rep, kre, mangled = sys.argv[1:4]
 lib = sys.argv[4] if len(sys.argv) > 4 else "paper_2502_01157_b200/librfb.so"
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
-cubin = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cubin)], capture_output=True,
-                      text=True).stdout.split("\n")
-start = next(i for i, l in enumerate(sass) if l.startswith(".text." + mangled))
+for cubin in sorted(f for f in os.listdir(tmp) if f.endswith(".cubin")):
+    sass = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cubin)], capture_output=True,
+                          text=True).stdout.split("\n")
+    start = next((i for i, l in enumerate(sass) if l.startswith(".text." + mangled)), None)
+    if start is not None:
+        break
 end = next((i for i in range(start + 1, len(sass)) if sass[i].startswith(".text.")), len(sass))
 cur = None
 a2l = {}
