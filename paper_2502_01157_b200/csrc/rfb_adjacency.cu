@@ -46,6 +46,9 @@ constexpr int kMaxPlanes = 128;    // pass-1 planes per cell, box included (8-bi
 #define RFB_ADJ_MAX_VERTS 256
 #endif
 constexpr int kMaxVerts = RFB_ADJ_MAX_VERTS;  // polytope vertices (dual triangles)
+#ifndef RFB_ADJ_CELL_SITES
+#define RFB_ADJ_CELL_SITES 2.0  // mean sites per grid cell over the bounding box
+#endif
 #ifndef RFB_ADJ_SPIRAL_G
 #define RFB_ADJ_SPIRAL_G 5
 #endif
@@ -571,6 +574,9 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
     const Grid &g = A.g;
     const int rmax = max(max(g.dim[0], g.dim[1]), g.dim[2]);
     for (int32_t item = blockIdx.x; item < count; item += gridDim.x) {
+#if RFB_ADJ_PROFILE
+        const long long clk0 = clock64();
+#endif
         const int64_t k = A.tail[item];
         const double4 s = A.pos[k];
         const int32_t self = A.ids[k];
@@ -652,6 +658,14 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
         if (warp == 0) {
             CellState S = SS;
             emit_site(A, C, lane, self, S);
+#if RFB_ADJ_PROFILE
+            if (lane == 0) {  // pass-2 cycles: [12] total, [14] hull sites' total
+                const unsigned long long dt = (unsigned long long)(clock64() - clk0);
+                unsigned long long *pc = reinterpret_cast<unsigned long long *>(A.flags + 12);
+                atomicAdd(pc, dt);
+                if (A.hull[self]) atomicAdd(pc + 1, dt);
+            }
+#endif
         }
         __syncthreads();
     }
@@ -895,7 +909,7 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
     if (!(emax > 0.0)) emax = 1.0;
     double vol = 1.0;
     for (int k = 0; k < 3; ++k) vol *= std::max(ext[k], emax * 1e-3);
-    double h = std::cbrt(2.0 * vol / (double)n);
+    double h = std::cbrt(RFB_ADJ_CELL_SITES * vol / (double)n);
     for (;;) {
         int64_t cells = 1;
         for (int k = 0; k < 3; ++k) {
@@ -976,6 +990,11 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
     stats[5] = *reinterpret_cast<int64_t *>(hflags + 8);   // clip tests, spiral (profile)
     stats[6] = *reinterpret_cast<int64_t *>(hflags + 10);  // clip tests, rings (profile)
     stats[7] = hflags[0];  // error flags (1 overflow, 2 duplicate, 4 degenerate)
+#if RFB_ADJ_PROFILE
+    cudaMemcpy(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost);
+    stats[5] = *reinterpret_cast<int64_t *>(hflags + 12);  // pass-2 cycles (all sites)
+    stats[6] = *reinterpret_cast<int64_t *>(hflags + 14);  // pass-2 cycles (hull sites)
+#endif
     if (hflags[0] & kErrDuplicate) return RFB_EDEGENERATE;
     if (hflags[0] & kErrOverflow) return RFB_ECAPACITY;
     if (hflags[0] & kErrDegenerate) return RFB_EDEGENERATE;

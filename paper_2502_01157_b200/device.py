@@ -143,6 +143,50 @@ class DeviceScene:
         return ctypes.byref(self._c)
 
     # -- device-resident updates (training) ------------------------------
+    def rebuild_adjacency(self, positions: torch.Tensor | None = None, packed=None,
+                          stream=None) -> dict:
+        """Re-triangulate on the device after the sites moved (train.py:247-256
+        rebuilds with delaunay.build; here rfb_build_adjacency) and re-pack the
+        scene in place: CSR, packed headers/edges, bounding box and width floor.
+        `positions` (device fp64 [n,3]) defaults to the current site4 xyz."""
+        from . import adjacency
+
+        pos = (self.site4[:, :3] if positions is None else positions).to(
+            self.device, torch.float64).contiguous()
+        off, nbr, hull, info = adjacency.build_device(pos, stream=stream)
+        n = self.n_sites
+        sig = self.site4[:, 3].contiguous()
+        self.n_edges = int(nbr.numel())
+        lo = pos.min(0).values.cpu().numpy()
+        hi = pos.max(0).values.cpu().numpy()
+        self.bbox_lo, self.bbox_hi = lo, hi
+        self.diagonal = float(np.linalg.norm(hi - lo))
+        self.center = 0.5 * (lo + hi)
+        self.width_floor = WIDTH_FLOOR_SCALE * self.diagonal
+        self.packed = bool(torch.equal(pos.float().double(), pos)) if packed is None \
+            else bool(packed)
+        dev = self.device
+        with torch.cuda.device(dev):
+            site4 = torch.empty((n, 4), dtype=torch.float64, device=dev)
+            self.offsets = torch.empty(n + 1, dtype=torch.int32, device=dev)
+            self.neighbors = torch.empty(max(self.n_edges, 1), dtype=torch.int32, device=dev)
+            if self.packed:
+                self.cells = torch.empty((n, 8), dtype=torch.int32, device=dev)
+                self.edges = torch.zeros((self.n_edges + 1, 4), dtype=torch.float32, device=dev)
+                self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
+            else:
+                self.cells = self.edges = self.sh32 = None
+            self.edge_meta = None
+            _lib.check(self.lib.rfb_pack_scene(
+                _ptr(pos), _ptr(sig), _ptr(self.sh), _ptr(off), _ptr(nbr), n, self.n_edges,
+                _ptr(site4), _ptr(self.offsets), _ptr(self.neighbors), _ptr(self.cells),
+                _ptr(self.edges), None, _ptr(self.sh32), _stream(stream)), "rfb_pack_scene")
+            self.site4 = site4
+        self.hull = hull
+        self._refresh_struct()
+        return info
+
+
     def set_raw_density(self, raw: torch.Tensor, stream=None):
         raw = raw.to(self.device, torch.float64).contiguous()
         _lib.check(self.lib.rfb_softplus(_ptr(raw), self.n_sites, None, _ptr(self.site4),

@@ -87,6 +87,11 @@ class DeviceTrainer:
                                               dv._ptr(self.raw), dv._stream(stream)),
                    "rfb_refresh_scene")
 
+    def rebuild_adjacency(self, stream=None) -> dict:
+        """Re-triangulate the moved sites on the device (train.py:247-256's
+        rebuild cadence; delaunay.build -> rfb_build_adjacency)."""
+        return self.ds.rebuild_adjacency(self.positions, packed=self.ds.packed, stream=stream)
+
     def step(self, origins, directions, t_min, t_max, start, targets, *, lr_position,
              lr_density, lr_sh, sh_warmup=False, quantile_scale=0.0, u_pairs=None,
              weight_floor=1e-4, m_global=None, epsilon=1e-3, step_limit=4096,
