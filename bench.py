@@ -65,6 +65,8 @@ def parse():
                          "u_pairs from rng(12); optim/config.py:34-36)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-adjacency", action="store_true",
+                    help="skip timing the device Delaunay rebuild (SURVEY §8f row 2)")
     ap.add_argument("--cpu-row-stride", type=int, default=8)
     ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5],
                     help="2: config 2 forward + config 3 fwd+bwd (1M, 1080p; default); "
@@ -416,6 +418,31 @@ def main():
               "loss_rgb": float(loss[0].item()) / (3.0 * m * n_train_views),
               "clocks": clocks_fb}
 
+    # -- device Delaunay rebuild of the same sites --------------
+    adjacency = None
+    if not args.no_adjacency and rank == 0:
+        from paper_2502_01157_b200 import adjacency as adj_mod
+        pos_d = torch.from_numpy(np.ascontiguousarray(scene.adjacency.positions)).to(dev)
+        off_d, nbr_d, _, ainfo = adj_mod.build_device(pos_d)  # warm-up
+        same = bool(torch.equal(off_d.cpu(), torch.from_numpy(scene.adjacency.offsets)) and
+                    torch.equal(nbr_d.cpu(), torch.from_numpy(scene.adjacency.neighbors)))
+        tms = []
+        for _ in range(3):
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            adj_mod.build_device(pos_d)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            tms.append(a0.elapsed_time(a1))
+        adjacency = {"ms": float(np.median(tms)), "sites": int(pos_d.shape[0]),
+                     "edges": ainfo["edges"], "csr_equals_fixture": same,
+                     "pass2_sites": ainfo["pass2_sites"],
+                     "api": "adjacency.build_device(positions) -> CSR + hull (rfb_build_adjacency)",
+                     "cpu_reference": "fixture CSR from scipy Qhull: ~127 s at 1M sites, 268 s "
+                                      "at 3M (SURVEY §8c; .foam_cache build logs)"}
+        del off_d, nbr_d
+
     # -- e2e through the public API (rank 0 view, host image out) -----------------
     e2e = None
     if not args.no_e2e and world == 1:
@@ -486,6 +513,7 @@ def main():
                    "scene_build_s": round(build_s, 1)},
         "fwd_bwd": fb,
         "e2e": e2e,
+        "adjacency_rebuild": adjacency,
         "gpu_launches": (3 * args.steps * len(views) if args.config != 5
                          else args.steps * len(train_views)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
