@@ -476,11 +476,14 @@ def main():
     peak, peak_kind = peaks()
     achieved = bytes_per_frame * len(views) / world / max(kernel_ms / 1e3, 1e-12) / 1e9
     traffic = None
+    l1_frac = None
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get("k_render_dram_bytes_per_launch")
+                tj = json.load(f)
+            traffic = tj.get("k_render_dram_bytes_per_launch")
+            l1_frac = tj.get("k_render_l1_data_pipe_frac")
         except Exception:
             traffic = None
     workload = {
@@ -521,7 +524,13 @@ def main():
                      "kernel": "k_render (walk + SH + composite)" if args.config != 5 else
                                "k_train (walk + composite + reverse pass)",
                      "algorithmic_bytes_per_launch": bytes_per_frame,
-                     "launch_ms": kernel_ms},
+                     "launch_ms": kernel_ms,
+                     "note": "achieved counts the algorithmic gather bytes of SURVEY §8d "
+                             "(no reuse); coherent rays share cells, so DRAM traffic per launch "
+                             "is `traffic` and frac can exceed 1. The binding unit is the L1 "
+                             "data pipe (binding_frac, from the ncu capture in profiles/).",
+                     "binding_unit": "l1tex data-pipe wavefronts",
+                     "binding_frac": l1_frac},
         "cpu_baseline": cpu,
         "clocks": clocks,
     }

@@ -276,13 +276,17 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
     t0 = time.perf_counter()
     res = dv.render_image_device(ds, camera, epsilon=epsilon, step_limit=step_limit, f64=True,
                                  lanes_per_ray=lanes_per_ray, workspace=fc["ws"], out=fc["out"])
-    fc["h_rgb"].copy_(res.rgb, non_blocking=True)
+    # D2H straight into a fresh pinned buffer from torch's caching host
+    # allocator; the returned array owns it (no host-side copy), and the block
+    # is recycled once the caller drops the image.
+    h_rgb = torch.empty((W * H, 3), dtype=torch.float64, pin_memory=True)
+    h_rgb.copy_(res.rgb, non_blocking=True)
     if weight_check:
         fc["h_wsum"].copy_(res.wsum, non_blocking=True)
         fc["h_resid"].copy_(res.residual, non_blocking=True)
     torch.cuda.current_stream(ds.device).synchronize()
     dt = time.perf_counter() - t0
-    img = fc["h_rgb"].numpy().reshape(H, W, 3).copy()
+    img = h_rgb.numpy().reshape(H, W, 3)
     if stats is not None:
         cnt = res.counters.cpu().numpy()
         status = res.status.cpu().numpy()
@@ -304,8 +308,7 @@ def _frame_cache(ds, W, H, weight_check):
     fc = cache.get(key)
     if fc is None:
         fc = {"ws": dv.Workspace(ds.device),
-              "out": dv.alloc_forward(W * H, ds.device, f64=True, per_ray=False),
-              "h_rgb": torch.empty((W * H, 3), dtype=torch.float64, pin_memory=True)}
+              "out": dv.alloc_forward(W * H, ds.device, f64=True, per_ray=False)}
         cache[key] = fc
     if weight_check and "h_wsum" not in fc:
         fc["h_wsum"] = torch.empty(W * H, dtype=torch.float64, pin_memory=True)

@@ -11,7 +11,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import ncu_summary  # noqa: E402
 
-tag, launches, rep = sys.argv[1:4]
+tag, launches = sys.argv[1:3]
+reps = sys.argv[3:]
 os.makedirs("profiles", exist_ok=True)
 rows = list(csv.reader(open(launches)))
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
@@ -35,21 +36,26 @@ fwd = sum(v[1] for k, v in agg.items() if "k_render" in k or "k_nearest" in k)
 lines += ["", f"k_render share of the forward step's kernel time: {100 * rend / fwd:.1f}%"]
 open(f"profiles/{tag}_launches_summary.txt", "w").write("\n".join(lines) + "\n")
 subprocess.run(["cp", launches, f"profiles/{tag}_launches.csv"])
-summ = ncu_summary.summarise(rep)
-open(f"profiles/{tag}_ncu_k_render_k_train.txt", "w").write(f"# {rep} (ncu --set full)\n" + summ + "\n")
+summ = "\n".join(f"# {rep} (ncu --set full)\n" + ncu_summary.summarise(rep) for rep in reps)
+open(f"profiles/{tag}_ncu_k_render_k_train.txt", "w").write(summ + "\n")
 # traffic per launch for bench.py's roofline.traffic
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rr = list(csv.reader(io.StringIO(out)))
-rh, ru = rr[0], rr[1]
 tr = {}
-for r in rr[2:]:
-    d = dict(zip(rh, r))
-    name = "k_render" if "k_render" in d["Kernel Name"] else "k_train"
-    scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
-    b = 0
-    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-        b += float(d[key]) * scale[ru[rh.index(key)]]
-    tr[f"{name}_dram_bytes_per_launch"] = int(b)
+for rep in reps:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rr = list(csv.reader(io.StringIO(out)))
+    rh, ru = rr[0], rr[1]
+    for r in rr[2:]:
+        d = dict(zip(rh, r))
+        name = "k_render" if "k_render" in d["Kernel Name"] else "k_train"
+        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
+        b = 0
+        for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            b += float(d[key]) * scale[ru[rh.index(key)]]
+        tr[f"{name}_dram_bytes_per_launch"] = int(b)
+        key = "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"
+        if key in d:
+            tr[f"{name}_l1_data_pipe_frac"] = round(float(d[key]) / 100.0, 4)
 tr["source"] = f"profiles/{tag}_ncu_k_render_k_train.txt (dram__bytes_read.sum + dram__bytes_write.sum)"
 json.dump(tr, open("profiles/traffic.json", "w"), indent=1)
 print("\n".join(lines))
