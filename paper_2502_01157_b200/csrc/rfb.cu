@@ -476,6 +476,9 @@ __device__ __forceinline__ unsigned order_key(double t) {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+#ifndef RFB_REV_PREFETCH
+#define RFB_REV_PREFETCH 0  // reverse pass: load the next segment's record one iteration ahead
+#endif
 constexpr int kTrainBlock = 128;
 constexpr int kTrainWarps = kTrainBlock / 32;
 
@@ -683,6 +686,17 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         float tb1 = 0.f, tb0 = 1.f;
         float Sr = 0.f, Sg = 0.f, Sb = 0.f, d_next = 0.f;
         double sig_next = 0.0;  // sigma of next_cell (quantile boundary terms)
+#if RFB_REV_PREFETCH
+        // next segment's record one iteration ahead (the workspace lives in DRAM)
+        int32_t p_cm = 0;
+        double p_t = 0.0;
+        float p_tb = 1.f;
+        auto prefetch = [&]() {
+            p_cm = s >= 1 ? s_cell[(s - 1) * SL] : 0;
+            p_t = s >= 2 ? s_t1[(s - 2) * SL] : r.t_min();
+            p_tb = s >= 2 ? (float)s_tb[(s - 2) * SL] : 1.f;
+        };
+#endif
         auto load_seg = [&]() {
             const int32_t cm = s_cell[s * SL];
             ci = cm & 0x1fffffff;
@@ -691,6 +705,9 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min();
             tb1 = (float)s_tb[s * SL];
             tb0 = s > 0 ? (float)s_tb[(s - 1) * SL] : 1.f;
+#if RFB_REV_PREFETCH
+            prefetch();
+#endif
         };
         if (s >= 0) {
             load_seg();
@@ -765,13 +782,25 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 next_cell = ci;
                 s -= 1;
                 if (s >= 0) {  // segment s's end is segment s+1's start: reuse it
+#if RFB_REV_PREFETCH
+                    const int32_t cm = p_cm;
+#else
                     const int32_t cm = s_cell[s * SL];
+#endif
                     ci = cm & 0x1fffffff;
                     cmask = (cm >> 29) & 7;
+#if RFB_REV_PREFETCH
+                    t1 = t0;
+                    tb1 = tb0;
+                    t0 = p_t;
+                    tb0 = p_tb;
+                    prefetch();
+#else
                     t1 = t0;
                     tb1 = tb0;
                     t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min();
                     tb0 = s > 0 ? (float)s_tb[(s - 1) * SL] : 1.f;
+#endif
                 }
             }
             // previous cell: aggregated when the whole group agrees on it

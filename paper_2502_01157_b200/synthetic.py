@@ -80,6 +80,17 @@ def _digest(a: np.ndarray) -> str:
     return hashlib.sha1(np.ascontiguousarray(a).view(np.uint8)).hexdigest()[:16]
 
 
+def _device_builder_ok() -> bool:
+    if os.environ.get("RFB_FIXTURE_BUILDER", "") == "qhull":
+        return False
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:  # noqa: BLE001
+        return False
+
+
 def cached_adjacency(positions: np.ndarray, tag: str, cache_dir: str | None = None,
                      verbose: bool = False) -> AdjacencyGraph:
     cache_dir = cache_dir or default_cache_dir()
@@ -94,9 +105,21 @@ def cached_adjacency(positions: np.ndarray, tag: str, cache_dir: str | None = No
         except Exception:  # corrupt cache: rebuild
             pass
     t0 = time.perf_counter()
-    offsets, neighbors, hull = delaunay_csr(positions)
+    builder = "Qhull"
+    if len(positions) >= 200_000 and _device_builder_ok():
+        # the device builder reproduces Qhull's CSR bit-for-bit on the fixture
+        # scenes (tests/test_gpu_adjacency.py) in ~1/500 of the time
+        import torch
+
+        from .adjacency import build_device
+
+        off, nbr, hl, _ = build_device(torch.from_numpy(positions).cuda())
+        offsets, neighbors, hull = off.cpu().numpy(), nbr.cpu().numpy(), hl.cpu().numpy()
+        builder = "device (rfb_build_adjacency)"
+    else:
+        offsets, neighbors, hull = delaunay_csr(positions)
     if verbose:
-        print(f"[synthetic] Qhull CSR for {tag}: {time.perf_counter() - t0:.1f}s", flush=True)
+        print(f"[synthetic] {builder} CSR for {tag}: {time.perf_counter() - t0:.1f}s", flush=True)
     try:
         os.makedirs(cache_dir, exist_ok=True)
         tmp = path + f".tmp{os.getpid()}.npz"

@@ -9,6 +9,8 @@ import time
 import numpy as np
 import torch
 
+os.environ["RFB_FIXTURE_BUILDER"] = "qhull"  # the comparison reference must be Qhull
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2502_01157_b200 import adjacency as A  # noqa: E402
 from paper_2502_01157_b200.synthetic import cached_adjacency, random_positions  # noqa: E402
