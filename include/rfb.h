@@ -23,6 +23,10 @@
  *   rfb_build_adjacency geometry/delaunay.py:445-520 build() +
  *                        adjacency.py:46-64 from_triangulation() (Voronoi
  *                        cell clipping on the GPU; rfb_adjacency.cu)
+ *   rfb_sh_basis, rfb_cell_colors, rfb_composite_segments,
+ *   rfb_backward_segments, rfb_quantile_segments
+ *                        tracer/kernels.py:38-73, 165-196, 250-369, 456-567
+ *                        over given segments (rfb_segments.cu)
  *   rfb_locate          geometry/adjacency.py:85-100 nearest_site()
  *                        (greedy walk on the CSR; same distance expression
  *                        and lowest-id tie rule as _grid_nearest 140-203)
@@ -228,6 +232,43 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
 int rfb_adjacency_emit(int64_t n_sites, int32_t max_degree, const int64_t *offsets,
                        int64_t *neighbors, uint8_t *hull, const void *workspace,
                        size_t workspace_bytes, void *stream);
+
+/* The reference's per-ray building blocks over caller-held segment lists
+ * (rfb_segments.cu; the hot path fuses them into rfb_render_rays, rfb_render_image
+ * and rfb_train_batch).
+ * Segments are CSR per ray: ray r owns seg_offsets[r] .. seg_offsets[r+1]-1
+ * (int64 offsets, int32 cells, f64 t0/t1).  All device pointers, fp64, the
+ * reference's operation order; background is host (3 doubles); gradient
+ * outputs accumulate (fp64 atomics).  Workspace: rfb_segments_workspace_bytes
+ * (rays, total segments). */
+int rfb_sh_basis(const double *dirs, int64_t m, double *out /* [m][16] */, void *stream);
+int rfb_cell_colors(const double *sh, const int32_t *cells, const double *basis, int64_t m,
+                    double *out /* [m][3] */, int32_t *masks /* nullable */, void *stream);
+int rfb_composite_segments(const double *sigma, const double *sh, const double *bases /* [m][16] */,
+                           int64_t m, const int64_t *seg_offsets, const int32_t *seg_cells,
+                           const double *seg_t0, const double *seg_t1, const double *background,
+                           double *out_rgb, double *out_T /* nullable */,
+                           double *out_wsum /* nullable */, void *stream);
+/* face_t_gradient (kernels.py:340-369) for m boundaries: ij [m][2] sites
+ * (i, j), ray q's origin/direction, crossing depth t[q] and dt[q]. */
+int rfb_face_t_gradients(const double *positions, const int32_t *ij, const double *origins,
+                         const double *directions, const double *t, const double *dt, int64_t m,
+                         double *d_pos, void *stream);
+size_t rfb_segments_workspace_bytes(int64_t m, int64_t n_segments);
+int rfb_backward_segments(const double *positions, const double *sigma, const double *sh,
+                          const double *background, const double *origins,
+                          const double *directions, const double *bases /* [m][16] */,
+                          const double *adjoints, int64_t m, const int64_t *seg_offsets,
+                          const int32_t *seg_cells, const double *seg_t0, const double *seg_t1,
+                          double *d_sigma, double *d_sh, double *d_pos, void *workspace,
+                          size_t workspace_bytes, void *stream);
+int rfb_quantile_segments(const double *positions, const double *sigma, const double *origins,
+                          const double *directions, int64_t m, const int64_t *seg_offsets,
+                          const int32_t *seg_cells, const double *seg_t0, const double *seg_t1,
+                          const double *u_pairs /* [m][P][2] */, int32_t n_pairs,
+                          double weight_floor, double scale, double *d_sigma, double *d_pos,
+                          double *loss_out /* [m], nullable */, void *workspace,
+                          size_t workspace_bytes, void *stream);
 
 /* out[q] = nearest site to queries[q] (greedy CSR walk from seed_site). */
 int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t seed_site,

@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librfb.so")
-CU_FILES = [os.path.join(CSRC, f) for f in ("rfb.cu", "rfb_adjacency.cu")]
+CU_FILES = [os.path.join(CSRC, f) for f in ("rfb.cu", "rfb_adjacency.cu", "rfb_segments.cu")]
 SOURCES = CU_FILES + [os.path.join(CSRC, "rfb_device.cuh")] + [
     os.path.join(REPO, "include", "rfb.h")
 ]

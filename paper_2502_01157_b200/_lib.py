@@ -116,6 +116,17 @@ SIGNATURES = {
     "rfb_build_adjacency": (ctypes.c_int, [VP, I64, I32, VP, VP, I64, VP, P(ctypes.c_int64), VP,
                                            SZ, VP]),
     "rfb_adjacency_emit": (ctypes.c_int, [I64, I32, VP, VP, VP, VP, SZ, VP]),
+    "rfb_sh_basis": (ctypes.c_int, [VP, I64, VP, VP]),
+    "rfb_cell_colors": (ctypes.c_int, [VP, VP, VP, I64, VP, VP, VP]),
+    "rfb_composite_segments": (ctypes.c_int, [VP, VP, VP, I64, VP, VP, VP, VP,
+                                              P(ctypes.c_double), VP, VP, VP, VP]),
+    "rfb_segments_workspace_bytes": (SZ, [I64, I64]),
+    "rfb_face_t_gradients": (ctypes.c_int, [VP, VP, VP, VP, VP, VP, I64, VP, VP]),
+    "rfb_backward_segments": (ctypes.c_int, [VP, VP, VP, P(ctypes.c_double), VP, VP, VP, VP,
+                                             I64, VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP]),
+    "rfb_quantile_segments": (ctypes.c_int, [VP, VP, VP, VP, I64, VP, VP, VP, VP, VP, I32,
+                                             ctypes.c_double, ctypes.c_double, VP, VP, VP, VP,
+                                             SZ, VP]),
     "rfb_effect_rays": (ctypes.c_int, [VP, VP, VP, I64, P(ctypes.c_double), I32, ctypes.c_double,
                                        VP, VP, VP]),
     "rfb_render_rays": (ctypes.c_int, [P(rfb_scene), P(rfb_rays), P(rfb_params), P(rfb_fwd_out),

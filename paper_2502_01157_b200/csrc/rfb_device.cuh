@@ -218,7 +218,7 @@ __device__ __forceinline__ void sh_basis_f32(float dx, float dy, float dz, float
 
 // Reference-exact channel value (kernels.py:66-68) from the fp64 table;
 // out of line so its registers do not count against the walk.
-__device__ __noinline__ double exact_channel(const double *row, int ch, int nb, double dx,
+static __device__ __noinline__ double exact_channel(const double *row, int ch, int nb, double dx,
                                              double dy, double dz) {
     double basis[16];
     sh_basis(dx, dy, dz, basis);

@@ -523,3 +523,105 @@ def coherent_order(origins: torch.Tensor, directions: torch.Tensor, bits: int = 
     _, oid = torch.unique(origins, dim=0, return_inverse=True)
     key = (oid << (2 * bits)) | _spread10(ix) | (_spread10(iy) << 1)
     return torch.argsort(key).to(torch.int32)
+
+
+# ---------------------------------------------------------------------------
+# The reference's per-ray building blocks over caller-held segment lists
+# (rfb_segments.cu; kernels.py:38-73, 165-196, 250-369, 456-567).  Segments
+# are CSR per ray: seg_offsets [m+1] int64, seg_cells int32, t0/t1 fp64.
+# ---------------------------------------------------------------------------
+def _f64(a, dev):
+    return torch.as_tensor(a).to(dev, torch.float64).contiguous()
+
+
+def _segs_args(seg_offsets, seg_cells, seg_t0, seg_t1, dev):
+    """Coerce a segment CSR to the ABI dtypes (int64 offsets, int32 cells, f64 depths)."""
+    return (torch.as_tensor(seg_offsets).to(dev, torch.int64).contiguous(),
+            torch.as_tensor(seg_cells).to(dev, torch.int32).contiguous(),
+            _f64(seg_t0, dev), _f64(seg_t1, dev))
+
+
+def sh_basis_device(dirs: torch.Tensor, stream=None) -> torch.Tensor:
+    lib = _lib.load()
+    d = dirs.to(torch.float64).reshape(-1, 3).contiguous()
+    out = torch.empty((d.shape[0], 16), dtype=torch.float64, device=d.device)
+    _lib.check(lib.rfb_sh_basis(_ptr(d), d.shape[0], _ptr(out), _stream(stream)), "rfb_sh_basis")
+    return out
+
+
+def cell_colors_device(sh: torch.Tensor, cells: torch.Tensor, basis: torch.Tensor, stream=None):
+    lib = _lib.load()
+    c = cells.to(torch.int32).contiguous()
+    b = basis.to(torch.float64).reshape(-1, 16).contiguous()
+    out = torch.empty((c.shape[0], 3), dtype=torch.float64, device=c.device)
+    masks = torch.empty(c.shape[0], dtype=torch.int32, device=c.device)
+    _lib.check(lib.rfb_cell_colors(_ptr(sh), _ptr(c), _ptr(b), c.shape[0], _ptr(out),
+                                   _ptr(masks), _stream(stream)), "rfb_cell_colors")
+    return out, masks
+
+
+def composite_segments_device(sigma, sh, basis, seg_offsets, seg_cells, seg_t0, seg_t1,
+                              background, stream=None):
+    """kernels.py:165-196 per ray -> (rgb [m,3], T [m], wsum [m])."""
+    lib = _lib.load()
+    dev = sigma.device
+    seg_offsets, seg_cells, seg_t0, seg_t1 = _segs_args(seg_offsets, seg_cells, seg_t0, seg_t1,
+                                                        dev)
+    m = seg_offsets.shape[0] - 1
+    rgb = torch.empty((m, 3), dtype=torch.float64, device=dev)
+    T = torch.empty(m, dtype=torch.float64, device=dev)
+    ws = torch.empty(m, dtype=torch.float64, device=dev)
+    bg = (ctypes.c_double * 3)(*[float(v) for v in background])
+    _lib.check(lib.rfb_composite_segments(
+        _ptr(sigma), _ptr(sh), _ptr(basis.contiguous()), m, _ptr(seg_offsets), _ptr(seg_cells),
+        _ptr(seg_t0), _ptr(seg_t1), bg, _ptr(rgb), _ptr(T), _ptr(ws), _stream(stream)),
+        "rfb_composite_segments")
+    return rgb, T, ws
+
+
+def backward_segments_device(positions, sigma, sh, background, origins, dirs, basis, adjoints,
+                             seg_offsets, seg_cells, seg_t0, seg_t1, d_sigma, d_sh, d_pos,
+                             stream=None):
+    """kernels.py:250-337 (+ face_t_gradient) per ray; accumulates (fp64)."""
+    lib = _lib.load()
+    seg_offsets, seg_cells, seg_t0, seg_t1 = _segs_args(seg_offsets, seg_cells, seg_t0, seg_t1,
+                                                        sigma.device)
+    m = seg_offsets.shape[0] - 1
+    S = int(seg_cells.shape[0])
+    ws = torch.empty(max(int(lib.rfb_segments_workspace_bytes(m, S)) // 8, 1),
+                     dtype=torch.float64, device=sigma.device)
+    bg = (ctypes.c_double * 3)(*[float(v) for v in background])
+    _lib.check(lib.rfb_backward_segments(
+        _ptr(positions), _ptr(sigma), _ptr(sh), bg, _ptr(origins), _ptr(dirs),
+        _ptr(basis.contiguous()), _ptr(adjoints), m, _ptr(seg_offsets), _ptr(seg_cells),
+        _ptr(seg_t0), _ptr(seg_t1), _ptr(d_sigma), _ptr(d_sh), _ptr(d_pos), _ptr(ws),
+        ws.numel() * 8, _stream(stream)), "rfb_backward_segments")
+
+
+def quantile_segments_device(positions, sigma, origins, dirs, seg_offsets, seg_cells, seg_t0,
+                             seg_t1, u_pairs, weight_floor, scale, d_sigma, d_pos, stream=None):
+    """kernels.py:456-567 for every pair of every ray; accumulates, returns the
+    per-ray loss (sum over its pairs)."""
+    lib = _lib.load()
+    seg_offsets, seg_cells, seg_t0, seg_t1 = _segs_args(seg_offsets, seg_cells, seg_t0, seg_t1,
+                                                        sigma.device)
+    m = seg_offsets.shape[0] - 1
+    S = int(seg_cells.shape[0])
+    up = u_pairs.to(torch.float64).reshape(m, -1, 2).contiguous()
+    ws = torch.empty(max(int(lib.rfb_segments_workspace_bytes(m, S)) // 8, 1),
+                     dtype=torch.float64, device=sigma.device)
+    loss = torch.empty(m, dtype=torch.float64, device=sigma.device)
+    _lib.check(lib.rfb_quantile_segments(
+        _ptr(positions), _ptr(sigma), _ptr(origins), _ptr(dirs), m, _ptr(seg_offsets),
+        _ptr(seg_cells), _ptr(seg_t0), _ptr(seg_t1), _ptr(up), up.shape[1], float(weight_floor),
+        float(scale), _ptr(d_sigma), _ptr(d_pos), _ptr(loss), _ptr(ws), ws.numel() * 8,
+        _stream(stream)), "rfb_quantile_segments")
+    return loss
+
+
+def face_t_gradients_device(positions, ij, origins, dirs, t, dt, d_pos, stream=None):
+    lib = _lib.load()
+    m = ij.shape[0]
+    _lib.check(lib.rfb_face_t_gradients(_ptr(positions), _ptr(ij.to(torch.int32).contiguous()),
+                                        _ptr(origins), _ptr(dirs), _ptr(t), _ptr(dt), m,
+                                        _ptr(d_pos), _stream(stream)), "rfb_face_t_gradients")

@@ -7,6 +7,9 @@ reference's numba functions, so a caller (``render.py:103``,
   render_rays   tracer/kernels.py:199-247
   train_batch   tracer/kernels.py:372-453
   walk_ray      tracer/kernels.py:76-162   (single ray, returns (nseg, status, residual))
+  sh_basis_into, cell_color, composite_segments, backward_ray,
+  face_t_gradient, quantile_backward_ray     kernels.py:38-73, 165-196, 250-369, 456-567
+                (single ray over given segments, via rfb_segments.cu)
 
 The GPU has no worker pool: ``n_workers`` is accepted, every ray's
 contribution lands in worker 0's slice of the per-worker buffers
@@ -113,3 +116,92 @@ def train_batch(positions, offsets, neighbors, sigma, sh, background, origins, d
     d_sh_w[0] += gb.sh.double().cpu().numpy().reshape(d_sh_w[0].shape)
     loss_w[0] += loss.cpu().numpy()
     counters[0, :] += res.counters.cpu().numpy().astype(counters.dtype)
+
+
+# ---------------------------------------------------------------------------
+# Per-ray building blocks (tracer/kernels.py:38-73, 165-196, 250-369, 456-567)
+# with the reference's signatures; the arithmetic runs in rfb_segments.cu
+# (fp64, reference operation order).  Outputs are written / accumulated in
+# place like the numba originals.
+# ---------------------------------------------------------------------------
+def _one_ray_segments(seg_cells, seg_t0, seg_t1, nseg):
+    n = int(nseg)
+    off = torch.tensor([0, n], dtype=torch.int64, device="cuda")
+    cells = _dev(np.asarray(seg_cells[:n]), torch.int32)
+    return off, cells, _dev(np.asarray(seg_t0[:n])), _dev(np.asarray(seg_t1[:n]))
+
+
+def sh_basis_into(dx, dy, dz, out):
+    """kernels.py:38-58."""
+    b = dv.sh_basis_device(torch.tensor([[dx, dy, dz]], dtype=torch.float64, device="cuda"))
+    out[:16] = b.cpu().numpy()[0]
+
+
+def cell_color(sh, i, basis, out):
+    """kernels.py:61-73: clamped colour of cell i; returns the clamp mask."""
+    row = _dev(np.asarray(sh).reshape(-1, 48)[int(i)][None, :])
+    col, mask = dv.cell_colors_device(row, torch.zeros(1, dtype=torch.int32, device="cuda"),
+                                      _dev(np.asarray(basis, dtype=np.float64)[None, :16]))
+    out[:3] = col.cpu().numpy()[0]
+    return int(mask.item())
+
+
+def composite_segments(seg_cells, seg_t0, seg_t1, nseg, sigma, sh, basis, bg_r, bg_g, bg_b,
+                       out_rgb):
+    """kernels.py:165-196: returns (residual transmittance, weight sum)."""
+    off, cells, t0, t1 = _one_ray_segments(seg_cells, seg_t0, seg_t1, nseg)
+    rgb, T, ws = dv.composite_segments_device(
+        _dev(sigma), _dev(np.asarray(sh).reshape(-1, 48)),
+        _dev(np.asarray(basis, dtype=np.float64)[None, :16]), off, cells, t0, t1,
+        (bg_r, bg_g, bg_b))
+    out_rgb[:3] = rgb.cpu().numpy()[0]
+    return float(T.item()), float(ws.item())
+
+
+def backward_ray(positions, offsets, neighbors, sigma, sh, background, ox, oy, oz, dx, dy, dz,
+                 adj_r, adj_g, adj_b, seg_cells, seg_t0, seg_t1, nseg, t_min_q, basis, d_sigma,
+                 d_sh, d_pos):
+    """kernels.py:250-337: accumulates into d_sigma (n), d_sh (n, 48), d_pos (n, 3)."""
+    if int(nseg) == 0:
+        return
+    off, cells, t0, t1 = _one_ray_segments(seg_cells, seg_t0, seg_t1, nseg)
+    n = len(sigma)
+    gs = torch.zeros(n, dtype=torch.float64, device="cuda")
+    gsh = torch.zeros((n, 48), dtype=torch.float64, device="cuda")
+    gp = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+    dv.backward_segments_device(
+        _dev(positions), _dev(sigma), _dev(np.asarray(sh).reshape(-1, 48)), background,
+        _dev(np.array([[ox, oy, oz]])), _dev(np.array([[dx, dy, dz]])),
+        _dev(np.asarray(basis, dtype=np.float64)[None, :16]),
+        _dev(np.array([[adj_r, adj_g, adj_b]])), off, cells, t0, t1, gs, gsh, gp)
+    d_sigma += gs.cpu().numpy()
+    d_sh.reshape(n, 48)[...] += gsh.cpu().numpy()
+    d_pos += gp.cpu().numpy()
+
+
+def face_t_gradient(positions, i, j, ox, oy, oz, dx, dy, dz, t, dt, d_pos):
+    """kernels.py:340-369: accumulates dt * dt/d(x_i, x_j) into d_pos (n, 3)."""
+    gp = torch.zeros((len(positions), 3), dtype=torch.float64, device="cuda")
+    dv.face_t_gradients_device(
+        _dev(positions), torch.tensor([[int(i), int(j)]], dtype=torch.int32, device="cuda"),
+        _dev(np.array([[ox, oy, oz]])), _dev(np.array([[dx, dy, dz]])), _dev(np.array([t])),
+        _dev(np.array([dt])), gp)
+    d_pos += gp.cpu().numpy()
+
+
+def quantile_backward_ray(seg_cells, seg_t0, seg_t1, nseg, sigma, u_pair, weight_floor,
+                          positions, ox, oy, oz, dx, dy, dz, scale, d_sigma, d_pos):
+    """kernels.py:456-567: one (u1, u2) pair; returns the loss term."""
+    if int(nseg) == 0:
+        return 0.0
+    off, cells, t0, t1 = _one_ray_segments(seg_cells, seg_t0, seg_t1, nseg)
+    n = len(sigma)
+    gs = torch.zeros(n, dtype=torch.float64, device="cuda")
+    gp = torch.zeros((n, 3), dtype=torch.float64, device="cuda")
+    loss = dv.quantile_segments_device(
+        _dev(positions), _dev(sigma), _dev(np.array([[ox, oy, oz]])),
+        _dev(np.array([[dx, dy, dz]])), off, cells, t0, t1,
+        _dev(np.asarray(u_pair, dtype=np.float64).reshape(1, 1, 2)), weight_floor, scale, gs, gp)
+    d_sigma += gs.cpu().numpy()
+    d_pos += gp.cpu().numpy()
+    return float(loss.item())

@@ -9,7 +9,7 @@ for spec in "$@"; do
   for kv in $spec; do flags="$flags -D$kv"; done
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false -std=c++17 $flags \
        -Xcompiler -fPIC -shared -o build/variants/librfb_$name.so paper_2502_01157_b200/csrc/rfb.cu \
-       paper_2502_01157_b200/csrc/rfb_adjacency.cu &
+       paper_2502_01157_b200/csrc/rfb_adjacency.cu paper_2502_01157_b200/csrc/rfb_segments.cu &
 done
 wait
 ls build/variants
