@@ -95,6 +95,8 @@ struct Args {
     int32_t *deg;            // [n]
     uint8_t *hull;           // [n]
     int32_t *tail;           // [n] sorted indices of sites queued for pass 2
+    float *tail_key;         // [n] their cell extent after the spiral (schedule key)
+    int32_t *tail_next;      // pass-2 work counter
     int32_t *flags;          // [0]: OR of errors, [1]: sites queued for pass 2,
                              // [2]: max vertices, [3]: max planes used
 };
@@ -483,9 +485,76 @@ __global__ void __launch_bounds__(32 * kWarps) k_voronoi(Args A) {
         } else if (lane == 0) {  // not final after the spiral, or outgrew the buffer
             const int q = atomicAdd(A.flags + 1, 1);
             A.tail[q] = (int32_t)k;
+            A.tail_key[q] = (float)S.R2;
         }
         __syncwarp();
     }
+}
+
+// Unbounded cells (their vertices on the box are "far") are what makes pass 2
+// expensive: the far vertices' balls B(v, |v|) cover half-spaces, so the ball
+// box spans the grid.  The few far vertices are kept apart; a site x (local
+// coordinates) can cut the cell only if |x| < 2 Rn (Rn = farthest non-box
+// vertex) or |x|^2 - 2 x.v < 0 for a far vertex v.
+constexpr int kMaxFar = 32;
+struct FarSet {
+    double x[kMaxFar], y[kMaxFar], z[kMaxFar];
+    double Rn2;  // max |v|^2 over vertices not on the box
+    int n;       // far vertices, or -1 when there are too many (no pruning)
+};
+
+template <class Cell>
+__device__ void far_refresh(const Cell &C, int lane, const CellState &S, FarSet &F,
+                            int32_t *prof = nullptr) {
+    double m = 0.0;
+    int cnt = 0;
+    for (int base = 0; base < S.nv; base += 32) {
+        const int v = base + lane;
+        bool far = false;
+        double r2 = 0.0;
+        if (v < S.nv) {
+            const uint32_t t = C.tri[v];
+            far = C.pid[t & 255] < 0 || C.pid[(t >> 8) & 255] < 0 || C.pid[(t >> 16) & 255] < 0;
+            r2 = C.vx[v] * C.vx[v] + C.vy[v] * C.vy[v] + C.vz[v] * C.vz[v];
+            if (!far) m = fmax(m, r2);
+        }
+        const unsigned fm = __ballot_sync(kFull, far);
+        if (far) {
+            const int slot = cnt + __popc(fm & lanemask_lt());
+            if (slot < kMaxFar) {
+                F.x[slot] = C.vx[v];
+                F.y[slot] = C.vy[v];
+                F.z[slot] = C.vz[v];
+            }
+        }
+        cnt += __popc(fm);
+    }
+    m = warp_max(m);
+    if (lane == 0) {
+        F.Rn2 = m;
+        F.n = cnt <= kMaxFar ? cnt : -1;
+#if RFB_ADJ_PROFILE
+        if (prof) atomicMax(prof, cnt);  // largest far-vertex count seen
+#endif
+    }
+}
+
+// Can any point of the local box [l, h] lie in some far ball?  (|x|^2 - 2 x.v
+// minimised per axis at the box point nearest v; no |v|^2 is formed, so the
+// huge radii cost no precision; the slack is relative.)
+__device__ __forceinline__ bool box_meets_far(const FarSet &F, const double *l, const double *h) {
+    for (int k = 0; k < F.n; ++k) {
+        const double v[3] = {F.x[k], F.y[k], F.z[k]};
+        double sum = 0.0, mag = 0.0;
+        for (int a = 0; a < 3; ++a) {
+            const double xa = fmin(fmax(v[a], l[a]), h[a]);
+            const double term = xa * xa - 2.0 * xa * v[a];
+            sum += term;
+            mag += fabs(term);
+        }
+        if (sum < 1e-12 * mag) return true;
+    }
+    return false;
 }
 
 // Grid-cell bounds of the union of the vertex balls B(v, |v|) (warp 0).
@@ -570,10 +639,18 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
     __shared__ bool fin;
     __shared__ int32_t queue[kTailQueue];
     __shared__ int qn, box[6];
+    __shared__ FarSet far;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const Grid &g = A.g;
     const int rmax = max(max(g.dim[0], g.dim[1]), g.dim[2]);
-    for (int32_t item = blockIdx.x; item < count; item += gridDim.x) {
+    __shared__ int32_t s_item;
+    for (;;) {
+        // dynamic schedule over the queue, sorted by decreasing cell extent
+        // (longest-processing-time first: the unbounded cells start first)
+        if (tid == 0) s_item = atomicAdd(A.tail_next, 1);
+        __syncthreads();
+        const int32_t item = s_item;
+        if (item >= count) break;
 #if RFB_ADJ_PROFILE
         const long long clk0 = clock64();
 #endif
@@ -587,6 +664,7 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
             init_cell(C, lane, A.box, S);
             const bool done = spiral_phase(A, C, lane, s, self, ix, iy, iz, S);
             ball_box(C, lane, S, s, g, box);
+            far_refresh(C, lane, S, far, A.flags + 7);
             if (lane == 0) {
                 fin = done || S.err != 0;
                 SS = S;
@@ -599,6 +677,8 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
             // or the ring lies outside the ball box
             const double lb = (double)(r - 1) * g.h;
             if (lb * lb >= 4.0 * SS.R2 * (1.0 + 1e-12)) break;
+            // with no far vertices Rn = R, and the line above is the security radius
+            const bool use_far = far.n > 0;
             if (max(max(ix - box[0], box[3] - ix), max(max(iy - box[1], box[4] - iy),
                                                        max(iz - box[2], box[5] - iz))) < r)
                 break;
@@ -609,7 +689,20 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                 if (t < total) {
                     int cx, cy, cz;
                     RB.cell(t, cx, cy, cz);
-                    {
+                    bool live = true;
+                    if (use_far) {  // cell box (local): beyond 2 Rn and outside every far ball?
+                        const double l[3] = {g.lo[0] + cx * g.h - s.x, g.lo[1] + cy * g.h - s.y,
+                                             g.lo[2] + cz * g.h - s.z};
+                        const double h[3] = {l[0] + g.h, l[1] + g.h, l[2] + g.h};
+                        double dmin2 = 0.0;
+                        for (int a = 0; a < 3; ++a) {
+                            const double da = l[a] > 0.0 ? l[a] : (h[a] < 0.0 ? -h[a] : 0.0);
+                            dmin2 += da * da;
+                        }
+                        live = dmin2 < 4.0 * far.Rn2 * (1.0 + 1e-9) + 1e-300 ||
+                               box_meets_far(far, l, h);
+                    }
+                    if (live) {
                         const int cell = cell_index(g, cx, cy, cz);
                         const int c0 = __ldg(A.cstart + cell), c1 = __ldg(A.cstart + cell + 1);
                         for (int q = c0; q < c1; ++q) {
@@ -623,8 +716,17 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                             if (!may_cut(SS, dx, dy, dz, d2)) continue;
                             const double o = 0.5 * d2;
                             bool cut = false;
-                            for (int v = 0; v < SS.nv && !cut; ++v)
-                                cut = dx * C.vx[v] + dy * C.vy[v] + dz * C.vz[v] > o;
+                            if (use_far && d2 >= 4.0 * far.Rn2 * (1.0 + 1e-9)) {
+                                // beyond 2 Rn only the far vertices can be cut (conservative
+                                // test; clip() decides exactly)
+                                for (int k = 0; k < far.n && !cut; ++k) {
+                                    const double pv = dx * far.x[k] + dy * far.y[k] + dz * far.z[k];
+                                    cut = d2 - 2.0 * pv < 1e-12 * (d2 + 2.0 * fabs(pv));
+                                }
+                            } else {
+                                for (int v = 0; v < SS.nv && !cut; ++v)
+                                    cut = dx * C.vx[v] + dy * C.vy[v] + dz * C.vz[v] > o;
+                            }
                             if (cut) {
                                 const int slot = atomicAdd(&qn, 1);
                                 if (slot < kTailQueue) queue[slot] = q;
@@ -652,7 +754,10 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                 __syncthreads();
                 if (nq > kTailQueue) t0 -= kTailThreads;  // overflowed: this batch again
             }
-            if (warp == 0) ball_box(C, lane, SS, s, g, box);
+            if (warp == 0) {
+                ball_box(C, lane, SS, s, g, box);
+                far_refresh(C, lane, SS, far, A.flags + 7);
+            }
             __syncthreads();
         }
         if (warp == 0) {
@@ -818,7 +923,8 @@ static std::vector<int4> spiral_table() {
 static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 struct Layout {
-    size_t keys, keys2, vals, vals2, pos, cstart, rows, deg, hull, spiral, flags, part, miss, tail, deg64,
+    size_t keys, keys2, vals, vals2, pos, cstart, rows, deg, hull, spiral, flags, part, miss, tail,
+        tail_key, deg64,
         cub, total;
 };
 
@@ -836,10 +942,11 @@ static Layout layout(int64_t n, int32_t cap, int64_t max_cells) {
     L.deg = take(4 * n);
     L.hull = take(n);
     L.spiral = take(sizeof(int4) * kSpiralN);
-    L.flags = take(64);
+    L.flags = take(128);
     L.part = take(6 * 8 * 1024);
     L.miss = take(8 * (size_t)std::max<int64_t>(n, 1024));
     L.tail = take(4 * n);
+    L.tail_key = take(4 * n);
     L.deg64 = take(8 * (n + 1));
     size_t cub_sort = 0, cub_scan = 0;
     cub::DoubleBuffer<uint32_t> kb(nullptr, nullptr);
@@ -878,7 +985,7 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
     char *ws = (char *)workspace;
     for (int k = 0; k < 8; ++k) stats[k] = 0;
     int32_t *flags = (int32_t *)(ws + L.flags);
-    cudaMemsetAsync(flags, 0, 64, st);
+    cudaMemsetAsync(flags, 0, 128, st);
     // finite coordinates (delaunay.py:456-457) and bounding box
     k_finite<<<1024, 256, 0, st>>>(positions, 3 * n, flags + 4);
     double *part = (double *)(ws + L.part);
@@ -958,6 +1065,8 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
     A.hull = (uint8_t *)(ws + L.hull);
     A.flags = flags;
     A.tail = (int32_t *)(ws + L.tail);
+    A.tail_key = (float *)(ws + L.tail_key);
+    A.tail_next = flags + 16;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -974,7 +1083,17 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tper, k_voronoi_tail, kTailThreads, 0);
         const unsigned tgrid =
             (unsigned)std::min<int64_t>(hflags[1], (int64_t)sms * std::max(tper, 1));
-        k_voronoi_tail<<<tgrid, kTailThreads, 0, st>>>(A, hflags[1]);
+        // schedule by decreasing extent: sort (key, site) pairs descending
+        const int cnt = hflags[1];
+        float *k2 = (float *)(ws + L.keys);   // reuse the grid-sort buffers (no longer read)
+        int32_t *v2 = (int32_t *)(ws + L.keys2);
+        cub::DoubleBuffer<float> tkb(A.tail_key, k2);
+        cub::DoubleBuffer<int32_t> tvb(A.tail, v2);
+        size_t tb = workspace_bytes - L.cub;
+        cub::DeviceRadixSort::SortPairsDescending(ws + L.cub, tb, tkb, tvb, cnt, 0, 32, st);
+        A.tail = tvb.Current();
+        cudaMemsetAsync(A.tail_next, 0, sizeof(int32_t), st);
+        k_voronoi_tail<<<tgrid, kTailThreads, 0, st>>>(A, cnt);
     }
     // symmetrise (union): queue reverse edges that are missing
     int2 *miss = (int2 *)(ws + L.miss);
@@ -991,6 +1110,7 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
     stats[6] = *reinterpret_cast<int64_t *>(hflags + 10);  // clip tests, rings (profile)
     stats[7] = hflags[0];  // error flags (1 overflow, 2 duplicate, 4 degenerate)
 #if RFB_ADJ_PROFILE
+    stats[4] = hflags[7];  // (profile) largest far-vertex count
     cudaMemcpy(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost);
     stats[5] = *reinterpret_cast<int64_t *>(hflags + 12);  // pass-2 cycles (all sites)
     stats[6] = *reinterpret_cast<int64_t *>(hflags + 14);  // pass-2 cycles (hull sites)
