@@ -18,15 +18,6 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef RFB_SUBTILE_W
 #define RFB_SUBTILE_W 4  // a warp's 32 rays cover a 4 x 8 pixel patch (measured best)
 #endif
-constexpr int kBlockTile = 1024;  // rays claimed per block at a time (one 32x32 tile)
-#ifndef RFB_BLOCK_TILES
-#define RFB_BLOCK_TILES 0
-#endif
-#ifndef RFB_OTF_BASIS
-#define RFB_OTF_BASIS 0
-#endif
-constexpr bool kBlockTiles = RFB_BLOCK_TILES != 0;
-constexpr bool kOtfBasis = RFB_OTF_BASIS != 0;
 #ifndef RFB_F32_FILTER
 #define RFB_F32_FILTER 1
 #endif
@@ -271,15 +262,8 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
     constexpr int kRayFields = Src::kUniform ? 4 : 9;
     __shared__ double s_ray[kRayFields * 256];
     __shared__ double s_uni[5];
-    __shared__ float s_basis[kOtfBasis ? 1 : 16 * 256];  // [k][thread] when not on the fly
-    // block-level work claiming: the block takes kBlockTile consecutive rays
-    // (one 32x32 image tile for rfb_render_image) at a time and its warps
-    // split it, so co-resident warps walk the same cells and share L1.
-    __shared__ int s_lock, s_used;
-    __shared__ unsigned long long s_tile;
+    __shared__ float s_basis[16 * 256];  // fp32 SH basis, [k][thread]
     if (threadIdx.x == 0) {
-        s_lock = 0;
-        s_used = kBlockTile;
         if constexpr (Src::kUniform) src.uniform(s_uni);
     }
     __syncthreads();
@@ -291,24 +275,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
 
     for (;;) {
         unsigned long long base = 0;
-        if (!kBlockTiles) {
-            if (lane == 0) base = atomicAdd(ray_counter, (unsigned long long)RPW);
-        } else if (lane == 0) {
-            while (atomicCAS(&s_lock, 0, 1) != 0) {
-            }
-            __threadfence_block();
-            int used = *(volatile int *)&s_used;
-            unsigned long long tile = *(volatile unsigned long long *)&s_tile;
-            if (used + RPW > kBlockTile) {
-                tile = atomicAdd(ray_counter, (unsigned long long)kBlockTile);
-                used = 0;
-                *(volatile unsigned long long *)&s_tile = tile;
-            }
-            base = tile + (unsigned long long)used;
-            *(volatile int *)&s_used = used + RPW;
-            __threadfence_block();
-            atomicExch(&s_lock, 0);
-        }
+        if (lane == 0) base = atomicAdd(ray_counter, (unsigned long long)RPW);
         base = __shfl_sync(kFull, base, 0);
         if ((int64_t)base >= total) break;
         int64_t q = (int64_t)base + lane / G;
@@ -332,13 +299,11 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
             if (SHDEG > 0) {
                 float bf[16];
                 *bsum_p = basis_setup(rr, bf);
-                if constexpr (!kOtfBasis) {
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) s_basis[k * 256 + threadIdx.x] = bf[k];
-                }
+                for (int k = 0; k < 16; ++k) s_basis[k * 256 + threadIdx.x] = bf[k];
             } else {
                 *bsum_p = kC0;
-                if constexpr (!kOtfBasis) s_basis[threadIdx.x] = (float)kC0;
+                s_basis[threadIdx.x] = (float)kC0;
             }
         }
         // colour accumulation in fp32 (image tolerance 1e-4); transmittance and
@@ -354,16 +319,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 double delta = t1 - t0;
                 const double alpha = (double)(-expm1f(-(float)(sigma * delta)));
                 double col[3];
-                if constexpr (kOtfBasis) {
-                    float bf[16];  // on-the-fly fp32 basis (registers only during colour)
-                    if (SHDEG > 0)
-                        sh_basis_f32((float)r.dx(), (float)r.dy(), (float)r.dz(), bf);
-                    else
-                        bf[0] = (float)kC0;
-                    cell_color<SHDEG, PACKED, 1, true>(S, cell, bf, r, *bsum_p, col);
-                } else {
-                    cell_color<SHDEG, PACKED, 256>(S, cell, s_basis + threadIdx.x, r, *bsum_p, col);
-                }
+                cell_color<SHDEG, PACKED, 256>(S, cell, s_basis + threadIdx.x, r, *bsum_p, col);
                 const double w = T * alpha;
                 wsum += w;
                 const float wf = (float)w;
@@ -476,9 +432,6 @@ __device__ __forceinline__ unsigned order_key(double t) {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-#ifndef RFB_REV_PREFETCH
-#define RFB_REV_PREFETCH 0  // reverse pass: load the next segment's record one iteration ahead
-#endif
 constexpr int kTrainBlock = 128;
 constexpr int kTrainWarps = kTrainBlock / 32;
 
@@ -686,17 +639,6 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         float tb1 = 0.f, tb0 = 1.f;
         float Sr = 0.f, Sg = 0.f, Sb = 0.f, d_next = 0.f;
         double sig_next = 0.0;  // sigma of next_cell (quantile boundary terms)
-#if RFB_REV_PREFETCH
-        // next segment's record one iteration ahead (the workspace lives in DRAM)
-        int32_t p_cm = 0;
-        double p_t = 0.0;
-        float p_tb = 1.f;
-        auto prefetch = [&]() {
-            p_cm = s >= 1 ? s_cell[(s - 1) * SL] : 0;
-            p_t = s >= 2 ? s_t1[(s - 2) * SL] : r.t_min();
-            p_tb = s >= 2 ? (float)s_tb[(s - 2) * SL] : 1.f;
-        };
-#endif
         auto load_seg = [&]() {
             const int32_t cm = s_cell[s * SL];
             ci = cm & 0x1fffffff;
@@ -705,9 +647,6 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
             t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min();
             tb1 = (float)s_tb[s * SL];
             tb0 = s > 0 ? (float)s_tb[(s - 1) * SL] : 1.f;
-#if RFB_REV_PREFETCH
-            prefetch();
-#endif
         };
         if (s >= 0) {
             load_seg();
@@ -782,25 +721,13 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 next_cell = ci;
                 s -= 1;
                 if (s >= 0) {  // segment s's end is segment s+1's start: reuse it
-#if RFB_REV_PREFETCH
-                    const int32_t cm = p_cm;
-#else
                     const int32_t cm = s_cell[s * SL];
-#endif
                     ci = cm & 0x1fffffff;
                     cmask = (cm >> 29) & 7;
-#if RFB_REV_PREFETCH
-                    t1 = t0;
-                    tb1 = tb0;
-                    t0 = p_t;
-                    tb0 = p_tb;
-                    prefetch();
-#else
                     t1 = t0;
                     tb1 = tb0;
                     t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min();
                     tb0 = s > 0 ? (float)s_tb[(s - 1) * SL] : 1.f;
-#endif
                 }
             }
             // previous cell: aggregated when the whole group agrees on it

@@ -192,30 +192,6 @@ struct SceneView {
 // recomputed exactly (fp64 basis from the direction, fp64 coefficients), so
 // the clamp mask -- which gates the SH gradient -- is always the reference's
 // and the colour is within ~1e-6 of it.
-// fp32 SH basis of an fp32 direction (same formulas as sh_basis).  Each value
-// is within 2^-18 of the fp64 basis of the fp64 direction: <= ~5 roundings of
-// the inputs/products (|.| <= 1.9) plus the (5z^2-1)-style differences
-// (<= 29u absolute), i.e. < 30u = 2^-19.1.
-__device__ __forceinline__ void sh_basis_f32(float dx, float dy, float dz, float *out) {
-    const float xx = dx * dx, yy = dy * dy, zz = dz * dz;
-    out[0] = (float)kC0;
-    out[1] = (float)kC1 * dy;
-    out[2] = (float)kC1 * dz;
-    out[3] = (float)kC1 * dx;
-    out[4] = (float)kC2_0 * dx * dy;
-    out[5] = (float)kC2_0 * dy * dz;
-    out[6] = (float)kC2_2 * (3.0f * zz - 1.0f);
-    out[7] = (float)kC2_0 * dx * dz;
-    out[8] = (float)kC2_4 * (xx - yy);
-    out[9] = (float)kC3_0 * dy * (3.0f * xx - yy);
-    out[10] = (float)kC3_1 * dx * dy * dz;
-    out[11] = (float)kC3_2 * dy * (5.0f * zz - 1.0f);
-    out[12] = (float)kC3_3 * dz * (5.0f * zz - 3.0f);
-    out[13] = (float)kC3_2 * dx * (5.0f * zz - 1.0f);
-    out[14] = (float)kC3_5 * dz * (xx - yy);
-    out[15] = (float)kC3_0 * dx * (xx - 3.0f * yy);
-}
-
 // Reference-exact channel value (kernels.py:66-68) from the fp64 table;
 // out of line so its registers do not count against the walk.
 static __device__ __noinline__ double exact_channel(const double *row, int ch, int nb, double dx,
@@ -227,9 +203,8 @@ static __device__ __noinline__ double exact_channel(const double *row, int ch, i
     return a;
 }
 
-// OTF: basis_f is the on-the-fly fp32 basis (sh_basis_f32), within 2^-18 per
-// value of the fp64 basis -> extra colour error <= 16 * cmax * 2^-18.
-template <int SHDEG, bool PACKED, int BSTRIDE = 1, bool OTF = false, class RayT>
+// basis_f: the ray's fp32 SH basis (BSTRIDE apart); bsum = sum |fp64 basis|.
+template <int SHDEG, bool PACKED, int BSTRIDE = 1, class RayT>
 __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
                                           const float *basis_f, const RayT &ray,
                                           double bsum, double *col) {
@@ -281,8 +256,7 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
             for (int ch = 0; ch < 3; ++ch) acc[ch] += basis[k] * __ldg(row + k * 3 + ch);
     }
     const double tol =
-        PACKED ? ((double)cmax * bsum + 1.0) * 0x1p-19 + (OTF ? (double)cmax * 0x1p-14 : 0.0)
-               : 0.0;
+        PACKED ? ((double)cmax * bsum + 1.0) * 0x1p-19 : 0.0;
     int mask = 0;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
