@@ -40,8 +40,14 @@
 namespace rfb_adj {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kWarps = 2;          // sites (warps) per block
-constexpr int kMaxPlanes = 128;    // pass-1 planes per cell, box included (8-bit ids)
+#ifndef RFB_ADJ_WARPS
+#define RFB_ADJ_WARPS 2
+#endif
+#ifndef RFB_ADJ_MAX_PLANES
+#define RFB_ADJ_MAX_PLANES 128
+#endif
+constexpr int kWarps = RFB_ADJ_WARPS;            // sites (warps) per block
+constexpr int kMaxPlanes = RFB_ADJ_MAX_PLANES;   // pass-1 planes per cell, box included
 #ifndef RFB_ADJ_MAX_VERTS
 #define RFB_ADJ_MAX_VERTS 256
 #endif
@@ -468,7 +474,10 @@ __device__ __forceinline__ void site_cell(const Grid &g, const double4 &s, int &
 
 // Pass 1: one warp per site, spiral only.  Cells not final after the
 // spiral (near the hull: long or unbounded cells) are queued for pass 2.
-__global__ void __launch_bounds__(32 * kWarps) k_voronoi(Args A) {
+#ifndef RFB_ADJ_MINB
+#define RFB_ADJ_MINB 1
+#endif
+__global__ void __launch_bounds__(32 * kWarps, RFB_ADJ_MINB) k_voronoi(Args A) {
     __shared__ WarpCell cells[kWarps];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     WarpCell &C = cells[w];
@@ -975,7 +984,7 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
                         uint8_t *hull, int64_t *stats, void *workspace, size_t workspace_bytes,
                         void *stream) {
     if (!positions || !offsets || !stats || n_sites <= 0 || n_sites >= (1 << 30) ||
-        max_degree <= 0 || max_degree > kMaxPlanes)
+        max_degree <= 0 || max_degree > BigCell::kPlanes)
         return RFB_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = n_sites;
