@@ -80,3 +80,46 @@ def test_device_training_iteration(cuda_ok):
     assert float(tr.loss[0]) == pytest.approx(g["loss_w"].sum(0)[0], rel=1e-6)
     s4 = tr.ds.site4.cpu().numpy()
     np.testing.assert_allclose(s4[:, 3], softplus(tr.raw.cpu().numpy()), rtol=1e-13)
+
+
+def test_device_training_loop_with_rebuilds(cuda_ok):
+    """Several device-resident iterations (train_batch + Adam + refresh) with
+    the Delaunay adjacency rebuilt on the device every few steps, as the
+    reference's loop does (optim/train.py:247-256): the loss falls, and after
+    each rebuild the device CSR equals a host (Qhull) triangulation of the
+    moved sites."""
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200.synthetic import delaunay_csr
+    from paper_2502_01157_b200.train import DeviceTrainer
+
+    g = load_golden("train_2k_deg3_q")
+    scene = golden_scene(g)
+    d = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)  # noqa
+    # targets: the scene's own render with perturbed colours (a reachable fit)
+    rng = np.random.default_rng(8)
+    m = 4096
+    o = np.tile([0.0, 0.0, 3.0], (m, 1))
+    dirs = rng.normal(size=(m, 3)) * [0.25, 0.25, 0.0] + [0.0, 0.0, -1.0]
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    tr = DeviceTrainer(scene)
+    start = int(tr.ds.locate(d(o[:1])).item())
+    tmax = tr.ds.default_t_max(o[:1])
+    ref = dv.render_rays_device(tr.ds, d(o), d(dirs), d(np.zeros(m)), d(np.full(m, tmax)),
+                                d(np.full(m, start), torch.int32), f64=True)
+    targets = (ref.rgb * 0.8 + 0.1).contiguous()
+    losses = []
+    for it in range(12):
+        start = int(tr.ds.locate(d(o[:1])).item())
+        tmax = tr.ds.default_t_max(o[:1])
+        loss = tr.step(d(o), d(dirs), d(np.zeros(m)), d(np.full(m, tmax)),
+                       d(np.full(m, start), torch.int32), targets, lr_position=1e-4,
+                       lr_density=0.05, lr_sh=2e-2)
+        losses.append(float(loss[0].item()) / (3 * m))
+        if (it + 1) % 4 == 0:
+            info = tr.rebuild_adjacency()
+            pos = tr.positions.cpu().numpy()
+            off, nbr, _ = delaunay_csr(pos)
+            np.testing.assert_array_equal(tr.ds.offsets.cpu().numpy(), off)
+            np.testing.assert_array_equal(tr.ds.neighbors.cpu().numpy(), nbr)
+            assert info["reverse_edges_added"] == 0
+    assert losses[-1] < 0.7 * losses[0], losses
