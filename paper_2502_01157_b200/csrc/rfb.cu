@@ -373,10 +373,10 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
 // fp32 accumulators changes.
 // ---------------------------------------------------------------------------
 struct Scratch {
-    int32_t *cell;  // [cap][slots]: cell id | clamp mask << 29
-    double *t1;     // [cap][slots]: exit depth (the entry of s+1)
-    double *tb;     // [cap][slots]: T_before[s+1] = prod exp(-sigma*delta) (kernels.py:270-275)
-    float *col;     // [3*cap][slots]: clamped colour
+    // one 32-byte record per segment in two 16-byte halves (one vector store each):
+    float4 *a;      // [cap][slots]: {cell id | clamp mask << 29 (int bits), clamped colour rgb}
+    double2 *b;     // [cap][slots]: {exit depth t1 (the entry of s+1),
+                    //                T_before[s+1] = prod exp(-sigma*delta) (kernels.py:270-275)}
     int64_t slots;
 };
 
@@ -451,14 +451,21 @@ struct QHit {
 };
 template <class RayT>
 __device__ __forceinline__ QHit quantile_hit(const double4 *__restrict__ site4, const int32_t *cellp,
-                                             const double *t1p, const double *tbp, int64_t SL,
-                                             int32_t nseg, const RayT &r, double u, double tot) {
+                                             int64_t SLa, const double *t1p, const double *tbp,
+                                             int64_t SL, int32_t nseg, const RayT &r, double u,
+                                             double tot) {
     const double target = u * tot;
-    int32_t sh = 0;
-    while (sh < nseg - 1 && (1.0 - tbp[sh * SL]) < target) sh += 1;
+    // first segment with W_{s+1} = 1 - T_before[s+1] >= target (capped at the
+    // last), as kernels.py:503-505's linear scan: T_before is non-increasing
+    // (every factor exp(-sigma*delta) <= 1), so a binary search finds the same one
+    int32_t sh = 0, hi = nseg - 1;
+    while (sh < hi) {
+        const int32_t mid = (sh + hi) >> 1;
+        if ((1.0 - tbp[mid * SL]) < target) sh = mid + 1; else hi = mid;
+    }
     QHit h;
     h.seg = sh;
-    h.sigma = ld_sigma(site4 + (cellp[sh * SL] & 0x1fffffff));
+    h.sigma = ld_sigma(site4 + (cellp[sh * SLa] & 0x1fffffff));
     const double ts0 = sh > 0 ? t1p[(sh - 1) * SL] : r.t_min();
     const double Tbs = sh > 0 ? tbp[(sh - 1) * SL] : 1.0;
     if (h.sigma <= 0.0) {
@@ -491,11 +498,15 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
     __shared__ double s_qg[QUANT ? kQSamples : 1][kTrainBlock];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t slot = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t SL = scr.slots;
-    int32_t *s_cell = scr.cell + slot;
-    double *s_t1 = scr.t1 + slot;
-    double *s_tb = scr.tb + slot;
-    float *s_col = scr.col + slot;
+    // strided views of this slot's records: s_cell steps SLa ints per segment,
+    // s_t1 / s_tb step SL doubles (the two halves of rec_b are interleaved)
+    const int64_t SL4 = scr.slots;             // records per segment row
+    const int64_t SLa = 4 * SL4, SL = 2 * SL4;
+    float4 *rec_a = scr.a + slot;
+    double2 *rec_b = scr.b + slot;
+    const int32_t *s_cell = reinterpret_cast<const int32_t *>(rec_a);
+    const double *s_t1 = reinterpret_cast<const double *>(rec_b);
+    const double *s_tb = s_t1 + 1;
     double loss_rgb = 0.0, loss_q = 0.0;
     unsigned int my_cells = 0, my_visits = 0;
     const int64_t total = src.count();
@@ -552,12 +563,9 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                     cg += wf * (float)col[1];
                     cb += wf * (float)col[2];
                     Tb = Tn;
-                    s_cell[s * SL] = cell | (mask << 29);
-                    s_t1[s * SL] = t1;
-                    s_tb[s * SL] = Tn;
-                    s_col[(3 * s) * SL] = (float)col[0];
-                    s_col[(3 * s + 1) * SL] = (float)col[1];
-                    s_col[(3 * s + 2) * SL] = (float)col[2];
+                    rec_a[s * SL4] = make_float4(__int_as_float(cell | (mask << 29)),
+                                                 (float)col[0], (float)col[1], (float)col[2]);
+                    rec_b[s * SL4] = make_double2(t1, Tn);
                 });
             my_cells += (unsigned)cells;
             my_visits += (unsigned)visits;
@@ -602,9 +610,9 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 if (!(tot < weight_floor)) {
                     for (int32_t p = 0; p < np; ++p) {
                         const double *up = u_pairs + (q * n_pairs + p) * 2;
-                        const QHit h0 = quantile_hit(S.site4, s_cell, s_t1, s_tb, SL, nseg, r,
+                        const QHit h0 = quantile_hit(S.site4, s_cell, SLa, s_t1, s_tb, SL, nseg, r,
                                                      up[0], tot);
-                        const QHit h1 = quantile_hit(S.site4, s_cell, s_t1, s_tb, SL, nseg, r,
+                        const QHit h1 = quantile_hit(S.site4, s_cell, SLa, s_t1, s_tb, SL, nseg, r,
                                                      up[1], tot);
                         const double diff = h0.t - h1.t;
                         loss_q += fabs(diff);
@@ -640,7 +648,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         float Sr = 0.f, Sg = 0.f, Sb = 0.f, d_next = 0.f;
         double sig_next = 0.0;  // sigma of next_cell (quantile boundary terms)
         auto load_seg = [&]() {
-            const int32_t cm = s_cell[s * SL];
+            const int32_t cm = s_cell[s * SLa];
             ci = cm & 0x1fffffff;
             cmask = (cm >> 29) & 7;
             t1 = s_t1[s * SL];
@@ -674,8 +682,8 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 const float sig = (float)sig_d;
                 const float delta = (float)(t1 - t0);
                 const float w = tb0 - tb1;
-                const float c0 = s_col[(3 * s) * SL], c1 = s_col[(3 * s + 1) * SL],
-                            c2 = s_col[(3 * s + 2) * SL];
+                const float4 ra = rec_a[s * SL4];  // one 16-byte load: cell bits + colour
+                const float c0 = ra.y, c1 = ra.z, c2 = ra.w;
                 const float common =
                     ar * (tb1 * c0 - Sr) + ag * (tb1 * c1 - Sg) + ab * (tb1 * c2 - Sb);
                 v[6] = delta * common;
@@ -721,13 +729,19 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 next_cell = ci;
                 s -= 1;
                 if (s >= 0) {  // segment s's end is segment s+1's start: reuse it
-                    const int32_t cm = s_cell[s * SL];
+                    const int32_t cm = s_cell[s * SLa];
                     ci = cm & 0x1fffffff;
                     cmask = (cm >> 29) & 7;
                     t1 = t0;
                     tb1 = tb0;
-                    t0 = s > 0 ? s_t1[(s - 1) * SL] : r.t_min();
-                    tb0 = s > 0 ? (float)s_tb[(s - 1) * SL] : 1.f;
+                    if (s > 0) {
+                        const double2 rb = rec_b[(s - 1) * SL4];  // {t0, T_before[s]}
+                        t0 = rb.x;
+                        tb0 = (float)rb.y;
+                    } else {
+                        t0 = r.t_min();
+                        tb0 = 1.f;
+                    }
                 }
             }
             // previous cell: aggregated when the whole group agrees on it
@@ -782,8 +796,8 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 for (int32_t p = kQFusedPairs; p < n_pairs; ++p) {
                     const double *up = u_pairs + (q * n_pairs + p) * 2;
                     const QHit hh[2] = {
-                        quantile_hit(S.site4, s_cell, s_t1, s_tb, SL, nseg, r, up[0], tot),
-                        quantile_hit(S.site4, s_cell, s_t1, s_tb, SL, nseg, r, up[1], tot)};
+                        quantile_hit(S.site4, s_cell, SLa, s_t1, s_tb, SL, nseg, r, up[0], tot),
+                        quantile_hit(S.site4, s_cell, SLa, s_t1, s_tb, SL, nseg, r, up[1], tot)};
                     const double diff = hh[0].t - hh[1].t;
                     loss_q += fabs(diff);
                     if (diff == 0.0) continue;
@@ -797,7 +811,7 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                         for (int32_t k = 0; k < nseg; ++k) {  // kernels.py:534-548
                             const double k_t0 = prev_t1, k_t1 = s_t1[k * SL];
                             prev_t1 = k_t1;
-                            const int32_t ck = s_cell[k * SL] & 0x1fffffff;
+                            const int32_t ck = s_cell[k * SLa] & 0x1fffffff;
                             const double dA = T_end_q * (k_t1 - k_t0);
                             double contrib;
                             if (k_t0 < t_u) {
@@ -809,8 +823,8 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                             atomicAdd(gr.g4 + 4 * (int64_t)ck + 3, (float)contrib);
                         }
                         for (int32_t mm = 1; mm < nseg; ++mm) {  // kernels.py:552-566
-                            const int32_t im = s_cell[(mm - 1) * SL] & 0x1fffffff;
-                            const int32_t jm = s_cell[mm * SL] & 0x1fffffff;
+                            const int32_t im = s_cell[(mm - 1) * SLa] & 0x1fffffff;
+                            const int32_t jm = s_cell[mm * SLa] & 0x1fffffff;
                             const double dsig = ld_sigma(S.site4 + im) - ld_sigma(S.site4 + jm);
                             if (dsig == 0.0) continue;
                             const double tbq = s_t1[(mm - 1) * SL];
@@ -1308,13 +1322,9 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     scr.slots = slots;
     const int64_t cap = p->step_limit;
     char *c = base + 256;
-    scr.t1 = reinterpret_cast<double *>(c);
-    c += cap * slots * 8;
-    scr.tb = reinterpret_cast<double *>(c);
-    c += cap * slots * 8;
-    scr.cell = reinterpret_cast<int32_t *>(c);
-    c += cap * slots * 4;
-    scr.col = reinterpret_cast<float *>(c);
+    scr.a = reinterpret_cast<float4 *>(c);
+    c += cap * slots * 16;
+    scr.b = reinterpret_cast<double2 *>(c);
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
     FwdOut O = dev_out(out);
     ArrayRays src{rays->origins, rays->directions, rays->t_min, rays->t_max, rays->start_sites,
