@@ -432,6 +432,9 @@ __device__ __forceinline__ unsigned order_key(double t) {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+#ifndef RFB_REV_COLREG
+#define RFB_REV_COLREG 1  // reverse pass: load cell + colour together when advancing
+#endif
 constexpr int kTrainBlock = 128;
 constexpr int kTrainWarps = kTrainBlock / 32;
 
@@ -647,8 +650,19 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
         float tb1 = 0.f, tb0 = 1.f;
         float Sr = 0.f, Sg = 0.f, Sb = 0.f, d_next = 0.f;
         double sig_next = 0.0;  // sigma of next_cell (quantile boundary terms)
+#if RFB_REV_COLREG
+        float cc0 = 0.f, cc1 = 0.f, cc2 = 0.f;  // colour of the current segment
+#endif
         auto load_seg = [&]() {
+#if RFB_REV_COLREG
+            const float4 ra = rec_a[s * SL4];
+            const int32_t cm = __float_as_int(ra.x);
+            cc0 = ra.y;
+            cc1 = ra.z;
+            cc2 = ra.w;
+#else
             const int32_t cm = s_cell[s * SLa];
+#endif
             ci = cm & 0x1fffffff;
             cmask = (cm >> 29) & 7;
             t1 = s_t1[s * SL];
@@ -682,8 +696,12 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 const float sig = (float)sig_d;
                 const float delta = (float)(t1 - t0);
                 const float w = tb0 - tb1;
+#if RFB_REV_COLREG
+                const float c0 = cc0, c1 = cc1, c2 = cc2;
+#else
                 const float4 ra = rec_a[s * SL4];  // one 16-byte load: cell bits + colour
                 const float c0 = ra.y, c1 = ra.z, c2 = ra.w;
+#endif
                 const float common =
                     ar * (tb1 * c0 - Sr) + ag * (tb1 * c1 - Sg) + ab * (tb1 * c2 - Sb);
                 v[6] = delta * common;
@@ -729,7 +747,15 @@ __global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
                 next_cell = ci;
                 s -= 1;
                 if (s >= 0) {  // segment s's end is segment s+1's start: reuse it
+#if RFB_REV_COLREG
+                    const float4 ra = rec_a[s * SL4];
+                    const int32_t cm = __float_as_int(ra.x);
+                    cc0 = ra.y;
+                    cc1 = ra.z;
+                    cc2 = ra.w;
+#else
                     const int32_t cm = s_cell[s * SLa];
+#endif
                     ci = cm & 0x1fffffff;
                     cmask = (cm >> 29) & 7;
                     t1 = t0;
