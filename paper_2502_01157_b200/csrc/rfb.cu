@@ -438,8 +438,13 @@ __device__ __forceinline__ unsigned order_key(double t) {
 constexpr int kTrainBlock = 128;
 constexpr int kTrainWarps = kTrainBlock / 32;
 
+// resident blocks per SM (register budget): 7 x 128 threads (72 regs) for the
+// L2 / adjoint passes, 6 (80 regs) when the quantile state is live (measured)
 #ifndef RFB_TRAIN_MINB
-#define RFB_TRAIN_MINB 6
+#define RFB_TRAIN_MINB 7
+#endif
+#ifndef RFB_TRAIN_MINB_Q
+#define RFB_TRAIN_MINB_Q 6
 #endif
 // Quantile pairs folded into the cooperative reverse pass (the first
 // kQFusedPairs pairs; any further pairs take the per-lane scatter path).
@@ -486,7 +491,7 @@ __device__ __forceinline__ QHit quantile_hit(const double4 *__restrict__ site4, 
 }
 
 template <int SHDEG, bool PACKED, bool TRAIN, bool QUANT>
-__global__ void __launch_bounds__(kTrainBlock, RFB_TRAIN_MINB) k_train(
+__global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TRAIN_MINB) k_train(
     SceneView<PACKED> S, ArrayRays src, double epsilon, double log_eps, double width_floor,
     int32_t step_limit, const double *adjoints, const double *targets, double rgb_scale,
     double q_scale, const double *u_pairs, int32_t n_pairs, double weight_floor, FwdOut O,
@@ -1291,9 +1296,14 @@ static int64_t bwd_slot_bytes(int32_t step_limit) {
     return (int64_t)step_limit * (4 + 8 + 8 + 12);
 }
 
-static int64_t bwd_slots_max() {
+static int64_t bwd_slots_max(bool quant) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_train<3, true, true, true>, kTrainBlock, 0);
+    if (quant)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_train<3, true, true, true>,
+                                                      kTrainBlock, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_train<3, true, true, false>,
+                                                      kTrainBlock, 0);
     return (int64_t)num_sms() * std::max(per_sm, 1) * kTrainBlock;
 }
 
@@ -1339,7 +1349,7 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     const int64_t per = bwd_slot_bytes(p->step_limit);
     if (!ws || ws_bytes < 256 + (size_t)per * kTrainBlock) return RFB_EINVAL;
     int64_t slots = (int64_t)((ws_bytes - 256) / (size_t)per);
-    slots = std::min<int64_t>(slots, bwd_slots_max());
+    slots = std::min<int64_t>(slots, bwd_slots_max(train && q_scale > 0.0));
     slots = std::min<int64_t>(slots, ((rays->m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
     slots = (slots / kTrainBlock) * kTrainBlock;
     char *base = reinterpret_cast<char *>(ws);
@@ -1506,7 +1516,7 @@ int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t
 
 size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind) {
     if (kind == 0) return 256;
-    int64_t slots = std::min<int64_t>(bwd_slots_max(),
+    int64_t slots = std::min<int64_t>(std::max(bwd_slots_max(false), bwd_slots_max(true)),
                                       ((m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
     slots = std::max<int64_t>(slots, kTrainBlock);
     return 256 + (size_t)slots * (size_t)bwd_slot_bytes(step_limit);
