@@ -368,7 +368,8 @@ def main():
             for (origins, dirs, t_min, t_max, start, targets, u_pairs) in batches:
                 dv.train_batch_device(ds, origins, dirs, t_min, t_max, start, targets, gb, loss,
                                       rgb_scale=rgb_scale, quantile_scale=q_scale,
-                                      u_pairs=u_pairs, workspace=wsb, out=out_fb)
+                                      u_pairs=u_pairs, workspace=wsb, out=out_fb,
+                                      order=None)  # rays already in tile order
             if world > 1:
                 dist.all_reduce(gb.flat)
                 dist.all_reduce(loss)

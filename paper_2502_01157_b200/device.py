@@ -319,7 +319,19 @@ def rays_struct(origins, directions, t_min, t_max, start, order=None) -> _lib.rf
     return r
 
 
-def _order32(order, m, device):
+AUTO_ORDER_MIN_RAYS = 16384
+
+
+def _order32(order, m, device, origins=None, directions=None):
+    """None: the given order; "auto": coherent_order for batches of >= 16384
+    rays (random training pixels: 1.1x at 65k rays, 3.4x at 1M,
+    tools/train_batch_probe.py); else an explicit permutation."""
+    if isinstance(order, str):
+        if order != "auto":
+            raise ValueError(f"unknown order {order!r}")
+        if m < AUTO_ORDER_MIN_RAYS:
+            return None
+        order = coherent_order(origins.to(device), directions.to(device))
     if order is None:
         return None
     o = order.to(device=device, dtype=torch.int32).contiguous()
@@ -428,13 +440,13 @@ def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, sta
                          grads: GradBuffers, *, epsilon=DEFAULT_EPSILON,
                          step_limit=DEFAULT_STEP_LIMIT, f64=False,
                          workspace: Workspace | None = None, out: ForwardResult | None = None,
-                         order=None, stream=None) -> ForwardResult:
-    """rfb_backward_rays (render.py:152-221 generic adjoint)."""
+                         order="auto", stream=None) -> ForwardResult:
+    """rfb_backward_rays (render.py:152-221 generic adjoint).  ``order``: see _order32."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
     p = make_params(epsilon, ds.width_floor, step_limit, 1)
-    order = _order32(order, m, ds.device)
+    order = _order32(order, m, ds.device, origins, directions)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)
     g = grads.struct()
@@ -450,13 +462,14 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        quantile_scale: float = 0.0, u_pairs=None, weight_floor: float = 1e-4,
                        epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
-                       order=None, stream=None) -> ForwardResult:
-    """rfb_train_batch (kernels.py:372-453).  ``loss`` float64 [2] accumulates."""
+                       order="auto", stream=None) -> ForwardResult:
+    """rfb_train_batch (kernels.py:372-453).  ``loss`` float64 [2] accumulates.
+    ``order``: "auto" sorts batches of >= 16384 rays coherently (see _order32)."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
     p = make_params(epsilon, ds.width_floor, step_limit, 1)
-    order = _order32(order, m, ds.device)
+    order = _order32(order, m, ds.device, origins, directions)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)
     g = grads.struct()

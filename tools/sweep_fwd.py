@@ -73,10 +73,10 @@ if args.train:
             up = torch.rand((m, 2, 2), dtype=torch.float64, device="cuda")
             dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
                                   rgb_scale=1.0 / (3 * m), quantile_scale=0.01 / (2 * m),
-                                  u_pairs=up, workspace=wsb, out=fo)
+                                  u_pairs=up, workspace=wsb, out=fo, order=None)
         else:
             dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
-                                  rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo)
+                                  rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo, order=None)
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / reps
     print(f"train: {ms:8.2f} ms/step  {m / ms / 1e3:8.2f} Mrays/s", flush=True)
