@@ -432,6 +432,9 @@ __device__ __forceinline__ unsigned order_key(double t) {
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+#ifndef RFB_REV_ADAPTIVE
+#define RFB_REV_ADAPTIVE 1  // per-lane reverse pass for incoherent warps
+#endif
 #ifndef RFB_REV_COLREG
 #define RFB_REV_COLREG 1  // reverse pass: load cell + colour together when advancing
 #endif
@@ -681,17 +684,39 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
             Sg = tb1 * (float)S.bg[1];
             Sb = tb1 * (float)S.bg[2];
         }
+        // Incoherent warps (random training pixels: lanes rarely share a cell)
+        // gain nothing from grouping and pay one iteration per lane-segment;
+        // they walk back per lane and scatter with vector atomics instead
+        // (65,536 random pixels: 12.3 -> 4.7 ms).
+        bool per_lane = false;
+#if RFB_REV_ADAPTIVE
+        {
+            // coherence probe: the cell at the middle of each lane's path (the
+            // first and last cells are shared by any rays with a common origin
+            // or exit)
+            const int32_t mid = s >= 0 ? (s_cell[(s / 2) * SLa] & 0x1fffffff) : -1 - lane;
+            const unsigned peers = __match_any_sync(kFull, mid);
+            const bool first = (__ffs(peers) - 1) == lane;
+            const int groups = __popc(__ballot_sync(kFull, first && s >= 0));
+            const int active = __popc(__ballot_sync(kFull, s >= 0));
+            per_lane = groups * 4 > active * 3;
+        }
+#endif
         for (;;) {
             const bool act = s >= 0;
             if (!__any_sync(kFull, act)) break;
-#ifdef RFB_COUNT_ITERS  // profiling knob: O.counters[1] += reverse iterations (per warp)
-            if (lane == 0) atomicAdd(O.counters + 1, 1ull);
+#ifdef RFB_COUNT_ITERS  // profiling knob: O.counters[0] += reverse iterations (per warp)
+            if (lane == 0) atomicAdd(O.counters + 0, 1ull);
 #endif
-            const unsigned key = act ? order_key(t0) : 0u;
-            const unsigned kmax = __reduce_max_sync(kFull, key);
-            const int leader = __ffs(__ballot_sync(kFull, act && key == kmax)) - 1;
-            const int32_t lc = __shfl_sync(kFull, ci, leader);
-            const bool in = act && ci == lc;
+            int32_t lc = ci;
+            bool in = act;
+            if (!per_lane) {
+                const unsigned key = act ? order_key(t0) : 0u;
+                const unsigned kmax = __reduce_max_sync(kFull, key);
+                const int leader = __ffs(__ballot_sync(kFull, act && key == kmax)) - 1;
+                lc = __shfl_sync(kFull, ci, leader);
+                in = act && ci == lc;
+            }
             float v[11];
 #pragma unroll
             for (int k = 0; k < 11; ++k) v[k] = 0.f;
@@ -774,6 +799,27 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                         tb0 = 1.f;
                     }
                 }
+            }
+            if (per_lane) {  // this lane's segment straight to its cell (kernels.py:309-337)
+                if (in) {
+                    const float *b = &s_basis[warp][lane][0];
+                    float *row = gr.sh + 48 * (int64_t)lc;
+                    if (v[0] != 0.f || v[1] != 0.f || v[2] != 0.f) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 12; ++q4) {
+                            float e4[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int idx = 4 * q4 + u;  // k * 3 + ch
+                                e4[u] = v[idx % 3] * b[idx / 3];
+                            }
+                            red4(row + 4 * q4, e4[0], e4[1], e4[2], e4[3]);
+                        }
+                    }
+                    red4(gr.g4 + 4 * (int64_t)lc, v[3], v[4], v[5], v[6]);
+                    if (jn >= 0) red4(gr.g4 + 4 * (int64_t)jn, v[7], v[8], v[9], 0.f);
+                }
+                continue;
             }
             // previous cell: aggregated when the whole group agrees on it
             const int32_t jany = __reduce_max_sync(kFull, in ? jn : -1);

@@ -319,12 +319,13 @@ def rays_struct(origins, directions, t_min, t_max, start, order=None) -> _lib.rf
     return r
 
 
-AUTO_ORDER_MIN_RAYS = 16384
+AUTO_ORDER_MIN_RAYS = 500_000
 
 
 def _order32(order, m, device, origins=None, directions=None):
-    """None: the given order; "auto": coherent_order for batches of >= 16384
-    rays (random training pixels: 1.1x at 65k rays, 3.4x at 1M,
+    """None: the given order; "auto": coherent_order for batches of >= 500k
+    rays (random training pixels: 1.5x at 1M rays; at 262k neutral, at 65k the
+    per-lane reverse pass of incoherent warps is faster unsorted --
     tools/train_batch_probe.py); else an explicit permutation."""
     if isinstance(order, str):
         if order != "auto":
@@ -464,7 +465,7 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
                        order="auto", stream=None) -> ForwardResult:
     """rfb_train_batch (kernels.py:372-453).  ``loss`` float64 [2] accumulates.
-    ``order``: "auto" sorts batches of >= 16384 rays coherently (see _order32)."""
+    ``order``: "auto" sorts batches of >= 500k rays coherently (see _order32)."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
