@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--m", type=int, nargs="+", default=[65536, 262144, 1048576])
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--views", type=int, default=8)
+ap.add_argument("--forward", action="store_true", help="time render_rays_device instead")
 args = ap.parse_args()
 
 W, H = 1920, 1080
@@ -46,8 +47,13 @@ for m in args.m:
     for label in ("given order", "coherent_order"):
         def run():
             order = dv.coherent_order(o, d) if label == "coherent_order" else None
-            dv.train_batch_device(ds, o, d, tmin, tmax, st, tg, gb, loss, rgb_scale=1.0 / (3 * m),
-                                  workspace=ws, out=out, order=order)
+            if args.forward:
+                dv.render_rays_device(ds, o, d, tmin, tmax, st, workspace=ws, out=out,
+                                      order=order)
+            else:
+                dv.train_batch_device(ds, o, d, tmin, tmax, st, tg, gb, loss,
+                                      rgb_scale=1.0 / (3 * m), workspace=ws, out=out,
+                                      order=order)
         run()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
