@@ -68,13 +68,24 @@ def parse():
     ap.add_argument("--no-adjacency", action="store_true",
                     help="skip timing the device Delaunay rebuild (SURVEY §8f row 2)")
     ap.add_argument("--cpu-row-stride", type=int, default=8)
-    ap.add_argument("--config", type=int, default=2, choices=[2, 4, 5],
-                    help="2: config 2 forward + config 3 fwd+bwd (1M, 1080p; default); "
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 4, 5],
+                    help="1: the reference's CPU-runnable case (10k sites, SH deg 0, "
+                         "128x128); 2: config 2 forward + config 3 fwd+bwd (1M, 1080p; default); "
                          "4: 3M-site surface foam, one 4K frame tile-sharded over the ranks; "
                          "5: 3M surface foam, 8 orbit views at 1080p fwd+bwd split over the "
                          "ranks + NCCL gradient all-reduce")
     args = ap.parse_args()
     args.kind = "uniform"
+    args.sh_degree = 3
+    if args.config == 1:  # configs[0]: 10k-site foam, SH deg 0, one 128x128 frame
+        if args.n_sites == 1_000_000:
+            args.n_sites = 10_000
+        if args.seed == 1:
+            args.seed = 0
+        if (args.width, args.height) == (1920, 1080):
+            args.width, args.height = 128, 128
+        args.sh_degree = 0
+        args.cpu_row_stride = 1
     if args.config in (4, 5):
         args.kind = "surface"
         if args.n_sites == 1_000_000:
@@ -183,7 +194,8 @@ def run_reference(args):
            "steps": args.steps, "warmup": args.warmup, "impl": "reference",
            "ms_per_step": line["ms_per_step"], "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "config 2: 1M-site foam, SH deg 3, 1920x1080 forward",
+           "config": {"workload": f"config {args.config}: {args.n_sites}-site {args.kind} foam, "
+                                  f"SH deg {args.sh_degree}, {args.width}x{args.height} forward",
                       "sample": line["sample"], "n_sites": args.n_sites},
            "cpu_baseline": {"value": line["value"], "unit": UNIT, "cores": line["cores"],
                             "kind": "port", "sample": line["sample"]},
@@ -198,7 +210,8 @@ def cpu_baseline_measure(args, steps=1, warmup=0, scene=None, cam=None):
     from paper_2502_01157_b200.synthetic import make_foam
 
     if scene is None:
-        scene = make_foam(args.n_sites, args.seed, 3, kind=getattr(args, "kind", "uniform"))
+        scene = make_foam(args.n_sites, args.seed, getattr(args, "sh_degree", 3),
+                          kind=getattr(args, "kind", "uniform"))
     adj = scene.adjacency
     sa = orc.SceneArrays(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density),
                          scene.sh_coeffs.reshape(-1, 48), scene.background)
@@ -256,11 +269,11 @@ def main():
     W, H = args.width, args.height
     lanes = args.lanes if args.lanes > 0 else dv.DEFAULT_LANES
     t_build = time.perf_counter()
-    scene = make_foam(args.n_sites, args.seed, 3, kind=args.kind, verbose=(rank == 0))
+    scene = make_foam(args.n_sites, args.seed, args.sh_degree, kind=args.kind, verbose=(rank == 0))
     ds = dv.DeviceScene(scene, device=dev)
     build_s = time.perf_counter() - t_build
     scaling = "weak"
-    if args.config == 2:
+    if args.config in (1, 2):
         views = make_views(world, W, H)  # one view per rank per step, tile-sharded
         train_views = [views[rank]]
     elif args.config == 4:
@@ -354,7 +367,7 @@ def main():
                        .to(dev)[perm].contiguous() if args.quantile else None)
             batches.append((origins, dirs, t_min, t_max, start, targets, u_pairs))
         m = W * H
-        n_train_views = len(train_views) * world if args.config == 2 else 8
+        n_train_views = len(train_views) * world if args.config in (1, 2) else 8
         gb = dv.GradBuffers(ds.n_sites, dev)
         loss = torch.zeros(2, dtype=torch.float64, device=dev)
         out_fb = dv.alloc_forward(m, dev, per_ray=True)
@@ -407,6 +420,7 @@ def main():
               "ms_per_step": fb_ms / args.steps,
               "workload": ("config 3: 1080p forward+backward, per-site fp32 gradients"
                            if args.config == 2 else
+                           "config 1 scene: 128x128 forward+backward" if args.config == 1 else
                            "config 5: 3M-site surface foam, 8 orbit views at 1080p "
                            "forward+backward split over the ranks")
                           + (", L2 adjoint + quantile regulariser (lambda 0.01, P=2)"
@@ -488,6 +502,8 @@ def main():
         except Exception:
             traffic = None
     workload = {
+        1: "config 1: 10k-site foam (seed 0), SH deg 0, 128x128 forward render per view, "
+           "camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
         2: "config 2: 1M-site foam (seed 1), SH deg 3, 1920x1080 forward render per view, "
            "camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
         4: "config 4: 3M-site surface foam (seed 2), SH deg 3, one 3840x2160 frame per step "
@@ -503,6 +519,12 @@ def main():
         achieved = fb["achieved_GBps"]
         bytes_per_frame = fb["algorithmic_bytes_per_view"]
         kernel_ms = fb["ms_per_step"] / max(len(train_views), 1)
+    scene_mb = sum(t.numel() * t.element_size() for t in
+                   (ds.site4, ds.offsets, ds.neighbors, ds.sh, ds.cells, ds.edges, ds.sh32)
+                   if t is not None) / 1e6
+    l2_note = (f"inputs larger than L2 (scene {scene_mb:.0f} MB vs 126 MB L2); no flush"
+               if scene_mb > 126 else
+               f"scene ({scene_mb:.0f} MB) fits in L2; no flush (small-config case)")
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -511,7 +533,7 @@ def main():
         "config": {"workload": workload,
                    "n_sites": args.n_sites, "n_edges": ds.n_edges, "views_per_step": len(views),
                    "tiles": "32x32 interleaved over ranks", "lanes_per_ray": lanes,
-                   "l2": "inputs larger than L2 (scene 482 MB vs 126 MB L2); no flush",
+                   "l2": l2_note,
                    "cells_per_ray": C_tot / m0, "neighbor_visits_per_ray": V_tot / m0,
                    "segments_per_ray": N_tot / m0, "failed_rays": failed,
                    "scene_build_s": round(build_s, 1)},
