@@ -50,10 +50,11 @@ def render_rays(positions, offsets, neighbors, sigma, sh, background, origins, d
     m = len(origins)
     if m == 0:
         return
-    res = dv.render_rays_device(ds, _dev(origins).view(m, 3), _dev(directions).view(m, 3),
-                                _dev(t_min), _dev(t_max), _dev(start_sites, torch.int32),
+    o, d = _dev(origins).view(m, 3), _dev(directions).view(m, 3)
+    order, lanes = dv.forward_schedule(o, d)
+    res = dv.render_rays_device(ds, o, d, _dev(t_min), _dev(t_max), _dev(start_sites, torch.int32),
                                 epsilon=epsilon, step_limit=int(step_limit), f64=True,
-                                per_ray=False)
+                                per_ray=False, order=order, lanes_per_ray=lanes)
     torch.cuda.synchronize()
     out_rgb[...] = res.rgb.cpu().numpy().reshape(out_rgb.shape)
     out_residual[...] = res.residual.cpu().numpy()

@@ -197,8 +197,7 @@ def _to_dev(a, dtype, device):
 
 def render_ray_batch(scene, origins, directions, t_min=None, t_max=None, start_sites=None,
                      epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, workers=None,
-                     stats=None, return_wsum=False, device_scene=None,
-                     lanes_per_ray=dv.DEFAULT_LANES):
+                     stats=None, return_wsum=False, device_scene=None, lanes_per_ray=None):
     """Forward-render arbitrary rays; returns (rgb, residual, status[, wsum]).
 
     ``workers`` is accepted for signature compatibility (the GPU has no
@@ -240,9 +239,9 @@ def render_ray_batch(scene, origins, directions, t_min=None, t_max=None, start_s
         grid_queries = 0
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    # large batches are scheduled in a coherent order (device Morton sort of
-    # directions); results are written per ray, so the order is invisible
-    order = dv.coherent_order(o_d, d_d) if m >= 16384 else None
+    order, auto_lanes = dv.forward_schedule(o_d, d_d)  # scheduling only
+    if lanes_per_ray is None:
+        lanes_per_ray = auto_lanes
     res = dv.render_rays_device(ds, o_d, d_d, tmin_d, tmax_d, start_d, epsilon=epsilon,
                                 step_limit=step_limit, f64=True, per_ray=False,
                                 lanes_per_ray=lanes_per_ray, order=order)

@@ -19,6 +19,7 @@ ap.add_argument("--m", type=int, nargs="+", default=[65536, 262144, 1048576])
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--views", type=int, default=8)
 ap.add_argument("--forward", action="store_true", help="time render_rays_device instead")
+ap.add_argument("--lanes", type=int, default=1, help="lanes per ray (forward only)")
 args = ap.parse_args()
 
 W, H = 1920, 1080
@@ -49,7 +50,7 @@ for m in args.m:
             order = dv.coherent_order(o, d) if label == "coherent_order" else None
             if args.forward:
                 dv.render_rays_device(ds, o, d, tmin, tmax, st, workspace=ws, out=out,
-                                      order=order)
+                                      order=order, lanes_per_ray=args.lanes)
             else:
                 dv.train_batch_device(ds, o, d, tmin, tmax, st, tg, gb, loss,
                                       rgb_scale=1.0 / (3 * m), workspace=ws, out=out,
