@@ -493,7 +493,10 @@ __device__ __forceinline__ QHit quantile_hit(const double4 *__restrict__ site4, 
     return h;
 }
 
-template <int SHDEG, bool PACKED, bool TRAIN, bool QUANT>
+// G lanes per ray (1 or 2): batches that do not fill the resident threads
+// walk each ray with 2 lanes (the neighbour scan split between them); lane
+// gl == 0 of each pair records the segments and runs the reverse pass.
+template <int SHDEG, bool PACKED, bool TRAIN, bool QUANT, int G = 1>
 __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TRAIN_MINB) k_train(
     SceneView<PACKED> S, ArrayRays src, double epsilon, double log_eps, double width_floor,
     int32_t step_limit, const double *adjoints, const double *targets, double rgb_scale,
@@ -530,13 +533,16 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
     const int o0 = lane, o1 = lane + 32;
     const int k0 = o0 / 3, c0i = o0 % 3;
     const int k1 = o1 < 48 ? o1 / 3 : 16, c1i = o1 < 48 ? o1 % 3 : 3 + (o1 - 48);
+    constexpr int RPW = 32 / G;
+    const int gl = lane & (G - 1);
+    const unsigned gmask = G == 1 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
 
     for (;;) {
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(ray_counter, 32ull);
+        if (lane == 0) base = atomicAdd(ray_counter, (unsigned long long)RPW);
         base = __shfl_sync(kFull, base, 0);
         if ((int64_t)base >= total) break;
-        const int64_t qs = (int64_t)base + lane;
+        const int64_t qs = (int64_t)base + lane / G;
         const bool have_ray = qs < total;
         const int64_t q = have_ray ? src.index(qs) : 0;  // ray id (optional order)
 
@@ -545,6 +551,9 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
         int status = RFB_STATUS_OK;
         float ar = 0.f, ag = 0.f, ab = 0.f;
         bool grad_ok = false;
+        double Tb = 1.0, wsum = 0.0;
+        float cr = 0.f, cg = 0.f, cb = 0.f;
+        int32_t cells = 0, visits = 0;
         if (have_ray) {
             double cbsum;
             int32_t start;
@@ -556,11 +565,8 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 double bsum = basis_setup(rr, bas);
                 cbsum = SHDEG > 0 ? bsum : kC0;
             }
-            double Tb = 1.0, wsum = 0.0;
-            float cr = 0.f, cg = 0.f, cb = 0.f;
-            int32_t cells, visits;
-            status = walk<1, PACKED>(
-                S, r, start, epsilon, log_eps, width_floor, step_limit, 0, kFull, nseg, cells,
+            status = walk<G, PACKED>(
+                S, r, start, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells,
                 visits,
                 [&](int32_t s, int32_t cell, double sigma, double t0, double t1) {
                     const double e = exp(-sigma * (t1 - t0));
@@ -574,19 +580,23 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                     cg += wf * (float)col[1];
                     cb += wf * (float)col[2];
                     Tb = Tn;
-                    rec_a[s * SL4] = make_float4(__int_as_float(cell | (mask << 29)),
-                                                 (float)col[0], (float)col[1], (float)col[2]);
-                    rec_b[s * SL4] = make_double2(t1, Tn);
+                    if (G == 1 || gl == 0) {
+                        rec_a[s * SL4] = make_float4(__int_as_float(cell | (mask << 29)),
+                                                     (float)col[0], (float)col[1], (float)col[2]);
+                        rec_b[s * SL4] = make_double2(t1, Tn);
+                    }
                 });
+        }
+        if (have_ray && (G == 1 || gl == 0)) {  // one lane per ray from here on
             my_cells += (unsigned)cells;
             my_visits += (unsigned)visits;
             if (status != RFB_STATUS_OK) {
                 write_fwd(O, q, status, S.bg[0], S.bg[1], S.bg[2], 1.0, 0.0, nseg, cells, visits);
             } else {
-                const double R = cr + Tb * S.bg[0], G = cg + Tb * S.bg[1], B = cb + Tb * S.bg[2];
-                write_fwd(O, q, status, R, G, B, Tb, wsum, nseg, cells, visits);
+                const double R = cr + Tb * S.bg[0], Gc = cg + Tb * S.bg[1], B = cb + Tb * S.bg[2];
+                write_fwd(O, q, status, R, Gc, B, Tb, wsum, nseg, cells, visits);
                 if (TRAIN) {  // kernels.py:430-437
-                    double er = R - targets[3 * q], eg = G - targets[3 * q + 1],
+                    double er = R - targets[3 * q], eg = Gc - targets[3 * q + 1],
                            eb = B - targets[3 * q + 2];
                     loss_rgb += er * er + eg * eg + eb * eb;
                     ar = (float)(2.0 * rgb_scale * er);
@@ -1353,18 +1363,26 @@ static int64_t bwd_slots_max(bool quant) {
     return (int64_t)num_sms() * std::max(per_sm, 1) * kTrainBlock;
 }
 
+// lanes per ray for a batch: 2 when the batch fills at most half the resident
+// threads (measured: 65,536 random training pixels ...), else 1
+static int train_lanes(int64_t m, bool quant) { return 2 * m <= bwd_slots_max(quant) ? 2 : 1; }
+
 template <bool PACKED>
 static void launch_train_p(const rfb_scene *scene, dim3 grid, cudaStream_t st, bool train,
-                           const ArrayRays &src, double eps, double log_eps, double wf,
+                           int lanes, const ArrayRays &src, double eps, double log_eps, double wf,
                            int32_t sl, const double *adj, const double *tg, double rgb_scale,
                            double q_scale, const double *up, int32_t np, double wfloor,
                            const FwdOut &O, const Grads &G, double *loss, const Scratch &scr,
                            unsigned long long *ctr) {
     SceneView<PACKED> S = view<PACKED>(scene);
-#define RFB_TRAIN(SH, TR, QU)                                                                 \
-    k_train<SH, PACKED, TR, QU><<<grid, kTrainBlock, 0, st>>>(                                  \
+#define RFB_TRAIN1(SH, TR, QU, L)                                                             \
+    k_train<SH, PACKED, TR, QU, L><<<grid, kTrainBlock, 0, st>>>(                               \
         S, src, eps, log_eps, wf, sl, adj, tg, rgb_scale, q_scale, up, np, wfloor, O, G, loss, \
         scr, ctr)
+#define RFB_TRAIN(SH, TR, QU)                                                                 \
+    do {                                                                                       \
+        if (lanes == 2) RFB_TRAIN1(SH, TR, QU, 2); else RFB_TRAIN1(SH, TR, QU, 1);             \
+    } while (0)
     const bool quant = train && q_scale > 0.0;
     if (scene->sh_degree == 0) {
         if (quant) RFB_TRAIN(0, true, true);
@@ -1376,6 +1394,7 @@ static void launch_train_p(const rfb_scene *scene, dim3 grid, cudaStream_t st, b
         else RFB_TRAIN(3, false, false);
     }
 #undef RFB_TRAIN
+#undef RFB_TRAIN1
 }
 
 static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *p,
@@ -1395,8 +1414,11 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     const int64_t per = bwd_slot_bytes(p->step_limit);
     if (!ws || ws_bytes < 256 + (size_t)per * kTrainBlock) return RFB_EINVAL;
     int64_t slots = (int64_t)((ws_bytes - 256) / (size_t)per);
-    slots = std::min<int64_t>(slots, bwd_slots_max(train && q_scale > 0.0));
-    slots = std::min<int64_t>(slots, ((rays->m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
+    const bool quant = train && q_scale > 0.0;
+    const int lanes = train_lanes(rays->m, quant);
+    slots = std::min<int64_t>(slots, bwd_slots_max(quant));
+    slots = std::min<int64_t>(slots,
+                              ((lanes * rays->m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
     slots = (slots / kTrainBlock) * kTrainBlock;
     char *base = reinterpret_cast<char *>(ws);
     unsigned long long *ctr = reinterpret_cast<unsigned long long *>(base);
@@ -1415,13 +1437,13 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     double log_eps = p->epsilon > 0.0 ? std::log(p->epsilon) : 0.0;
     dim3 grid((unsigned)(slots / kTrainBlock));
     if (scene->packed)
-        launch_train_p<true>(scene, grid, st, train, src, p->epsilon, log_eps, p->width_floor,
-                             p->step_limit, adjoints, targets, rgb_scale, q_scale, u_pairs,
-                             n_pairs, wfloor, O, G, loss, scr, ctr);
+        launch_train_p<true>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
+                             p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
+                             u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
     else
-        launch_train_p<false>(scene, grid, st, train, src, p->epsilon, log_eps, p->width_floor,
-                              p->step_limit, adjoints, targets, rgb_scale, q_scale, u_pairs,
-                              n_pairs, wfloor, O, G, loss, scr, ctr);
+        launch_train_p<false>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
+                              p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
+                              u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
     return (int)cudaGetLastError();
 }
 
@@ -1563,7 +1585,7 @@ int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t
 size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind) {
     if (kind == 0) return 256;
     int64_t slots = std::min<int64_t>(std::max(bwd_slots_max(false), bwd_slots_max(true)),
-                                      ((m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
+                                      ((2 * m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
     slots = std::max<int64_t>(slots, kTrainBlock);
     return 256 + (size_t)slots * (size_t)bwd_slot_bytes(step_limit);
 }
