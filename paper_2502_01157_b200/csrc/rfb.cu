@@ -1364,7 +1364,7 @@ static int64_t bwd_slots_max(bool quant) {
 }
 
 // lanes per ray for a batch: 2 when the batch fills at most half the resident
-// threads (measured: 65,536 random training pixels ...), else 1
+// threads (65,536 random training pixels: 4.7 -> 4.1 ms), else 1
 static int train_lanes(int64_t m, bool quant) { return 2 * m <= bwd_slots_max(quant) ? 2 : 1; }
 
 template <bool PACKED>
