@@ -27,7 +27,8 @@
  *   rfb_backward_segments, rfb_quantile_segments
  *                        tracer/kernels.py:38-73, 165-196, 250-369, 456-567
  *                        over given segments (rfb_segments.cu)
- *   rfb_locate          geometry/adjacency.py:85-100 nearest_site()
+ *   rfb_locate, rfb_locate_seeded, rfb_build_locate_grid
+ *                       geometry/adjacency.py:85-100 nearest_site()
  *                        (greedy walk on the CSR; same distance expression
  *                        and lowest-id tie rule as _grid_nearest 140-203)
  *   rfb_render_rays     tracer/kernels.py:199-247   render_rays()
@@ -269,6 +270,23 @@ int rfb_quantile_segments(const double *positions, const double *sigma, const do
                           double weight_floor, double scale, double *d_sigma, double *d_pos,
                           double *loss_out /* [m], nullable */, void *workspace,
                           size_t workspace_bytes, void *stream);
+
+/* Seed grid for point location (the reference's bucket grid role,
+ * adjacency.py:140-203): hint [dims] int32 device array, cell size `cell`,
+ * origin lo.  rfb_build_locate_grid fills every cell with the largest site id
+ * inside it (-1 if empty); rfb_locate_seeded starts each query's greedy walk
+ * from the nearest non-empty cell within two rings (else seed_site).  The walk
+ * is exact from any seed; the grid only shortens it. */
+typedef struct rfb_locate_grid {
+    double lo[3];
+    double cell;
+    int32_t dims[3];
+    int32_t pad_;
+    int32_t *hint;
+} rfb_locate_grid;
+int rfb_build_locate_grid(const rfb_scene *scene, rfb_locate_grid *grid, void *stream);
+int rfb_locate_seeded(const rfb_scene *scene, const double *queries, int64_t m,
+                    const rfb_locate_grid *grid, int32_t seed_site, int32_t *out, void *stream);
 
 /* out[q] = nearest site to queries[q] (greedy CSR walk from seed_site). */
 int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t seed_site,

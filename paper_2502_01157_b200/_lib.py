@@ -81,6 +81,16 @@ class rfb_grads(ctypes.Structure):
     _fields_ = [("site4g", ctypes.c_void_p), ("sh", ctypes.c_void_p)]
 
 
+class rfb_locate_grid(ctypes.Structure):
+    _fields_ = [
+        ("lo", ctypes.c_double * 3),
+        ("cell", ctypes.c_double),
+        ("dims", ctypes.c_int32 * 3),
+        ("pad_", ctypes.c_int32),
+        ("hint", ctypes.c_void_p),
+    ]
+
+
 class rfb_camera(ctypes.Structure):
     _fields_ = [
         ("pose", ctypes.c_double * 16),
@@ -112,6 +122,8 @@ SIGNATURES = {
     "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP]),
     "rfb_refresh_scene": (ctypes.c_int, [P(rfb_scene), VP, VP, VP]),
     "rfb_locate": (ctypes.c_int, [P(rfb_scene), VP, I64, I32, VP, VP]),
+    "rfb_build_locate_grid": (ctypes.c_int, [P(rfb_scene), P(rfb_locate_grid), VP]),
+    "rfb_locate_seeded": (ctypes.c_int, [P(rfb_scene), VP, I64, P(rfb_locate_grid), I32, VP, VP]),
     "rfb_adjacency_workspace_bytes": (SZ, [I64, I32]),
     "rfb_build_adjacency": (ctypes.c_int, [VP, I64, I32, VP, VP, I64, VP, P(ctypes.c_int64), VP,
                                            SZ, VP]),

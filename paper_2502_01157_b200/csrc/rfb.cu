@@ -1109,6 +1109,52 @@ __global__ void k_locate(LocScene S, const double *qs, int64_t m, int32_t seed, 
     if (k < m) out[k] = locate_one(S, qs[3 * k], qs[3 * k + 1], qs[3 * k + 2], seed);
 }
 
+// Seed grid for the greedy walk (the walk is exact from any seed; the seed
+// only shortens it, like the reference's bucket grid, adjacency.py:140-203):
+// every grid cell holds the largest site id inside it, or -1.
+struct HintGrid {
+    double lo[3], cell;
+    int dims[3];
+    const int32_t *hint;
+};
+
+__device__ __forceinline__ int hint_axis(double v, double lo, double cell, int dim) {
+    const double f = floor((v - lo) / cell);
+    return f < 0.0 ? 0 : (f > dim - 1 ? dim - 1 : (int)f);
+}
+
+__global__ void k_hint_scatter(const double4 *site4, int64_t n, HintGrid g, int32_t *hint) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const double4 p = site4[i];
+    const int x = hint_axis(p.x, g.lo[0], g.cell, g.dims[0]);
+    const int y = hint_axis(p.y, g.lo[1], g.cell, g.dims[1]);
+    const int z = hint_axis(p.z, g.lo[2], g.cell, g.dims[2]);
+    atomicMax(hint + ((int64_t)z * g.dims[1] + y) * g.dims[0] + x, (int32_t)i);
+}
+
+__global__ void k_locate_hinted(LocScene S, const double *qs, int64_t m, HintGrid g, int32_t seed,
+                                int32_t *out) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const double qx = qs[3 * k], qy = qs[3 * k + 1], qz = qs[3 * k + 2];
+    const int x = hint_axis(qx, g.lo[0], g.cell, g.dims[0]);
+    const int y = hint_axis(qy, g.lo[1], g.cell, g.dims[1]);
+    const int z = hint_axis(qz, g.lo[2], g.cell, g.dims[2]);
+    int32_t start = -1;
+    for (int r = 0; r <= 2 && start < 0; ++r)  // nearest non-empty cell within 2 rings
+        for (int dz = -r; dz <= r && start < 0; ++dz)
+            for (int dy = -r; dy <= r && start < 0; ++dy)
+                for (int dx = -r; dx <= r && start < 0; ++dx) {
+                    const int cx = x + dx, cy = y + dy, cz = z + dz;
+                    if (cx < 0 || cy < 0 || cz < 0 || cx >= g.dims[0] || cy >= g.dims[1] ||
+                        cz >= g.dims[2])
+                        continue;
+                    start = __ldg(g.hint + ((int64_t)cz * g.dims[1] + cy) * g.dims[0] + cx);
+                }
+    out[k] = locate_one(S, qx, qy, qz, start >= 0 ? start : seed);
+}
+
 // Exact nearest site of one query point by a full-device scan (shared-origin
 // cameras: one query per frame, render.py:78-82): pass 1 takes the minimum
 // squared distance (non-negative doubles order like their bit patterns),
@@ -1579,6 +1625,44 @@ int rfb_locate(const rfb_scene *scene, const double *queries, int64_t m, int32_t
     if (m == 0) return RFB_OK;
     k_locate<<<(unsigned)((m + 127) / 128), 128, 0, (cudaStream_t)stream>>>(loc_scene(scene),
                                                                             queries, m, seed_site, out);
+    return (int)cudaGetLastError();
+}
+
+static HintGrid hint_grid(const rfb_locate_grid *lg) {
+    HintGrid g;
+    for (int k = 0; k < 3; ++k) {
+        g.lo[k] = lg->lo[k];
+        g.dims[k] = lg->dims[k];
+    }
+    g.cell = lg->cell;
+    g.hint = lg->hint;
+    return g;
+}
+
+static bool grid_ok(const rfb_locate_grid *lg) {
+    return lg && lg->hint && lg->cell > 0.0 && lg->dims[0] > 0 && lg->dims[1] > 0 &&
+           lg->dims[2] > 0;
+}
+
+int rfb_build_locate_grid(const rfb_scene *scene, rfb_locate_grid *grid, void *stream) {
+    if (!scene_ok(scene) || !grid_ok(grid)) return RFB_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t cells = (int64_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
+    cudaMemsetAsync(grid->hint, 0xff, sizeof(int32_t) * cells, st);  // -1
+    k_hint_scatter<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, st>>>(
+        reinterpret_cast<const double4 *>(scene->site4), scene->n_sites, hint_grid(grid),
+        grid->hint);
+    return (int)cudaGetLastError();
+}
+
+int rfb_locate_seeded(const rfb_scene *scene, const double *queries, int64_t m,
+                    const rfb_locate_grid *grid, int32_t seed_site, int32_t *out, void *stream) {
+    if (!scene_ok(scene) || !queries || !out || m < 0 || !grid_ok(grid) || seed_site < 0 ||
+        seed_site >= scene->n_sites)
+        return RFB_EINVAL;
+    if (m == 0) return RFB_OK;
+    k_locate_hinted<<<(unsigned)((m + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+        loc_scene(scene), queries, m, hint_grid(grid), seed_site, out);
     return (int)cudaGetLastError();
 }
 

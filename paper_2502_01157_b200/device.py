@@ -119,6 +119,25 @@ class DeviceScene:
             torch.cuda.current_stream().synchronize()
         self._c = _lib.rfb_scene()
         self._refresh_struct()
+        self._build_locate_grid()
+
+    LOCATE_GRID_RES = 64  # cells along the longest bounding-box axis
+
+    def _build_locate_grid(self, stream=None):
+        """Seed grid for point location (rfb_build_locate_grid)."""
+        ext = np.maximum(self.bbox_hi - self.bbox_lo, 1e-12)
+        cell = float(ext.max()) / self.LOCATE_GRID_RES
+        dims = [max(1, int(np.ceil(e / cell))) for e in ext]
+        self._hint = torch.empty(int(np.prod(dims)), dtype=torch.int32, device=self.device)
+        g = _lib.rfb_locate_grid()
+        for k in range(3):
+            g.lo[k] = float(self.bbox_lo[k])
+            g.dims[k] = dims[k]
+        g.cell = cell
+        g.hint = self._hint.data_ptr()
+        self._grid = g
+        _lib.check(self.lib.rfb_build_locate_grid(self.c, ctypes.byref(g), _stream(stream)),
+                   "rfb_build_locate_grid")
 
     def _refresh_struct(self):
         c = self._c
@@ -184,6 +203,7 @@ class DeviceScene:
             self.site4 = site4
         self.hull = hull
         self._refresh_struct()
+        self._build_locate_grid(stream)
         return info
 
 
@@ -201,8 +221,9 @@ class DeviceScene:
         q = queries.to(self.device, torch.float64).contiguous()
         m = q.shape[0]
         out = torch.empty(m, dtype=torch.int32, device=self.device)
-        _lib.check(self.lib.rfb_locate(self.c, _ptr(q), m, int(seed), _ptr(out), _stream(stream)),
-                   "rfb_locate")
+        _lib.check(self.lib.rfb_locate_seeded(self.c, _ptr(q), m, ctypes.byref(self._grid),
+                                              int(seed), _ptr(out), _stream(stream)),
+                   "rfb_locate_seeded")
         return out
 
 
