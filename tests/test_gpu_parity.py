@@ -342,3 +342,36 @@ def test_effect_rays_device(cuda_ok, kind):
     for i in range(len(g["d"])):
         r = rd.apply_effect(rd.Ray(g["o"][i], g["d"][i], 0.0, 9.0), n, kind, 1.5, g["t_at"][i])
         np.testing.assert_allclose(od.cpu().numpy()[i], r.direction, rtol=0, atol=1e-14)
+
+
+def test_generic_layout_fp64_positions_vs_oracle(cuda_ok):
+    """Sites that are not fp32-representable (as after an Adam step on the
+    positions) take the generic fp64 layout; per-ray counters/status must
+    still be the oracle's bit for bit, and the image within 1e-4."""
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200.synthetic import delaunay_csr
+
+    rng = np.random.default_rng(21)
+    n = 3000
+    pos = rng.uniform(-1, 1, (n, 3)) + rng.normal(0, 1e-9, (n, 3))  # fp64 positions
+    assert not np.array_equal(pos.astype(np.float32).astype(np.float64), pos)
+    off, nbr, _ = delaunay_csr(pos)
+    raw = rng.normal(0, 1, n)
+    sh = rng.normal(0, 0.3, (n, 48))
+    from paper_2502_01157_b200.scene import softplus
+    sa = orc.SceneArrays(pos, off, nbr, softplus(raw), sh, np.array([0.1, 0.2, 0.3]))
+    ds = dv.DeviceScene.from_arrays(pos, off, nbr, softplus(raw), sh, np.array([0.1, 0.2, 0.3]))
+    assert not ds.packed
+    m = 2048
+    o = np.tile([0.0, 0.0, 3.0], (m, 1))
+    d = rng.normal(size=(m, 3)) * [0.3, 0.3, 0.0] + [0.0, 0.0, -1.0]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    start = int(orc.nearest_sites(pos, o[:1])[0])
+    tmax = ds.default_t_max(o[:1])
+    ref = orc.render_rays(sa, o, d, 0.0, tmax, start)
+    res = dv.render_rays_device(ds, _dev(o), _dev(d), _dev(np.zeros(m)), _dev(np.full(m, tmax)),
+                                _dev(np.full(m, start), torch.int32), f64=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
+    assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= IMG_TOL
