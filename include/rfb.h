@@ -67,7 +67,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 7
+#define RFB_ABI_VERSION 8
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
@@ -95,7 +95,9 @@ typedef struct rfb_scene {
     float sh_absmax;          /* packed: >= max |sh| over the scene (fp32 colour bound) */
     int32_t sh_degree;        /* 0: read the DC band only (exact when bands 1..15 are
                                  all zero), 3: all 16 bands */
-    int32_t pad_;
+    int32_t positions_f64;    /* packed: 0 = every coordinate is fp32-exact; 1 = not: the
+                                 fp32 copies are rounded, the pre-filter bound is widened
+                                 (n1max) and the exact phase reads site4 */
     double background[3];     /* (host value) */
 } rfb_scene;
 
@@ -169,7 +171,8 @@ int rfb_device_ok(void);                /* 1 when an sm_100 device is current */
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
-                   void *cells, void *edges, void *edge_meta, float *sh32, void *stream);
+                   void *cells, void *edges, void *edge_meta, float *sh32,
+                   int32_t positions_f64, void *stream);
 
 /* sigma = softplus_10(raw) for device-resident training, written to out
  * (nullable), site4[:,3] (nullable) and the packed headers (nullable). */

@@ -34,7 +34,7 @@ class rfb_scene(ctypes.Structure):
         ("packed", ctypes.c_int32),
         ("sh_absmax", ctypes.c_float),
         ("sh_degree", ctypes.c_int32),
-        ("pad_", ctypes.c_int32),
+        ("positions_f64", ctypes.c_int32),
         ("background", ctypes.c_double * 3),
     ]
 
@@ -116,7 +116,8 @@ SIGNATURES = {
     "rfb_abi_version": (ctypes.c_int, []),
     "rfb_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rfb_device_ok": (ctypes.c_int, []),
-    "rfb_pack_scene": (ctypes.c_int, [VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP, VP, VP, VP]),
+    "rfb_pack_scene": (ctypes.c_int, [VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP, VP, VP,
+                                      I32, VP]),
     "rfb_softplus": (ctypes.c_int, [VP, I64, VP, VP, VP, VP]),
     "rfb_camera_rays": (ctypes.c_int, [P(rfb_camera), I64, I64, VP, VP]),
     "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP]),
@@ -176,7 +177,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rfb_abi_version() != 7:
+        if lib.rfb_abi_version() != 8:
             raise ExtensionMissing("librfb.so ABI version mismatch; rebuild")
         if path is None:
             _lib = lib

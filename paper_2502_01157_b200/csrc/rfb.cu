@@ -166,7 +166,7 @@ __device__ __forceinline__ void write_fwd(const FwdOut &O, int64_t q, int status
 // group.  rec(index, cell, header, t0, t1) is called for every recorded
 // segment, in order.  Returns the status code.
 // ---------------------------------------------------------------------------
-template <int G, bool PACKED, class RayT, class Rec>
+template <int G, int PACKED, class RayT, class Rec>
 __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, int32_t start,
                                     double epsilon,
                                     double log_eps, double width_floor, int32_t step_limit,
@@ -190,7 +190,7 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
         double best_t;
         int32_t best_j;
         if constexpr (PACKED && kUseF32Filter)
-            exit_face_f32<G>(S, c, c.hf, r, entry, df, gl, gmask, best_t, best_j);
+            exit_face_f32<G, PACKED>(S, i, c, c.hf, r, entry, df, gl, gmask, best_t, best_j);
         else
             exit_face<G, PACKED>(S, c, r, gl, gmask, best_t, best_j);
         if (best_j < 0 || best_t >= r.t_max()) {  // hull exit or far plane
@@ -251,7 +251,7 @@ __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
 #ifndef RFB_FWD_MINB
 #define RFB_FWD_MINB 4
 #endif
-template <int G, int SHDEG, bool PACKED, class Src>
+template <int G, int SHDEG, int PACKED, class Src>
 __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> S, Src src, double epsilon,
                                                 double log_eps, double width_floor,
                                                 int32_t step_limit, FwdOut O,
@@ -496,7 +496,7 @@ __device__ __forceinline__ QHit quantile_hit(const double4 *__restrict__ site4, 
 // G lanes per ray (1 or 2): batches that do not fill the resident threads
 // walk each ray with 2 lanes (the neighbour scan split between them); lane
 // gl == 0 of each pair records the segments and runs the reverse pass.
-template <int SHDEG, bool PACKED, bool TRAIN, bool QUANT, int G = 1>
+template <int SHDEG, int PACKED, bool TRAIN, bool QUANT, int G = 1>
 __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TRAIN_MINB) k_train(
     SceneView<PACKED> S, ArrayRays src, double epsilon, double log_eps, double width_floor,
     int32_t step_limit, const double *adjoints, const double *targets, double rgb_scale,
@@ -948,9 +948,19 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
 // ---------------------------------------------------------------------------
 // Scene packing, activation, camera rays, start-cell location.
 // ---------------------------------------------------------------------------
+// Positions that are not fp32-exact (positions_f64): the fp32 copies differ
+// from the sites by <= u X per coordinate (X = the largest |coordinate| of
+// the cell and its neighbours), which adds <= 4uX to the denominator error
+// and <= uX (6 Hm + 2 N + 2) to the numerator error of exit_face_f32's
+// bound.  Storing n1max = N + 2 max(X, 1/4) covers both: the bound's own
+// terms grow by 16uX and 16uX Hm + 8uNX + 8uX^2 >= uX (6 Hm + 2 N + 2).
+__device__ __forceinline__ float pos64_widen(double xabs) {
+    return (float)(2.0 * fmax(xabs, 0.25)) * (1.0f + 0x1p-20f);
+}
+
 __global__ void k_pack_sites(const double *pos, const double *sigma, const double *sh, int64_t n,
                              const int64_t *off64, const int64_t *nbr64, double4 *site4,
-                             int32_t *off32, CellHdr *cells, float *sh32) {
+                             int32_t *off32, CellHdr *cells, float *sh32, int pos64) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n) return;
     off32[i] = (int32_t)off64[i];
@@ -962,12 +972,15 @@ __global__ void k_pack_sites(const double *pos, const double *sigma, const doubl
                 sh32[i * 48 + 16 * ch + k] = (float)sh[i * 48 + 3 * k + ch];  // channel-major
         const float xi = (float)pos[3 * i], yi = (float)pos[3 * i + 1], zi = (float)pos[3 * i + 2];
         float n1max = 0.f;
+        double xabs = fmax(fabs(pos[3 * i]), fmax(fabs(pos[3 * i + 1]), fabs(pos[3 * i + 2])));
         for (int64_t k = off64[i]; k < off64[i + 1]; ++k) {  // same fp32 ops as exit_face_f32
             const int64_t j = nbr64[k];
             const float nx = (float)pos[3 * j] - xi, ny = (float)pos[3 * j + 1] - yi,
                         nz = (float)pos[3 * j + 2] - zi;
             n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
+            xabs = fmax(xabs, fmax(fabs(pos[3 * j]), fmax(fabs(pos[3 * j + 1]), fabs(pos[3 * j + 2]))));
         }
+        if (pos64) n1max += pos64_widen(xabs);
         CellHdr h;
         h.x = xi;
         h.y = yi;
@@ -1262,13 +1275,31 @@ __global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double
 // Refresh the kernel arrays from updated parameters (render.py:49-54 on
 // device): site4 = {pos, softplus(raw)}, packed headers' sigma, sh32.
 __global__ void k_refresh_scene(int64_t n, const double *pos, const double *raw,
-                                const double *sh, double4 *site4, CellHdr *cells, float *sh32) {
+                                const double *sh, double4 *site4, CellHdr *cells, float *sh32,
+                                const int32_t *off, const int32_t *nbr, int pos64) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double x = raw[i];
     const double sig = fmax(x, 0.0) + log1p(exp(-fabs(10.0 * x))) / 10.0;
     site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sig);
     if (cells) cells[i].sigma = sig;
+    if (cells && pos64) {  // moved sites: fp32 copies and the widened bound (k_pack_sites)
+        const float xi = (float)pos[3 * i], yi = (float)pos[3 * i + 1], zi = (float)pos[3 * i + 2];
+        float n1max = 0.f;
+        double xabs = fmax(fabs(pos[3 * i]), fmax(fabs(pos[3 * i + 1]), fabs(pos[3 * i + 2])));
+        for (int32_t k = off[i]; k < off[i + 1]; ++k) {
+            const int32_t j = nbr[k];
+            const float nx = (float)pos[3 * j] - xi, ny = (float)pos[3 * j + 1] - yi,
+                        nz = (float)pos[3 * j + 2] - zi;
+            n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
+            xabs = fmax(xabs, fmax(fabs(pos[3 * j]), fmax(fabs(pos[3 * j + 1]), fabs(pos[3 * j + 2]))));
+        }
+        CellHdr &h = cells[i];
+        h.x = xi;
+        h.y = yi;
+        h.z = zi;
+        h.n1max = n1max * (1.0f + 0x1p-20f) + pos64_widen(xabs);
+    }
     if (sh32)
         for (int k = 0; k < 16; ++k)
             for (int ch = 0; ch < 3; ++ch) sh32[i * 48 + 16 * ch + k] = (float)sh[i * 48 + 3 * k + ch];
@@ -1288,12 +1319,13 @@ static int num_sms() {
     return sms;
 }
 
-template <bool PACKED>
+template <int PACKED>
 static SceneView<PACKED> view(const rfb_scene *s) {
     SceneView<PACKED> v;
     v.hdr = reinterpret_cast<const CellHdr *>(s->cells);
     v.edge = reinterpret_cast<const float4 *>(s->edges);
     v.emeta = reinterpret_cast<const int2 *>(s->edge_meta);
+    v.pos64 = s->positions_f64 != 0;
     v.site4 = reinterpret_cast<const double4 *>(s->site4);
     v.off = s->offsets;
     v.nbr = s->neighbors;
@@ -1344,7 +1376,7 @@ static bool out_ok(const rfb_fwd_out *o) {
     return true;
 }
 
-template <int G, bool PACKED, class Src>
+template <int G, int PACKED, class Src>
 static void launch_render_g(const rfb_scene *scene, const Src &src, double eps, double log_eps,
                             double wf, int32_t sl, const FwdOut &O, unsigned long long *ctr,
                             cudaStream_t st) {
@@ -1365,10 +1397,12 @@ template <int G, class Src>
 static void launch_render_p(const rfb_scene *scene, const Src &src, double eps, double log_eps,
                             double wf, int32_t sl, const FwdOut &O, unsigned long long *ctr,
                             cudaStream_t st) {
-    if (scene->packed)
-        launch_render_g<G, true>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
+    if (scene->packed && !scene->positions_f64)
+        launch_render_g<G, 1>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
+    else if (scene->packed && G <= 2)  // fp64 sites: widened bound (G > 2: generic walk)
+        launch_render_g<G, 2>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
     else
-        launch_render_g<G, false>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
+        launch_render_g<G, 0>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
 }
 
 template <class Src>
@@ -1413,7 +1447,7 @@ static int64_t bwd_slots_max(bool quant) {
 // threads (65,536 random training pixels: 4.7 -> 4.1 ms), else 1
 static int train_lanes(int64_t m, bool quant) { return 2 * m <= bwd_slots_max(quant) ? 2 : 1; }
 
-template <bool PACKED>
+template <int PACKED>
 static void launch_train_p(const rfb_scene *scene, dim3 grid, cudaStream_t st, bool train,
                            int lanes, const ArrayRays &src, double eps, double log_eps, double wf,
                            int32_t sl, const double *adj, const double *tg, double rgb_scale,
@@ -1482,14 +1516,18 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     Grads G{grads->site4g, grads->sh};
     double log_eps = p->epsilon > 0.0 ? std::log(p->epsilon) : 0.0;
     dim3 grid((unsigned)(slots / kTrainBlock));
-    if (scene->packed)
-        launch_train_p<true>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
-                             p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
-                             u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
+    if (scene->packed && !scene->positions_f64)
+        launch_train_p<1>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
+                          p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
+                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
+    else if (scene->packed)
+        launch_train_p<2>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
+                          p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
+                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
     else
-        launch_train_p<false>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
-                              p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
-                              u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
+        launch_train_p<0>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
+                          p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
+                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
     return (int)cudaGetLastError();
 }
 
@@ -1535,7 +1573,8 @@ int rfb_device_ok(void) {
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
-                   void *cells, void *edges, void *edge_meta, float *sh32, void *stream) {
+                   void *cells, void *edges, void *edge_meta, float *sh32,
+                   int32_t positions_f64, void *stream) {
     if (!positions || !sigma || !offsets || !neighbors || !site4 || !offsets32 || !neighbors32 ||
         n_sites <= 0 || n_edges < 0 || n_edges >= ((int64_t)1 << 31) ||
         ((cells || edges || sh32) && (!cells || !edges || !sh32 || !sh)))
@@ -1543,7 +1582,7 @@ int rfb_pack_scene(const double *positions, const double *sigma, const double *s
     cudaStream_t st = (cudaStream_t)stream;
     k_pack_sites<<<(unsigned)((n_sites + 1 + 255) / 256), 256, 0, st>>>(
         positions, sigma, sh, n_sites, offsets, neighbors, reinterpret_cast<double4 *>(site4),
-        offsets32, reinterpret_cast<CellHdr *>(cells), sh32);
+        offsets32, reinterpret_cast<CellHdr *>(cells), sh32, positions_f64 ? 1 : 0);
     if (n_edges > 0)
         k_pack_edges<<<(unsigned)((n_edges + 255) / 256), 256, 0, st>>>(
             neighbors, offsets, positions, n_edges, neighbors32, reinterpret_cast<float4 *>(edges),
@@ -1582,12 +1621,29 @@ int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positio
     return (int)cudaGetLastError();
 }
 
+__global__ void k_refresh_edges(const int32_t *nbr, const double *pos, int64_t E, float4 *edges) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= E) return;
+    const int32_t j = nbr[k];
+    edges[k] = make_float4((float)pos[3 * j], (float)pos[3 * j + 1], (float)pos[3 * j + 2],
+                           __int_as_float(j));
+}
+
 int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const double *raw_density,
                       void *stream) {
     if (!scene_ok(scene) || !positions || !raw_density) return RFB_EINVAL;
-    k_refresh_scene<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+    // a packed scene with fp32-exact positions cannot take moved sites in place
+    const bool pos64 = scene->packed && scene->positions_f64;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_refresh_scene<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, st>>>(
         scene->n_sites, positions, raw_density, scene->sh, (double4 *)scene->site4,
-        (CellHdr *)scene->cells, (float *)scene->sh32);
+        scene->packed ? (CellHdr *)scene->cells : nullptr,
+        scene->packed ? (float *)scene->sh32 : nullptr, scene->offsets, scene->neighbors,
+        pos64 ? 1 : 0);
+    if (pos64 && scene->n_edges > 0)
+        k_refresh_edges<<<(unsigned)((scene->n_edges + 255) / 256), 256, 0, st>>>(
+            scene->neighbors, positions, scene->n_edges,
+            reinterpret_cast<float4 *>(const_cast<void *>(scene->edges)));
     return (int)cudaGetLastError();
 }
 

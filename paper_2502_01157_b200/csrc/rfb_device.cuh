@@ -112,11 +112,12 @@ __device__ __forceinline__ void ldg256(const void *p, float4 &a, float4 &b) {
         : "l"(p));
 }
 
-template <bool PACKED>
+template <int PACKED>
 struct SceneView {
     const CellHdr *hdr;     // PACKED
     const float4 *edge;     // PACKED
     const int2 *emeta;      // PACKED: [E] {k0_j, k1_j} of the edge's target site
+    bool pos64;             // PACKED: positions not fp32-exact -> exact phase reads site4
     const double4 *site4;   // both (backward gradients use fp64 positions)
     const int32_t *off;     // generic
     const int32_t *nbr;     // generic
@@ -204,7 +205,7 @@ static __device__ __noinline__ double exact_channel(const double *row, int ch, i
 }
 
 // basis_f: the ray's fp32 SH basis (BSTRIDE apart); bsum = sum |fp64 basis|.
-template <int SHDEG, bool PACKED, int BSTRIDE = 1, class RayT>
+template <int SHDEG, int PACKED, int BSTRIDE = 1, class RayT>
 __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
                                           const float *basis_f, const RayT &ray,
                                           double bsum, double *col) {
@@ -359,7 +360,7 @@ __device__ __forceinline__ bool below_epsilon(double log_T, double epsilon, doub
 #define RFB_STR_(x) #x
 #define RFB_PRAGMA_UNROLL(n) _Pragma(RFB_STR_(unroll n))
 
-template <int G, bool PACKED, class RayT>
+template <int G, int PACKED, class RayT>
 __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell &c,
                                           const RayT &r, int gl, unsigned gmask, double &best_t,
                                           int32_t &best_j) {
@@ -447,6 +448,9 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #ifndef RFB_F32_UNROLL
 #define RFB_F32_UNROLL 4
 #endif
+#ifndef RFB_POS64
+#define RFB_POS64 1  // support packed scenes with non-fp32-exact sites (positions_f64)
+#endif
 #ifndef RFB_PAIR_UNROLL
 #define RFB_PAIR_UNROLL 2  // edge pairs per unrolled phase-1 iteration (LDG.256 path)
 #endif
@@ -458,8 +462,9 @@ typedef unsigned long long cand_mask_t;
 constexpr int kMaskBits = 64;
 #endif
 
-template <int G, class RayT>
-__device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Cell &c,
+// PK: 1 = packed with fp32-exact sites, 2 = packed with fp64 sites (positions_f64)
+template <int G, int PK, class RayT>
+__device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci, const Cell &c,
                                               const float4 &hdr_f, const RayT &r, double entry,
                                               const float *df, int gl, unsigned gmask,
                                               double &best_t, int32_t &best_j) {
@@ -571,7 +576,27 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
         U = fminf(U, s + es);
 #endif
     }
-    const double cx = hdr_f.x, cy = hdr_f.y, cz = hdr_f.z;  // exact widening
+    double cx = hdr_f.x, cy = hdr_f.y, cz = hdr_f.z;  // exact widening (fp32-exact sites)
+    constexpr bool pos64 = PK == 2;
+    if (pos64) {  // the sites themselves (the fp32 copies are rounded)
+        const double4 si = ld_site(S.site4 + ci);
+        cx = si.x;
+        cy = si.y;
+        cz = si.z;
+    }
+    // neighbour j's exact coordinates: the widened fp32 record, or site4
+    auto site_of = [&](const float4 &e, double &x, double &y, double &z) {
+        if (pos64) {
+            const double4 sj = ld_site(S.site4 + __float_as_int(e.w));
+            x = sj.x;
+            y = sj.y;
+            z = sj.z;
+        } else {
+            x = e.x;
+            y = e.y;
+            z = e.z;
+        }
+    };
     // phase 2: exact fp64 re-evaluation of the candidates, CSR order
     best_t = dinf();
     best_j = -1;
@@ -587,7 +612,8 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
         }
         const int32_t k = k0 + idx * G;
         const float4 e = __ldg(S.edge + k);
-        const double xj = e.x, yj = e.y, zj = e.z;
+        double xj, yj, zj;
+        site_of(e, xj, yj, zj);
         const double nx = xj - cx, ny = yj - cy, nz = zj - cz;
         const double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
         if (denom <= 0.0) continue;
@@ -602,7 +628,8 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<true> &S, const Ce
     for (int32_t idx = kMaskBits; idx < nexact; ++idx) {  // rows longer than the mask
         const int32_t k = k0 + idx * G;
         const float4 e = __ldg(S.edge + k);
-        const double xj = e.x, yj = e.y, zj = e.z;
+        double xj, yj, zj;
+        site_of(e, xj, yj, zj);
         const double nx = xj - cx, ny = yj - cy, nz = zj - cz;
         const double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
         if (denom <= 0.0) continue;

@@ -54,24 +54,25 @@ class DeviceScene:
     device instead (device-resident training).
     """
 
-    def __init__(self, scene, device=None, sh_degree=None, packed=None):
+    def __init__(self, scene, device=None, sh_degree=None, packed=None, positions_f64=None):
         adj = scene.require_adjacency()
         sh = np.asarray(scene.sh_coeffs, dtype=np.float64).reshape(len(adj.positions), 48)
         self._init(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density), sh,
-                   scene.background, adj.bbox_lo, adj.bbox_hi, device, sh_degree, packed)
+                   scene.background, adj.bbox_lo, adj.bbox_hi, device, sh_degree, packed,
+                   positions_f64)
 
     @classmethod
     def from_arrays(cls, positions, offsets, neighbors, sigma, sh_flat, background, device=None,
-                    sh_degree=None, packed=None):
+                    sh_degree=None, packed=None, positions_f64=None):
         """Flat kernel arrays as passed to kernels.render_rays (kernels.py:199-209)."""
         self = cls.__new__(cls)
         pos = np.asarray(positions, dtype=np.float64)
         self._init(pos, offsets, neighbors, sigma, sh_flat, background, pos.min(axis=0),
-                   pos.max(axis=0), device, sh_degree, packed)
+                   pos.max(axis=0), device, sh_degree, packed, positions_f64)
         return self
 
     def _init(self, positions, offsets, neighbors, sigma, sh_flat, background, bbox_lo, bbox_hi,
-              device, sh_degree, packed):
+              device, sh_degree, packed, positions_f64=None):
         self.lib = _lib.load()
         self.device = torch.device(device or "cuda")
         pos = np.ascontiguousarray(positions, dtype=np.float64)
@@ -89,9 +90,12 @@ class DeviceScene:
         # fp32 upper bound of max |coefficient| (colour rounding bound, packed layout)
         self.sh_absmax = float(np.float32(np.abs(sh).max() if sh.size else 0.0) * np.float32(1.0001))
         sigma = np.ascontiguousarray(sigma, dtype=np.float64)
-        # packed layout only when every coordinate survives an fp32 round trip
-        self.packed = bool(np.array_equal(pos.astype(np.float32).astype(np.float64), pos)) \
-            if packed is None else bool(packed)
+        # packed layout by default; positions that do not survive an fp32 round trip
+        # (or that will move, positions_f64=True) use the widened pre-filter bound
+        # and exact phase from site4 (rfb_scene.positions_f64)
+        self.packed = True if packed is None else bool(packed)
+        exact32 = bool(np.array_equal(pos.astype(np.float32).astype(np.float64), pos))
+        self.positions_f64 = (not exact32) if positions_f64 is None else bool(positions_f64)
         dev = self.device
         with torch.cuda.device(dev):
             self.site4 = torch.empty((n, 4), dtype=torch.float64, device=dev)
@@ -114,7 +118,7 @@ class DeviceScene:
                 _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
                 self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
                 _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_meta), _ptr(self.sh32),
-                _stream()),
+                1 if self.positions_f64 else 0, _stream()),
                 "rfb_pack_scene")
             torch.cuda.current_stream().synchronize()
         self._c = _lib.rfb_scene()
@@ -152,6 +156,7 @@ class DeviceScene:
         c.edge_meta = None
         c.sh32 = self.sh32.data_ptr() if self.packed else None
         c.packed = 1 if self.packed else 0
+        c.positions_f64 = 1 if (self.packed and self.positions_f64) else 0
         c.sh_absmax = self.sh_absmax
         c.sh_degree = self.sh_degree
         for k in range(3):
@@ -182,8 +187,10 @@ class DeviceScene:
         self.diagonal = float(np.linalg.norm(hi - lo))
         self.center = 0.5 * (lo + hi)
         self.width_floor = WIDTH_FLOOR_SCALE * self.diagonal
-        self.packed = bool(torch.equal(pos.float().double(), pos)) if packed is None \
-            else bool(packed)
+        if packed is not None:
+            self.packed = bool(packed)
+        if not self.positions_f64:  # a scene built as fp32-exact stays so only if it still is
+            self.positions_f64 = not bool(torch.equal(pos.float().double(), pos))
         dev = self.device
         with torch.cuda.device(dev):
             site4 = torch.empty((n, 4), dtype=torch.float64, device=dev)
@@ -199,7 +206,8 @@ class DeviceScene:
             _lib.check(self.lib.rfb_pack_scene(
                 _ptr(pos), _ptr(sig), _ptr(self.sh), _ptr(off), _ptr(nbr), n, self.n_edges,
                 _ptr(site4), _ptr(self.offsets), _ptr(self.neighbors), _ptr(self.cells),
-                _ptr(self.edges), None, _ptr(self.sh32), _stream(stream)), "rfb_pack_scene")
+                _ptr(self.edges), None, _ptr(self.sh32), 1 if self.positions_f64 else 0,
+                _stream(stream)), "rfb_pack_scene")
             self.site4 = site4
         self.hull = hull
         self._refresh_struct()

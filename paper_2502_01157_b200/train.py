@@ -48,8 +48,10 @@ class DeviceTrainer:
 
     def __init__(self, scene, device=None, update_positions=True):
         self.update_positions = bool(update_positions)
+        # moving sites: packed layout with the fp64-position bound from the start
+        # (rfb_refresh_scene then re-derives the fp32 copies after every step)
         self.ds = dv.DeviceScene(scene, device=device,
-                                 packed=False if update_positions else None)
+                                 positions_f64=True if update_positions else None)
         self.device = self.ds.device
         n = self.ds.n_sites
         self.n = n
@@ -90,7 +92,7 @@ class DeviceTrainer:
     def rebuild_adjacency(self, stream=None) -> dict:
         """Re-triangulate the moved sites on the device (train.py:247-256's
         rebuild cadence; delaunay.build -> rfb_build_adjacency)."""
-        return self.ds.rebuild_adjacency(self.positions, packed=self.ds.packed, stream=stream)
+        return self.ds.rebuild_adjacency(self.positions, stream=stream)
 
     def step(self, origins, directions, t_min, t_max, start, targets, *, lr_position,
              lr_density, lr_sh, sh_warmup=False, quantile_scale=0.0, u_pairs=None,

@@ -344,10 +344,13 @@ def test_effect_rays_device(cuda_ok, kind):
         np.testing.assert_allclose(od.cpu().numpy()[i], r.direction, rtol=0, atol=1e-14)
 
 
-def test_generic_layout_fp64_positions_vs_oracle(cuda_ok):
+@pytest.mark.parametrize("packed", [True, False])
+def test_fp64_positions_vs_oracle(cuda_ok, packed):
     """Sites that are not fp32-representable (as after an Adam step on the
-    positions) take the generic fp64 layout; per-ray counters/status must
-    still be the oracle's bit for bit, and the image within 1e-4."""
+    positions): the packed layout with the widened pre-filter bound
+    (positions_f64) and the generic fp64 layout; per-ray cell sequences,
+    counters and status must be the oracle's bit for bit, the image within
+    1e-4."""
     from paper_2502_01157_b200 import device as dv
     from paper_2502_01157_b200.synthetic import delaunay_csr
 
@@ -360,8 +363,9 @@ def test_generic_layout_fp64_positions_vs_oracle(cuda_ok):
     sh = rng.normal(0, 0.3, (n, 48))
     from paper_2502_01157_b200.scene import softplus
     sa = orc.SceneArrays(pos, off, nbr, softplus(raw), sh, np.array([0.1, 0.2, 0.3]))
-    ds = dv.DeviceScene.from_arrays(pos, off, nbr, softplus(raw), sh, np.array([0.1, 0.2, 0.3]))
-    assert not ds.packed
+    ds = dv.DeviceScene.from_arrays(pos, off, nbr, softplus(raw), sh, np.array([0.1, 0.2, 0.3]),
+                                    packed=packed)
+    assert ds.packed == packed and ds.positions_f64
     m = 2048
     o = np.tile([0.0, 0.0, 3.0], (m, 1))
     d = rng.normal(size=(m, 3)) * [0.3, 0.3, 0.0] + [0.0, 0.0, -1.0]
@@ -370,8 +374,12 @@ def test_generic_layout_fp64_positions_vs_oracle(cuda_ok):
     tmax = ds.default_t_max(o[:1])
     ref = orc.render_rays(sa, o, d, 0.0, tmax, start)
     res = dv.render_rays_device(ds, _dev(o), _dev(d), _dev(np.zeros(m)), _dev(np.full(m, tmax)),
-                                _dev(np.full(m, start), torch.int32), f64=True)
+                                _dev(np.full(m, start), torch.int32), f64=True, seg_capacity=512)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
     np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
     assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= IMG_TOL
+    cells = res.seg_cells.cpu().numpy()
+    for q in range(0, m, 97):
+        c, a, b, *_ = orc.walk_ray(sa, o[q], d[q], 0.0, tmax, start)
+        np.testing.assert_array_equal(cells[q, :len(c)], c)

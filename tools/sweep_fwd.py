@@ -27,11 +27,18 @@ ap.add_argument("--once", action="store_true")
 ap.add_argument("--view", type=int, default=0)
 ap.add_argument("--packed", type=int, default=-1)
 ap.add_argument("--quantile", action="store_true")
+ap.add_argument("--fp64", action="store_true",
+                help="perturb the sites by 1e-12 (not fp32-exact; same Delaunay graph)")
 args = ap.parse_args()
 print("lib", os.environ.get("RFB_LIB", "default"), flush=True)
 
 scene = make_foam(args.n_sites, 1, 3)
+if args.fp64:
+    import numpy as np
+    scene.adjacency.positions += np.random.default_rng(0).normal(0, 1e-12, scene.adjacency.positions.shape)
+    scene.positions = scene.adjacency.positions
 ds = dv.DeviceScene(scene, packed=None if args.packed < 0 else bool(args.packed))
+print("packed", ds.packed, "positions_f64", getattr(ds, "positions_f64", None), flush=True)
 cam = make_views(args.view + 1, args.width, args.height)[args.view]
 ws = dv.Workspace(ds.device)
 out = dv.alloc_forward(args.width * args.height, ds.device, per_ray=False)

@@ -45,5 +45,5 @@ for _ in range(n):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / n
-print(f"training iteration (65,536 random pixels, 1M sites, generic fp64 layout): {ms:.2f} ms "
+print(f"training iteration (65,536 random pixels, 1M sites, moving fp64 sites): {ms:.2f} ms "
       f"= {m / ms / 1e3:.1f} M rays/s; loss {float(loss[0]) / (3 * m):.4f}")
