@@ -1325,7 +1325,6 @@ static SceneView<PACKED> view(const rfb_scene *s) {
     v.hdr = reinterpret_cast<const CellHdr *>(s->cells);
     v.edge = reinterpret_cast<const float4 *>(s->edges);
     v.emeta = reinterpret_cast<const int2 *>(s->edge_meta);
-    v.pos64 = s->positions_f64 != 0;
     v.site4 = reinterpret_cast<const double4 *>(s->site4);
     v.off = s->offsets;
     v.nbr = s->neighbors;

@@ -112,12 +112,13 @@ __device__ __forceinline__ void ldg256(const void *p, float4 &a, float4 &b) {
         : "l"(p));
 }
 
+// PACKED: 0 generic (site4 + int32 CSR), 1 packed with fp32-exact sites,
+// 2 packed with fp64 sites (rounded fp32 copies, widened bound; rfb_scene.positions_f64)
 template <int PACKED>
 struct SceneView {
     const CellHdr *hdr;     // PACKED
     const float4 *edge;     // PACKED
     const int2 *emeta;      // PACKED: [E] {k0_j, k1_j} of the edge's target site
-    bool pos64;             // PACKED: positions not fp32-exact -> exact phase reads site4
     const double4 *site4;   // both (backward gradients use fp64 positions)
     const int32_t *off;     // generic
     const int32_t *nbr;     // generic
@@ -447,9 +448,6 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #endif
 #ifndef RFB_F32_UNROLL
 #define RFB_F32_UNROLL 4
-#endif
-#ifndef RFB_POS64
-#define RFB_POS64 1  // support packed scenes with non-fp32-exact sites (positions_f64)
 #endif
 #ifndef RFB_PAIR_UNROLL
 #define RFB_PAIR_UNROLL 2  // edge pairs per unrolled phase-1 iteration (LDG.256 path)
