@@ -9,6 +9,7 @@ import pytest
 import torch
 
 from oracle import oracle as orc
+from paper_2502_01157_b200.synthetic import delaunay_csr  # noqa: E402
 
 pytestmark = pytest.mark.gpu
 
@@ -103,3 +104,38 @@ def test_random_scene_parity(cuda_ok, seed):
     assert rel(g4[:, 3], ds_) <= 1e-3
     assert rel(g4[:, :3], dp) <= 1e-3
     assert rel(gb.sh.double().cpu().numpy(), dsh) <= 1e-3
+
+
+@pytest.mark.parametrize("scale,offset", [(1e-3, 0.0), (1e-3, 0.02), (50.0, 0.0), (3.0, 2000.0)])
+def test_fp64_sites_scaled_vs_oracle(cuda_ok, scale, offset):
+    """The packed fp64-site bound (n1max + 2 max(X, 1/4)) across coordinate
+    magnitudes: tiny scenes (X < 1/4), large ones, and a small scene far from
+    the origin (X >> cell size); cell counters and status bit-exact."""
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200.scene import softplus
+
+    rng = np.random.default_rng(int(scale * 7 + offset))
+    n = 2500
+    pos = rng.uniform(-1, 1, (n, 3)) * scale + offset + rng.normal(0, 1e-9 * scale, (n, 3))
+    off, nbr, _ = delaunay_csr(pos)
+    raw = rng.normal(0, 1, n) - np.log(scale)  # keep optical depth O(1)
+    sh = rng.normal(0, 0.4, (n, 48))
+    bg = np.array([0.2, 0.1, 0.3])
+    sa = orc.SceneArrays(pos, off, nbr, softplus(raw), sh, bg)
+    ds = dv.DeviceScene.from_arrays(pos, off, nbr, softplus(raw), sh, bg)
+    assert ds.packed and ds.positions_f64
+    m = 1024
+    eye = np.array([offset, offset, offset + 3.0 * scale])
+    o = np.tile(eye, (m, 1))
+    d = rng.normal(size=(m, 3)) * [0.3, 0.3, 0.0] + [0.0, 0.0, -1.0]
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    start = int(orc.nearest_sites(pos, o[:1])[0])
+    tmax = ds.default_t_max(o[:1])
+    ref = orc.render_rays(sa, o, d, 0.0, tmax, start)
+    dev = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)  # noqa
+    res = dv.render_rays_device(ds, dev(o), dev(d), dev(np.zeros(m)), dev(np.full(m, tmax)),
+                                dev(np.full(m, start), torch.int32), f64=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
+    assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= 1e-4
