@@ -43,6 +43,7 @@
  *                        (+ quantile_backward_ray 456-567)
  *   rfb_post_grad_adam  optim/train.py:195-209 + optim/adam.py:15-31
  *   rfb_refresh_scene   diffrender/render.py:49-54 after a device-side update
+ *                        (moved sites: re-derives the packed copies and bounds)
  *
  * Per-ray status semantics are the reference's (tracer/kernels.py:11-21):
  * 0 ok, 2 step limit, 3 cycle; failed rays render the background with
@@ -71,11 +72,13 @@ extern "C" {
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
- *  packed (packed != 0, positions exactly representable in fp32): per-site
- *   32-byte cell headers {float x,y,z; int k0; double sigma; int k1;
- *   float n1max} and per-edge 16-byte records {float xj,yj,zj; int j} in CSR
- *   order, per-edge int2 {k0, k1} of the target site (edge_meta), plus
- *   fp32 SH (sh32) with the fp64 table kept for the exact clamp fallback.
+ *  packed (packed != 0): per-site 32-byte cell headers {float x,y,z; int k0;
+ *   double sigma; int k1; float n1max} and per-edge 16-byte records
+ *   {float xj,yj,zj; int j} in CSR order, plus fp32 SH (sh32) with the fp64
+ *   table kept for the exact clamp fallback.  With positions_f64 == 0 the
+ *   fp32 coordinates are the sites themselves; with positions_f64 != 0 they
+ *   are rounded copies, n1max carries the widened pre-filter bound and the
+ *   exact phase reads site4 (rfb_pack_scene and rfb_refresh_scene derive both).
  *   The generic arrays are always present (backward, locate). */
 typedef struct rfb_scene {
     int64_t n_sites;
@@ -166,8 +169,10 @@ int rfb_device_ok(void);                /* 1 when an sm_100 device is current */
 /* Build the device layout from fp64/int64 device arrays:
  * positions [n][3], sigma [n], sh [n][48], offsets [n+1], neighbors [E]
  * -> site4 [n][4] f64, offsets32 [n+1], neighbors32 [E] and, when
- * cells/edges/sh32 are non-NULL, the packed layout (caller guarantees the
- * positions are exactly representable in fp32). */
+ * cells/edges/sh32 are non-NULL, the packed layout.  positions_f64 must be
+ * nonzero unless every coordinate is exactly representable in fp32 (and
+ * stays so: set it for scenes whose sites will move); the same value goes
+ * into rfb_scene.positions_f64.  edge_meta (optional) is unused by the walk. */
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
