@@ -184,6 +184,20 @@ def algorithmic_bytes(C, V, N, m, sh_bytes):
 
 
 # ---------------------------------------------------------------------------
+def _train_roofline():
+    """k_train's measured binding unit and DRAM traffic (profiles/traffic.json, from the
+    committed ncu capture)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        return {"kernel": "k_train (walk + record + reverse pass)",
+                "binding_unit": "l1tex data-pipe wavefronts",
+                "binding_frac": tj.get("k_train_l1_data_pipe_frac"),
+                "traffic": tj.get("k_train_dram_bytes_per_launch"), "source": tj.get("source")}
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def run_reference(args):
     """CPU reference arm: the oracle port on all host threads (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -429,6 +443,7 @@ def main():
               "views_per_step": n_train_views,
               "algorithmic_bytes_per_view": fb_bytes,
               "achieved_GBps": fb_bytes * n_train_views / world / (fb_ms / args.steps / 1e3) / 1e9,
+              "roofline": _train_roofline(),
               "cells_per_ray": int(out_fb.ray_counters[:, 0].sum().item()) / m,
               "loss_rgb": float(loss[0].item()) / (3.0 * m * n_train_views),
               "clocks": clocks_fb}
