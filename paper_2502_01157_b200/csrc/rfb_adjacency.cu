@@ -639,7 +639,10 @@ __device__ __forceinline__ RingBox ring_box(int r, int ix, int iy, int iz, const
 // shared memory and warp 0 clips by them.  After every ring the box and the
 // security radius are refreshed, so a long cell that gets capped stops
 // scanning early; unbounded (hull) cells scan to the grid's edge.
-constexpr int kTailThreads = 256;
+#ifndef RFB_ADJ_TAIL_THREADS
+#define RFB_ADJ_TAIL_THREADS 256
+#endif
+constexpr int kTailThreads = RFB_ADJ_TAIL_THREADS;
 constexpr int kTailQueue = 512;
 
 __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t count) {
