@@ -383,3 +383,35 @@ def test_fp64_positions_vs_oracle(cuda_ok, packed):
     for q in range(0, m, 97):
         c, a, b, *_ = orc.walk_ray(sa, o[q], d[q], 0.0, tmax, start)
         np.testing.assert_array_equal(cells[q, :len(c)], c)
+
+
+def test_train_batch_step_limit_failures_vs_oracle(cuda_ok):
+    """Rays that hit the step limit render the background and contribute no
+    gradient (kernels.py:230-236, 408-412); the rest are trained normally."""
+    from paper_2502_01157_b200 import device as dv
+
+    g = load_golden("train_2k_deg3_q")
+    sa = golden_scene_arrays(g)
+    m = len(g["origins"])
+    ref = orc.train_batch(sa, g["origins"], g["dirs"], np.zeros(m), g["t_max"], g["start"],
+                          g["targets"], float(g["rgb_scale"]), float(g["quantile_scale"]),
+                          g["u_pairs"], 1e-4, epsilon=float(g["epsilon"]), step_limit=22,
+                          threads=8)
+    assert (ref["status"] == 2).any() and (ref["status"] == 0).any()
+    ds = dv.DeviceScene(golden_scene(g))
+    gb = dv.GradBuffers(ds.n_sites, ds.device)
+    loss = torch.zeros(2, dtype=torch.float64, device="cuda")
+    res = dv.train_batch_device(ds, _dev(g["origins"]), _dev(g["dirs"]), _dev(np.zeros(m)),
+                                _dev(g["t_max"]), _dev(g["start"], torch.int32),
+                                _dev(g["targets"]), gb, loss, rgb_scale=float(g["rgb_scale"]),
+                                quantile_scale=float(g["quantile_scale"]),
+                                u_pairs=_dev(g["u_pairs"]), weight_floor=1e-4,
+                                epsilon=float(g["epsilon"]), step_limit=22, f64=True)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= IMG_TOL
+    np.testing.assert_allclose(loss.cpu().numpy(), ref["loss_w"].sum(axis=0), rtol=1e-6)
+    g4 = gb.g4.double().cpu().numpy()
+    assert rel_err(g4[:, 3], ref["d_sigma_w"].sum(axis=0)) <= GRAD_RTOL
+    assert rel_err(g4[:, :3], ref["d_pos_w"].sum(axis=0)) <= GRAD_RTOL
+    assert rel_err(gb.sh.double().cpu().numpy(), ref["d_sh_w"].sum(axis=0)) <= GRAD_RTOL
