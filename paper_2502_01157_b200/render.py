@@ -20,6 +20,7 @@ kernel arrays on every call too, render.py:49-54).
 from __future__ import annotations
 
 import time
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -36,6 +37,11 @@ WIDTH_FLOOR_SCALE = dv.WIDTH_FLOOR_SCALE
 STATUS_OK = 0
 STATUS_STEP_LIMIT = 2
 STATUS_CYCLE = 3
+
+# render_image returns frames that live in pinned host buffers (no host-side
+# copy); at most this many per resolution, further frames a caller still holds
+# go to pageable memory
+PINNED_FRAMES = 2
 
 
 @dataclass
@@ -275,17 +281,29 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
     t0 = time.perf_counter()
     res = dv.render_image_device(ds, camera, epsilon=epsilon, step_limit=step_limit, f64=True,
                                  lanes_per_ray=lanes_per_ray, workspace=fc["ws"], out=fc["out"])
-    # D2H straight into a fresh pinned buffer from torch's caching host
-    # allocator; the returned array owns it (no host-side copy), and the block
-    # is recycled once the caller drops the image.
-    h_rgb = torch.empty((W * H, 3), dtype=torch.float64, pin_memory=True)
-    h_rgb.copy_(res.rgb, non_blocking=True)
+    # D2H straight into a free pinned buffer of this resolution and return a
+    # view of it (no host-side copy); a buffer is free once the caller dropped
+    # the image it holds.  With PINNED_FRAMES buffers in use the frame goes to
+    # fresh pageable memory instead (slower, but callers that keep every frame
+    # never accumulate pinned memory).
+    pool = fc["h_rgb"]  # [(pinned tensor, weakref to the array handed out)]
+    free = next((e for e in pool if e[1] is None or e[1]() is None), None)
+    if free is None and len(pool) < PINNED_FRAMES:
+        free = [torch.empty((W * H, 3), dtype=torch.float64, pin_memory=True), None]
+        pool.append(free)
+    if free is not None:
+        free[0].copy_(res.rgb, non_blocking=True)
+        root = free[0].numpy()
+        free[1] = weakref.ref(root)
+    else:
+        root = np.empty((W * H, 3), dtype=np.float64)
+        torch.from_numpy(root).copy_(res.rgb)
     if weight_check:
         fc["h_wsum"].copy_(res.wsum, non_blocking=True)
         fc["h_resid"].copy_(res.residual, non_blocking=True)
     torch.cuda.current_stream(ds.device).synchronize()
     dt = time.perf_counter() - t0
-    img = h_rgb.numpy().reshape(H, W, 3)
+    img = root.reshape(H, W, 3)
     if stats is not None:
         cnt = res.counters.cpu().numpy()
         status = res.status.cpu().numpy()
@@ -307,7 +325,8 @@ def _frame_cache(ds, W, H, weight_check):
     fc = cache.get(key)
     if fc is None:
         fc = {"ws": dv.Workspace(ds.device),
-              "out": dv.alloc_forward(W * H, ds.device, f64=True, per_ray=False)}
+              "out": dv.alloc_forward(W * H, ds.device, f64=True, per_ray=False),
+              "h_rgb": []}
         cache[key] = fc
     if weight_check and "h_wsum" not in fc:
         fc["h_wsum"] = torch.empty(W * H, dtype=torch.float64, pin_memory=True)

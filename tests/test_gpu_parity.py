@@ -415,3 +415,22 @@ def test_train_batch_step_limit_failures_vs_oracle(cuda_ok):
     assert rel_err(g4[:, 3], ref["d_sigma_w"].sum(axis=0)) <= GRAD_RTOL
     assert rel_err(g4[:, :3], ref["d_pos_w"].sum(axis=0)) <= GRAD_RTOL
     assert rel_err(gb.sh.double().cpu().numpy(), ref["d_sh_w"].sum(axis=0)) <= GRAD_RTOL
+
+
+def test_render_image_frames_are_independent(cuda_ok):
+    """render_image returns frames backed by a small pool of pinned buffers:
+    frames the caller keeps must never be overwritten by later renders."""
+    from paper_2502_01157_b200 import render as rd
+    from paper_2502_01157_b200.camera import PINHOLE, CameraModel, look_at
+
+    g = load_golden("frame_2k_deg3")
+    scene = golden_scene(g)
+    from paper_2502_01157_b200 import device as dv
+    ds = dv.DeviceScene(scene)
+    cams = [CameraModel.from_angle_x(PINHOLE, 64, 48, 0.9, look_at((0.3 * k, 0.0, 3.0), (0, 0, 0)))
+            for k in range(5)]
+    kept = [rd.render_image(scene, c, device_scene=ds) for c in cams]
+    again = [rd.render_image(scene, c, device_scene=ds).copy() for c in cams]
+    for a, b in zip(kept, again):
+        np.testing.assert_array_equal(a, b)
+    assert not np.array_equal(kept[0], kept[1])
