@@ -54,8 +54,10 @@ def build_device(positions: torch.Tensor, max_degree: int = MAX_DEGREE, stream=N
         if code == -3:  # RFB_EDEGENERATE
             if not torch.isfinite(pos).all():
                 raise DegenerateInput("non-finite coordinates")
-            raise DuplicatePoints("sites within duplicate tolerance "
-                                  f"{1e-7 * _diag(pos):g}")
+            if int(stats[7]) & 2:
+                raise DuplicatePoints("sites within duplicate tolerance "
+                                      f"{1e-7 * _diag(pos):g}")
+            raise DegenerateInput("degenerate configuration (coplanar cell faces)")
         if code == -2:
             raise DeviceError(f"rfb_build_adjacency: capacity exceeded (flags {int(stats[7])}, "
                               f"max vertices {int(stats[3])}, max planes {int(stats[4])})")
@@ -66,10 +68,25 @@ def build_device(positions: torch.Tensor, max_degree: int = MAX_DEGREE, stream=N
         _lib.check(lib.rfb_adjacency_emit(n, max_degree, _ptr(offsets), _ptr(neighbors),
                                           _ptr(hull), _ptr(ws), ws.numel(), st),
                    "rfb_adjacency_emit")
+    if bool(hull.all()) and _coplanar(pos):
+        raise DegenerateInput("all points collinear or coplanar")  # delaunay.py:494-495
     info = {"edges": E, "reverse_edges_added": int(stats[1]), "pass2_sites": int(stats[2]),
             "max_cell_vertices": int(stats[3]), "max_cell_planes": int(stats[4]),
             "clip_tests_spiral": int(stats[5]), "clip_tests_rings": int(stats[6])}
     return offsets, neighbors[:E], hull.bool(), info
+
+
+def _coplanar(pos: torch.Tensor) -> bool:
+    """Every site on one plane (checked only when every cell is unbounded):
+    fp64 orientation of all sites against three spread-out ones is exactly 0."""
+    p = pos - pos[0]
+    a = p[int(torch.argmax((p * p).sum(1)))]
+    c = torch.linalg.cross(p, a.expand_as(p))
+    b = p[int(torch.argmax((c * c).sum(1)))]
+    normal = torch.linalg.cross(a, b)
+    if not bool(torch.any(normal != 0)):
+        return True  # collinear
+    return not bool(torch.any(p @ normal != 0))
 
 
 def _diag(pos: torch.Tensor) -> float:

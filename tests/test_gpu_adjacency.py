@@ -59,6 +59,12 @@ def test_adjacency_errors_and_host_api(cuda_ok):
         A.build(bad)
     with pytest.raises(DegenerateInput):
         A.build(pos[:3])
+    plane = np.c_[np.random.default_rng(1).uniform(0, 1, (400, 2)), np.zeros(400)]
+    with pytest.raises(DegenerateInput):
+        A.build(plane)  # delaunay.py:494-495
+    lattice = np.stack(np.meshgrid(*[np.arange(6.0)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    with pytest.raises(DegenerateInput):  # cospherical sets: outside the device builder's scope
+        A.build(lattice)
 
 
 def test_device_scene_rebuild_matches_host_build(cuda_ok):
