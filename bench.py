@@ -65,6 +65,8 @@ def parse():
                          "u_pairs from rng(12); optim/config.py:34-36)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-train-iter", action="store_true",
+                    help="skip timing a reference-style training iteration (65,536 random pixels)")
     ap.add_argument("--no-adjacency", action="store_true",
                     help="skip timing the device Delaunay rebuild (SURVEY §8f row 2)")
     ap.add_argument("--cpu-row-stride", type=int, default=8)
@@ -448,6 +450,50 @@ def main():
               "loss_rgb": float(loss[0].item()) / (3.0 * m * n_train_views),
               "clocks": clocks_fb}
 
+    # -- one training iteration as the reference's loop runs it (optim/train.py:131-209)
+    train_iter = None
+    if not args.no_train_iter and rank == 0 and world == 1 and args.config in (1, 2):
+        from paper_2502_01157_b200.train import DeviceTrainer
+        tr = DeviceTrainer(scene, device=dev)
+        mb = 65536
+        tv = orbit_views(W, H, 8)
+        tdirs = torch.stack([c.ray_directions_device(device=dev) for c in tv])
+        torig = torch.from_numpy(np.stack([c.position for c in tv])).to(dev)
+        timgs = torch.rand((len(tv), W * H, 3), dtype=torch.float64, device=dev,
+                           generator=torch.Generator(device=dev).manual_seed(13))
+        tgen = torch.Generator(device=dev).manual_seed(14)
+        t_far = tr.ds.default_t_max(np.stack([c.position for c in tv]))
+
+        def train_step():
+            flat = torch.randint(0, len(tv) * W * H, (mb,), device=dev, generator=tgen)
+            vi, pi = flat // (W * H), flat % (W * H)
+            st = tr.ds.locate(torig)
+            return tr.step(torig[vi], tdirs[vi, pi],
+                           torch.zeros(mb, dtype=torch.float64, device=dev),
+                           torch.full((mb,), t_far, dtype=torch.float64, device=dev),
+                           st[vi].contiguous(), timgs[vi, pi], lr_position=1e-5,
+                           lr_density=0.05, lr_sh=5e-3)
+
+        for _ in range(3):
+            train_step()
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        n_it = 10
+        a0.record(stream)
+        for _ in range(n_it):
+            train_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        it_ms = a0.elapsed_time(a1) / n_it
+        train_iter = {"ms": it_ms, "rays_per_iteration": mb, "value": mb / (it_ms / 1e3),
+                      "unit": UNIT,
+                      "workload": "65,536 random pixels of 8 orbit views (the reference's "
+                                  "batch_rays) -> start cells, train_batch, gradient chain + clip "
+                                  "+ Adam on every parameter, scene refresh (moving fp64 sites); "
+                                  "train.DeviceTrainer.step"}
+        del tr, tdirs, timgs
+
     # -- device Delaunay rebuild of the same sites --------------
     adjacency = None
     if not args.no_adjacency and rank == 0:
@@ -555,6 +601,7 @@ def main():
         "fwd_bwd": fb,
         "e2e": e2e,
         "adjacency_rebuild": adjacency,
+        "train_iteration": train_iter,
         "gpu_launches": (3 * args.steps * len(views) if args.config != 5
                          else args.steps * len(train_views)),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
