@@ -1276,7 +1276,7 @@ __global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double
 // device): site4 = {pos, softplus(raw)}, packed headers' sigma, sh32.
 __global__ void k_refresh_scene(int64_t n, const double *pos, const double *raw,
                                 const double *sh, double4 *site4, CellHdr *cells, float *sh32,
-                                const int32_t *off, const int32_t *nbr, int pos64) {
+                                const int32_t *off, const float4 *edges, int pos64) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double x = raw[i];
@@ -1284,25 +1284,25 @@ __global__ void k_refresh_scene(int64_t n, const double *pos, const double *raw,
     site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sig);
     if (cells) cells[i].sigma = sig;
     if (cells && pos64) {  // moved sites: fp32 copies and the widened bound (k_pack_sites)
+        // reads the refreshed fp32 edge records (k_refresh_edges ran first): the
+        // same fp32 n as k_pack_sites; |x| <= |fl32(x)| (1 + 2^-23)
         const float xi = (float)pos[3 * i], yi = (float)pos[3 * i + 1], zi = (float)pos[3 * i + 2];
         float n1max = 0.f;
         double xabs = fmax(fabs(pos[3 * i]), fmax(fabs(pos[3 * i + 1]), fabs(pos[3 * i + 2])));
+        float xabs_f = 0.f;
         for (int32_t k = off[i]; k < off[i + 1]; ++k) {
-            const int32_t j = nbr[k];
-            const float nx = (float)pos[3 * j] - xi, ny = (float)pos[3 * j + 1] - yi,
-                        nz = (float)pos[3 * j + 2] - zi;
+            const float4 e = __ldg(edges + k);
+            const float nx = e.x - xi, ny = e.y - yi, nz = e.z - zi;
             n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
-            xabs = fmax(xabs, fmax(fabs(pos[3 * j]), fmax(fabs(pos[3 * j + 1]), fabs(pos[3 * j + 2]))));
+            xabs_f = fmaxf(xabs_f, fmaxf(fabsf(e.x), fmaxf(fabsf(e.y), fabsf(e.z))));
         }
+        xabs = fmax(xabs, (double)xabs_f * (1.0 + 0x1p-22));
         CellHdr &h = cells[i];
         h.x = xi;
         h.y = yi;
         h.z = zi;
         h.n1max = n1max * (1.0f + 0x1p-20f) + pos64_widen(xabs);
     }
-    if (sh32)
-        for (int k = 0; k < 16; ++k)
-            for (int ch = 0; ch < 3; ++ch) sh32[i * 48 + 16 * ch + k] = (float)sh[i * 48 + 3 * k + ch];
 }
 
 // ---------------------------------------------------------------------------
@@ -1620,6 +1620,15 @@ int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positio
     return (int)cudaGetLastError();
 }
 
+// fp32 channel-major SH copy, one thread per output float (coalesced rows)
+__global__ void k_refresh_sh32(int64_t n, const double *sh, float *sh32) {
+    const int64_t o = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (o >= 48 * n) return;
+    const int64_t i = o / 48;
+    const int r = (int)(o - 48 * i), ch = r / 16, k = r - 16 * ch;
+    sh32[o] = (float)sh[48 * i + 3 * k + ch];
+}
+
 __global__ void k_refresh_edges(const int32_t *nbr, const double *pos, int64_t E, float4 *edges) {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= E) return;
@@ -1634,15 +1643,17 @@ int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const dou
     // a packed scene with fp32-exact positions cannot take moved sites in place
     const bool pos64 = scene->packed && scene->positions_f64;
     cudaStream_t st = (cudaStream_t)stream;
-    k_refresh_scene<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, st>>>(
-        scene->n_sites, positions, raw_density, scene->sh, (double4 *)scene->site4,
-        scene->packed ? (CellHdr *)scene->cells : nullptr,
-        scene->packed ? (float *)scene->sh32 : nullptr, scene->offsets, scene->neighbors,
-        pos64 ? 1 : 0);
-    if (pos64 && scene->n_edges > 0)
+    if (pos64 && scene->n_edges > 0)  // first: k_refresh_scene reads the new records
         k_refresh_edges<<<(unsigned)((scene->n_edges + 255) / 256), 256, 0, st>>>(
             scene->neighbors, positions, scene->n_edges,
             reinterpret_cast<float4 *>(const_cast<void *>(scene->edges)));
+    k_refresh_scene<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, st>>>(
+        scene->n_sites, positions, raw_density, scene->sh, (double4 *)scene->site4,
+        scene->packed ? (CellHdr *)scene->cells : nullptr,
+        nullptr, scene->offsets, reinterpret_cast<const float4 *>(scene->edges), pos64 ? 1 : 0);
+    if (scene->packed && scene->sh32)
+        k_refresh_sh32<<<(unsigned)((48 * scene->n_sites + 255) / 256), 256, 0, st>>>(
+            scene->n_sites, scene->sh, (float *)scene->sh32);
     return (int)cudaGetLastError();
 }
 
