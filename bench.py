@@ -109,6 +109,32 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def gather_ceilings():
+    """Random-gather ceilings measured on a B200 by tools/gather_peak.cu, read from
+    the committed profile so the bench line shows which memory level the walk runs at."""
+    path = os.path.join(REPO, "profiles", "r09_gather_peak.jsonl")
+    try:
+        rows = [json.loads(x) for x in open(path) if x.startswith("{")]
+    except OSError:
+        return None
+    g = [r for r in rows if r["kind"] == "gather"]
+
+    def best(access, lo, hi):
+        sel = [r["useful_GBps"] for r in g if r["access"] == access and lo <= r["working_set_bytes"] <= hi]
+        return max(sel) if sel else None
+
+    l2 = (4 << 20, 64 << 20)
+    hbm = (1 << 30, 4 << 30)
+    return {"unit": "GB/s useful",
+            "l2_lane16": best("lane16", *l2), "l2_lane32": best("lane32", *l2),
+            "l2_warp512": best("warp512", *l2),
+            "hbm_lane16": best("lane16", *hbm), "hbm_lane32": best("lane32", *hbm),
+            "hbm_warp512": best("warp512", *hbm),
+            "latency_ns": {str(r["working_set_bytes"]): r["ns_per_hop"] for r in rows
+                           if r["kind"] == "chase"},
+            "source": "profiles/r09_gather_peak.jsonl (tools/gather_peak.cu)"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
 
@@ -615,7 +641,8 @@ def main():
                              "is `traffic` and frac can exceed 1. The binding unit is the L1 "
                              "data pipe (binding_frac, from the ncu capture in profiles/).",
                      "binding_unit": "l1tex data-pipe wavefronts",
-                     "binding_frac": l1_frac},
+                     "binding_frac": l1_frac,
+                     "gather_ceilings": gather_ceilings()},
         "cpu_baseline": cpu,
         "clocks": clocks,
     }
