@@ -19,10 +19,13 @@ gradient buffer is all-reduced.  Per-rank work is fixed as N grows:
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 synchronize, timed with CUDA events on the launching stream, max over ranks.
-The scene (482 MB) is larger than L2 (126 MB).  nvidia-smi clocks are
+The scene (~950 MB packed at config 2) is larger than L2 (126 MB).  nvidia-smi clocks are
 sampled during the timed region.  ``e2e`` times the public API
 (render.render_image with a resident scene: camera in, (H,W,3) float64 image
-copied to host) including the device->host copy of the image.
+copied to host) including the device->host copy of the image; at N>1 the
+tile-sharded distributed.ShardedRenderer with the frame assembled on rank 0
+and copied to the host there.  RFB_BENCH_DIST=1 takes the collective path at
+N=1 too (a 1-rank NCCL group), to exercise it on one GPU.
 
 --impl reference: the reference algorithm's CPU implementation on the host
 cores (the C oracle port of rfoam/tracer/kernels.py, every host thread), on
@@ -299,13 +302,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # RFB_BENCH_DIST=1 runs the collective code path even at world size 1 (a 1-rank NCCL
+    # group), so the N>1 plumbing can be exercised on the single GPU this round has
+    dist_on = world > 1 or os.environ.get("RFB_BENCH_DIST") == "1"
     torch.cuda.set_device(local)
-    if world > 1:
+    if dist_on:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     def barrier():
-        if world > 1:
+        if dist_on:
             dist.barrier()
 
     W, H = args.width, args.height
@@ -335,11 +341,11 @@ def main():
 
     def fwd_step():
         for k, cam in enumerate(views):
-            if world > 1:
+            if dist_on:
                 frames[k].rgb.zero_()
             dv.render_image_device(ds, cam, tile_ids=my_tiles, lanes_per_ray=lanes, workspace=ws,
                                    out=frames[k])
-        if world > 1:
+        if dist_on:
             for fr in frames:
                 dist.reduce(fr.rgb, dst=0)
 
@@ -382,7 +388,7 @@ def main():
     kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
     clocks = clk.stop() if rank == 0 else None
     t = torch.tensor([fwd_ms], dtype=torch.float64, device=dev)
-    if world > 1:
+    if dist_on:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     fwd_ms = float(t.item())
     rays_total = args.steps * W * H * len(views)
@@ -425,7 +431,7 @@ def main():
                                       rgb_scale=rgb_scale, quantile_scale=q_scale,
                                       u_pairs=u_pairs, workspace=wsb, out=out_fb,
                                       order=None)  # rays already in tile order
-            if world > 1:
+            if dist_on:
                 dist.all_reduce(gb.flat)
                 dist.all_reduce(loss)
 
@@ -449,7 +455,7 @@ def main():
         fb_ms = e0.elapsed_time(e1)
         clocks_fb = clk2.stop() if rank == 0 else None
         t = torch.tensor([fb_ms], dtype=torch.float64, device=dev)
-        if world > 1:
+        if dist_on:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         fb_ms = float(t.item())
         fb_C = int(out_fb.ray_counters[:, 0].sum().item())
@@ -467,7 +473,7 @@ def main():
                            "forward+backward split over the ranks")
                           + (", L2 adjoint + quantile regulariser (lambda 0.01, P=2)"
                              if args.quantile else ", L2 adjoint, quantile off")
-                          + (", NCCL all-reduce" if world > 1 else ""),
+                          + (", NCCL all-reduce" if dist_on else ""),
               "views_per_step": n_train_views,
               "algorithmic_bytes_per_view": fb_bytes,
               "achieved_GBps": fb_bytes * n_train_views / world / (fb_ms / args.steps / 1e3) / 1e9,
@@ -547,7 +553,7 @@ def main():
 
     # -- e2e through the public API (rank 0 view, host image out) -----------------
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and not dist_on:
         cam = views[0]
         rd.render_image(scene, cam, device_scene=ds, lanes_per_ray=lanes)
         torch.cuda.synchronize()
@@ -559,9 +565,36 @@ def main():
         e2e = {"value": W * H / float(np.median(ts)), "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": int(img.nbytes),
                "api": "render.render_image(scene, camera, device_scene=ds) -> (H,W,3) f64 host"}
+    elif not args.no_e2e:
+        # N > 1: the sharded public API -- every rank renders its tiles of each view, the
+        # frame is assembled on rank 0 and copied to the host there; max over ranks
+        from paper_2502_01157_b200.distributed import ShardedRenderer
+        sr = ShardedRenderer(ds, W, H, lanes_per_ray=lanes)
+
+        def e2e_step():
+            imgs = [sr.render_to_host(cam, dst=0) for cam in views]
+            return [x for x in imgs if x is not None]
+
+        e2e_step()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(max(3, min(args.steps, 10))):
+            barrier()
+            t0 = time.perf_counter()
+            imgs = e2e_step()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        t = torch.tensor([float(np.median(ts))], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = {"value": len(views) * W * H / float(t.item()), "unit": UNIT,
+               "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": int(sum(x.nbytes for x in imgs)) if rank == 0 else 0,
+               "api": "distributed.ShardedRenderer(ds, W, H).render_to_host(camera) per view "
+                      "(tile-sharded over the ranks, NCCL reduce to rank 0) -> pinned host frame",
+               "timing": "median over steps of the per-rank wall clock, max over ranks"}
 
     if rank != 0:
-        if world > 1:
+        if dist_on:
             dist.destroy_process_group()
         return
 
@@ -647,7 +680,7 @@ def main():
         "clocks": clocks,
     }
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if dist_on:
         dist.destroy_process_group()
 
 

@@ -113,3 +113,20 @@ class ShardedRenderer:
                                     tile_ids=self.tiles, tile_w=self.tile_w, tile_h=self.tile_h,
                                     lanes_per_ray=self.lanes, workspace=self.ws, out=self.out)
         return assemble_frame(self.out.rgb, dst=dst)
+
+    def render_to_host(self, camera, epsilon=1e-3, step_limit=4096, dst: int = 0):
+        """render() plus the device->host copy of the assembled frame on ``dst`` into a
+        pinned buffer (two alternate, so the previous frame stays valid for one more call).
+        Returns the (H*W, 3) float32 host frame on ``dst`` and None elsewhere."""
+        frame = self.render(camera, epsilon=epsilon, step_limit=step_limit, dst=dst)
+        if self.rank != dst:
+            return None
+        if not hasattr(self, "_pinned"):
+            self._pinned = [torch.empty(frame.shape, dtype=frame.dtype, pin_memory=True)
+                            for _ in range(2)]
+            self._next = 0
+        host = self._pinned[self._next]
+        self._next ^= 1
+        host.copy_(frame, non_blocking=True)
+        torch.cuda.current_stream(frame.device).synchronize()
+        return host

@@ -77,6 +77,23 @@ def test_tile_sharded_assembly_bitwise(cuda_ok, scene100k):
     assert torch.equal(acc, full)
 
 
+def test_sharded_renderer_host_frame(cuda_ok, scene100k):
+    """distributed.ShardedRenderer (world size 1 here) gives the single render's frame,
+    in a pinned host buffer that stays valid for one more call."""
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200.distributed import ShardedRenderer
+
+    W, H = 200, 120
+    ds = dv.DeviceScene(scene100k)
+    cams = [_cam(W, H, k) for k in range(2)]
+    full = [dv.render_image_device(ds, c).rgb.cpu() for c in cams]
+    sr = ShardedRenderer(ds, W, H)
+    h0 = sr.render_to_host(cams[0])
+    h1 = sr.render_to_host(cams[1])
+    assert h0.is_pinned() and h0.data_ptr() != h1.data_ptr()
+    assert torch.equal(h0, full[0]) and torch.equal(h1, full[1])
+
+
 def test_train_100k_gradients(cuda_ok, scene100k):
     from paper_2502_01157_b200 import device as dv
 
