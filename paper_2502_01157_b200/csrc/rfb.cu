@@ -226,6 +226,7 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
                 return RFB_STATUS_CYCLE;
             }
         }
+        RFB_BOUND(best_j, S.n_sites);
         i = best_j;
     }
 }
@@ -581,6 +582,8 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                     cb += wf * (float)col[2];
                     Tb = Tn;
                     if (G == 1 || gl == 0) {
+                        RFB_BOUND(s, step_limit);
+                        RFB_BOUND(slot, SL4);
                         rec_a[s * SL4] = make_float4(__int_as_float(cell | (mask << 29)),
                                                      (float)col[0], (float)col[1], (float)col[2]);
                         rec_b[s * SL4] = make_double2(t1, Tn);
@@ -813,7 +816,9 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
             if (per_lane) {  // this lane's segment straight to its cell (kernels.py:309-337)
                 if (in) {
                     const float *b = &s_basis[warp][lane][0];
-                    float *row = gr.sh + 48 * (int64_t)lc;
+                    RFB_BOUND(lc, S.n_sites);
+                    RFB_BOUND(lc, S.n_sites);
+            float *row = gr.sh + 48 * (int64_t)lc;
                     if (v[0] != 0.f || v[1] != 0.f || v[2] != 0.f) {
 #pragma unroll
                         for (int q4 = 0; q4 < 12; ++q4) {
@@ -827,6 +832,7 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                         }
                     }
                     red4(gr.g4 + 4 * (int64_t)lc, v[3], v[4], v[5], v[6]);
+                    RFB_BOUND(jn + 1, S.n_sites + 1);  // -1: none
                     if (jn >= 0) red4(gr.g4 + 4 * (int64_t)jn, v[7], v[8], v[9], 0.f);
                 }
                 continue;
@@ -1334,6 +1340,8 @@ static SceneView<PACKED> view(const rfb_scene *s) {
     v.bg[0] = s->background[0];
     v.bg[1] = s->background[1];
     v.bg[2] = s->background[2];
+    v.n_sites = s->n_sites;
+    v.n_edges = s->n_edges;
     return v;
 }
 

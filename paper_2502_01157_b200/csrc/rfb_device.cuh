@@ -27,6 +27,15 @@
 #ifndef RFB_HDR256
 #define RFB_HDR256 0  // one 256-bit load per cell header
 #endif
+#ifndef RFB_CHECK
+#define RFB_CHECK 0  // 1: device-side bounds asserts on every scene gather / record (debug build)
+#endif
+#if RFB_CHECK
+#include <cassert>
+#define RFB_BOUND(i, n) assert((int64_t)(i) >= 0 && (int64_t)(i) < (int64_t)(n))
+#else
+#define RFB_BOUND(i, n) ((void)0)
+#endif
 
 namespace rfb {
 
@@ -126,12 +135,14 @@ struct SceneView {
     const double *sh;       // [n][48] fp64 (reference values)
     float sh_absmax;        // max |sh coefficient| over the scene (colour rounding bound)
     double bg[3];
+    int64_t n_sites, n_edges;  // extents (RFB_CHECK builds assert every index against them)
 
     // Per-step cell record.  PACKED: only the fp32 header fields (the walk
     // widens x,y,z exactly where the fp64 path needs them and fetches sigma
     // when a segment is recorded) -- fewer live registers across the
     // neighbour loop.
     __device__ __forceinline__ Cell cell(int32_t i) const {
+        RFB_BOUND(i, n_sites);
         Cell c;
         if (PACKED) {
             const float4 *p = reinterpret_cast<const float4 *>(hdr + i);
@@ -147,6 +158,8 @@ struct SceneView {
             c.k0 = __float_as_int(a.w);
             c.k1 = __float_as_int(b.x);
             c.n1max = b.y;
+            RFB_BOUND(c.k0, c.k1 + 1);
+            RFB_BOUND(c.k1, n_edges + 1);
         } else {
             double4 s = ld_site(site4 + i);
             c.x = s.x;
@@ -161,12 +174,14 @@ struct SceneView {
     }
 
     __device__ __forceinline__ double sigma_of(int32_t i, const Cell &c) const {
+        RFB_BOUND(i, n_sites);
         if (PACKED) return __ldg(&hdr[i].sigma);
         return c.sigma;
     }
 
     __device__ __forceinline__ void edge_at(int32_t k, double &x, double &y, double &z,
                                             int32_t &j) const {
+        RFB_BOUND(k, n_edges);
         if (PACKED) {
             float4 e = __ldg(edge + k);
             x = e.x;
@@ -175,6 +190,7 @@ struct SceneView {
             j = __float_as_int(e.w);
         } else {
             j = __ldg(nbr + k);
+            RFB_BOUND(j, n_sites);
             double4 s = ld_site(site4 + j);
             x = s.x;
             y = s.y;
@@ -210,6 +226,7 @@ template <int SHDEG, int PACKED, int BSTRIDE = 1, class RayT>
 __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
                                           const float *basis_f, const RayT &ray,
                                           double bsum, double *col) {
+    RFB_BOUND(i, S.n_sites);
     const float cmax = S.sh_absmax;
     constexpr int NB = SHDEG == 0 ? 1 : 16;
     double acc[3] = {0.5, 0.5, 0.5};
@@ -514,6 +531,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
         RFB_PRAGMA_UNROLL(RFB_PAIR_UNROLL)
         for (int32_t kp = c.k0 & ~1; kp < c.k1; kp += 2) {
             float4 e0, e1;
+            RFB_BOUND(kp + 1, S.n_edges + 1);  // the pad record after the array
+#if RFB_CHECK
+            assert((reinterpret_cast<uintptr_t>(S.edge + kp) & 31) == 0);
+#endif
             ldg256(S.edge + kp, e0, e1);
             visit(e0, kp - k0, kp >= k0);
             visit(e1, kp + 1 - k0, kp + 1 < c.k1);
@@ -523,6 +544,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
 #endif
     RFB_PRAGMA_UNROLL(RFB_F32_UNROLL)
     for (int32_t k = k0; k < c.k1; k += G, ++nk) {
+        RFB_BOUND(k, S.n_edges);
         const float4 e = __ldg(S.edge + k);
         const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
         const float den = __fmaf_rn(df[2], nz, __fmaf_rn(df[1], ny, df[0] * nx));
@@ -584,6 +606,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     }
     // neighbour j's exact coordinates: the widened fp32 record, or site4
     auto site_of = [&](const float4 &e, double &x, double &y, double &z) {
+        RFB_BOUND(__float_as_int(e.w), S.n_sites);
         if (pos64) {
             const double4 sj = ld_site(S.site4 + __float_as_int(e.w));
             x = sj.x;
@@ -609,6 +632,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
             break;
         }
         const int32_t k = k0 + idx * G;
+        RFB_BOUND(k, S.n_edges);
         const float4 e = __ldg(S.edge + k);
         double xj, yj, zj;
         site_of(e, xj, yj, zj);
@@ -625,6 +649,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     }
     for (int32_t idx = kMaskBits; idx < nexact; ++idx) {  // rows longer than the mask
         const int32_t k = k0 + idx * G;
+        RFB_BOUND(k, S.n_edges);
         const float4 e = __ldg(S.edge + k);
         double xj, yj, zj;
         site_of(e, xj, yj, zj);
