@@ -652,7 +652,7 @@ def main():
         "data": "synthetic (SURVEY.md §8d foam generator; random-init scene, no dataset)",
         "config": {"workload": workload,
                    "n_sites": args.n_sites, "n_edges": ds.n_edges, "views_per_step": len(views),
-                   "tiles": "32x32 interleaved over ranks", "lanes_per_ray": lanes,
+                   "tiles": "32x32 interleaved over ranks", "lanes_per_ray": lanes or "auto",
                    "l2": l2_note,
                    "cells_per_ray": C_tot / m0, "neighbor_visits_per_ray": V_tot / m0,
                    "segments_per_ray": N_tot / m0, "failed_rays": failed,

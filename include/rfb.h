@@ -109,8 +109,9 @@ typedef struct rfb_params {
     double epsilon;       /* early-termination transmittance, 0 disables */
     double width_floor;   /* WIDTH_FLOOR_SCALE * diagonal */
     int32_t step_limit;   /* hard per-ray cell cap */
-    int32_t lanes_per_ray;/* 0 = library default; 1, 2, 4, 8, 16 or 32 lanes cooperate
-                             on one ray (forward only) */
+    int32_t lanes_per_ray;/* 1, 2, 4, 8, 16 or 32 lanes cooperate on one ray (forward
+                             only); 0 = auto: the largest power of two <= 8 whose lanes x rays
+                             fit the resident threads (small batches use more lanes) */
 } rfb_params;
 
 /* A batch of rays (render.py:57-125 arguments). */

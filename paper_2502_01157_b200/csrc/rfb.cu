@@ -33,7 +33,7 @@ struct ArrayRays {
     const int32_t *start;
     int64_t m;
     const int32_t *order;  // optional processing order (a permutation of 0..m-1)
-    __device__ __forceinline__ int64_t count() const { return m; }
+    __host__ __device__ __forceinline__ int64_t count() const { return m; }
     __device__ __forceinline__ int64_t index(int64_t slot) const {
         return order ? (int64_t)order[slot] : slot;
     }
@@ -96,7 +96,7 @@ struct TileRays {
     int32_t tile_w, tile_h, tiles_x;
     double t_min, t_max;
     const int32_t *start_ptr;  // device scalar (located start cell)
-    __device__ __forceinline__ int64_t count() const { return n_tiles * tile_w * tile_h; }
+    __host__ __device__ __forceinline__ int64_t count() const { return n_tiles * tile_w * tile_h; }
     __device__ __forceinline__ void uniform(double *u) const {
         u[0] = cam.o[0];
         u[1] = cam.o[1];
@@ -1420,7 +1420,17 @@ static int launch_render(const rfb_scene *scene, const Src &src, const rfb_param
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
     FwdOut O = dev_out(out);
     double log_eps = p->epsilon > 0.0 ? std::log(p->epsilon) : 0.0;
-    int g = p->lanes_per_ray <= 0 ? 1 : p->lanes_per_ray;
+    int g = p->lanes_per_ray;
+    if (g <= 0) {
+        // auto: batches too small to fill the resident threads (148 SMs x RFB_FWD_MINB x 256)
+        // spread each ray over more lanes -- the largest power of two <= 8 with g * m within
+        // them (measured: 128x128 frames 0.30 -> 0.15 ms with 8 lanes, 256x256 0.35 -> 0.25 ms
+        // with 2, >= 480x270 best with 1; tools/sweep_fwd.py --sizes)
+        const int64_t resident = (int64_t)num_sms() * RFB_FWD_MINB * 256;
+        const int64_t m = src.count();
+        g = 1;
+        while (g < 8 && 2 * g * m <= resident) g *= 2;
+    }
     const double e = p->epsilon, wf = p->width_floor;
     const int32_t sl = p->step_limit;
     switch (g) {
@@ -1452,6 +1462,7 @@ static int64_t bwd_slots_max(bool quant) {
 
 // lanes per ray for a batch: 2 when the batch fills at most half the resident
 // threads (65,536 random training pixels: 4.7 -> 4.1 ms), else 1
+// (4 lanes per ray measured slower for training: 128x128 fwd+bwd 0.35 -> 0.47 ms)
 static int train_lanes(int64_t m, bool quant) { return 2 * m <= bwd_slots_max(quant) ? 2 : 1; }
 
 template <int PACKED>

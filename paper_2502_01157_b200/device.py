@@ -28,7 +28,7 @@ from .scene import softplus
 DEFAULT_EPSILON = 1e-3     # tracer/rays.py:12
 DEFAULT_STEP_LIMIT = 4096  # tracer/rays.py:13
 WIDTH_FLOOR_SCALE = 1e-12  # tracer/rays.py:14
-DEFAULT_LANES = 1
+DEFAULT_LANES = 0  # auto (rfb.h: rfb_params.lanes_per_ray)
 
 
 def _ptr(t):

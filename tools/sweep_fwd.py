@@ -19,7 +19,10 @@ from paper_2502_01157_b200.synthetic import make_foam  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--lanes", default="1,2,4,8,16")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--sizes", default="", help="WxH list (e.g. 128x128,480x270): frame sizes to sweep")
 ap.add_argument("--n-sites", type=int, default=1_000_000)
+ap.add_argument("--seed", type=int, default=1)
+ap.add_argument("--sh-degree", type=int, default=3)
 ap.add_argument("--width", type=int, default=1920)
 ap.add_argument("--height", type=int, default=1080)
 ap.add_argument("--train", action="store_true")
@@ -32,7 +35,7 @@ ap.add_argument("--fp64", action="store_true",
 args = ap.parse_args()
 print("lib", os.environ.get("RFB_LIB", "default"), flush=True)
 
-scene = make_foam(args.n_sites, 1, 3)
+scene = make_foam(args.n_sites, args.seed, args.sh_degree)
 if args.fp64:
     import numpy as np
     scene.adjacency.positions += np.random.default_rng(0).normal(0, 1e-12, scene.adjacency.positions.shape)
@@ -42,6 +45,23 @@ print("packed", ds.packed, "positions_f64", getattr(ds, "positions_f64", None), 
 cam = make_views(args.view + 1, args.width, args.height)[args.view]
 ws = dv.Workspace(ds.device)
 out = dv.alloc_forward(args.width * args.height, ds.device, per_ray=False)
+sizes = [tuple(int(v) for v in x.split("x")) for x in args.sizes.split(",")] if args.sizes else []
+for (sw, sh_) in sizes:
+    c2 = make_views(args.view + 1, sw, sh_)[args.view]
+    o2 = dv.alloc_forward(sw * sh_, ds.device, per_ray=False)
+    for lanes in [int(x) for x in args.lanes.split(",")]:
+        dv.render_image_device(ds, c2, lanes_per_ray=lanes, workspace=ws, out=o2)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.reps):
+            dv.render_image_device(ds, c2, lanes_per_ray=lanes, workspace=ws, out=o2)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.reps
+        print(f"{sw}x{sh_} lanes={lanes:2d}: {ms:8.3f} ms  {sw * sh_ / ms / 1e3:8.2f} Mrays/s", flush=True)
+if sizes:
+    sys.exit(0)
 for lanes in [int(x) for x in args.lanes.split(",")]:
     reps = 1 if args.once else args.reps
     if not args.once:
