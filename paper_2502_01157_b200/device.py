@@ -262,12 +262,14 @@ def effect_rays_device(origins, directions, t_at, normal, effect="mirror", eta=1
 def forward_schedule(origins: torch.Tensor, directions: torch.Tensor):
     """(order, lanes_per_ray) for a forward batch of arbitrary rays -- scheduling
     only, results stay per ray: batches too small to fill the resident threads
-    walk each ray with 2 lanes, large ones are sorted coherently.  Measured on
-    random training pixels (tools/train_batch_probe.py --forward): 65k rays
-    3.6 -> 2.6 ms with 2 lanes; 262k rays 8.8 -> 7.0 ms sorted."""
+    walk each ray with several lanes (lanes_per_ray 0 = the library's auto rule),
+    large ones are sorted coherently.  Measured on random training pixels
+    (tools/train_batch_probe.py --forward --lanes L): 16k rays 2.85 / 1.93 / 1.54 /
+    1.35 ms with 1 / 2 / 4 / 8 lanes, 65k rays 3.52 / 2.53 / 3.07 / 4.46 ms (the
+    auto rule picks 8 and 2); 262k rays 8.8 -> 7.0 ms sorted."""
     m = origins.shape[0]
     order = coherent_order(origins, directions) if m >= 200_000 else None
-    return order, (2 if m < 100_000 else 1)
+    return order, 0
 
 
 def make_params(epsilon=DEFAULT_EPSILON, width_floor=0.0, step_limit=DEFAULT_STEP_LIMIT,
