@@ -33,6 +33,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <vector>
 
 #include "../../include/rfb.h"
@@ -644,7 +645,40 @@ __device__ __forceinline__ RingBox ring_box(int r, int ix, int iy, int iz, const
 #endif
 constexpr int kTailThreads = RFB_ADJ_TAIL_THREADS;
 constexpr int kTailQueue = 512;
+#ifndef RFB_ADJ_COARSE
+#define RFB_ADJ_COARSE 1  // pass 2 scans rings of CB^3-cell blocks pruned by the vertex balls
+#endif
+#ifndef RFB_ADJ_CB
+#define RFB_ADJ_CB 4
+#endif
+constexpr int kCB = RFB_ADJ_CB;
 
+// Does the box [l, h] (site-relative) meet a vertex ball B(v, |v|) of the cell?
+// min over the box of |x - v|^2 - |v|^2 = sum_a (x_a^2 - 2 x_a v_a) at x_a = clamp(v_a);
+// near-zero counts as meeting (conservative).
+template <class Cell>
+__device__ __forceinline__ bool box_meets_balls(const Cell &C, int nv, const double *l,
+                                                const double *h) {
+    for (int v = 0; v < nv; ++v) {
+        const double w[3] = {C.vx[v], C.vy[v], C.vz[v]};
+        double sum = 0.0, mag = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double xa = fmin(fmax(w[a], l[a]), h[a]);
+            const double term = xa * xa - 2.0 * xa * w[a];
+            sum += term;
+            mag += fabs(term);
+        }
+        if (sum < 1e-12 * mag) return true;
+    }
+    return false;
+}
+
+#if RFB_ADJ_PROFILE
+#define RFB_PC(i, v) do { if (A.hull[self]) atomicAdd(reinterpret_cast<unsigned long long *>(A.flags + 18 + 2 * (i)), (unsigned long long)(v)); } while (0)
+#else
+#define RFB_PC(i, v) ((void)0)
+#endif
 __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t count) {
     __shared__ BigCell C;
     __shared__ CellState SS;
@@ -652,6 +686,9 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
     __shared__ int32_t queue[kTailQueue];
     __shared__ int qn, box[6];
     __shared__ FarSet far;
+#if RFB_ADJ_COARSE
+    __shared__ int live[kTailThreads], nlive;
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const Grid &g = A.g;
     const int rmax = max(max(g.dim[0], g.dim[1]), g.dim[2]);
@@ -684,6 +721,140 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
             }
         }
         __syncthreads();
+        // one grid cell's sites against the current cell (the exact clip test, or the far
+        // vertices only beyond 2 Rn); survivors go to the shared queue
+        auto scan_cell = [&](int cx, int cy, int cz, bool use_far) {
+            const int cell = cell_index(g, cx, cy, cz);
+            const int c0 = __ldg(A.cstart + cell), c1 = __ldg(A.cstart + cell + 1);
+            RFB_PC(2, 1);
+            RFB_PC(3, c1 - c0);
+            for (int q = c0; q < c1; ++q) {
+                const double4 p = A.pos[q];
+                const double dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
+                const double d2 = dx * dx + dy * dy + dz * dz;
+                if (d2 <= A.dup2) {
+                    atomicOr(A.flags, kErrDuplicate);
+                    continue;
+                }
+                if (!may_cut(SS, dx, dy, dz, d2)) continue;
+                RFB_PC(4, 1);
+                const double o = 0.5 * d2;
+                bool cut = false;
+                if (use_far && d2 >= 4.0 * far.Rn2 * (1.0 + 1e-9)) {
+                    // beyond 2 Rn only the far vertices can be cut (conservative
+                    // test; clip() decides exactly)
+                    for (int k = 0; k < far.n && !cut; ++k) {
+                        const double pv = dx * far.x[k] + dy * far.y[k] + dz * far.z[k];
+                        cut = d2 - 2.0 * pv < 1e-12 * (d2 + 2.0 * fabs(pv));
+                    }
+                } else {
+                    for (int v = 0; v < SS.nv && !cut; ++v)
+                        cut = dx * C.vx[v] + dy * C.vy[v] + dz * C.vz[v] > o;
+                }
+                if (cut) {
+                    const int slot = atomicAdd(&qn, 1);
+                    if (slot < kTailQueue) queue[slot] = q;
+                }
+            }
+        };
+        // warp 0 clips by the queued sites (between two barriers); returns the queue length
+        auto flush_queue = [&]() -> int {
+            __syncthreads();
+            const int nq = qn;
+            if (nq > 0 && warp == 0) {
+#if RFB_ADJ_PROFILE
+                const long long cq0 = clock64();
+#endif
+                CellState S = SS;
+                for (int i = 0; i < min(nq, kTailQueue) && S.err == 0; ++i) {
+                    const int q = queue[i];
+                    const double4 p = A.pos[q];
+                    const double dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
+                    const double d2 = dx * dx + dy * dy + dz * dz;
+                    if (may_cut(S, dx, dy, dz, d2))
+                        clip(C, lane, dx, dy, dz, 0.5 * d2, __ldg(A.ids + q), S);
+                }
+                if (lane == 0) {
+                    SS = S;
+                    qn = 0;
+                    RFB_PC(5, nq);
+#if RFB_ADJ_PROFILE
+                    RFB_PC(6, clock64() - cq0);
+#endif
+                }
+            }
+            __syncthreads();
+            return nq;
+        };
+#if RFB_ADJ_COARSE
+        // Rings of CB^3-cell blocks outward from the site's block, restricted to the ball
+        // box.  A block (then each of its cells) is scanned only if its box meets a vertex
+        // ball B(v, |v|) of the current cell -- the exact region from which a site can cut it
+        // (x cuts iff |x - v| < |v| for some vertex v); the test against an earlier, larger
+        // cell is conservative for every later one.  Unbounded hull cells thus skip the bulk
+        // of the grid instead of testing every site against their vertices.
+        {
+            const int bx = ix / kCB, by = iy / kCB, bz = iz / kCB;
+            const int rbmax = (rmax + kCB - 1) / kCB;
+            // ring 0 (the site's own block) only holds cells beyond the spiral when
+            // CB > kSpiralG + 1
+            for (int R = kCB - 1 > kSpiralG ? 0 : 1; R <= rbmax && !fin; ++R) {
+                // cells of block ring R >= 1 are >= (R-1) CB + 1 cells from the site's cell,
+                // so their sites are >= (R-1) CB h away (ring 0: the site's own block, whose
+                // cells beyond the spiral's reach are scanned too when CB > kSpiralG + 1)
+                const double lb = (double)(max(R - 1, 0) * kCB) * g.h;
+                if (lb * lb >= 4.0 * SS.R2 * (1.0 + 1e-12)) break;
+                const int bbox[6] = {box[0] / kCB, box[1] / kCB, box[2] / kCB,
+                                     box[3] / kCB, box[4] / kCB, box[5] / kCB};
+                if (max(max(bx - bbox[0], bbox[3] - bx), max(max(by - bbox[1], bbox[4] - by),
+                                                           max(bz - bbox[2], bbox[5] - bz))) < R)
+                    break;
+                const RingBox RB = ring_box(R, bx, by, bz, bbox);  // (ring_box lists r = 0 twice)
+                const int total = R == 0 ? 1 : RB.total();
+                if (tid == 0) { RFB_PC(0, 1); RFB_PC(1, (total + kTailThreads - 1) / kTailThreads); }
+                for (int b0 = 0; b0 < total && SS.err == 0; b0 += kTailThreads) {
+                    if (tid == 0) nlive = 0;
+                    __syncthreads();
+                    if (b0 + tid < total) {
+                        int cbx = bx, cby = by, cbz = bz;
+                        if (R > 0) RB.cell(b0 + tid, cbx, cby, cbz);
+                        const double l[3] = {g.lo[0] + cbx * kCB * g.h - s.x,
+                                             g.lo[1] + cby * kCB * g.h - s.y,
+                                             g.lo[2] + cbz * kCB * g.h - s.z};
+                        const double h[3] = {l[0] + kCB * g.h, l[1] + kCB * g.h, l[2] + kCB * g.h};
+                        if (box_meets_balls(C, SS.nv, l, h))
+                            live[atomicAdd(&nlive, 1)] = (cbz * 1024 + cby) * 1024 + cbx;
+                    }
+                    __syncthreads();
+                    const bool use_far = far.n > 0;
+                    const int items = nlive * kCB * kCB * kCB;
+                    for (int t0 = 0; t0 < items && SS.err == 0; t0 += kTailThreads) {
+                        const int t = t0 + tid;
+                        if (t < items) {
+                            const int bid = live[t / (kCB * kCB * kCB)], c = t % (kCB * kCB * kCB);
+                            const int cx = (bid % 1024) * kCB + c % kCB;
+                            const int cy = ((bid / 1024) % 1024) * kCB + (c / kCB) % kCB;
+                            const int cz = (bid / (1024 * 1024)) * kCB + c / (kCB * kCB);
+                            const int dch = max(max(abs(cx - ix), abs(cy - iy)), abs(cz - iz));
+                            if (cx < g.dim[0] && cy < g.dim[1] && cz < g.dim[2] && dch > kSpiralG) {
+                                const double l[3] = {g.lo[0] + cx * g.h - s.x,
+                                                     g.lo[1] + cy * g.h - s.y,
+                                                     g.lo[2] + cz * g.h - s.z};
+                                const double h[3] = {l[0] + g.h, l[1] + g.h, l[2] + g.h};
+                                if (box_meets_balls(C, SS.nv, l, h)) scan_cell(cx, cy, cz, use_far);
+                            }
+                        }
+                        if (flush_queue() > kTailQueue) t0 -= kTailThreads;  // overflowed: again
+                    }
+                }
+                if (warp == 0) {
+                    ball_box(C, lane, SS, s, g, box);
+                    far_refresh(C, lane, SS, far, A.flags + 7);
+                }
+                __syncthreads();
+            }
+        }
+#else
         for (int r = kSpiralG + 1; r <= rmax && !fin; ++r) {
             // stop: remaining sites are >= (r-1) h away, beyond the security radius,
             // or the ring lies outside the ball box
@@ -696,6 +867,7 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                 break;
             const RingBox RB = ring_box(r, ix, iy, iz, box);
             const int total = RB.total();
+            if (tid == 0) { RFB_PC(0, 1); RFB_PC(1, (total + kTailThreads - 1) / kTailThreads); }
             for (int t0 = 0; t0 < total && SS.err == 0; t0 += kTailThreads) {
                 const int t = t0 + tid;
                 if (t < total) {
@@ -717,6 +889,8 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                     if (live) {
                         const int cell = cell_index(g, cx, cy, cz);
                         const int c0 = __ldg(A.cstart + cell), c1 = __ldg(A.cstart + cell + 1);
+                        RFB_PC(2, 1);
+                        RFB_PC(3, c1 - c0);
                         for (int q = c0; q < c1; ++q) {
                             const double4 p = A.pos[q];
                             const double dx = p.x - s.x, dy = p.y - s.y, dz = p.z - s.z;
@@ -726,6 +900,7 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                                 continue;
                             }
                             if (!may_cut(SS, dx, dy, dz, d2)) continue;
+                            RFB_PC(4, 1);
                             const double o = 0.5 * d2;
                             bool cut = false;
                             if (use_far && d2 >= 4.0 * far.Rn2 * (1.0 + 1e-9)) {
@@ -749,6 +924,9 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                 __syncthreads();
                 const int nq = qn;
                 if (nq > 0 && warp == 0) {
+#if RFB_ADJ_PROFILE
+                    const long long cq0 = clock64();
+#endif
                     CellState S = SS;
                     for (int i = 0; i < min(nq, kTailQueue) && S.err == 0; ++i) {
                         const int q = queue[i];
@@ -761,6 +939,10 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
                     if (lane == 0) {
                         SS = S;
                         qn = 0;
+                        RFB_PC(5, nq);
+#if RFB_ADJ_PROFILE
+                        RFB_PC(6, clock64() - cq0);
+#endif
                     }
                 }
                 __syncthreads();
@@ -772,6 +954,7 @@ __global__ void __launch_bounds__(kTailThreads) k_voronoi_tail(Args A, int32_t c
             }
             __syncthreads();
         }
+#endif
         if (warp == 0) {
             CellState S = SS;
             emit_site(A, C, lane, self, S);
@@ -1126,6 +1309,14 @@ int rfb_build_adjacency(const double *positions, int64_t n_sites, int32_t max_de
     cudaMemcpy(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost);
     stats[5] = *reinterpret_cast<int64_t *>(hflags + 12);  // pass-2 cycles (all sites)
     stats[6] = *reinterpret_cast<int64_t *>(hflags + 14);  // pass-2 cycles (hull sites)
+    {
+        int32_t all[32];
+        cudaMemcpy(all, flags, sizeof(all), cudaMemcpyDeviceToHost);
+        const long long *c = reinterpret_cast<const long long *>(all + 18);
+        fprintf(stderr, "[adj profile, hull sites] rings %lld batches %lld live_cells %lld "
+                "sites_in_live %lld may_cut_pass %lld queued %lld clip_cycles %lld\n",
+                c[0], c[1], c[2], c[3], c[4], c[5], c[6]);
+    }
 #endif
     if (hflags[0] & kErrDuplicate) return RFB_EDEGENERATE;
     if (hflags[0] & kErrOverflow) return RFB_ECAPACITY;
