@@ -312,6 +312,9 @@ __device__ bool clip(Cell &C, int lane, double pnx, double pny, double pnz, doub
 }
 
 // Offer the points of `cell` (lane-private, may be -1) to the clipper.
+#ifndef RFB_ADJ_SORTED
+#define RFB_ADJ_SORTED 1  // pass 1: offer a batch's candidates nearest first (1M: 100.6 -> 96.3 ms)
+#endif
 #ifndef RFB_ADJ_PROFILE
 #define RFB_ADJ_PROFILE 0  // count candidate clip tests per phase into stats[5..6]
 #endif
@@ -352,10 +355,29 @@ __device__ __forceinline__ void offer_cells(const Args &A, Cell &C, int lane, in
             d2 = dx * dx + dy * dy + dz * dz;
             has = jid != self && (d2 <= A.dup2 || may_cut(S, dx, dy, dz, d2));
         }
+#if RFB_ADJ_SORTED
+        // nearest candidate first: the cell shrinks fastest, so fewer later candidates
+        // survive may_cut / cut anything
+        bool pend = has;
+        while (__any_sync(kFull, pend)) {
+            double key = pend ? d2 : INFINITY;
+            int L = lane;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ok = __shfl_xor_sync(kFull, key, off);
+                const int oL = __shfl_xor_sync(kFull, L, off);
+                if (ok < key || (ok == key && oL < L)) {
+                    key = ok;
+                    L = oL;
+                }
+            }
+            if (lane == L) pend = false;
+#else
         unsigned m = __ballot_sync(kFull, has);
         while (m) {
             const int L = __ffs(m) - 1;
             m &= m - 1;
+#endif
             const double bx = __shfl_sync(kFull, dx, L), by = __shfl_sync(kFull, dy, L),
                          bz = __shfl_sync(kFull, dz, L), b2 = __shfl_sync(kFull, d2, L);
             const int32_t bj = __shfl_sync(kFull, jid, L);
