@@ -205,13 +205,24 @@ __device__ bool clip(Cell &C, int lane, double pnx, double pny, double pnz, doub
                      int32_t j, CellState &S) {
     int &nv = S.nv, &np = S.np, &err = S.err;
     int nrem = 0;
+    bool on = false;
     for (int base = 0; base < nv; base += 32) {
         const int v = base + lane;
         bool rem = false;
-        if (v < nv) rem = pnx * C.vx[v] + pny * C.vy[v] + pnz * C.vz[v] > po;
+        if (v < nv) {
+            const double d = pnx * C.vx[v] + pny * C.vy[v] + pnz * C.vz[v];
+            rem = d > po;
+            on |= d == po;
+        }
         const unsigned b = __ballot_sync(kFull, rem);
         if (lane == 0) C.rmask[base >> 5] = b;
         nrem += __popc(b);
+    }
+    // a vertex exactly on the new plane: five or more cospherical sites (e.g. a lattice),
+    // which the reference resolves by symbolic perturbation -- outside this builder's scope
+    if (__any_sync(kFull, on)) {
+        err |= kErrDegenerate;
+        return false;
     }
     if (nrem == 0) return true;
     __syncwarp();
@@ -313,7 +324,7 @@ __device__ bool clip(Cell &C, int lane, double pnx, double pny, double pnz, doub
 
 // Offer the points of `cell` (lane-private, may be -1) to the clipper.
 #ifndef RFB_ADJ_SORTED
-#define RFB_ADJ_SORTED 1  // pass 1: offer a batch's candidates nearest first (1M: 100.6 -> 96.3 ms)
+#define RFB_ADJ_SORTED 1  // pass 1: offer a batch's candidates nearest first
 #endif
 #ifndef RFB_ADJ_PROFILE
 #define RFB_ADJ_PROFILE 0  // count candidate clip tests per phase into stats[5..6]
@@ -426,6 +437,27 @@ __device__ void init_cell(Cell &C, int lane, double B, CellState &S) {
 
 // Clip by the sites of the spiral table's cells, nearest first, until the
 // security radius is reached.  Returns true when the cell is final.
+// Does the box [l, h] (site-relative) meet a vertex ball B(v, |v|) of the cell?
+// min over the box of |x - v|^2 - |v|^2 = sum_a (x_a^2 - 2 x_a v_a) at x_a = clamp(v_a);
+// near-zero counts as meeting (conservative).
+template <class Cell>
+__device__ __forceinline__ bool box_meets_balls(const Cell &C, int nv, const double *l,
+                                                const double *h) {
+    for (int v = 0; v < nv; ++v) {
+        const double w[3] = {C.vx[v], C.vy[v], C.vz[v]};
+        double sum = 0.0, mag = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double xa = fmin(fmax(w[a], l[a]), h[a]);
+            const double term = xa * xa - 2.0 * xa * w[a];
+            sum += term;
+            mag += fabs(term);
+        }
+        if (sum < 1e-12 * mag) return true;
+    }
+    return false;
+}
+
 template <class Cell>
 __device__ bool spiral_phase(const Args &A, Cell &C, int lane, const double4 &s, int32_t self,
                              int ix, int iy, int iz, CellState &S) {
@@ -675,26 +707,6 @@ constexpr int kTailQueue = 512;
 #endif
 constexpr int kCB = RFB_ADJ_CB;
 
-// Does the box [l, h] (site-relative) meet a vertex ball B(v, |v|) of the cell?
-// min over the box of |x - v|^2 - |v|^2 = sum_a (x_a^2 - 2 x_a v_a) at x_a = clamp(v_a);
-// near-zero counts as meeting (conservative).
-template <class Cell>
-__device__ __forceinline__ bool box_meets_balls(const Cell &C, int nv, const double *l,
-                                                const double *h) {
-    for (int v = 0; v < nv; ++v) {
-        const double w[3] = {C.vx[v], C.vy[v], C.vz[v]};
-        double sum = 0.0, mag = 0.0;
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const double xa = fmin(fmax(w[a], l[a]), h[a]);
-            const double term = xa * xa - 2.0 * xa * w[a];
-            sum += term;
-            mag += fabs(term);
-        }
-        if (sum < 1e-12 * mag) return true;
-    }
-    return false;
-}
 
 #if RFB_ADJ_PROFILE
 #define RFB_PC(i, v) do { if (A.hull[self]) atomicAdd(reinterpret_cast<unsigned long long *>(A.flags + 18 + 2 * (i)), (unsigned long long)(v)); } while (0)
