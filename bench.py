@@ -224,7 +224,8 @@ def _train_roofline():
         return {"kernel": "k_train (walk + record + reverse pass)",
                 "binding_unit": "l1tex data-pipe wavefronts",
                 "binding_frac": tj.get("k_train_l1_data_pipe_frac"),
-                "traffic": tj.get("k_train_dram_bytes_per_launch"), "source": tj.get("source")}
+                "traffic": tj.get("k_train_dram_bytes_per_launch"),
+                "source": tj.get("k_train_source", tj.get("source"))}
     except Exception:  # noqa: BLE001
         return None
 
@@ -612,6 +613,7 @@ def main():
     achieved = bytes_per_frame * len(views) / world / max(kernel_ms / 1e3, 1e-12) / 1e9
     traffic = None
     l1_frac = None
+    render_src = None
     tpath = os.path.join(REPO, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
@@ -619,6 +621,7 @@ def main():
                 tj = json.load(f)
             traffic = tj.get("k_render_dram_bytes_per_launch")
             l1_frac = tj.get("k_render_l1_data_pipe_frac")
+            render_src = tj.get("k_render_source")
         except Exception:
             traffic = None
     workload = {
@@ -673,6 +676,7 @@ def main():
                              "(no reuse); coherent rays share cells, so DRAM traffic per launch "
                              "is `traffic` and frac can exceed 1. The binding unit is the L1 "
                              "data pipe (binding_frac, from the ncu capture in profiles/).",
+                     "traffic_source": render_src,
                      "binding_unit": "l1tex data-pipe wavefronts",
                      "binding_frac": l1_frac,
                      "gather_ceilings": gather_ceilings()},

@@ -39,7 +39,12 @@ subprocess.run(["cp", launches, f"profiles/{tag}_launches.csv"])
 summ = "\n".join(f"# {rep} (ncu --set full)\n" + ncu_summary.summarise(rep) for rep in reps)
 open(f"profiles/{tag}_ncu_k_render_k_train.txt", "w").write(summ + "\n")
 # traffic per launch for bench.py's roofline.traffic
-tr = {}
+import math  # noqa: E402
+
+try:  # merge: a round may capture only some kernels
+    tr = json.load(open("profiles/traffic.json"))
+except (OSError, ValueError):
+    tr = {}
 for rep in reps:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
@@ -47,16 +52,20 @@ for rep in reps:
     rh, ru = rr[0], rr[1]
     for r in rr[2:]:
         d = dict(zip(rh, r))
-        name = "k_render" if "k_render" in d["Kernel Name"] else "k_train"
-        scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
-        b = 0
+        kname = d["Kernel Name"]
+        name = next((k for k in ("k_render", "k_train", "k_voronoi_tail", "k_voronoi")
+                     if k in kname), kname.split("(")[0])
+        scale = {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}
+        b = 0.0
         for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
-            b += float(d[key]) * scale[ru[rh.index(key)]]
-        tr[f"{name}_dram_bytes_per_launch"] = int(b)
+            b += float(d[key].replace(",", "")) * scale.get(ru[rh.index(key)], float("nan"))
+        if not math.isnan(b):
+            tr[f"{name}_dram_bytes_per_launch"] = int(b)
+            tr[f"{name}_source"] = f"profiles/{tag}_ncu_k_render_k_train.txt"
         key = "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"
-        if key in d:
-            tr[f"{name}_l1_data_pipe_frac"] = round(float(d[key]) / 100.0, 4)
-tr["source"] = f"profiles/{tag}_ncu_k_render_k_train.txt (dram__bytes_read.sum + dram__bytes_write.sum)"
+        if key in d and not math.isnan(float(d[key].replace(",", "") or "nan")):
+            tr[f"{name}_l1_data_pipe_frac"] = round(float(d[key].replace(",", "")) / 100.0, 4)
+tr["source"] = "per kernel: <kernel>_source (dram__bytes_read.sum + dram__bytes_write.sum)"
 json.dump(tr, open("profiles/traffic.json", "w"), indent=1)
 print("\n".join(lines))
 print(json.dumps(tr))
