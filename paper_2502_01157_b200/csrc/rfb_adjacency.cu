@@ -45,12 +45,12 @@ constexpr unsigned kFull = 0xffffffffu;
 #define RFB_ADJ_WARPS 2
 #endif
 #ifndef RFB_ADJ_MAX_PLANES
-#define RFB_ADJ_MAX_PLANES 128
+#define RFB_ADJ_MAX_PLANES 80
 #endif
 constexpr int kWarps = RFB_ADJ_WARPS;            // sites (warps) per block
 constexpr int kMaxPlanes = RFB_ADJ_MAX_PLANES;   // pass-1 planes per cell, box included
 #ifndef RFB_ADJ_MAX_VERTS
-#define RFB_ADJ_MAX_VERTS 256
+#define RFB_ADJ_MAX_VERTS 128
 #endif
 constexpr int kMaxVerts = RFB_ADJ_MAX_VERTS;  // polytope vertices (dual triangles)
 #ifndef RFB_ADJ_CELL_SITES
@@ -530,7 +530,7 @@ __device__ __forceinline__ void site_cell(const Grid &g, const double4 &s, int &
 // Pass 1: one warp per site, spiral only.  Cells not final after the
 // spiral (near the hull: long or unbounded cells) are queued for pass 2.
 #ifndef RFB_ADJ_MINB
-#define RFB_ADJ_MINB 1
+#define RFB_ADJ_MINB 10  // 96 registers, 10 blocks (20 warps) per SM with the 128/80 buffers
 #endif
 __global__ void __launch_bounds__(32 * kWarps, RFB_ADJ_MINB) k_voronoi(Args A) {
     __shared__ WarpCell cells[kWarps];
