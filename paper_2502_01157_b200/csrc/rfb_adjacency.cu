@@ -695,7 +695,7 @@ __device__ __forceinline__ RingBox ring_box(int r, int ix, int iy, int iz, const
 // security radius are refreshed, so a long cell that gets capped stops
 // scanning early; unbounded (hull) cells scan to the grid's edge.
 #ifndef RFB_ADJ_TAIL_THREADS
-#define RFB_ADJ_TAIL_THREADS 256
+#define RFB_ADJ_TAIL_THREADS 128
 #endif
 constexpr int kTailThreads = RFB_ADJ_TAIL_THREADS;
 constexpr int kTailQueue = 512;
