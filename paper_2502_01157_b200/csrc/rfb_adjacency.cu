@@ -323,6 +323,13 @@ __device__ bool clip(Cell &C, int lane, double pnx, double pny, double pnz, doub
 }
 
 // Offer the points of `cell` (lane-private, may be -1) to the clipper.
+#ifndef RFB_ADJ_FLAT
+#define RFB_ADJ_FLAT 1  // sparse spiral batches scanned as one flat candidate list (1M: 71 -> 66 ms)
+#endif
+#ifndef RFB_ADJ_FLAT_MAX
+#define RFB_ADJ_FLAT_MAX 128  // candidates per batch up to which the flat order is used
+#endif
+constexpr int kFlatMax = RFB_ADJ_FLAT_MAX;
 #ifndef RFB_ADJ_SORTED
 #define RFB_ADJ_SORTED 1  // pass 1: offer a batch's candidates nearest first
 #endif
@@ -352,16 +359,47 @@ __device__ __forceinline__ void offer_cells(const Args &A, Cell &C, int lane, in
         c1 = __ldg(A.cstart + cell + 1);
     }
     int cnt = c1 - c0;
-    int maxcnt = cnt;
+    // Sparse batches (uniform scenes: ~2 sites per grid cell) are scanned as one flat list,
+    // 32 candidates per round (inclusive warp scan of the counts; each lane finds the cell
+    // owning its flat index by binary search over the prefix sums), instead of max-per-cell
+    // rounds with most lanes idle.  Dense batches (the 3M surface shell: ~60 per cell) keep
+    // the round-robin order -- one site of every cell per round, a spatially spread sample
+    // that shrinks the cell fastest (flat order there is 2.3x slower).
+    int incl = cnt, maxcnt = cnt;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(kFull, incl, off);
+        if (lane >= off) incl += o;
+    }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) maxcnt = max(maxcnt, __shfl_xor_sync(kFull, maxcnt, off));
-    for (int q = 0; q < maxcnt; ++q) {
-        bool has = q < cnt;
+    const int total = __shfl_sync(kFull, incl, 31);
+    const int excl = incl - cnt;
+    const bool flat = RFB_ADJ_FLAT && total <= kFlatMax;
+    const int rounds = flat ? (total + 31) / 32 : maxcnt;
+    for (int q = 0; q < rounds; ++q) {
+        bool has;
+        int idx;
+        if (flat) {
+            const int t = q * 32 + lane;
+            int lo = 0;  // owner = first lane whose inclusive prefix exceeds t
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const int probe = __shfl_sync(kFull, incl, lo + step - 1);
+                if (probe <= t) lo += step;
+            }
+            const int oc0 = __shfl_sync(kFull, c0, lo & 31), oex = __shfl_sync(kFull, excl, lo & 31);
+            has = t < total;
+            idx = oc0 + (t - oex);
+        } else {
+            has = q < cnt;
+            idx = c0 + q;
+        }
         double dx = 0, dy = 0, dz = 0, d2 = 0;
         int32_t jid = -1;
         if (has) {
-            const double4 p = A.pos[c0 + q];
-            jid = __ldg(A.ids + c0 + q);
+            const double4 p = A.pos[idx];
+            jid = __ldg(A.ids + idx);
             dx = p.x - sx; dy = p.y - sy; dz = p.z - sz;
             d2 = dx * dx + dy * dy + dz * dz;
             has = jid != self && (d2 <= A.dup2 || may_cut(S, dx, dy, dz, d2));
