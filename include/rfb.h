@@ -167,6 +167,12 @@ int rfb_abi_version(void);
 const char *rfb_error_string(int code); /* (host) static string */
 int rfb_device_ok(void);                /* 1 when an sm_100 device is current */
 
+/* Device address of page-locked host memory (cudaHostGetDevicePointer), so a
+ * kernel can store its per-ray outputs straight into the caller's host frame
+ * (the D2H then overlaps the walk; render.py:128-149 returns a host image).
+ * Returns 0, RFB_EINVAL, or the cudaError_t when the memory is not mapped. */
+int rfb_host_device_pointer(void *host, void **device_ptr);
+
 /* Build the device layout from fp64/int64 device arrays:
  * positions [n][3], sigma [n], sh [n][48], offsets [n+1], neighbors [E]
  * -> site4 [n][4] f64, offsets32 [n+1], neighbors32 [E] and, when

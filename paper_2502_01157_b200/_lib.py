@@ -116,6 +116,7 @@ SIGNATURES = {
     "rfb_abi_version": (ctypes.c_int, []),
     "rfb_error_string": (ctypes.c_char_p, [ctypes.c_int]),
     "rfb_device_ok": (ctypes.c_int, []),
+    "rfb_host_device_pointer": (ctypes.c_int, [VP, P(VP)]),
     "rfb_pack_scene": (ctypes.c_int, [VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP, VP, VP,
                                       I32, VP]),
     "rfb_softplus": (ctypes.c_int, [VP, I64, VP, VP, VP, VP]),

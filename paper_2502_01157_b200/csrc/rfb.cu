@@ -1588,6 +1588,17 @@ int rfb_device_ok(void) {
     return major == 10 ? 1 : 0;
 }
 
+int rfb_host_device_pointer(void *host, void **device_ptr) {
+    if (!host || !device_ptr) return RFB_EINVAL;
+    *device_ptr = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(device_ptr, host, 0);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();  // not sticky: clear it for the caller's next launch
+        *device_ptr = nullptr;
+    }
+    return (int)e;
+}
+
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,

@@ -422,12 +422,27 @@ def tile_grid(width: int, height: int, tile_w: int = 32, tile_h: int = 32):
     return tiles_x, tiles_y
 
 
+def host_device_pointer(lib, host: torch.Tensor) -> int | None:
+    """Device address of a pinned host tensor (rfb_host_device_pointer), or
+    None when the memory is not mapped into the device address space."""
+    dev = ctypes.c_void_p()
+    if lib.rfb_host_device_pointer(ctypes.c_void_p(host.data_ptr()), ctypes.byref(dev)) != 0:
+        return None
+    return dev.value
+
+
 def render_image_device(ds: DeviceScene, camera, *, epsilon=DEFAULT_EPSILON,
                         step_limit=DEFAULT_STEP_LIMIT, t_max=None, start_site=-1, tile_ids=None,
                         tile_w=32, tile_h=32, f64=False, per_ray=False,
                         lanes_per_ray=DEFAULT_LANES, workspace: Workspace | None = None,
-                        out: ForwardResult | None = None, stream=None) -> ForwardResult:
-    """Fused ray generation + render over a tile list (render.py:128-149)."""
+                        out: ForwardResult | None = None, stream=None,
+                        rgb_ptr: int | None = None) -> ForwardResult:
+    """Fused ray generation + render over a tile list (render.py:128-149).
+
+    ``rgb_ptr``: optional device address (``host_device_pointer``) of a mapped
+    page-locked (W*H, 3) host frame of ``out.rgb``'s dtype; the kernel then
+    stores each ray's colour straight into host memory and ``out.rgb`` is
+    left untouched."""
     W, H = int(camera.width), int(camera.height)
     m = W * H
     if tile_ids is None:
@@ -440,6 +455,8 @@ def render_image_device(ds: DeviceScene, camera, *, epsilon=DEFAULT_EPSILON,
     p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
     cam = camera_struct(camera)
     o = fwd_struct(res)
+    if rgb_ptr is not None:
+        o.rgb = int(rgb_ptr)
     _lib.check(ds.lib.rfb_render_image(ds.c, ctypes.byref(cam), ctypes.byref(p), 0.0, float(t_max),
                                        int(start_site), _ptr(tile_ids), int(tile_ids.numel()),
                                        int(tile_w), int(tile_h), ctypes.byref(o), _ptr(ws),

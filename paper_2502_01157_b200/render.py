@@ -19,6 +19,7 @@ kernel arrays on every call too, render.py:49-54).
 
 from __future__ import annotations
 
+import os
 import time
 import weakref
 from dataclasses import dataclass, field
@@ -42,6 +43,9 @@ STATUS_CYCLE = 3
 # copy); at most this many per resolution, further frames a caller still holds
 # go to pageable memory
 PINNED_FRAMES = 2
+# the walk kernel stores the frame straight into the mapped pinned buffer (the
+# D2H overlaps the walk instead of following it); off: render to HBM + copy
+ZERO_COPY_FRAMES = os.environ.get("RFB_ZERO_COPY", "1") != "0"
 
 
 @dataclass
@@ -277,22 +281,28 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
     ds = _device_scene(scene, device_scene)
     H, W = camera.height, camera.width
     fc = _frame_cache(ds, W, H, weight_check)
+    # The frame goes to a free pinned buffer of this resolution and the caller
+    # gets a view of it (no host-side copy); a buffer is free once the caller
+    # dropped the image it holds.  With ZERO_COPY_FRAMES the kernel writes the
+    # buffer directly through its mapped device address, otherwise it renders
+    # to HBM and one D2H follows.  With PINNED_FRAMES buffers in use the frame
+    # goes to fresh pageable memory instead (slower, but callers that keep
+    # every frame never accumulate pinned memory).
+    pool = fc["h_rgb"]  # [pinned tensor, weakref to the array handed out, mapped address]
+    free = next((e for e in pool if e[1] is None or e[1]() is None), None)
+    if free is None and len(pool) < PINNED_FRAMES:
+        h = torch.empty((W * H, 3), dtype=torch.float64, pin_memory=True)
+        free = [h, None, dv.host_device_pointer(ds.lib, h) if ZERO_COPY_FRAMES else None]
+        pool.append(free)
+    direct = free is not None and free[2] is not None
     torch.cuda.synchronize(ds.device)
     t0 = time.perf_counter()
     res = dv.render_image_device(ds, camera, epsilon=epsilon, step_limit=step_limit, f64=True,
-                                 lanes_per_ray=lanes_per_ray, workspace=fc["ws"], out=fc["out"])
-    # D2H straight into a free pinned buffer of this resolution and return a
-    # view of it (no host-side copy); a buffer is free once the caller dropped
-    # the image it holds.  With PINNED_FRAMES buffers in use the frame goes to
-    # fresh pageable memory instead (slower, but callers that keep every frame
-    # never accumulate pinned memory).
-    pool = fc["h_rgb"]  # [(pinned tensor, weakref to the array handed out)]
-    free = next((e for e in pool if e[1] is None or e[1]() is None), None)
-    if free is None and len(pool) < PINNED_FRAMES:
-        free = [torch.empty((W * H, 3), dtype=torch.float64, pin_memory=True), None]
-        pool.append(free)
+                                 lanes_per_ray=lanes_per_ray, workspace=fc["ws"], out=fc["out"],
+                                 rgb_ptr=free[2] if direct else None)
     if free is not None:
-        free[0].copy_(res.rgb, non_blocking=True)
+        if not direct:
+            free[0].copy_(res.rgb, non_blocking=True)
         root = free[0].numpy()
         free[1] = weakref.ref(root)
     else:

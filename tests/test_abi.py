@@ -98,3 +98,4 @@ def test_argument_validation_without_device(lib):
     assert lib.rfb_pack_scene(None, None, None, None, None, 0, 0, None, None, None, None, None,
                               None, None, 0, None) == -1
     assert lib.rfb_softplus(None, 1, None, None, None, None) == -1
+    assert lib.rfb_host_device_pointer(None, None) == -1

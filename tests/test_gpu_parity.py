@@ -434,3 +434,30 @@ def test_render_image_frames_are_independent(cuda_ok):
     for a, b in zip(kept, again):
         np.testing.assert_array_equal(a, b)
     assert not np.array_equal(kept[0], kept[1])
+
+
+def test_render_image_zero_copy_equals_copy_path(cuda_ok, monkeypatch):
+    """The walk kernel storing the frame straight into the mapped pinned buffer
+    (render.ZERO_COPY_FRAMES) gives the same bits as rendering to HBM + D2H,
+    and the mapped path is the one taken on the B200."""
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200 import render as rd
+    from paper_2502_01157_b200.camera import PINHOLE, CameraModel, look_at
+
+    g = load_golden("frame_2k_deg3")
+    scene = golden_scene(g)
+    cams = [CameraModel.from_angle_x(PINHOLE, 96, 64, 0.9, look_at((0.2 * k, 0.1, 3.0), (0, 0, 0)))
+            for k in range(3)]
+    frames = {}
+    for zc in (True, False):
+        monkeypatch.setattr(rd, "ZERO_COPY_FRAMES", zc)
+        ds = dv.DeviceScene(scene)
+        frames[zc] = [rd.render_image(scene, c, device_scene=ds).copy() for c in cams]
+        pool = ds._frame_cache[(96, 64)]["h_rgb"]
+        assert all((e[2] is not None) == zc for e in pool)
+    for a, b in zip(frames[True], frames[False]):
+        np.testing.assert_array_equal(a, b)
+    cam = CameraModel(str(g["kind"]), int(g["width"]), int(g["height"]), float(g["focal"]), g["pose"])
+    monkeypatch.setattr(rd, "ZERO_COPY_FRAMES", True)
+    img = rd.render_image(scene, cam, epsilon=float(g["epsilon"]))
+    assert np.abs(img - g["img"]).max() <= IMG_TOL
