@@ -68,7 +68,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 8
+#define RFB_ABI_VERSION 9
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
@@ -198,18 +198,21 @@ int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void 
  * each), m_raw, v_raw (n each), m_sh, v_sh (48n each).  hyper (host) is
  * 3 x {lr, beta1, beta2, eps, 1-beta1^step, 1-beta2^step} for positions,
  * densities and SH.  sh_warmup zeroes the SH bands 1..15 gradient;
- * update_positions = 0 skips positions (lr_pos == 0 tail). */
+ * update_positions = 0 skips positions (lr_pos == 0 tail).  sh32 (nullable):
+ * the packed scene's fp32 channel-major SH copy (rfb_scene.sh32), rewritten
+ * from the updated coefficients in the same pass. */
 int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positions,
                        double *raw_density, double *sh, double *adam_state, double clip,
                        int32_t sh_warmup, int32_t update_positions, const double *hyper,
-                       void *stream);
+                       float *sh32, void *stream);
 
 /* After a parameter update: site4 = {positions, softplus(raw)}, packed
- * headers' sigma and the fp32 SH copy are refreshed from scene->sh.  (The
- * packed edge records hold positions: a scene whose positions moved must be
- * re-packed, or used with packed = 0.) */
+ * headers' sigma and, when refresh_sh32 is nonzero, the fp32 SH copy are
+ * refreshed from scene->sh (pass 0 when rfb_post_grad_adam already wrote
+ * scene->sh32).  (The packed edge records hold positions: a scene whose
+ * positions moved must be re-packed, or used with packed = 0.) */
 int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const double *raw_density,
-                      void *stream);
+                      int32_t refresh_sh32, void *stream);
 
 /* dirs [pix_count][3] f64 for row-major pixels pix_begin .. pix_begin+count-1. */
 int rfb_camera_rays(const rfb_camera *camera, int64_t pix_begin, int64_t pix_count,

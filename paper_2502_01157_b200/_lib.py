@@ -121,8 +121,8 @@ SIGNATURES = {
                                       I32, VP]),
     "rfb_softplus": (ctypes.c_int, [VP, I64, VP, VP, VP, VP]),
     "rfb_camera_rays": (ctypes.c_int, [P(rfb_camera), I64, I64, VP, VP]),
-    "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP]),
-    "rfb_refresh_scene": (ctypes.c_int, [P(rfb_scene), VP, VP, VP]),
+    "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP, VP]),
+    "rfb_refresh_scene": (ctypes.c_int, [P(rfb_scene), VP, VP, I32, VP]),
     "rfb_locate": (ctypes.c_int, [P(rfb_scene), VP, I64, I32, VP, VP]),
     "rfb_build_locate_grid": (ctypes.c_int, [P(rfb_scene), P(rfb_locate_grid), VP]),
     "rfb_locate_seeded": (ctypes.c_int, [P(rfb_scene), VP, I64, P(rfb_locate_grid), I32, VP, VP]),
@@ -178,7 +178,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rfb_abi_version() != 8:
+        if lib.rfb_abi_version() != 9:
             raise ExtensionMissing("librfb.so ABI version mismatch; rebuild")
         if path is None:
             _lib = lib

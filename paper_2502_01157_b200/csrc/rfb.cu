@@ -1255,13 +1255,18 @@ __device__ __forceinline__ double clipd(double x, double c) { return fmin(fmax(x
 __global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double *pos,
                             double *raw, double *sh, double *m_pos, double *v_pos, double *m_raw,
                             double *v_raw, double *m_sh, double *v_sh, double clip, int sh_warmup,
-                            int update_pos, AdamArgs a_pos, AdamArgs a_raw, AdamArgs a_sh) {
+                            int update_pos, AdamArgs a_pos, AdamArgs a_raw, AdamArgs a_sh,
+                            float *sh32) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n * 52) return;
     if (t < n * 48) {  // SH coefficient t = i*48 + k*3 + ch
         double g = (double)gsh[t];
-        if (sh_warmup && (t % 48) >= 3) g = 0.0;  // train.py:197-198
+        const int r = (int)(t % 48);
+        if (sh_warmup && r >= 3) g = 0.0;  // train.py:197-198
         adam1(sh[t], clipd(g, clip), m_sh[t], v_sh[t], a_sh);
+        // the walk's fp32 channel-major copy (k_refresh_sh32's layout), written
+        // here so the refresh does not re-read the fp64 rows
+        if (sh32) sh32[t - r + (r % 3) * 16 + r / 3] = (float)sh[t];
         return;
     }
     const int64_t u = t - n * 48;
@@ -1631,7 +1636,7 @@ int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void 
 int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positions,
                        double *raw_density, double *sh, double *adam_state, double clip,
                        int32_t sh_warmup, int32_t update_positions, const double *hyper,
-                       void *stream) {
+                       float *sh32, void *stream) {
     if (n_sites <= 0 || !grads_flat || !positions || !raw_density || !sh || !adam_state ||
         !hyper || !(clip > 0.0))
         return RFB_EINVAL;
@@ -1646,7 +1651,7 @@ int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positio
     const int64_t total = n * 52;
     k_post_adam<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         n, grads_flat, grads_flat + 4 * n, positions, raw_density, sh, m_pos, v_pos, m_raw, v_raw,
-        m_sh, v_sh, clip, sh_warmup, update_positions, a[0], a[1], a[2]);
+        m_sh, v_sh, clip, sh_warmup, update_positions, a[0], a[1], a[2], sh32);
     return (int)cudaGetLastError();
 }
 
@@ -1668,7 +1673,7 @@ __global__ void k_refresh_edges(const int32_t *nbr, const double *pos, int64_t E
 }
 
 int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const double *raw_density,
-                      void *stream) {
+                      int32_t refresh_sh32, void *stream) {
     if (!scene_ok(scene) || !positions || !raw_density) return RFB_EINVAL;
     // a packed scene with fp32-exact positions cannot take moved sites in place
     const bool pos64 = scene->packed && scene->positions_f64;
@@ -1681,7 +1686,7 @@ int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const dou
         scene->n_sites, positions, raw_density, scene->sh, (double4 *)scene->site4,
         scene->packed ? (CellHdr *)scene->cells : nullptr,
         nullptr, scene->offsets, reinterpret_cast<const float4 *>(scene->edges), pos64 ? 1 : 0);
-    if (scene->packed && scene->sh32)
+    if (refresh_sh32 && scene->packed && scene->sh32)
         k_refresh_sh32<<<(unsigned)((48 * scene->n_sites + 255) / 256), 256, 0, st>>>(
             scene->n_sites, scene->sh, (float *)scene->sh32);
     return (int)cudaGetLastError();

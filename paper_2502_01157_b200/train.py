@@ -30,6 +30,10 @@ from . import _lib
 from . import device as dv
 from .distributed import allreduce_gradients, world
 
+# the Adam pass also writes the packed scene's fp32 SH copy (rfb_post_grad_adam
+# sh32), so rfb_refresh_scene skips its fp64 -> fp32 SH pass
+FUSE_SH32 = True
+
 
 @dataclass
 class AdamHyper:
@@ -80,13 +84,16 @@ class DeviceTrainer:
             h[6 * k: 6 * k + 6] = (lrs[k], hyper.beta1, hyper.beta2, hyper.eps,
                                    1.0 - hyper.beta1 ** s, 1.0 - hyper.beta2 ** s)
         hp = np.ascontiguousarray(h)
+        fuse = FUSE_SH32 and self.ds.sh32 is not None
+        sh32 = dv._ptr(self.ds.sh32) if fuse else None
         _lib.check(self.lib.rfb_post_grad_adam(
             self.n, dv._ptr(self.grads.flat), dv._ptr(self.positions), dv._ptr(self.raw),
             dv._ptr(self.sh), dv._ptr(self.adam_state), float(hyper.grad_clip),
             1 if sh_warmup else 0, 1 if do_pos else 0,
-            hp.ctypes.data_as(ctypes.c_void_p), dv._stream(stream)), "rfb_post_grad_adam")
+            hp.ctypes.data_as(ctypes.c_void_p), sh32, dv._stream(stream)), "rfb_post_grad_adam")
         _lib.check(self.lib.rfb_refresh_scene(self.ds.c, dv._ptr(self.positions),
-                                              dv._ptr(self.raw), dv._stream(stream)),
+                                              dv._ptr(self.raw), 0 if fuse else 1,
+                                              dv._stream(stream)),
                    "rfb_refresh_scene")
 
     def rebuild_adjacency(self, stream=None) -> dict:
