@@ -295,10 +295,13 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
         free = [h, None, dv.host_device_pointer(ds.lib, h) if ZERO_COPY_FRAMES else None]
         pool.append(free)
     direct = free is not None and free[2] is not None
-    torch.cuda.synchronize(ds.device)
+    if stats is not None:  # counters and the timer only matter for stats
+        fc["out"].counters.zero_()
+        torch.cuda.synchronize(ds.device)
     t0 = time.perf_counter()
     res = dv.render_image_device(ds, camera, epsilon=epsilon, step_limit=step_limit, f64=True,
-                                 lanes_per_ray=lanes_per_ray, workspace=fc["ws"], out=fc["out"],
+                                 tile_ids=fc["tiles"], lanes_per_ray=lanes_per_ray,
+                                 workspace=fc["ws"], out=fc["out"],
                                  rgb_ptr=free[2] if direct else None)
     if free is not None:
         if not direct:
@@ -334,14 +337,15 @@ def _frame_cache(ds, W, H, weight_check):
     key = (W, H)
     fc = cache.get(key)
     if fc is None:
+        tx, ty = dv.tile_grid(W, H)
         fc = {"ws": dv.Workspace(ds.device),
               "out": dv.alloc_forward(W * H, ds.device, f64=True, per_ray=False),
+              "tiles": torch.arange(tx * ty, dtype=torch.int32, device=ds.device),
               "h_rgb": []}
         cache[key] = fc
     if weight_check and "h_wsum" not in fc:
         fc["h_wsum"] = torch.empty(W * H, dtype=torch.float64, pin_memory=True)
         fc["h_resid"] = torch.empty(W * H, dtype=torch.float64, pin_memory=True)
-    fc["out"].counters.zero_()
     return fc
 
 
