@@ -223,6 +223,15 @@ class DeviceScene:
     def default_t_max(self, origins: np.ndarray) -> float:
         """Batch fallback t_max (render.py:72-76)."""
         o = np.asarray(origins, dtype=np.float64).reshape(-1, 3)
+        if len(o) == 1:  # one camera origin per frame: memoised on the inputs' bits
+            key = (o.tobytes(), np.asarray(self.center).tobytes(), self.diagonal)
+            memo = self.__dict__.setdefault("_t_max_memo", {})
+            t = memo.get(key)
+            if t is None:
+                if len(memo) > 64:
+                    memo.clear()
+                t = memo[key] = DeviceScene.default_t_max(self, np.concatenate([o, o]))
+            return t
         return float(np.linalg.norm(o - self.center, axis=1).max() + 2.0 * self.diagonal + 1.0)
 
     def locate(self, queries: torch.Tensor, seed: int = 0, stream=None) -> torch.Tensor:
@@ -384,9 +393,7 @@ def _order32(order, m, device, origins=None, directions=None):
 
 def camera_struct(camera) -> _lib.rfb_camera:
     c = _lib.rfb_camera()
-    pose = np.asarray(camera.pose, dtype=np.float64).reshape(16)
-    for k in range(16):
-        c.pose[k] = float(pose[k])
+    c.pose[:] = np.asarray(camera.pose, dtype=np.float64).reshape(16).tolist()
     c.width = int(camera.width)
     c.height = int(camera.height)
     c.focal = float(camera.focal)
