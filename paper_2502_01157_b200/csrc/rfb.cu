@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "rfb_device.cuh"
 
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
     constexpr int kRayFields = Src::kUniform ? 4 : 9;
     __shared__ double s_ray[kRayFields * 256];
     __shared__ double s_uni[5];
-    __shared__ float s_basis[16 * 256];  // fp32 SH basis, [k][thread]
+    __shared__ float s_basis[15 * 256];  // fp32 SH basis k = 1..15, [k-1][thread] (k = 0: kC0)
     if (threadIdx.x == 0) {
         if constexpr (Src::kUniform) src.uniform(s_uni);
     }
@@ -301,10 +302,9 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 float bf[16];
                 *bsum_p = basis_setup(rr, bf);
 #pragma unroll
-                for (int k = 0; k < 16; ++k) s_basis[k * 256 + threadIdx.x] = bf[k];
+                for (int k = 1; k < 16; ++k) s_basis[(k - 1) * 256 + threadIdx.x] = bf[k];
             } else {
                 *bsum_p = kC0;
-                s_basis[threadIdx.x] = (float)kC0;
             }
         }
         // colour accumulation in fp32 (image tolerance 1e-4); transmittance and
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 double delta = t1 - t0;
                 const double alpha = (double)(-expm1f(-(float)(sigma * delta)));
                 double col[3];
-                cell_color<SHDEG, PACKED, 256>(S, cell, s_basis + threadIdx.x, r, *bsum_p, col);
+                cell_color<SHDEG, PACKED, 256, 1>(S, cell, s_basis + threadIdx.x, r, *bsum_p, col);
                 const double w = T * alpha;
                 wsum += w;
                 const float wf = (float)w;
@@ -1388,6 +1388,29 @@ static bool out_ok(const rfb_fwd_out *o) {
     return true;
 }
 
+// Shared-memory carveout for k_render: 4 blocks x (23.6 KB static + 1 KB
+// reserved) fit the 100 KB configuration, which leaves 156 KB of the SM's
+// 256 KB to L1 for the neighbour gathers (the default pick was 132 KB).
+// RFB_CARVEOUT (percent of the 228 KB maximum; -1 = driver default) overrides.
+static int render_carveout() {
+    static const int v = [] {
+        const char *e = getenv("RFB_CARVEOUT");
+        return e ? atoi(e) : 43;
+    }();
+    return v;
+}
+
+template <auto K>
+static void prefer_carveout() {
+    static bool done = false;  // once per kernel instantiation
+    if (!done) {
+        if (cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 render_carveout()) != cudaSuccess)
+            (void)cudaGetLastError();
+        done = true;
+    }
+}
+
 template <int G, int PACKED, class Src>
 static void launch_render_g(const rfb_scene *scene, const Src &src, double eps, double log_eps,
                             double wf, int32_t sl, const FwdOut &O, unsigned long long *ctr,
@@ -1396,10 +1419,12 @@ static void launch_render_g(const rfb_scene *scene, const Src &src, double eps, 
     int per_sm = 0;
     if (scene->sh_degree == 0) {
         auto k = k_render<G, 0, PACKED, Src>;
+        prefer_carveout<k_render<G, 0, PACKED, Src>>();
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
         k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr);
     } else {
         auto k = k_render<G, 3, PACKED, Src>;
+        prefer_carveout<k_render<G, 3, PACKED, Src>>();
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
         k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr);
     }

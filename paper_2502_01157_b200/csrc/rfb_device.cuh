@@ -222,7 +222,10 @@ static __device__ __noinline__ double exact_channel(const double *row, int ch, i
 }
 
 // basis_f: the ray's fp32 SH basis (BSTRIDE apart); bsum = sum |fp64 basis|.
-template <int SHDEG, int PACKED, int BSTRIDE = 1, class RayT>
+// SKIP0: basis_f holds k = 1..15 only (k = 0 is the direction-independent
+// constant kC0, sh.py:17), which keeps k_render's shared memory per block
+// under the 100 KB carveout step at 4 blocks per SM.
+template <int SHDEG, int PACKED, int BSTRIDE = 1, int SKIP0 = 0, class RayT>
 __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
                                           const float *basis_f, const RayT &ray,
                                           double bsum, double *col) {
@@ -230,13 +233,17 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
     const float cmax = S.sh_absmax;
     constexpr int NB = SHDEG == 0 ? 1 : 16;
     double acc[3] = {0.5, 0.5, 0.5};
+    auto bk = [&](int k) -> float {
+        if (SKIP0) return k == 0 ? (float)kC0 : basis_f[(k - 1) * BSTRIDE];
+        return basis_f[k * BSTRIDE];
+    };
     if (PACKED) {
         // sh32 is channel-major per site: [ch][16]; fp32 FMA accumulation
         const float *row = S.sh32 + (int64_t)i * 48;
         if (SHDEG == 0) {
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch)
-                acc[ch] = (double)__fmaf_rn(basis_f[0], __ldg(row + 16 * ch), 0.5f);
+                acc[ch] = (double)__fmaf_rn(bk(0), __ldg(row + 16 * ch), 0.5f);
         } else {
 #pragma unroll 1
             for (int ch = 0; ch < 3; ++ch) {  // one channel (4 x 16 B) in flight: registers
@@ -254,10 +261,10 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
 #else
                     const float4 v = __ldg(r4 + q);
 #endif
-                    a = __fmaf_rn(basis_f[(4 * q) * BSTRIDE], v.x, a);
-                    a = __fmaf_rn(basis_f[(4 * q + 1) * BSTRIDE], v.y, a);
-                    a = __fmaf_rn(basis_f[(4 * q + 2) * BSTRIDE], v.z, a);
-                    a = __fmaf_rn(basis_f[(4 * q + 3) * BSTRIDE], v.w, a);
+                    a = __fmaf_rn(bk(4 * q), v.x, a);
+                    a = __fmaf_rn(bk(4 * q + 1), v.y, a);
+                    a = __fmaf_rn(bk(4 * q + 2), v.z, a);
+                    a = __fmaf_rn(bk(4 * q + 3), v.w, a);
                 }
                 acc[ch] = (double)a;
             }
