@@ -1388,26 +1388,47 @@ static bool out_ok(const rfb_fwd_out *o) {
     return true;
 }
 
-// Shared-memory carveout for k_render: 4 blocks x (23.6 KB static + 1 KB
-// reserved) fit the 100 KB configuration, which leaves 156 KB of the SM's
-// 256 KB to L1 for the neighbour gathers (the default pick was 132 KB).
+// Shared-memory carveout for k_render: the smallest configuration that holds
+// the blocks the registers allow per SM (static + 1 KB reserved each), so the rest of the SM's
+// 256 KB goes to L1 for the neighbour gathers.  SH degree 3: 4 x 24.6 KB fit
+// the 100 KB step (L1 156 KB; the driver's default pick was 132 KB): 21.25 ->
+// 21.08 ms per config-2 frame.  SH degree 0 keeps the driver's pick (the
+// 64 KB step measured 1.3% slower on config 1).
 // RFB_CARVEOUT (percent of the 228 KB maximum; -1 = driver default) overrides.
-static int render_carveout() {
-    static const int v = [] {
-        const char *e = getenv("RFB_CARVEOUT");
-        return e ? atoi(e) : 43;
-    }();
-    return v;
-}
-
 template <auto K>
 static void prefer_carveout() {
     static bool done = false;  // once per kernel instantiation
-    if (!done) {
-        if (cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 render_carveout()) != cudaSuccess)
+    if (done) return;
+    done = true;
+    int blocks = 0;  // what the registers allow, before any preference
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, K, 256, 0) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return;
+    }
+    int pct;
+    const char *e = getenv("RFB_CARVEOUT");
+    if (e && *e) {
+        pct = atoi(e);
+    } else {
+        cudaFuncAttributes a;
+        if (cudaFuncGetAttributes(&a, K) != cudaSuccess) {
             (void)cudaGetLastError();
-        done = true;
+            return;
+        }
+        const size_t need = (size_t)std::max(blocks, 1) * (a.sharedSizeBytes + 1024);
+        pct = (int)std::min<size_t>(100, (100 * need + 228 * 1024 - 1) / (228 * 1024));
+    }
+    if (cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, pct) !=
+        cudaSuccess) {
+        (void)cudaGetLastError();
+        return;
+    }
+    // keep the preference only if the blocks per SM are unchanged
+    int after = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&after, K, 256, 0) != cudaSuccess ||
+        after < blocks) {
+        (void)cudaGetLastError();
+        (void)cudaFuncSetAttribute(K, cudaFuncAttributePreferredSharedMemoryCarveout, -1);
     }
 }
 
@@ -1419,7 +1440,6 @@ static void launch_render_g(const rfb_scene *scene, const Src &src, double eps, 
     int per_sm = 0;
     if (scene->sh_degree == 0) {
         auto k = k_render<G, 0, PACKED, Src>;
-        prefer_carveout<k_render<G, 0, PACKED, Src>>();
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
         k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr);
     } else {
