@@ -37,6 +37,9 @@
  *   rfb_render_image    diffrender/render.py:128-149 render_image() (fused
  *                        ray generation + shared-origin start cell + render,
  *                        over a list of image tiles for multi-GPU sharding)
+ *   rfb_host_device_pointer  render_image() returns a host image: the mapped
+ *                        address of a pinned host frame, so rfb_render_image
+ *                        stores the image to host memory during the walk
  *   rfb_backward_rays   diffrender/render.py:152-221 render_rays_with_gradients()
  *                        (backward_ray 250-337 + face_t_gradient 340-369)
  *   rfb_train_batch     tracer/kernels.py:372-453   train_batch()
