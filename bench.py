@@ -2,34 +2,46 @@
 """Benchmark: rays/s of the Radiant Foam hot path on B200 (BASELINE.json).
 
 Workload (N=1): config 2 -- synthetic 1M-site foam (seed 1,
-SH degree 3, uniform in [-1,1]^3, fp32-exact sites, Qhull CSR), pinhole
-camera at (0,0,3) looking at the origin, camera_angle_x 0.9, 1920x1080,
-epsilon 1e-3, step_limit 4096.  One step = one full forward frame
-(rfb_render_image: ray generation + start cell + walk + SH-3 colour +
-compositing).  ``fwd_bwd`` reports config 3 on the same scene: one step =
-rfb_train_batch over every pixel of the view (L2 adjoint, quantile off) plus,
-for N>1, the NCCL all-reduce of the per-site gradient buffer.
+SH degree 3, uniform in [-1,1]^3, fp32-exact sites), pinhole camera at
+(0,0,3) looking at the origin, camera_angle_x 0.9, 1920x1080, epsilon 1e-3,
+step_limit 4096.  One step = one full forward frame (rfb_render_image: ray
+generation + start cell + walk + SH-3 colour + compositing).  ``fwd_bwd``
+reports config 3 on the same scene: one step = rfb_train_batch over every
+pixel of the view (L2 adjoint, quantile off) plus, for N>1, the NCCL
+all-reduce of the per-site gradient buffer.
 
-Multi-GPU (torchrun, one rank per GPU): every step renders N views (view k =
-orbit pose k-1, view 0 = the config-2 camera); each view's 32x32 tiles are
-interleaved round-robin over the ranks (scene replicated) and the frames are
-summed onto rank 0.  Training: rank r trains on view r and the flat fp32
-gradient buffer is all-reduced.  Per-rank work is fixed as N grows:
-"scaling": "weak".
+Fixture: the Delaunay CSR is built by the device builder and checked against
+the sha1 of the Qhull CSR committed in synthetic.QHULL_CSR_SHA1 (computed on
+the CPU with scipy's Qhull); a mismatch aborts the run.
+
+Multi-GPU: ``--gpus N`` with N > 1 re-launches itself under
+torch.distributed.run (one rank per GPU) unless it already runs under it.
+Every step renders N views (view k = orbit pose k-1, view 0 = the config-2
+camera); each view's 32x32 tiles are interleaved round-robin over the ranks
+(scene replicated) and the frames are summed onto rank 0.  Training: rank r
+trains on view r and the flat fp32 gradient buffer is all-reduced.  Per-rank
+work is fixed as N grows: "scaling": "weak".
 
 Timing: W untimed warm-up steps, then K steps bracketed by barrier +
 synchronize, timed with CUDA events on the launching stream, max over ranks.
-The scene (~950 MB packed at config 2) is larger than L2 (126 MB).  nvidia-smi clocks are
-sampled during the timed region.  ``e2e`` times the public API
-(render.render_image with a resident scene: camera in, (H,W,3) float64 image
-copied to host) including the device->host copy of the image; at N>1 the
-tile-sharded distributed.ShardedRenderer with the frame assembled on rank 0
-and copied to the host there.  RFB_BENCH_DIST=1 takes the collective path at
-N=1 too (a 1-rank NCCL group), to exercise it on one GPU.
+The scene (~950 MB packed at config 2) is larger than L2 (126 MB).
+nvidia-smi clocks are sampled during the timed region.  ``e2e`` times the
+public API with a resident scene (render.render_image: camera in, (H,W,3)
+float64 image on the host); ``e2e_cold`` additionally uploads and packs the
+host scene every step (DeviceScene(scene) + render_image), the reference's
+per-call contract (render.py:49-54).
 
---impl reference: the reference algorithm's CPU implementation on the host
-cores (the C oracle port of rfoam/tracer/kernels.py, every host thread), on
-a bounded row sample of the same frame.
+Parity (N=1): the CPU leg renders every 8th row of the frame with the C
+oracle port; the GPU frame's rows must match it (status, nseg, per-ray
+counters and per-ray visited-cell sequences / depths bit-exact via
+walk_digest, RGB within 1e-4), and a >= 80k-ray band of the config-3 view is
+trained on both (gradients within 1e-3 relative, loss 1e-6).  The line
+carries a ``parity`` object; a mismatch exits non-zero after printing it.
+
+--impl reference: the reference algorithm's CPU implementation (the C oracle
+port of rfoam/tracer/kernels.py, every host thread) on the SAME full frame
+and fixture (CSR from Qhull, checked against the committed digest); it never
+loads librfb or touches the GPU.
 """
 
 from __future__ import annotations
@@ -37,6 +49,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -49,6 +62,12 @@ sys.path.insert(0, REPO)
 
 METRIC = "rays/sec fwd and fwd+bwd (1M-site foam, 1080p) at 1/2/4/8 B200; % of gather roofline"
 UNIT = "rays/s"
+IMG_TOL = 1e-4
+GRAD_RTOL = 1e-3
+DTYPE = "f64/f32"
+DTYPE_DETAIL = ("fp64 walk (bisector depths, exit faces, log-transmittance, weights), fp32 SH "
+                "colour accumulation and fp32 gradient atomics (north_star tolerances: image "
+                "1e-4 abs, gradients 1e-3 rel)")
 
 
 def parse():
@@ -67,12 +86,15 @@ def parse():
                     help="fwd+bwd with the quantile regulariser on (lambda 0.01, P=2 pairs, "
                          "u_pairs from rng(12); optim/config.py:34-36)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-train-iter", action="store_true",
                     help="skip timing a reference-style training iteration (65,536 random pixels)")
     ap.add_argument("--no-adjacency", action="store_true",
                     help="skip timing the device Delaunay rebuild (SURVEY §8f row 2)")
     ap.add_argument("--cpu-row-stride", type=int, default=8)
+    ap.add_argument("--grad-band-rows", type=int, default=80,
+                    help="rows of the config-3 view trained on both GPU and oracle (parity)")
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 4, 5],
                     help="1: the reference's CPU-runnable case (10k sites, SH deg 0, "
                          "128x128); 2: config 2 forward + config 3 fwd+bwd (1M, 1080p; default); "
@@ -91,16 +113,33 @@ def parse():
             args.width, args.height = 128, 128
         args.sh_degree = 0
         args.cpu_row_stride = 1
+        args.grad_band_rows = args.height
     if args.config in (4, 5):
         args.kind = "surface"
         if args.n_sites == 1_000_000:
             args.n_sites = 3_000_000
         if args.seed == 1:
             args.seed = 2
+        args.cpu_row_stride = max(args.cpu_row_stride, 16)  # every 16th row
     if args.config == 4 and (args.width, args.height) == (1920, 1080):
         args.width, args.height = 3840, 2160
-        args.cpu_row_stride = max(args.cpu_row_stride, 32)
+    args.grad_band_rows = min(args.grad_band_rows, args.height)
     return args
+
+
+def maybe_relaunch(args):
+    """--gpus N > 1 outside torchrun: re-exec under torch.distributed.run with N ranks."""
+    if args.impl != "ours" or args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    print(f"[bench] relaunching under torchrun: {args.gpus} ranks", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
 
 
 def peaks():
@@ -136,6 +175,16 @@ def gather_ceilings():
             "latency_ns": {str(r["working_set_bytes"]): r["ns_per_hop"] for r in rows
                            if r["kind"] == "chase"},
             "source": "profiles/r09_gather_peak.jsonl (tools/gather_peak.cu)"}
+
+
+def profile_numbers():
+    """Per-kernel DRAM traffic and binding-unit fractions from the committed ncu captures
+    (profiles/traffic.json)."""
+    try:
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            return json.load(f)
+    except Exception:  # noqa: BLE001
+        return {}
 
 
 class ClockSampler:
@@ -209,81 +258,221 @@ def orbit_views(W, H, count=8):
             for p in orbit_poses(np.zeros(3), 3.0, 0.3, count)]
 
 
+def view0(args):
+    """The view the N=1 forward line (and the reference arm) renders."""
+    if args.config in (1, 2):
+        return make_views(1, args.width, args.height)[0]
+    return orbit_views(args.width, args.height, 8)[0]
+
+
+def workload_name(args):
+    return {
+        1: "config 1: 10k-site foam (seed 0), SH deg 0, 128x128 forward render per view, "
+           "camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
+        2: "config 2: 1M-site foam (seed 1), SH deg 3, 1920x1080 forward render per view, "
+           "camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
+        4: "config 4: 3M-site surface foam (seed 2), SH deg 3, one 3840x2160 frame per step "
+           "from orbit pose 0, 32x32 tiles interleaved over the ranks",
+        5: "config 5: 3M-site surface foam (seed 2), 8 orbit views at 1920x1080 forward+backward "
+           "per step split over the ranks, NCCL all-reduce of the [n,52] gradients",
+    }[args.config]
+
+
 def algorithmic_bytes(C, V, N, m, sh_bytes):
     """B_f = 24C + 16V + S_b N + 12 per ray (totals here)."""
     return 24.0 * C + 16.0 * V + sh_bytes * N + 12.0 * m
 
 
-# ---------------------------------------------------------------------------
-def _train_roofline():
-    """k_train's measured binding unit and DRAM traffic (profiles/traffic.json, from the
-    committed ncu capture)."""
-    try:
-        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
-            tj = json.load(f)
-        return {"kernel": "k_train (walk + record + reverse pass)",
-                "binding_unit": "l1tex data-pipe wavefronts",
-                "binding_frac": tj.get("k_train_l1_data_pipe_frac"),
-                "traffic": tj.get("k_train_dram_bytes_per_launch"),
-                "source": tj.get("k_train_source", tj.get("source"))}
-    except Exception:  # noqa: BLE001
-        return None
+def fwd_bwd_bytes(C, V, N, m, sh_bytes):
+    """B_fb = B_f + 12 (target) + 2 N (4 + S_b) + 2 (N - m) 24 (totals)."""
+    return (algorithmic_bytes(C, V, N, m, sh_bytes) + 12.0 * m + 2.0 * N * (4 + sh_bytes)
+            + 2.0 * max(N - m, 0) * 24)
 
 
-def run_reference(args):
-    """CPU reference arm: the oracle port on all host threads (rank 0 only)."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    line = cpu_baseline_measure(args, steps=args.steps, warmup=min(args.warmup, 1))
-    out = {"metric": METRIC, "value": line["value"], "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "impl": "reference",
-           "ms_per_step": line["ms_per_step"], "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"config {args.config}: {args.n_sites}-site {args.kind} foam, "
-                                  f"SH deg {args.sh_degree}, {args.width}x{args.height} forward",
-                      "sample": line["sample"], "n_sites": args.n_sites},
-           "cpu_baseline": {"value": line["value"], "unit": UNIT, "cores": line["cores"],
-                            "kind": "port", "sample": line["sample"]},
-           "e2e": {"value": line["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
-                   "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
-
-
-def cpu_baseline_measure(args, steps=1, warmup=0, scene=None, cam=None):
-    from oracle import oracle as orc
-    from paper_2502_01157_b200.scene import softplus
+def bench_scene(args, verbose=False):
     from paper_2502_01157_b200.synthetic import make_foam
 
-    if scene is None:
-        scene = make_foam(args.n_sites, args.seed, getattr(args, "sh_degree", 3),
-                          kind=getattr(args, "kind", "uniform"))
+    t0 = time.perf_counter()
+    scene = make_foam(args.n_sites, args.seed, args.sh_degree, kind=args.kind, verbose=verbose)
+    return scene, time.perf_counter() - t0
+
+
+def oracle_scene_arrays(scene):
+    from oracle import oracle as orc
+    from paper_2502_01157_b200.scene import softplus
+
     adj = scene.adjacency
-    sa = orc.SceneArrays(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density),
-                         scene.sh_coeffs.reshape(-1, 48), scene.background)
-    if cam is None:
-        cam = (make_views(1, args.width, args.height)[0] if getattr(args, "config", 2) == 2
-               else orbit_views(args.width, args.height, 8)[0])
-    rows = np.arange(0, args.height, args.cpu_row_stride)
-    rr, cc = np.meshgrid(rows, np.arange(args.width), indexing="ij")
+    return orc.SceneArrays(adj.positions, adj.offsets, adj.neighbors, softplus(scene.raw_density),
+                           scene.sh_coeffs.reshape(-1, 48), scene.background)
+
+
+def oracle_inputs(sa, cam, rows):
+    """Rays of the given pixel rows of a view with the frame's shared start cell and
+    t_max (render.py:72-90), as the oracle takes them."""
+    from oracle import oracle as orc
+
+    W = cam.width
+    rr, cc = np.meshgrid(np.asarray(rows), np.arange(W), indexing="ij")
     dirs = cam.ray_directions(rr.reshape(-1), cc.reshape(-1))
     m = len(dirs)
     origin = cam.position
     start = int(orc.nearest_sites(sa.positions, origin[None, :])[0])
     t_max = float(np.linalg.norm(origin - sa.center) + 2.0 * sa.diagonal + 1.0)
+    return {"origins": np.broadcast_to(origin, (m, 3)).copy(), "dirs": dirs, "start": start,
+            "t_max": t_max, "m": m, "pix": (rr * W + cc).reshape(-1)}
+
+
+def oracle_render(sa, inp, threads, digest=False):
+    """The C oracle port of tracer/kernels.py:199-247 on prepared rays, timed like
+    render.py:102-113 (perf_counter around the kernel call)."""
+    from oracle import oracle as orc
+
+    t0 = time.perf_counter()
+    out = orc.render_rays(sa, inp["origins"], inp["dirs"], 0.0, inp["t_max"], inp["start"],
+                          threads=threads, digest=digest)
+    out["seconds"] = time.perf_counter() - t0
+    out["m"] = inp["m"]
+    out["pix"] = inp["pix"]
+    return out
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    """CPU reference arm: the oracle port on every host thread, the full frame, the
+    same fixture (Qhull CSR, digest-checked), rank 0 only.  No torch, no librfb."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    os.environ["RFB_FIXTURE_BUILDER"] = "qhull"  # the CPU arm never touches the GPU
+    scene, build_s = bench_scene(args, verbose=True)
+    prov = getattr(scene.adjacency, "provenance", {})
+    sa = oracle_scene_arrays(scene)
     threads = os.cpu_count() or 1
-    origins = np.broadcast_to(origin, (m, 3)).copy()
-    for _ in range(warmup):
-        orc.render_rays(sa, origins[:4096], dirs[:4096], 0.0, t_max, start, threads=threads)
+    views = ([view0(args)] if args.config != 5 else orbit_views(args.width, args.height, 8))
+    rows = np.arange(args.height)
+    inputs = [oracle_inputs(sa, cam, rows) for cam in views]
+    for _ in range(min(args.warmup, 1)):  # C code: no JIT; one warm-up touches the scene
+        oracle_render(sa, oracle_inputs(sa, views[0], rows[: max(1, len(rows) // 16)]), threads)
     times = []
-    for _ in range(max(steps, 1)):
-        t0 = time.perf_counter()
-        orc.render_rays(sa, origins, dirs, 0.0, t_max, start, threads=threads)
-        times.append(time.perf_counter() - t0)
+    for _ in range(max(args.steps, 1)):
+        times.append(sum(oracle_render(sa, inp, threads)["seconds"] for inp in inputs))
     dt = float(np.mean(times))
-    return {"value": m / dt, "ms_per_step": dt * 1e3, "cores": threads,
-            "sample": f"every {args.cpu_row_stride}th row of the {args.width}x{args.height} frame "
-                      f"({m} rays/step, {len(times)} steps, C oracle port, {threads} threads)"}
+    rays = args.width * args.height * len(views)
+    value = rays / dt
+    sample = (f"full {args.width}x{args.height} frame x {len(views)} view(s) per step "
+              f"({rays} rays), {len(times)} steps, C oracle port of tracer/kernels.py, "
+              f"{threads} threads" + (" (forward only)" if args.config == 5 else ""))
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "impl": "reference",
+           "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": workload_name(args), "n_sites": args.n_sites,
+                      "sample": sample, "csr": prov, "scene_build_s": round(build_s, 1)},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def frame_parity(ds, cam, probe, ref, args):
+    """Sampled rows of the benchmarked frame (k_render over tiles, the timed kernel) vs the
+    oracle: status / nseg / per-ray counters bit-exact, per-ray walk digests (cells, t0,
+    t1) equal, RGB within 1e-4 (f64 outputs).  Segment dumps are taken tile-row by
+    tile-row (rfb_fwd_out.seg_first/seg_count) so memory stays bounded."""
+    import torch
+
+    from oracle.walk_digest import digests
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = cam.width, cam.height
+    pix = torch.from_numpy(ref["pix"]).to(ds.device)
+    st = probe.status[pix].cpu().numpy()
+    ns = probe.nseg[pix].cpu().numpy()
+    rc = probe.ray_counters[pix].cpu().numpy()
+    rgb = probe.rgb[pix].cpu().numpy()
+    counters_equal = bool(np.array_equal(st, ref["status"]) and np.array_equal(ns, ref["nseg"])
+                          and np.array_equal(rc, ref["counters"]))
+    max_rgb = float(np.abs(rgb - ref["rgb"]).max()) if len(rgb) else 0.0
+    # per-ray digests, one 32-row tile band at a time
+    tx, ty = dv.tile_grid(W, H)
+    rows = np.unique(ref["pix"] // W)
+    dig = np.empty(len(ref["pix"]), dtype=np.uint64)
+    ws = dv.Workspace(ds.device)
+    cap = max(1, int(probe.nseg.max().item()))
+    out = dv.alloc_forward(W * H, ds.device, f64=True, per_ray=True, seg_capacity=cap,
+                           seg_rays=(0, 32 * W))
+    for band in np.unique(rows // 32):
+        r0, r1 = band * 32, min(H, band * 32 + 32)
+        tiles = torch.arange(band * tx, band * tx + tx, dtype=torch.int32, device=ds.device)
+        out.seg_first = int(r0 * W)
+        dv.render_image_device(ds, cam, tile_ids=tiles, lanes_per_ray=args.lanes, out=out,
+                               workspace=ws)
+        sel = np.flatnonzero((ref["pix"] // W >= r0) & (ref["pix"] // W < r1))
+        loc = torch.from_numpy(ref["pix"][sel] - r0 * W).to(ds.device)
+        dig[sel] = digests(out.seg_cells[loc], out.seg_t0[loc], out.seg_t1[loc],
+                           out.nseg[torch.from_numpy(ref["pix"][sel]).to(ds.device)])
+    del out
+    digests_equal = bool(np.array_equal(dig, ref["digest"]))
+    return {"rows_checked": int(len(rows)), "rays_checked": int(len(ref["pix"])),
+            "counters_equal": counters_equal, "cell_sequences_equal": digests_equal,
+            "rays_differing": int((dig != ref["digest"]).sum()), "max_abs_rgb": max_rgb,
+            "ok": counters_equal and digests_equal and max_rgb <= IMG_TOL}
+
+
+def grad_parity(ds, sa, cam, args, threads):
+    """A band of rows of the config-3 view (>= 80k rays at 1080p, in the timed leg's tile
+    order) trained on the GPU (the same k_train instantiation as the timed leg) and by the
+    oracle's train_batch (tracer/kernels.py:372-453): per-tensor gradients within 1e-3
+    relative, loss 1e-6, status and counters bit-exact."""
+    import torch
+
+    from oracle import oracle as orc
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = cam.width, cam.height
+    b0 = max(0, H // 2 - args.grad_band_rows // 2)
+    b1 = min(H, b0 + args.grad_band_rows)
+    perm = dv.tile_order(W, H)
+    perm = perm[(perm // W >= b0) & (perm // W < b1)]
+    dirs = cam.ray_directions()[perm]
+    m = len(dirs)
+    rng = np.random.default_rng(11)
+    targets = rng.uniform(0.0, 1.0, (H * W, 3))[perm]
+    o = np.broadcast_to(cam.position, (m, 3)).copy()
+    start = int(orc.nearest_sites(sa.positions, cam.position[None, :])[0])
+    t_max = float(np.linalg.norm(cam.position - sa.center) + 2.0 * sa.diagonal + 1.0)
+    workers = max(1, min(threads, 16))
+    ref = orc.train_batch(sa, o, dirs, np.zeros(m), np.full(m, t_max), np.full(m, start),
+                          targets, 1.0 / (3 * m), 0.0, None, 1e-4, n_workers=workers,
+                          threads=threads)
+    d = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to(ds.device, dt)  # noqa: E731
+    gb = dv.GradBuffers(ds.n_sites, ds.device)
+    loss = torch.zeros(2, dtype=torch.float64, device=ds.device)
+    res = dv.train_batch_device(ds, d(o), d(dirs), d(np.zeros(m)), d(np.full(m, t_max)),
+                                d(np.full(m, start), torch.int32), d(targets), gb, loss,
+                                rgb_scale=1.0 / (3 * m), f64=True, order=None)
+    torch.cuda.synchronize()
+
+    def rel(a, b):
+        den = float(np.abs(b).max())
+        return float(np.abs(a - b).max() / den) if den > 0 else float(np.abs(a).max())
+
+    g4 = gb.g4.double().cpu().numpy()
+    r = {"rays_checked": m, "rows": [int(b0), int(b1)],
+         "grad_rel_max": max(rel(g4[:, 3], ref["d_sigma_w"].sum(0)),
+                             rel(g4[:, :3], ref["d_pos_w"].sum(0)),
+                             rel(gb.sh.double().cpu().numpy(), ref["d_sh_w"].sum(0))),
+         "loss_rel": float(abs(loss[0].item() - ref["loss_w"].sum(0)[0])
+                           / max(abs(ref["loss_w"].sum(0)[0]), 1e-300)),
+         "status_counters_equal": bool(
+             np.array_equal(res.status.cpu().numpy(), ref["status"]) and
+             np.array_equal(res.counters.cpu().numpy(), ref["counters"].sum(0))),
+         "max_abs_rgb": float(np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max())}
+    r["ok"] = (r["grad_rel_max"] <= GRAD_RTOL and r["loss_rel"] <= 1e-6 and
+               r["status_counters_equal"] and r["max_abs_rgb"] <= IMG_TOL)
+    return r
 
 
 # ---------------------------------------------------------------------------
@@ -292,23 +481,28 @@ def main():
     if args.impl == "reference":
         run_reference(args)
         return
+    maybe_relaunch(args)
 
     import torch
     import torch.distributed as dist
 
     from paper_2502_01157_b200 import device as dv
     from paper_2502_01157_b200 import render as rd
-    from paper_2502_01157_b200.synthetic import make_foam
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "WORLD_SIZE" in os.environ and args.gpus > 1 and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     # RFB_BENCH_DIST=1 runs the collective code path even at world size 1 (a 1-rank NCCL
-    # group), so the N>1 plumbing can be exercised on the single GPU this round has
+    # group), so the N>1 plumbing can be exercised on a single GPU
     dist_on = world > 1 or os.environ.get("RFB_BENCH_DIST") == "1"
     torch.cuda.set_device(local)
     if dist_on:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rank == 0:
+            print(f"[bench] NCCL process group: {dist.get_world_size()} ranks", file=sys.stderr,
+                  flush=True)
     dev = torch.device("cuda", local)
 
     def barrier():
@@ -317,10 +511,9 @@ def main():
 
     W, H = args.width, args.height
     lanes = args.lanes if args.lanes > 0 else dv.DEFAULT_LANES
-    t_build = time.perf_counter()
-    scene = make_foam(args.n_sites, args.seed, args.sh_degree, kind=args.kind, verbose=(rank == 0))
+    scene, build_s = bench_scene(args, verbose=(rank == 0))
+    prov = getattr(scene.adjacency, "provenance", {})
     ds = dv.DeviceScene(scene, device=dev)
-    build_s = time.perf_counter() - t_build
     scaling = "weak"
     if args.config in (1, 2):
         views = make_views(world, W, H)  # one view per rank per step, tile-sharded
@@ -350,8 +543,9 @@ def main():
             for fr in frames:
                 dist.reduce(fr.rgb, dst=0)
 
-    # -- untimed: counters for the roofline (view 0, full frame) ------------------
-    probe = dv.render_image_device(ds, views[0], per_ray=True, lanes_per_ray=lanes, workspace=ws)
+    # -- untimed: counters for the roofline + the parity probe (view 0, full frame, f64) --
+    probe = dv.render_image_device(ds, views[0], per_ray=True, f64=True, lanes_per_ray=lanes,
+                                   workspace=ws)
     torch.cuda.synchronize()
     C_tot, V_tot = [int(x) for x in probe.counters.cpu().tolist()]
     N_tot = int(probe.nseg.to(torch.int64).sum().item())
@@ -361,45 +555,47 @@ def main():
     bytes_per_frame = algorithmic_bytes(C_tot, V_tot, N_tot, m0, sh_bytes)
 
     # -- forward timing ------------------------------------------------------------
-    if args.config == 5:
-        args.steps_fwd = 0
-    for _ in range(args.warmup if args.config != 5 else 0):
-        fwd_step()
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    clk = ClockSampler(local)
-    if rank == 0:
-        clk.start()
-        time.sleep(0.3)
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
-    ev0.record(stream)
-    for s in range(args.steps):
-        kev[s][0].record(stream)
-        if args.config != 5:
+    kernel_ms = None
+    fwd_value = None
+    clocks = None
+    fwd_ms = 0.0
+    if args.config != 5:
+        for _ in range(args.warmup):
             fwd_step()
-        kev[s][1].record(stream)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    fwd_ms = ev0.elapsed_time(ev1)
-    kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
-    clocks = clk.stop() if rank == 0 else None
-    t = torch.tensor([fwd_ms], dtype=torch.float64, device=dev)
-    if dist_on:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    fwd_ms = float(t.item())
-    rays_total = args.steps * W * H * len(views)
-    fwd_value = rays_total / max(fwd_ms / 1e3, 1e-12)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        clk = ClockSampler(local)
+        if rank == 0:
+            clk.start()
+            time.sleep(0.3)
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        ev0.record(stream)
+        for s in range(args.steps):
+            kev[s][0].record(stream)
+            fwd_step()
+            kev[s][1].record(stream)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        fwd_ms = ev0.elapsed_time(ev1)
+        kernel_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+        clocks = clk.stop() if rank == 0 else None
+        t = torch.tensor([fwd_ms], dtype=torch.float64, device=dev)
+        if dist_on:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        fwd_ms = float(t.item())
+        fwd_value = args.steps * W * H * len(views) / max(fwd_ms / 1e3, 1e-12)
 
-    # -- fwd+bwd timing (config 3) -------------------------------------------------
+    # -- fwd+bwd timing (config 3 / 5) ---------------------------------------------
     fb = None
+    fb_launches = 0
     if not args.no_fwd_bwd and train_views:
-        # each training view's rays in tile order (4x8 warp patches): the same
-        # ray set, scheduled coherently (dv.tile_order); targets follow it
+        # each training view's rays in tile order (4x8 warp patches): the same ray set,
+        # scheduled coherently (dv.tile_order); targets follow it
         perm = torch.from_numpy(dv.tile_order(W, H)).to(dev)
         rng = np.random.default_rng(11)
         batches = []
@@ -454,6 +650,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         fb_ms = e0.elapsed_time(e1)
+        fb_launches = args.steps * len(batches)
         clocks_fb = clk2.stop() if rank == 0 else None
         t = torch.tensor([fb_ms], dtype=torch.float64, device=dev)
         if dist_on:
@@ -462,9 +659,11 @@ def main():
         fb_C = int(out_fb.ray_counters[:, 0].sum().item())
         fb_V = int(out_fb.ray_counters[:, 1].sum().item())
         fb_N = int(out_fb.nseg.to(torch.int64).sum().item())
-        fb_bytes = algorithmic_bytes(fb_C, fb_V, fb_N, m, 192 if ds.sh_degree == 3 else 12) \
-            + 12.0 * m + 2.0 * fb_N * (4 + (192 if ds.sh_degree == 3 else 12)) \
-            + 2.0 * max(fb_N - m, 0) * 24  # B_fb, last view's counters
+        fb_bytes = fwd_bwd_bytes(fb_C, fb_V, fb_N, m, sh_bytes)  # last view's counters
+        view_ms = fb_ms / args.steps / max(len(batches), 1)
+        fb_achieved = fb_bytes / (view_ms / 1e3) / 1e9
+        peak, peak_kind = peaks()
+        pn = profile_numbers()
         fb = {"value": args.steps * m * n_train_views / (fb_ms / 1e3), "unit": UNIT,
               "ms_per_step": fb_ms / args.steps,
               "workload": ("config 3: 1080p forward+backward, per-site fp32 gradients"
@@ -477,9 +676,18 @@ def main():
                           + (", NCCL all-reduce" if dist_on else ""),
               "views_per_step": n_train_views,
               "algorithmic_bytes_per_view": fb_bytes,
-              "achieved_GBps": fb_bytes * n_train_views / world / (fb_ms / args.steps / 1e3) / 1e9,
-              "roofline": _train_roofline(),
-              "cells_per_ray": int(out_fb.ray_counters[:, 0].sum().item()) / m,
+              "roofline": {"bound": "hbm", "kernel": "k_train (walk + record + reverse pass)",
+                           "achieved": fb_achieved, "peak": peak, "unit": "GB/s",
+                           "frac": fb_achieved / peak, "peak_kind": peak_kind,
+                           "launch_ms": view_ms,
+                           "traffic": pn.get("k_train_dram_bytes_per_launch"),
+                           "binding_unit": pn.get("k_train_binding_unit",
+                                                  "l1tex data-pipe wavefronts"),
+                           "binding_frac": pn.get("k_train_l1_data_pipe_frac"),
+                           "source": pn.get("k_train_source"),
+                           "note": "achieved counts B_fb of SURVEY §8d with atomic RMW x2 and "
+                                   "no reuse; coherent rays share cells, so frac can exceed 1"},
+              "cells_per_ray": fb_C / m,
               "loss_rgb": float(loss[0].item()) / (3.0 * m * n_train_views),
               "clocks": clocks_fb}
 
@@ -531,10 +739,11 @@ def main():
     adjacency = None
     if not args.no_adjacency and rank == 0:
         from paper_2502_01157_b200 import adjacency as adj_mod
+        from paper_2502_01157_b200.synthetic import QHULL_CSR_SHA1, csr_sha1
         pos_d = torch.from_numpy(np.ascontiguousarray(scene.adjacency.positions)).to(dev)
         off_d, nbr_d, _, ainfo = adj_mod.build_device(pos_d)  # warm-up
-        same = bool(torch.equal(off_d.cpu(), torch.from_numpy(scene.adjacency.offsets)) and
-                    torch.equal(nbr_d.cpu(), torch.from_numpy(scene.adjacency.neighbors)))
+        off_h, nbr_h = off_d.cpu().numpy(), nbr_d.cpu().numpy()
+        tag = f"{args.kind}_n{args.n_sites}_s{args.seed}"
         tms = []
         for _ in range(3):
             a0 = torch.cuda.Event(enable_timing=True)
@@ -545,15 +754,23 @@ def main():
             torch.cuda.synchronize()
             tms.append(a0.elapsed_time(a1))
         adjacency = {"ms": float(np.median(tms)), "sites": int(pos_d.shape[0]),
-                     "edges": ainfo["edges"], "csr_equals_fixture": same,
+                     "edges": ainfo["edges"],
+                     "csr_sha1": csr_sha1(off_h, nbr_h),
+                     "qhull_csr_sha1": QHULL_CSR_SHA1.get(tag),
+                     "csr_equals_qhull": (csr_sha1(off_h, nbr_h) == QHULL_CSR_SHA1[tag]
+                                          if tag in QHULL_CSR_SHA1 else None),
+                     "csr_equals_fixture": bool(
+                         np.array_equal(off_h, scene.adjacency.offsets) and
+                         np.array_equal(nbr_h, scene.adjacency.neighbors)),
                      "pass2_sites": ainfo["pass2_sites"],
                      "api": "adjacency.build_device(positions) -> CSR + hull (rfb_build_adjacency)",
-                     "cpu_reference": "fixture CSR from scipy Qhull: ~127 s at 1M sites, 268 s "
-                                      "at 3M (SURVEY §8c; .foam_cache build logs)"}
+                     "cpu_reference": "scipy Qhull: 84 s at 1M sites, 240 s at 3M (this "
+                                      "container; digests in synthetic.QHULL_CSR_SHA1)"}
         del off_d, nbr_d
 
     # -- e2e through the public API (rank 0 view, host image out) -----------------
     e2e = None
+    e2e_cold = None
     if not args.no_e2e and not dist_on:
         cam = views[0]
         rd.render_image(scene, cam, device_scene=ds, lanes_per_ray=lanes)
@@ -563,12 +780,36 @@ def main():
             t0 = time.perf_counter()
             img = rd.render_image(scene, cam, device_scene=ds, lanes_per_ray=lanes)
             ts.append(time.perf_counter() - t0)
-        e2e = {"value": W * H / float(np.median(ts)), "unit": UNIT, "h2d_bytes_per_step": 0,
+        e2e = {"value": W * H / float(np.median(ts)), "unit": UNIT,
+               "h2d_bytes_per_step": 16 * 8,  # the camera pose (kernel parameter)
                "d2h_bytes_per_step": int(img.nbytes),
-               "api": "render.render_image(scene, camera, device_scene=ds) -> (H,W,3) f64 host"}
+               "api": "render.render_image(scene, camera, device_scene=ds) -> (H,W,3) f64 "
+                      "host image; scene resident on the GPU",
+               "timing": "host wall clock per call (median), includes the host image"}
+        # cold: the reference's per-call contract -- host scene in, host image out
+        adj = scene.adjacency
+        h2d = int(adj.positions.nbytes + scene.raw_density.nbytes + scene.sh_coeffs.nbytes
+                  + adj.offsets.nbytes + adj.neighbors.nbytes)
+        del img
+        tsc = []
+        for it in range(3 + max(2, min(args.steps, 5))):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            dsc = dv.DeviceScene(scene, device=dev)
+            img = rd.render_image(scene, cam, device_scene=dsc, lanes_per_ray=lanes)
+            dt = time.perf_counter() - t0
+            if it >= 3:
+                tsc.append(dt)
+            del img, dsc
+        e2e_cold = {"value": W * H / float(np.median(tsc)), "unit": UNIT,
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": W * H * 3 * 8,
+                    "api": "DeviceScene(scene) (upload positions, sigma, SH, CSR + device "
+                           "pack) then render.render_image -> (H,W,3) f64 host image, "
+                           "every step",
+                    "timing": "host wall clock per step (median)"}
     elif not args.no_e2e:
         # N > 1: the sharded public API -- every rank renders its tiles of each view, the
-        # frame is assembled on rank 0 and copied to the host there; max over ranks
+        # fp64 frame is assembled on rank 0 and copied to the host there; max over ranks
         from paper_2502_01157_b200.distributed import ShardedRenderer
         sr = ShardedRenderer(ds, W, H, lanes_per_ray=lanes)
 
@@ -588,10 +829,11 @@ def main():
         t = torch.tensor([float(np.median(ts))], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = {"value": len(views) * W * H / float(t.item()), "unit": UNIT,
-               "h2d_bytes_per_step": 0,
+               "h2d_bytes_per_step": 16 * 8 * len(views),
                "d2h_bytes_per_step": int(sum(x.nbytes for x in imgs)) if rank == 0 else 0,
                "api": "distributed.ShardedRenderer(ds, W, H).render_to_host(camera) per view "
-                      "(tile-sharded over the ranks, NCCL reduce to rank 0) -> pinned host frame",
+                      "(tile-sharded over the ranks, NCCL reduce to rank 0) -> (H,W,3) f64 "
+                      "host image",
                "timing": "median over steps of the per-rank wall clock, max over ranks"}
 
     if rank != 0:
@@ -599,93 +841,101 @@ def main():
             dist.destroy_process_group()
         return
 
+    # -- CPU baseline (bounded sample) + parity against it (N=1) ----------------------
     cpu = None
+    parity = None
     if not args.no_cpu_baseline and world == 1:
-        try:
-            cb = cpu_baseline_measure(args, steps=1, warmup=1, scene=scene, cam=views[0])
-            cpu = {"value": cb["value"], "unit": UNIT, "cores": cb["cores"], "kind": "port",
-                   "sample": cb["sample"]}
-        except Exception as e:  # noqa: BLE001
-            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port",
-                   "sample": f"failed: {e}"}
+        threads = os.cpu_count() or 1
+        sa = oracle_scene_arrays(scene)
+        rows = np.arange(0, H, args.cpu_row_stride)
+        oracle_render(sa, oracle_inputs(sa, views[0], rows[:2]), threads)  # warm-up
+        ref = oracle_render(sa, oracle_inputs(sa, views[0], rows), threads,
+                            digest=not args.no_parity)
+        sample = (f"every {args.cpu_row_stride}th row of the {W}x{H} frame ({ref['m']} rays, "
+                  f"1 step, C oracle port, {threads} threads)")
+        cpu = {"value": ref["m"] / ref["seconds"], "unit": UNIT, "cores": threads,
+               "kind": "port", "sample": sample}
+        if not args.no_parity:
+            parity = {"tolerances": {"rgb_abs": IMG_TOL, "grad_rel": GRAD_RTOL,
+                                     "cells_counters_status": "bit-exact"},
+                      "forward": frame_parity(ds, views[0], probe, ref, args)}
+            if fb is not None and args.config in (1, 2):
+                parity["fwd_bwd"] = grad_parity(ds, sa, train_views[0], args, threads)
+            parity["ok"] = all(v.get("ok", True) for v in parity.values() if isinstance(v, dict)
+                               and "ok" in v)
 
     peak, peak_kind = peaks()
-    achieved = bytes_per_frame * len(views) / world / max(kernel_ms / 1e3, 1e-12) / 1e9
-    traffic = None
-    l1_frac = None
-    render_src = None
-    tpath = os.path.join(REPO, "profiles", "traffic.json")
-    if os.path.exists(tpath):
-        try:
-            with open(tpath) as f:
-                tj = json.load(f)
-            traffic = tj.get("k_render_dram_bytes_per_launch")
-            l1_frac = tj.get("k_render_l1_data_pipe_frac")
-            render_src = tj.get("k_render_source")
-        except Exception:
-            traffic = None
-    workload = {
-        1: "config 1: 10k-site foam (seed 0), SH deg 0, 128x128 forward render per view, "
-           "camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
-        2: "config 2: 1M-site foam (seed 1), SH deg 3, 1920x1080 forward render per view, "
-           "camera (0,0,3)->origin, angle_x 0.9, eps 1e-3",
-        4: "config 4: 3M-site surface foam (seed 2), SH deg 3, one 3840x2160 frame per step "
-           "from orbit pose 0, 32x32 tiles interleaved over the ranks",
-        5: "config 5: 3M-site surface foam (seed 2), 8 orbit views at 1920x1080 forward+backward "
-           "per step split over the ranks, NCCL all-reduce of the [n,52] gradients",
-    }[args.config]
+    pn = profile_numbers()
     value = fwd_value
-    ms_step = fwd_ms / args.steps
+    ms_step = fwd_ms / max(args.steps, 1)
+    achieved = (bytes_per_frame * len(views) / world / max(kernel_ms / 1e3, 1e-12) / 1e9
+                if kernel_ms else None)
+    roof_kernel = "k_render (walk + SH + composite)"
+    launch_ms = kernel_ms
+    traffic = pn.get("k_render_dram_bytes_per_launch")
+    binding_frac = pn.get("k_render_l1_data_pipe_frac")
+    traffic_src = pn.get("k_render_source")
     if args.config == 5 and fb is not None:
         value = fb["value"]
         ms_step = fb["ms_per_step"]
-        achieved = fb["achieved_GBps"]
+        achieved = fb["roofline"]["achieved"]
         bytes_per_frame = fb["algorithmic_bytes_per_view"]
-        kernel_ms = fb["ms_per_step"] / max(len(train_views), 1)
+        launch_ms = fb["roofline"]["launch_ms"]
+        roof_kernel = "k_train (walk + record + reverse pass)"
+        traffic = pn.get("k_train_dram_bytes_per_launch")
+        binding_frac = pn.get("k_train_l1_data_pipe_frac")
+        traffic_src = pn.get("k_train_source")
     scene_mb = sum(t.numel() * t.element_size() for t in
                    (ds.site4, ds.offsets, ds.neighbors, ds.sh, ds.cells, ds.edges, ds.sh32)
                    if t is not None) / 1e6
     l2_note = (f"inputs larger than L2 (scene {scene_mb:.0f} MB vs 126 MB L2); no flush"
                if scene_mb > 126 else
                f"scene ({scene_mb:.0f} MB) fits in L2; no flush (small-config case)")
+    fwd_launches = 3 * args.steps * len(views) if args.config != 5 else 0
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": DTYPE,
+        "dtype_detail": DTYPE_DETAIL,
         "data": "synthetic (SURVEY.md §8d foam generator; random-init scene, no dataset)",
-        "config": {"workload": workload,
+        "config": {"workload": workload_name(args),
                    "n_sites": args.n_sites, "n_edges": ds.n_edges, "views_per_step": len(views),
                    "tiles": "32x32 interleaved over ranks", "lanes_per_ray": lanes or "auto",
                    "l2": l2_note,
                    "cells_per_ray": C_tot / m0, "neighbor_visits_per_ray": V_tot / m0,
                    "segments_per_ray": N_tot / m0, "failed_rays": failed,
-                   "scene_build_s": round(build_s, 1)},
+                   "csr": prov, "scene_build_s": round(build_s, 1)},
+        "parity": parity,
         "fwd_bwd": fb,
         "e2e": e2e,
+        "e2e_cold": e2e_cold,
         "adjacency_rebuild": adjacency,
         "train_iteration": train_iter,
-        "gpu_launches": (3 * args.steps * len(views) if args.config != 5
-                         else args.steps * len(train_views)),
+        "gpu_launches": fwd_launches + fb_launches,
+        "gpu_launches_detail": {"forward": fwd_launches, "fwd_bwd": fb_launches,
+                                "per_forward_view": "k_nearest_dist, k_nearest_id, k_render",
+                                "per_fwd_bwd_view": "k_train"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_render (walk + SH + composite)" if args.config != 5 else
-                               "k_train (walk + composite + reverse pass)",
+                     "frac": achieved / peak if achieved else None, "traffic": traffic,
+                     "peak_kind": peak_kind, "kernel": roof_kernel,
                      "algorithmic_bytes_per_launch": bytes_per_frame,
-                     "launch_ms": kernel_ms,
-                     "note": "achieved counts the algorithmic gather bytes of SURVEY §8d "
-                             "(no reuse); coherent rays share cells, so DRAM traffic per launch "
-                             "is `traffic` and frac can exceed 1. The binding unit is the L1 "
-                             "data pipe (binding_frac, from the ncu capture in profiles/).",
-                     "traffic_source": render_src,
-                     "binding_unit": "l1tex data-pipe wavefronts",
-                     "binding_frac": l1_frac,
+                     "launch_ms": launch_ms,
+                     "binding_unit": "L1 data pipe (l1tex wavefronts), not HBM: the walk's "
+                                     "gathers hit L2/L1 (DRAM traffic per launch is "
+                                     "`traffic`), so `frac` (algorithmic bytes / HBM peak, "
+                                     "SURVEY §8d) can exceed 1",
+                     "binding_frac": binding_frac,
+                     "traffic_source": traffic_src,
                      "gather_ceilings": gather_ceilings()},
         "cpu_baseline": cpu,
-        "clocks": clocks,
+        "clocks": clocks if clocks is not None else (fb or {}).get("clocks"),
     }
     print(json.dumps(out), flush=True)
     if dist_on:
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        print("[bench] PARITY FAILED: " + json.dumps(parity), file=sys.stderr, flush=True)
+        sys.exit(3)
 
 
 if __name__ == "__main__":

@@ -71,7 +71,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 9
+#define RFB_ABI_VERSION 10
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
@@ -105,6 +105,9 @@ typedef struct rfb_scene {
                                  fp32 copies are rounded, the pre-filter bound is widened
                                  (n1max) and the exact phase reads site4 */
     double background[3];     /* (host value) */
+    const float *sh_absmax_dev; /* nullable device scalar; when set the kernels read the colour
+                                 bound from it instead of sh_absmax (rfb_post_grad_adam raises it
+                                 after every update, so a training scene needs no host refresh) */
 } rfb_scene;
 
 /* Walk parameters (tracer/rays.py:12-14). */
@@ -112,9 +115,11 @@ typedef struct rfb_params {
     double epsilon;       /* early-termination transmittance, 0 disables */
     double width_floor;   /* WIDTH_FLOOR_SCALE * diagonal */
     int32_t step_limit;   /* hard per-ray cell cap */
-    int32_t lanes_per_ray;/* 1, 2, 4, 8, 16 or 32 lanes cooperate on one ray (forward
-                             only); 0 = auto: the largest power of two <= 8 whose lanes x rays
-                             fit the resident threads (small batches use more lanes) */
+    int32_t lanes_per_ray;/* forward: 1, 2, 4, 8, 16 or 32 lanes cooperate on one ray;
+                             0 = auto: the largest power of two <= 8 whose lanes x rays fit
+                             the resident threads (small batches use more lanes).
+                             backward / training: 1 or 2; 0 = auto (2 when the batch fills
+                             at most half the resident threads) */
 } rfb_params;
 
 /* A batch of rays (render.py:57-125 arguments). */
@@ -141,9 +146,11 @@ typedef struct rfb_fwd_out {
     unsigned long long *counters; /* [2] nullable: totals, ACCUMULATED (kernels.py:8-9) */
     int32_t f64_outputs;
     int32_t seg_capacity;      /* > 0 enables the segment dump below */
-    int32_t *seg_cells;        /* [m][seg_capacity] */
-    double *seg_t0;            /* [m][seg_capacity] */
-    double *seg_t1;            /* [m][seg_capacity] */
+    int32_t *seg_cells;        /* [seg rows][seg_capacity] */
+    double *seg_t0;            /* [seg rows][seg_capacity] */
+    double *seg_t1;            /* [seg rows][seg_capacity] */
+    int64_t seg_first;         /* the dump holds rays seg_first .. seg_first + seg_count - 1 */
+    int64_t seg_count;         /* (row r of the dump = ray seg_first + r); 0 = every ray */
 } rfb_fwd_out;
 
 /* Gradient accumulators (ACCUMULATED, like the reference's += buffers).
@@ -203,11 +210,14 @@ int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void 
  * densities and SH.  sh_warmup zeroes the SH bands 1..15 gradient;
  * update_positions = 0 skips positions (lr_pos == 0 tail).  sh32 (nullable):
  * the packed scene's fp32 channel-major SH copy (rfb_scene.sh32), rewritten
- * from the updated coefficients in the same pass. */
+ * from the updated coefficients in the same pass.  sh_absmax_dev (nullable):
+ * the scene's device colour bound (rfb_scene.sh_absmax_dev), raised to at
+ * least max |sh| of the updated coefficients (a running maximum: never
+ * lowered, so it stays an upper bound of every coefficient). */
 int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positions,
                        double *raw_density, double *sh, double *adam_state, double clip,
                        int32_t sh_warmup, int32_t update_positions, const double *hyper,
-                       float *sh32, void *stream);
+                       float *sh32, float *sh_absmax_dev, void *stream);
 
 /* After a parameter update: site4 = {positions, softplus(raw)}, packed
  * headers' sigma and, when refresh_sh32 is nonzero, the fp32 SH copy are

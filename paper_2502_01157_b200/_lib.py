@@ -13,6 +13,7 @@ import threading
 
 from .errors import DeviceError, ExtensionMissing
 
+ABI_VERSION = 10  # include/rfb.h RFB_ABI_VERSION
 _lock = threading.Lock()
 _lib = None
 
@@ -36,6 +37,7 @@ class rfb_scene(ctypes.Structure):
         ("sh_degree", ctypes.c_int32),
         ("positions_f64", ctypes.c_int32),
         ("background", ctypes.c_double * 3),
+        ("sh_absmax_dev", ctypes.c_void_p),
     ]
 
 
@@ -74,6 +76,8 @@ class rfb_fwd_out(ctypes.Structure):
         ("seg_cells", ctypes.c_void_p),
         ("seg_t0", ctypes.c_void_p),
         ("seg_t1", ctypes.c_void_p),
+        ("seg_first", ctypes.c_int64),
+        ("seg_count", ctypes.c_int64),
     ]
 
 
@@ -121,7 +125,7 @@ SIGNATURES = {
                                       I32, VP]),
     "rfb_softplus": (ctypes.c_int, [VP, I64, VP, VP, VP, VP]),
     "rfb_camera_rays": (ctypes.c_int, [P(rfb_camera), I64, I64, VP, VP]),
-    "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP, VP]),
+    "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP, VP, VP]),
     "rfb_refresh_scene": (ctypes.c_int, [P(rfb_scene), VP, VP, I32, VP]),
     "rfb_locate": (ctypes.c_int, [P(rfb_scene), VP, I64, I32, VP, VP]),
     "rfb_build_locate_grid": (ctypes.c_int, [P(rfb_scene), P(rfb_locate_grid), VP]),
@@ -178,7 +182,7 @@ def load(path: str | None = None):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.rfb_abi_version() != 9:
+        if lib.rfb_abi_version() != ABI_VERSION:
             raise ExtensionMissing("librfb.so ABI version mismatch; rebuild")
         if path is None:
             _lib = lib

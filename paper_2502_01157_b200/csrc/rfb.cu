@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 #include <cmath>
 #include <cstdint>
@@ -137,6 +138,7 @@ struct FwdOut {
     int32_t seg_cap;
     int32_t *seg_cells;
     double *seg_t0, *seg_t1;
+    int64_t seg_first, seg_count;  // dump row = ray - seg_first, for rays in [first, first+count)
 };
 
 __device__ __forceinline__ void store_out(void *p, int64_t idx, double v, int32_t f64) {
@@ -291,7 +293,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
         RayS r;
         r.p = s_ray + threadIdx.x;
         if constexpr (Src::kUniform) r.u = s_uni;
-        double *bsum_p = s_ray + (kRayFields - 1) * 256 + threadIdx.x;
+        double *tol_p = s_ray + (kRayFields - 1) * 256 + threadIdx.x;  // color_tol
         {
             Ray rr;
             oidx = src.get(q, rr);
@@ -300,11 +302,11 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
             r.store(rr);
             if (SHDEG > 0) {
                 float bf[16];
-                *bsum_p = basis_setup(rr, bf);
+                *tol_p = color_tol(S, basis_setup(rr, bf));
 #pragma unroll
                 for (int k = 1; k < 16; ++k) s_basis[(k - 1) * 256 + threadIdx.x] = bf[k];
             } else {
-                *bsum_p = kC0;
+                *tol_p = color_tol(S, kC0);
             }
         }
         // colour accumulation in fp32 (image tolerance 1e-4); transmittance and
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 double delta = t1 - t0;
                 const double alpha = (double)(-expm1f(-(float)(sigma * delta)));
                 double col[3];
-                cell_color<SHDEG, PACKED, 256, 1>(S, cell, s_basis + threadIdx.x, r, *bsum_p, col);
+                cell_color<SHDEG, PACKED, 256, 1>(S, cell, s_basis + threadIdx.x, r, *tol_p, col);
                 const double w = T * alpha;
                 wsum += w;
                 const float wf = (float)w;
@@ -328,8 +330,9 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 cg += wf * (float)col[1];
                 cb += wf * (float)col[2];
                 T *= 1.0 - alpha;
-                if (dump && s < O.seg_cap && gl == 0) {
-                    int64_t o = oidx * O.seg_cap + s;
+                if (dump && s < O.seg_cap && gl == 0 &&
+                    (uint64_t)(oidx - O.seg_first) < (uint64_t)O.seg_count) {
+                    int64_t o = (oidx - O.seg_first) * O.seg_cap + s;
                     O.seg_cells[o] = cell;
                     O.seg_t0[o] = t0;
                     O.seg_t1[o] = t1;
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
         float cr = 0.f, cg = 0.f, cb = 0.f;
         int32_t cells = 0, visits = 0;
         if (have_ray) {
-            double cbsum;
+            double ctol;
             int32_t start;
             {
                 Ray rr;
@@ -564,7 +567,7 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 r.store(rr);
                 start = rr.start_;
                 double bsum = basis_setup(rr, bas);
-                cbsum = SHDEG > 0 ? bsum : kC0;
+                ctol = color_tol(S, SHDEG > 0 ? bsum : kC0);
             }
             status = walk<G, PACKED>(
                 S, r, start, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells,
@@ -572,7 +575,7 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 [&](int32_t s, int32_t cell, double sigma, double t0, double t1) {
                     const double e = exp(-sigma * (t1 - t0));
                     double col[3];
-                    const int mask = cell_color<SHDEG, PACKED>(S, cell, bas, r, cbsum, col);
+                    const int mask = cell_color<SHDEG, PACKED>(S, cell, bas, r, ctol, col);
                     const double Tn = Tb * e;  // T_before[s+1] (kernels.py:275)
                     const double w = Tb - Tn;  // T_before[s] * alpha
                     wsum += w;
@@ -1256,7 +1259,7 @@ __global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double
                             double *raw, double *sh, double *m_pos, double *v_pos, double *m_raw,
                             double *v_raw, double *m_sh, double *v_sh, double clip, int sh_warmup,
                             int update_pos, AdamArgs a_pos, AdamArgs a_raw, AdamArgs a_sh,
-                            float *sh32) {
+                            float *sh32, unsigned *absmax_bits) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n * 52) return;
     if (t < n * 48) {  // SH coefficient t = i*48 + k*3 + ch
@@ -1267,6 +1270,12 @@ __global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double
         // the walk's fp32 channel-major copy (k_refresh_sh32's layout), written
         // here so the refresh does not re-read the fp64 rows
         if (sh32) sh32[t - r + (r % 3) * 16 + r / 3] = (float)sh[t];
+        if (absmax_bits) {  // running max |sh| (non-negative floats order like their bits)
+            const unsigned bits = __float_as_uint(__double2float_ru(fabs(sh[t])));
+            const unsigned am = __activemask();
+            const unsigned mx = __reduce_max_sync(am, bits);
+            if ((int)(threadIdx.x & 31) == __ffs(am) - 1) atomicMax(absmax_bits, mx);
+        }
         return;
     }
     const int64_t u = t - n * 48;
@@ -1342,6 +1351,7 @@ static SceneView<PACKED> view(const rfb_scene *s) {
     v.sh32 = s->sh32;
     v.sh = s->sh;
     v.sh_absmax = s->sh_absmax;
+    v.absmax_p = s->sh_absmax_dev;
     v.bg[0] = s->background[0];
     v.bg[1] = s->background[1];
     v.bg[2] = s->background[2];
@@ -1368,6 +1378,8 @@ static FwdOut dev_out(const rfb_fwd_out *o) {
     d.seg_cells = o->seg_cells;
     d.seg_t0 = o->seg_t0;
     d.seg_t1 = o->seg_t1;
+    d.seg_first = o->seg_count > 0 ? o->seg_first : 0;
+    d.seg_count = o->seg_count > 0 ? o->seg_count : INT64_MAX;
     return d;
 }
 
@@ -1384,7 +1396,9 @@ static bool scene_ok(const rfb_scene *s) {
 
 static bool out_ok(const rfb_fwd_out *o) {
     if (!o || !o->rgb) return false;
-    if (o->seg_capacity > 0 && (!o->seg_cells || !o->seg_t0 || !o->seg_t1)) return false;
+    if (o->seg_capacity > 0 && (!o->seg_cells || !o->seg_t0 || !o->seg_t1 || o->seg_first < 0 ||
+                                o->seg_count < 0))
+        return false;
     return true;
 }
 
@@ -1397,9 +1411,16 @@ static bool out_ok(const rfb_fwd_out *o) {
 // RFB_CARVEOUT (percent of the 228 KB maximum; -1 = driver default) overrides.
 template <auto K>
 static void prefer_carveout() {
-    static bool done = false;  // once per kernel instantiation
-    if (done) return;
-    done = true;
+    // once per kernel instantiation and device (the attribute is per device;
+    // concurrent host threads: the first to set the bit does the work)
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return;
+    }
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done.fetch_or(bit) & bit) return;
     int blocks = 0;  // what the registers allow, before any preference
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, K, 256, 0) != cudaSuccess) {
         (void)cudaGetLastError();
@@ -1563,7 +1584,8 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     if (!ws || ws_bytes < 256 + (size_t)per * kTrainBlock) return RFB_EINVAL;
     int64_t slots = (int64_t)((ws_bytes - 256) / (size_t)per);
     const bool quant = train && q_scale > 0.0;
-    const int lanes = train_lanes(rays->m, quant);
+    if (p->lanes_per_ray < 0 || p->lanes_per_ray > 2) return RFB_EINVAL;
+    const int lanes = p->lanes_per_ray > 0 ? p->lanes_per_ray : train_lanes(rays->m, quant);
     slots = std::min<int64_t>(slots, bwd_slots_max(quant));
     slots = std::min<int64_t>(slots,
                               ((lanes * rays->m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
@@ -1681,7 +1703,7 @@ int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void 
 int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positions,
                        double *raw_density, double *sh, double *adam_state, double clip,
                        int32_t sh_warmup, int32_t update_positions, const double *hyper,
-                       float *sh32, void *stream) {
+                       float *sh32, float *sh_absmax_dev, void *stream) {
     if (n_sites <= 0 || !grads_flat || !positions || !raw_density || !sh || !adam_state ||
         !hyper || !(clip > 0.0))
         return RFB_EINVAL;
@@ -1696,7 +1718,8 @@ int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positio
     const int64_t total = n * 52;
     k_post_adam<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         n, grads_flat, grads_flat + 4 * n, positions, raw_density, sh, m_pos, v_pos, m_raw, v_raw,
-        m_sh, v_sh, clip, sh_warmup, update_positions, a[0], a[1], a[2], sh32);
+        m_sh, v_sh, clip, sh_warmup, update_positions, a[0], a[1], a[2], sh32,
+        reinterpret_cast<unsigned *>(sh_absmax_dev));
     return (int)cudaGetLastError();
 }
 

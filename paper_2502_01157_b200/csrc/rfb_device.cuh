@@ -134,6 +134,7 @@ struct SceneView {
     const float *sh32;      // [n][3][16] fp32, channel-major (PACKED) -- exact fallback below
     const double *sh;       // [n][48] fp64 (reference values)
     float sh_absmax;        // max |sh coefficient| over the scene (colour rounding bound)
+    const float *absmax_p;  // nullable device copy of the bound (training: raised by Adam)
     double bg[3];
     int64_t n_sites, n_edges;  // extents (RFB_CHECK builds assert every index against them)
 
@@ -221,16 +222,26 @@ static __device__ __noinline__ double exact_channel(const double *row, int ch, i
     return a;
 }
 
-// basis_f: the ray's fp32 SH basis (BSTRIDE apart); bsum = sum |fp64 basis|.
+// Clamp-ambiguity tolerance of one ray for cell_color: (max|c| sum|basis| + 1) 2^-19,
+// bsum = sum |fp64 basis| of the ray.  Evaluated once per ray (the bound is read from
+// the device copy when the scene has one, so Adam steps that grow a coefficient
+// never leave the fp32 colour with a stale bound).
+template <int PACKED>
+__device__ __forceinline__ double color_tol(const SceneView<PACKED> &S, double bsum) {
+    if (!PACKED) return 0.0;
+    const float cmax = S.absmax_p ? __ldg(S.absmax_p) : S.sh_absmax;
+    return ((double)cmax * bsum + 1.0) * 0x1p-19;
+}
+
+// basis_f: the ray's fp32 SH basis (BSTRIDE apart); tol = color_tol(S, sum |fp64 basis|).
 // SKIP0: basis_f holds k = 1..15 only (k = 0 is the direction-independent
 // constant kC0, sh.py:17), which keeps k_render's shared memory per block
 // under the 100 KB carveout step at 4 blocks per SM.
 template <int SHDEG, int PACKED, int BSTRIDE = 1, int SKIP0 = 0, class RayT>
 __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
                                           const float *basis_f, const RayT &ray,
-                                          double bsum, double *col) {
+                                          double tol, double *col) {
     RFB_BOUND(i, S.n_sites);
-    const float cmax = S.sh_absmax;
     constexpr int NB = SHDEG == 0 ? 1 : 16;
     double acc[3] = {0.5, 0.5, 0.5};
     auto bk = [&](int k) -> float {
@@ -281,8 +292,6 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch) acc[ch] += basis[k] * __ldg(row + k * 3 + ch);
     }
-    const double tol =
-        PACKED ? ((double)cmax * bsum + 1.0) * 0x1p-19 : 0.0;
     int mask = 0;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {

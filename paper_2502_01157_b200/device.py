@@ -63,16 +63,18 @@ class DeviceScene:
 
     @classmethod
     def from_arrays(cls, positions, offsets, neighbors, sigma, sh_flat, background, device=None,
-                    sh_degree=None, packed=None, positions_f64=None):
-        """Flat kernel arrays as passed to kernels.render_rays (kernels.py:199-209)."""
+                    sh_degree=None, packed=None, positions_f64=None, keep_csr64=False):
+        """Flat kernel arrays as passed to kernels.render_rays (kernels.py:199-209).
+        ``keep_csr64`` keeps the int64 device CSR for ``update_params``."""
         self = cls.__new__(cls)
         pos = np.asarray(positions, dtype=np.float64)
         self._init(pos, offsets, neighbors, sigma, sh_flat, background, pos.min(axis=0),
-                   pos.max(axis=0), device, sh_degree, packed, positions_f64)
+                   pos.max(axis=0), device, sh_degree, packed, positions_f64, keep_csr64)
         return self
 
     def _init(self, positions, offsets, neighbors, sigma, sh_flat, background, bbox_lo, bbox_hi,
-              device, sh_degree, packed, positions_f64=None):
+              device, sh_degree, packed, positions_f64=None, keep_csr64=False):
+        self._sh_degree_arg = sh_degree
         self.lib = _lib.load()
         self.device = torch.device(device or "cuda")
         pos = np.ascontiguousarray(positions, dtype=np.float64)
@@ -102,6 +104,9 @@ class DeviceScene:
             self.offsets = torch.empty(n + 1, dtype=torch.int32, device=dev)
             self.neighbors = torch.empty(max(self.n_edges, 1), dtype=torch.int32, device=dev)
             self.sh = torch.from_numpy(sh).to(dev)
+            # device copy of the colour bound: rfb_post_grad_adam raises it when a
+            # training step grows a coefficient (the kernels read this copy)
+            self.sh_absmax_dev = torch.tensor([self.sh_absmax], dtype=torch.float32, device=dev)
             if self.packed:
                 self.cells = torch.empty((n, 8), dtype=torch.int32, device=dev)      # 32 B headers
                 # 16 B records + one readable pad record (the walk loads aligned pairs)
@@ -121,7 +126,53 @@ class DeviceScene:
                 1 if self.positions_f64 else 0, _stream()),
                 "rfb_pack_scene")
             torch.cuda.current_stream().synchronize()
+            self._csr64 = (off_d, nbr_d) if keep_csr64 else None
         self._c = _lib.rfb_scene()
+        self._refresh_struct()
+        self._build_locate_grid()
+
+    def update_params(self, positions, sigma, sh_flat, background=None):
+        """Re-derive the kernel arrays for new parameter values on the SAME
+        adjacency (the reference re-reads scene_arrays on every call and its
+        training loop moves sites / updates sigma and SH in place between
+        rebuilds, foam.py:70-80): upload positions, sigma and SH and re-pack
+        on the device, reusing the device CSR (needs ``keep_csr64``)."""
+        if self._csr64 is None:
+            raise RuntimeError("update_params needs a DeviceScene built with keep_csr64=True")
+        off_d, nbr_d = self._csr64
+        pos = np.ascontiguousarray(positions, dtype=np.float64)
+        n = self.n_sites
+        if pos.shape != (n, 3):
+            raise ValueError("positions shape changed: build a new DeviceScene")
+        sh = None if sh_flat is None else \
+            np.ascontiguousarray(np.asarray(sh_flat, dtype=np.float64).reshape(n, 48))
+        sigma = np.ascontiguousarray(sigma, dtype=np.float64)
+        self.bbox_lo, self.bbox_hi = pos.min(axis=0), pos.max(axis=0)
+        self.diagonal = float(np.linalg.norm(self.bbox_hi - self.bbox_lo))
+        self.center = 0.5 * (self.bbox_lo + self.bbox_hi)
+        self.width_floor = WIDTH_FLOOR_SCALE * self.diagonal
+        if background is not None:
+            self.background = np.asarray(background, dtype=np.float64).copy()
+        if sh is not None:  # None: colours unused by the caller (walk only)
+            if self._sh_degree_arg is None:
+                self.sh_degree = sh_degree_of(sh)
+            self.sh_absmax = float(np.float32(np.abs(sh).max() if sh.size else 0.0)
+                                   * np.float32(1.0001))
+        if not self.positions_f64:
+            self.positions_f64 = not bool(np.array_equal(pos.astype(np.float32).astype(np.float64),
+                                                         pos))
+        dev = self.device
+        with torch.cuda.device(dev):
+            if sh is not None:
+                self.sh.copy_(torch.from_numpy(sh))
+                self.sh_absmax_dev.fill_(self.sh_absmax)
+            pos_d = torch.from_numpy(pos).to(dev)
+            sig_d = torch.from_numpy(sigma).to(dev)
+            _lib.check(self.lib.rfb_pack_scene(
+                _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
+                self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
+                _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_meta), _ptr(self.sh32),
+                1 if self.positions_f64 else 0, _stream()), "rfb_pack_scene")
         self._refresh_struct()
         self._build_locate_grid()
 
@@ -158,6 +209,7 @@ class DeviceScene:
         c.packed = 1 if self.packed else 0
         c.positions_f64 = 1 if (self.packed and self.positions_f64) else 0
         c.sh_absmax = self.sh_absmax
+        c.sh_absmax_dev = self.sh_absmax_dev.data_ptr()
         c.sh_degree = self.sh_degree
         for k in range(3):
             c.background[k] = float(self.background[k])
@@ -303,6 +355,7 @@ class ForwardResult:
     seg_cells: torch.Tensor | None = None
     seg_t0: torch.Tensor | None = None
     seg_t1: torch.Tensor | None = None
+    seg_first: int = 0
 
 
 class Workspace:
@@ -319,7 +372,10 @@ class Workspace:
         return self.buf
 
 
-def alloc_forward(m: int, device, f64=False, per_ray=True, seg_capacity=0) -> ForwardResult:
+def alloc_forward(m: int, device, f64=False, per_ray=True, seg_capacity=0,
+                  seg_rays=None) -> ForwardResult:
+    """``seg_rays``: (first, count) -- dump the segments of rays first ..
+    first + count - 1 only (rfb_fwd_out.seg_first / seg_count); default all m."""
     fdt = torch.float64 if f64 else torch.float32
     r = ForwardResult(
         rgb=torch.empty((m, 3), dtype=fdt, device=device),
@@ -332,9 +388,11 @@ def alloc_forward(m: int, device, f64=False, per_ray=True, seg_capacity=0) -> Fo
         r.nseg = torch.empty(m, dtype=torch.int32, device=device)
         r.ray_counters = torch.empty((m, 2), dtype=torch.int32, device=device)
     if seg_capacity > 0:
-        r.seg_cells = torch.full((m, seg_capacity), -1, dtype=torch.int32, device=device)
-        r.seg_t0 = torch.zeros((m, seg_capacity), dtype=torch.float64, device=device)
-        r.seg_t1 = torch.zeros((m, seg_capacity), dtype=torch.float64, device=device)
+        rows = m if seg_rays is None else int(seg_rays[1])
+        r.seg_cells = torch.full((rows, seg_capacity), -1, dtype=torch.int32, device=device)
+        r.seg_t0 = torch.zeros((rows, seg_capacity), dtype=torch.float64, device=device)
+        r.seg_t1 = torch.zeros((rows, seg_capacity), dtype=torch.float64, device=device)
+        r.seg_first = 0 if seg_rays is None else int(seg_rays[0])
     return r
 
 
@@ -353,6 +411,8 @@ def fwd_struct(r: ForwardResult) -> _lib.rfb_fwd_out:
         o.seg_cells = r.seg_cells.data_ptr()
         o.seg_t0 = r.seg_t0.data_ptr()
         o.seg_t1 = r.seg_t1.data_ptr()
+        o.seg_first = int(r.seg_first)
+        o.seg_count = r.seg_cells.shape[0]
     else:
         o.seg_capacity = 0
     return o
@@ -507,12 +567,13 @@ def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, sta
                          grads: GradBuffers, *, epsilon=DEFAULT_EPSILON,
                          step_limit=DEFAULT_STEP_LIMIT, f64=False,
                          workspace: Workspace | None = None, out: ForwardResult | None = None,
-                         order="auto", stream=None) -> ForwardResult:
-    """rfb_backward_rays (render.py:152-221 generic adjoint).  ``order``: see _order32."""
+                         order="auto", lanes_per_ray=0, stream=None) -> ForwardResult:
+    """rfb_backward_rays (render.py:152-221 generic adjoint).  ``order``: see _order32;
+    ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
-    p = make_params(epsilon, ds.width_floor, step_limit, 1)
+    p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
     order = _order32(order, m, ds.device, origins, directions)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)
@@ -529,13 +590,14 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        quantile_scale: float = 0.0, u_pairs=None, weight_floor: float = 1e-4,
                        epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
-                       order="auto", stream=None) -> ForwardResult:
+                       order="auto", lanes_per_ray=0, stream=None) -> ForwardResult:
     """rfb_train_batch (kernels.py:372-453).  ``loss`` float64 [2] accumulates.
-    ``order``: "auto" sorts batches of >= 500k rays coherently (see _order32)."""
+    ``order``: "auto" sorts batches of >= 500k rays coherently (see _order32);
+    ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
-    p = make_params(epsilon, ds.width_floor, step_limit, 1)
+    p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
     order = _order32(order, m, ds.device, origins, directions)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)

@@ -60,7 +60,9 @@ def assemble_frame(local_frame: torch.Tensor, dst: int | None = 0, group=None) -
     _, ws = world()
     if ws == 1:
         return local_frame
-    if dst is None:
+    # gloo reduces device tensors only through all-reduce (its reduce is host-only)
+    gloo_dev = local_frame.is_cuda and dist.get_backend(group) == "gloo"
+    if dst is None or gloo_dev:
         dist.all_reduce(local_frame, op=dist.ReduceOp.SUM, group=group)
     else:
         dist.reduce(local_frame, dst=dst, op=dist.ReduceOp.SUM, group=group)
@@ -102,10 +104,11 @@ class ShardedRenderer:
         self.tiles = torch.from_numpy(tiles).to(device_scene.device)
         self.lanes = lanes_per_ray or dv.DEFAULT_LANES
         self.ws = dv.Workspace(device_scene.device)
-        self.out = dv.alloc_forward(width * height, device_scene.device, per_ray=False)
+        # fp64 frame: the reference's render_image contract (render.py:128-149)
+        self.out = dv.alloc_forward(width * height, device_scene.device, f64=True, per_ray=False)
 
     def render(self, camera, epsilon=1e-3, step_limit=4096, dst: int | None = 0):
-        """Render this rank's tiles and assemble the (H*W, 3) float32 frame on
+        """Render this rank's tiles and assemble the (H*W, 3) float64 frame on
         ``dst`` (None: everywhere)."""
         if self.world > 1:
             self.out.rgb.zero_()
@@ -117,7 +120,8 @@ class ShardedRenderer:
     def render_to_host(self, camera, epsilon=1e-3, step_limit=4096, dst: int = 0):
         """render() plus the device->host copy of the assembled frame on ``dst`` into a
         pinned buffer (two alternate, so the previous frame stays valid for one more call).
-        Returns the (H*W, 3) float32 host frame on ``dst`` and None elsewhere."""
+        Returns the (H, W, 3) float64 numpy image on ``dst`` -- render_image's contract
+        (render.py:128-149) -- and None elsewhere."""
         frame = self.render(camera, epsilon=epsilon, step_limit=step_limit, dst=dst)
         if self.rank != dst:
             return None
@@ -129,4 +133,4 @@ class ShardedRenderer:
         self._next ^= 1
         host.copy_(frame, non_blocking=True)
         torch.cuda.current_stream(frame.device).synchronize()
-        return host
+        return host.numpy().reshape(self.height, self.width, 3)

@@ -21,6 +21,8 @@ are accepted and ignored (device scratch is internal).  Gradients accumulate
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import torch
 
@@ -35,9 +37,33 @@ def _dev(a, dtype=torch.float64):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dtype)
 
 
-def _scene(positions, offsets, neighbors, sigma, sh, background):
-    return dv.DeviceScene.from_arrays(positions, offsets, neighbors, sigma,
-                                      np.asarray(sh).reshape(len(positions), 48), background)
+# One cached device scene per adjacency: the reference's callers pass the same
+# CSR arrays on every call between rebuilds (train.py:174-188 reads
+# adj.offsets / adj.neighbors) while positions, sigma and SH change, so the
+# CSR stays on the device and only the parameters are re-uploaded and
+# re-packed (DeviceScene.update_params).  Keyed on the CSR arrays' identity,
+# address and shape, with references held so an id cannot be reused.
+_SCENE_CACHE: dict = {}
+
+
+def _scene(positions, offsets, neighbors, sigma, sh, background, slot="shade"):
+    """slot "shade": full scene; "walk": geometry only (SH never uploaded again)."""
+    n = len(positions)
+    offsets = np.asarray(offsets)
+    neighbors = np.asarray(neighbors)
+    key = (id(offsets), id(neighbors), n, len(neighbors), offsets.ctypes.data,
+           neighbors.ctypes.data, int(offsets[-1]) if n else 0)
+    hit = _SCENE_CACHE.get(slot)
+    if hit is not None and hit[0] == key and hit[1] is offsets and hit[2] is neighbors:
+        ds = hit[3]
+        ds.update_params(positions, sigma,
+                         None if slot == "walk" else np.asarray(sh).reshape(n, 48), background)
+        return ds
+    sh = np.zeros((n, 48)) if slot == "walk" else np.asarray(sh).reshape(n, 48)
+    ds = dv.DeviceScene.from_arrays(positions, offsets, neighbors, sigma, sh, background,
+                                    keep_csr64=True)
+    _SCENE_CACHE[slot] = (key, offsets, neighbors, ds)
+    return ds
 
 
 def render_rays(positions, offsets, neighbors, sigma, sh, background, origins, directions,
@@ -67,8 +93,7 @@ def walk_ray(positions, offsets, neighbors, sigma, ox, oy, oz, dx, dy, dz, t_min
              start_site, epsilon, step_limit, width_floor, seg_cells, seg_t0, seg_t1, counters,
              worker):
     """kernels.py:76-162 for one ray: fills seg_* and returns (nseg, status, residual)."""
-    n = len(positions)
-    ds = _scene(positions, offsets, neighbors, sigma, np.zeros((n, 48)), np.zeros(3))
+    ds = _scene(positions, offsets, neighbors, sigma, None, np.zeros(3), slot="walk")
     ds.width_floor = float(width_floor)
     cap = int(step_limit)
     res = dv.render_rays_device(ds, _dev([[ox, oy, oz]]), _dev([[dx, dy, dz]]), _dev([t_min]),
@@ -82,10 +107,10 @@ def walk_ray(positions, offsets, neighbors, sigma, ox, oy, oz, dx, dy, dz, t_min
     rc = res.ray_counters.cpu().numpy()[0]
     counters[worker, 0] += int(rc[0])
     counters[worker, 1] += int(rc[1])
-    log_t = 0.0
-    for c, a, b in zip(seg_cells[:nseg], seg_t0[:nseg], seg_t1[:nseg]):
-        log_t -= sigma[c] * (b - a)
-    return nseg, int(res.status.item()), float(np.exp(log_t))
+    log_t = 0.0  # kernels.py:142 (libm exp, like numba's)
+    for c, a, b in zip(seg_cells[:nseg].tolist(), seg_t0[:nseg].tolist(), seg_t1[:nseg].tolist()):
+        log_t -= float(sigma[c]) * (b - a)
+    return nseg, int(res.status.item()), math.exp(log_t)
 
 
 def train_batch(positions, offsets, neighbors, sigma, sh, background, origins, directions, t_min,
@@ -111,10 +136,10 @@ def train_batch(positions, offsets, neighbors, sigma, sh, background, origins, d
     torch.cuda.synchronize()
     out_rgb[...] = res.rgb.cpu().numpy().reshape(out_rgb.shape)
     out_status[...] = res.status.cpu().numpy()
-    g4 = gb.g4.double().cpu().numpy()
+    g4 = gb.g4.cpu().numpy()  # fp32 over the bus, widened by the +=
     d_pos_w[0] += g4[:, :3]
     d_sigma_w[0] += g4[:, 3]
-    d_sh_w[0] += gb.sh.double().cpu().numpy().reshape(d_sh_w[0].shape)
+    d_sh_w[0] += gb.sh.cpu().numpy().reshape(d_sh_w[0].shape)
     loss_w[0] += loss.cpu().numpy()
     counters[0, :] += res.counters.cpu().numpy().astype(counters.dtype)
 

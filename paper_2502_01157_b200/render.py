@@ -19,6 +19,7 @@ kernel arrays on every call too, render.py:49-54).
 
 from __future__ import annotations
 
+import math
 import os
 import time
 import weakref
@@ -195,6 +196,29 @@ def _default_t_max(adj, ray):
     return float(np.linalg.norm(to_center) + 2.0 * adj.diagonal + 1.0)
 
 
+def _default_t_max_batch(adj, origins, directions):
+    """render.py:170-173 (``_default_t_max(adj, Ray(o_k, d_k))`` per ray) without the
+    per-ray Python loop: the same unit-direction validation as Ray (rays.py:29-31),
+    and the scalar expression evaluated once per distinct origin, so every value
+    has the reference's bits."""
+    m = len(origins)
+    if m == 0:
+        return np.zeros(0)
+    norms = np.linalg.norm(directions, axis=1)
+    bad = np.flatnonzero(np.abs(norms - 1.0) > 1e-6)
+    if len(bad):
+        raise ValueError(f"ray direction not unit length (|d| = {norms[bad[0]]:g})")
+    center = 0.5 * (adj.bbox_lo + adj.bbox_hi)
+
+    def one(o):
+        return float(np.linalg.norm(center - o) + 2.0 * adj.diagonal + 1.0)
+
+    if np.ptp(origins, axis=0).max() == 0.0:
+        return np.full(m, one(origins[0]))
+    uniq, inv = np.unique(origins, axis=0, return_inverse=True)
+    return np.array([one(u) for u in uniq])[inv.reshape(-1)]
+
+
 def _device_scene(scene, device_scene):
     if device_scene is not None:
         return device_scene
@@ -288,7 +312,10 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
     # to HBM and one D2H follows.  With PINNED_FRAMES buffers in use the frame
     # goes to fresh pageable memory instead (slower, but callers that keep
     # every frame never accumulate pinned memory).
-    pool = fc["h_rgb"]  # [pinned tensor, weakref to the array handed out, mapped address]
+    # [pinned tensor, weakref to the array handed out, mapped address]; shared by
+    # every scene on this device at this resolution (a fresh DeviceScene per call
+    # does not pay the page-locked allocation again)
+    pool = _PINNED_POOLS.setdefault((str(ds.device), W, H, ZERO_COPY_FRAMES), [])
     free = next((e for e in pool if e[1] is None or e[1]() is None), None)
     if free is None and len(pool) < PINNED_FRAMES:
         h = torch.empty((W * H, 3), dtype=torch.float64, pin_memory=True)
@@ -329,6 +356,9 @@ def render_image(scene, camera, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP
     return img
 
 
+_PINNED_POOLS: dict = {}
+
+
 def _frame_cache(ds, W, H, weight_check):
     """Per-(scene, resolution) device outputs, workspace and pinned host
     buffers, so the public render_image call does no allocation after the
@@ -340,8 +370,7 @@ def _frame_cache(ds, W, H, weight_check):
         tx, ty = dv.tile_grid(W, H)
         fc = {"ws": dv.Workspace(ds.device),
               "out": dv.alloc_forward(W * H, ds.device, f64=True, per_ray=False),
-              "tiles": torch.arange(tx * ty, dtype=torch.int32, device=ds.device),
-              "h_rgb": []}
+              "tiles": torch.arange(tx * ty, dtype=torch.int32, device=ds.device)}
         cache[key] = fc
     if weight_check and "h_wsum" not in fc:
         fc["h_wsum"] = torch.empty(W * H, dtype=torch.float64, pin_memory=True)
@@ -365,7 +394,7 @@ def render_rays_with_gradients(scene, origins, directions, adjoints, t_min=None,
         t_min = np.zeros(m)
     t_min = np.ascontiguousarray(t_min, dtype=np.float64)
     if t_max is None:
-        t_max = np.array([_default_t_max(adj, Ray(origins[k], directions[k])) for k in range(m)])
+        t_max = _default_t_max_batch(adj, origins, directions)
     t_max = np.ascontiguousarray(t_max, dtype=np.float64)
     o_d = _to_dev(origins.reshape(m, 3), np.float64, dev)
     d_d = _to_dev(directions.reshape(m, 3), np.float64, dev)
@@ -386,10 +415,10 @@ def render_rays_with_gradients(scene, origins, directions, adjoints, t_min=None,
                                   _to_dev(adjoints.reshape(m, 3), np.float64, dev), gb,
                                   epsilon=epsilon, step_limit=step_limit, f64=True)
     torch.cuda.synchronize(dev)
-    g4 = gb.g4.double().cpu().numpy()
-    dsh = gb.sh.double().cpu().numpy()
+    # fp32 accumulators come back as fp32 (half the bytes) and are widened by the +=
+    g4 = gb.g4.cpu().numpy()
     grad.d_position += g4[:, :3]
-    grad.d_sh += dsh.reshape(n, 16, 3)
+    grad.d_sh += gb.sh.cpu().numpy().reshape(n, 16, 3)
     grad.d_raw_density += g4[:, 3] * softplus_grad(scene.raw_density)
     return res.rgb.cpu().numpy(), grad
 
@@ -428,9 +457,10 @@ def trace(scene, ray, epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, st
     t0 = res.seg_t0[0, :nseg].cpu().numpy()
     t1 = res.seg_t1[0, :nseg].cpu().numpy()
     # walk_ray's residual is exp(log_T) (kernels.py:142); recompute it on the
-    # host from the recorded segments with the same accumulation order.
+    # host from the recorded segments with the same accumulation order (and
+    # libm's exp, like numba's, rather than numpy's vectorised one)
     sig = softplus(scene.raw_density)
     log_T = 0.0
-    for c, a, b in zip(cells, t0, t1):
-        log_T -= sig[c] * (b - a)
-    return RaySegments(cells, t0, t1, float(np.exp(log_T)), status)
+    for c, a, b in zip(cells.tolist(), t0.tolist(), t1.tolist()):
+        log_T -= float(sig[c]) * (b - a)
+    return RaySegments(cells, t0, t1, math.exp(log_T), status)

@@ -76,6 +76,23 @@ def delaunay_csr(positions: np.ndarray):
     return offsets, dst.astype(np.int64), hull
 
 
+# sha1 over (offsets, neighbors) as little-endian int32 of the Qhull CSR
+# (delaunay_csr) of the bench scenes, computed once on the CPU (84 s / 240 s)
+# and committed, so the device-built fixture CSR is checked against Qhull on
+# every run instead of against itself (csr_sha1; make_foam records the result)
+QHULL_CSR_SHA1 = {
+    "uniform_n1000000_s1": "956f47a22b7a5da4798c7956fb00c8dd3d1102f3",  # 15,496,358 edges
+    "surface_n3000000_s2": "1cfd72e7ab744694f23b19b27f8c5daf6adb039b",  # 46,434,024 edges
+}
+
+
+def csr_sha1(offsets: np.ndarray, neighbors: np.ndarray) -> str:
+    h = hashlib.sha1()
+    h.update(np.ascontiguousarray(offsets, dtype="<i4").tobytes())
+    h.update(np.ascontiguousarray(neighbors, dtype="<i4").tobytes())
+    return h.hexdigest()
+
+
 def _digest(a: np.ndarray) -> str:
     return hashlib.sha1(np.ascontiguousarray(a).view(np.uint8)).hexdigest()[:16]
 
@@ -96,12 +113,17 @@ def cached_adjacency(positions: np.ndarray, tag: str, cache_dir: str | None = No
     cache_dir = cache_dir or default_cache_dir()
     path = os.path.join(cache_dir, f"csr_{tag}.npz")
     digest = _digest(positions)
+    expect = QHULL_CSR_SHA1.get(tag)
     if os.path.exists(path):
         try:
             z = np.load(path)
-            if str(z["digest"]) == digest:
-                return AdjacencyGraph(positions, z["offsets"].astype(np.int64),
-                                      z["neighbors"].astype(np.int64), z["hull"])
+            if str(z["digest"]) == digest and (
+                    expect is None or csr_sha1(z["offsets"], z["neighbors"]) == expect):
+                adj = AdjacencyGraph(positions, z["offsets"].astype(np.int64),
+                                     z["neighbors"].astype(np.int64), z["hull"])
+                adj.provenance = {"builder": "cache", "qhull_sha1": expect,
+                                  "matches_qhull": True if expect else None}
+                return adj
         except Exception:  # corrupt cache: rebuild
             pass
     t0 = time.perf_counter()
@@ -118,8 +140,15 @@ def cached_adjacency(positions: np.ndarray, tag: str, cache_dir: str | None = No
         builder = "device (rfb_build_adjacency)"
     else:
         offsets, neighbors, hull = delaunay_csr(positions)
+    build_s = time.perf_counter() - t0
+    matches = None
+    if expect is not None:
+        matches = csr_sha1(offsets, neighbors) == expect
+        if not matches:
+            raise RuntimeError(f"{builder} CSR for {tag} differs from the committed Qhull digest")
     if verbose:
-        print(f"[synthetic] {builder} CSR for {tag}: {time.perf_counter() - t0:.1f}s", flush=True)
+        print(f"[synthetic] {builder} CSR for {tag}: {build_s:.1f}s"
+              + ("" if matches is None else " (== Qhull sha1)"), flush=True)
     try:
         os.makedirs(cache_dir, exist_ok=True)
         tmp = path + f".tmp{os.getpid()}.npz"
@@ -128,7 +157,10 @@ def cached_adjacency(positions: np.ndarray, tag: str, cache_dir: str | None = No
         os.replace(tmp, path)
     except OSError:
         pass
-    return AdjacencyGraph(positions, offsets, neighbors, hull)
+    adj = AdjacencyGraph(positions, offsets, neighbors, hull)
+    adj.provenance = {"builder": builder, "seconds": round(build_s, 2), "qhull_sha1": expect,
+                      "matches_qhull": matches}
+    return adj
 
 
 @dataclass

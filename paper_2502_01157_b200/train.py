@@ -54,7 +54,10 @@ class DeviceTrainer:
         self.update_positions = bool(update_positions)
         # moving sites: packed layout with the fp64-position bound from the start
         # (rfb_refresh_scene then re-derives the fp32 copies after every step)
-        self.ds = dv.DeviceScene(scene, device=device,
+        # SH degree pinned to 3: a scene initialised with the DC band only
+        # (train.py:77 scene_from_sfm) gains higher bands once the SH warm-up
+        # ends, so the walk must read all 16 bands from the start
+        self.ds = dv.DeviceScene(scene, device=device, sh_degree=3,
                                  positions_f64=True if update_positions else None)
         self.device = self.ds.device
         n = self.ds.n_sites
@@ -74,6 +77,11 @@ class DeviceTrainer:
     def post_grad_adam(self, lr_position, lr_density, lr_sh, sh_warmup, hyper: AdamHyper,
                        stream=None):
         do_pos = lr_position > 0.0
+        if do_pos and not self.update_positions:
+            # the packed fp32-exact layout cannot take moved sites in place
+            # (rfb_refresh_scene would leave the fp32 edge records stale)
+            raise ValueError("lr_position > 0 on a DeviceTrainer built with "
+                             "update_positions=False")
         lrs = (lr_position, lr_density, lr_sh)
         h = np.zeros(18)
         for k in range(3):
@@ -90,7 +98,8 @@ class DeviceTrainer:
             self.n, dv._ptr(self.grads.flat), dv._ptr(self.positions), dv._ptr(self.raw),
             dv._ptr(self.sh), dv._ptr(self.adam_state), float(hyper.grad_clip),
             1 if sh_warmup else 0, 1 if do_pos else 0,
-            hp.ctypes.data_as(ctypes.c_void_p), sh32, dv._stream(stream)), "rfb_post_grad_adam")
+            hp.ctypes.data_as(ctypes.c_void_p), sh32, dv._ptr(self.ds.sh_absmax_dev),
+            dv._stream(stream)), "rfb_post_grad_adam")
         _lib.check(self.lib.rfb_refresh_scene(self.ds.c, dv._ptr(self.positions),
                                               dv._ptr(self.raw), 0 if fuse else 1,
                                               dv._stream(stream)),

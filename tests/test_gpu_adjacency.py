@@ -109,3 +109,18 @@ def test_device_scene_rebuild_matches_host_build(cuda_ok):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
     assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= 1e-4
+
+
+@pytest.mark.parametrize("tag", ["uniform_n1000000_s1", "surface_n3000000_s2"])
+def test_bench_scene_csr_equals_committed_qhull_digest(cuda_ok, tag):
+    """The bench scenes (configs 2-5): the device-built CSR has the sha1 of the
+    Qhull CSR computed once on the CPU and committed (synthetic.QHULL_CSR_SHA1),
+    so the benchmark's fixture is tied to Qhull, not to the builder itself."""
+    from paper_2502_01157_b200 import adjacency as A
+    from paper_2502_01157_b200.synthetic import QHULL_CSR_SHA1, csr_sha1, random_positions
+
+    kind, n, seed = tag.split("_")
+    pos = random_positions(int(n[1:]), int(seed[1:]), kind)
+    off, nbr, hull, info = A.build_device(torch.from_numpy(pos).cuda())
+    assert csr_sha1(off.cpu().numpy(), nbr.cpu().numpy()) == QHULL_CSR_SHA1[tag]
+    assert info["reverse_edges_added"] == 0

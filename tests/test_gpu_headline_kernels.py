@@ -1,0 +1,184 @@
+"""Parity of the exact kernel instantiations the benchmark numbers come from.
+
+bench.py's headline lines run one lane per ray: k_render<1, 3, 1, TileRays>
+(config 2, rfb_render_image over 32x32 tiles) and k_train<3, 1, *, *, 1>
+(config 3, a full view in tile order).  The library's auto rules pick one
+lane only for batches larger than about half the resident threads
+(rfb.cu launch_render / train_lanes), so the small golden frames never
+reach them; here the frames are large enough for the auto rule AND the
+lane count is forced, on a 100k-site foam (Qhull CSR):
+
+* every ray's visited-cell sequence and segment depths bit-exact (per-ray
+  walk_digest of the device's segment dump == the C oracle's), counters,
+  nseg and status bit-exact, image / wsum / residual within 1e-4 abs;
+* training (L2 loss, quantile off and on) and the generic adjoint backward:
+  per-tensor gradients within 1e-3 relative (max|d - ref| / max|ref|), loss
+  within 1e-6 relative (reference: tracer/kernels.py:199-247, 250-453).
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as orc
+from oracle.walk_digest import digests
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4
+GRAD_RTOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def scene100k():
+    from paper_2502_01157_b200.synthetic import make_foam
+
+    return make_foam(100_000, 21, 3)
+
+
+@pytest.fixture(scope="module")
+def sa100k(scene100k):
+    from paper_2502_01157_b200.scene import softplus
+
+    adj = scene100k.adjacency
+    return orc.SceneArrays(adj.positions, adj.offsets, adj.neighbors,
+                           softplus(scene100k.raw_density), scene100k.sh_coeffs.reshape(-1, 48),
+                           scene100k.background)
+
+
+@pytest.fixture(scope="module")
+def ds100k(scene100k):
+    from paper_2502_01157_b200 import device as dv
+
+    return dv.DeviceScene(scene100k)
+
+
+def _cam(W, H, k=0):
+    from bench import make_views
+
+    return make_views(k + 1, W, H)[k]
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.abs(a - b).max() / np.abs(b).max())
+
+
+@pytest.mark.parametrize("view,eps", [(0, 1e-3), (2, 0.0)])
+def test_render_image_one_lane_per_ray(cuda_ok, scene100k, sa100k, ds100k, view, eps):
+    """k_render<1, 3, 1, TileRays> (the config-2 kernel) on a 480x270 frame."""
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = 480, 270
+    m = W * H
+    assert 2 * m > 148 * 4 * 256, "frame must be large enough for the auto rule to pick 1 lane"
+    cam = _cam(W, H, view)
+    first = dv.render_image_device(ds100k, cam, epsilon=eps, f64=True, per_ray=True,
+                                   lanes_per_ray=1)
+    torch.cuda.synchronize()
+    cap = int(first.nseg.max().item())
+    out = dv.alloc_forward(m, ds100k.device, f64=True, per_ray=True, seg_capacity=cap)
+    res = dv.render_image_device(ds100k, cam, epsilon=eps, lanes_per_ray=1, out=out)
+    auto = dv.render_image_device(ds100k, cam, epsilon=eps, f64=True, per_ray=True)
+    torch.cuda.synchronize()
+    assert torch.equal(auto.rgb, res.rgb) and torch.equal(auto.ray_counters, res.ray_counters)
+
+    dirs = cam.ray_directions()
+    o = cam.position
+    start = int(orc.nearest_sites(sa100k.positions, o[None, :])[0])
+    t_max = float(np.linalg.norm(o - sa100k.center) + 2.0 * sa100k.diagonal + 1.0)
+    ref = orc.render_rays(sa100k, np.broadcast_to(o, (m, 3)), dirs, 0.0, t_max, start,
+                          epsilon=eps, threads=os.cpu_count() or 8, digest=True)
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    np.testing.assert_array_equal(res.nseg.cpu().numpy(), ref["nseg"])
+    np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
+    np.testing.assert_array_equal(res.counters.cpu().numpy(), ref["counters"].sum(axis=0))
+    dig = digests(res.seg_cells, res.seg_t0, res.seg_t1, res.nseg)
+    bad = np.flatnonzero(dig != ref["digest"])
+    assert len(bad) == 0, f"{len(bad)} rays differ in cells/t0/t1, first {bad[:5]}"
+    assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= IMG_TOL
+    assert np.abs(res.wsum.cpu().numpy() - ref["wsum"]).max() <= IMG_TOL
+    assert np.abs(res.residual.cpu().numpy() - ref["residual"]).max() <= IMG_TOL
+
+
+def _view_batch(cam, ds, order_tiles=True):
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = cam.width, cam.height
+    dirs = cam.ray_directions()
+    m = len(dirs)
+    if order_tiles:  # the bench's config-3 schedule: rays in rfb_render_image's tile order
+        perm = dv.tile_order(W, H)
+        dirs = dirs[perm]
+    o = np.broadcast_to(cam.position, (m, 3)).copy()
+    start = int(ds.locate(torch.from_numpy(o[:1]).cuda()).item())
+    t_max = np.full(m, ds.default_t_max(cam.position[None, :]))
+    return o, dirs, start, t_max
+
+
+def _d(a, dt=torch.float64):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
+
+
+@pytest.mark.parametrize("quantile", [False, True])
+def test_train_batch_one_lane_full_view(cuda_ok, sa100k, ds100k, quantile):
+    """k_train<3, 1, true, Q, 1> (the config-3 kernel) on an 81,920-ray view in tile
+    order, against the oracle's train_batch (kernels.py:372-453)."""
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = 320, 256
+    cam = _cam(W, H, 1)
+    o, dirs, start, t_max = _view_batch(cam, ds100k)
+    m = len(dirs)
+    assert 2 * m > 148 * 7 * 128, "batch must be large enough for the auto rule to pick 1 lane"
+    rng = np.random.default_rng(11)
+    targets = rng.uniform(0.0, 1.0, (m, 3))
+    u = rng.uniform(0.0, 1.0, (m, 2, 2)) if quantile else None
+    qs = 0.01 / (m * 2) if quantile else 0.0
+    ref = orc.train_batch(sa100k, o, dirs, np.zeros(m), t_max, np.full(m, start), targets,
+                          1.0 / (3 * m), qs, u, 1e-4, n_workers=4,
+                          threads=os.cpu_count() or 8)
+    gb = dv.GradBuffers(ds100k.n_sites, ds100k.device)
+    loss = torch.zeros(2, dtype=torch.float64, device="cuda")
+    res = dv.train_batch_device(ds100k, _d(o), _d(dirs), _d(np.zeros(m)), _d(t_max),
+                                _d(np.full(m, start), torch.int32), _d(targets), gb, loss,
+                                rgb_scale=1.0 / (3 * m), quantile_scale=qs,
+                                u_pairs=_d(u) if quantile else None, f64=True, order=None,
+                                lanes_per_ray=1)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    np.testing.assert_array_equal(res.counters.cpu().numpy(), ref["counters"].sum(axis=0))
+    assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= IMG_TOL
+    g4 = gb.g4.double().cpu().numpy()
+    assert rel(g4[:, 3], ref["d_sigma_w"].sum(0)) <= GRAD_RTOL
+    assert rel(g4[:, :3], ref["d_pos_w"].sum(0)) <= GRAD_RTOL
+    assert rel(gb.sh.double().cpu().numpy(), ref["d_sh_w"].sum(0)) <= GRAD_RTOL
+    np.testing.assert_allclose(loss.cpu().numpy(), ref["loss_w"].sum(0), rtol=1e-6)
+
+
+def test_backward_rays_one_lane_full_view(cuda_ok, sa100k, ds100k):
+    """k_train<3, 1, false, false, 1> (generic adjoint, render.py:152-221) on an
+    81,920-ray view against the oracle's sequential render_rays_with_gradients."""
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = 320, 256
+    cam = _cam(W, H, 3)
+    o, dirs, start, t_max = _view_batch(cam, ds100k)
+    m = len(dirs)
+    adj = np.random.default_rng(5).normal(0.0, 1.0 / m, (m, 3))
+    rgb, status, ds_ref, dsh_ref, dp_ref, _ = orc.render_rays_with_gradients(
+        sa100k, o, dirs, adj, np.zeros(m), t_max, np.full(m, start))
+    gb = dv.GradBuffers(ds100k.n_sites, ds100k.device)
+    res = dv.backward_rays_device(ds100k, _d(o), _d(dirs), _d(np.zeros(m)), _d(t_max),
+                                  _d(np.full(m, start), torch.int32), _d(adj), gb, f64=True,
+                                  order=None, lanes_per_ray=1)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(res.status.cpu().numpy(), status)
+    assert np.abs(res.rgb.cpu().numpy() - rgb).max() <= IMG_TOL
+    g4 = gb.g4.double().cpu().numpy()
+    assert rel(g4[:, 3], ds_ref) <= GRAD_RTOL
+    assert rel(g4[:, :3], dp_ref) <= GRAD_RTOL
+    assert rel(gb.sh.double().cpu().numpy(), dsh_ref) <= GRAD_RTOL

@@ -453,7 +453,7 @@ def test_render_image_zero_copy_equals_copy_path(cuda_ok, monkeypatch):
         monkeypatch.setattr(rd, "ZERO_COPY_FRAMES", zc)
         ds = dv.DeviceScene(scene)
         frames[zc] = [rd.render_image(scene, c, device_scene=ds).copy() for c in cams]
-        pool = ds._frame_cache[(96, 64)]["h_rgb"]
+        pool = rd._PINNED_POOLS[(str(ds.device), 96, 64, zc)]
         assert all((e[2] is not None) == zc for e in pool)
     for a, b in zip(frames[True], frames[False]):
         np.testing.assert_array_equal(a, b)
@@ -461,3 +461,119 @@ def test_render_image_zero_copy_equals_copy_path(cuda_ok, monkeypatch):
     monkeypatch.setattr(rd, "ZERO_COPY_FRAMES", True)
     img = rd.render_image(scene, cam, epsilon=float(g["epsilon"]))
     assert np.abs(img - g["img"]).max() <= IMG_TOL
+
+
+@pytest.mark.parametrize("name", FRAMES)
+def test_trace_matches_reference_traces(cuda_ok, name):
+    """render.trace (rays.py:81-115) against the reference's own trace() outputs
+    (golden tr_*): cells, depths, status and counters bit-exact; the residual
+    is walk_ray's exp(log_T) (bit-exact against the oracle's walk)."""
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200 import render as R
+
+    g = load_golden(name)
+    sa, origins, dirs, start, t_max = frame_rays(g)
+    scene = golden_scene(g)
+    ds = dv.DeviceScene(scene)
+    eps = float(g["epsilon"])
+    off = 0
+    for k, q in enumerate(g["tr_idx"]):
+        L = int(g["tr_len"][k])
+        cnt = np.zeros((1, 2), dtype=np.int64)
+        segs = R.trace(scene, R.Ray(origins[q], dirs[q]), epsilon=eps, counters=cnt,
+                       device_scene=ds)
+        assert g["tr_status"][k] == 0 and segs.status == 0
+        np.testing.assert_array_equal(segs.cells, g["tr_cells"][off:off + L])
+        np.testing.assert_array_equal(segs.t_entry, g["tr_t0"][off:off + L])
+        np.testing.assert_array_equal(segs.t_exit, g["tr_t1"][off:off + L])
+        np.testing.assert_array_equal(cnt[0], g["tr_counters"][k])
+        _, _, _, _, resid, _ = orc.walk_ray(sa, origins[q], dirs[q], 0.0, t_max, start,
+                                            epsilon=eps)
+        assert segs.residual_transmittance == resid
+        off += L
+
+
+def test_trace_failure_codes(cuda_ok):
+    """trace() raises StepLimit / CycleDetected like rays.py:109-112."""
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200 import render as R
+    from paper_2502_01157_b200.errors import StepLimit
+
+    g = load_golden("frame_2k_deg3")
+    sa, origins, dirs, start, t_max = frame_rays(g)
+    scene = golden_scene(g)
+    ds = dv.DeviceScene(scene)
+    q = int(g["tr_idx"][0])
+    with pytest.raises(StepLimit):
+        R.trace(scene, R.Ray(origins[q], dirs[q]), step_limit=3, device_scene=ds)
+    # an explicit start cell and a finite t_max are honoured
+    segs = R.trace(scene, R.Ray(origins[q], dirs[q], 0.0, 2.5), start_site=start,
+                   device_scene=ds)
+    c, a, b, st, resid, _ = orc.walk_ray(sa, origins[q], dirs[q], 0.0, 2.5, start)
+    np.testing.assert_array_equal(segs.cells, c)
+    np.testing.assert_array_equal(segs.t_exit, b)
+    assert segs.residual_transmittance == resid
+
+
+def test_flat_walk_ray_drop_in(cuda_ok):
+    """kernels.walk_ray (kernels.py:76-162) with the reference's positional
+    signature: fills the caller's segment buffers, returns (nseg, status,
+    residual), counters[worker] +=, against the golden traces."""
+    from paper_2502_01157_b200 import kernels as K
+
+    g = load_golden("frame_3k_surface")
+    sa, origins, dirs, start, t_max = frame_rays(g)
+    eps = float(g["epsilon"])
+    cells = np.empty(4096, dtype=np.int64)
+    t0 = np.empty(4096)
+    t1 = np.empty(4096)
+    off = 0
+    for k, q in enumerate(g["tr_idx"][:24]):
+        L = int(g["tr_len"][k])
+        cnt = np.zeros((3, 2), dtype=np.int64)
+        nseg, status, resid = K.walk_ray(sa.positions, sa.offsets, sa.neighbors, sa.sigma,
+                                         *origins[q], *dirs[q], 0.0, t_max, start, eps, 4096,
+                                         sa.width_floor, cells, t0, t1, cnt, 2)
+        assert (nseg, status) == (L, int(g["tr_status"][k]))
+        np.testing.assert_array_equal(cells[:L], g["tr_cells"][off:off + L])
+        np.testing.assert_array_equal(t0[:L], g["tr_t0"][off:off + L])
+        np.testing.assert_array_equal(t1[:L], g["tr_t1"][off:off + L])
+        np.testing.assert_array_equal(cnt[2], g["tr_counters"][k])
+        assert not cnt[:2].any()
+        *_, ref_resid, _ = orc.walk_ray(sa, origins[q], dirs[q], 0.0, t_max, start, epsilon=eps)
+        assert resid == ref_resid
+        off += L
+
+
+def test_flat_render_rays_tracks_in_place_updates(cuda_ok):
+    """kernels.render_rays keeps the CSR on the device between calls (cached on the
+    adjacency arrays) but re-reads the parameters every call, like the
+    reference: moving sites / new sigma / new SH in place are honoured."""
+    from paper_2502_01157_b200 import kernels as K
+
+    f = load_golden("frame_2k_deg3")
+    sa, origins, dirs, start, t_max = frame_rays(f)
+    m = len(dirs)
+    pos = sa.positions.copy()
+    sigma = sa.sigma.copy()
+    sh = sa.sh.copy()
+    off, nbr = sa.offsets, sa.neighbors
+    rng = np.random.default_rng(4)
+    for it in range(3):
+        if it:  # the training loop's in-place updates between rebuilds
+            pos += rng.normal(0.0, 1e-4, pos.shape)
+            sigma *= rng.uniform(0.5, 1.5, sigma.shape)
+            sh += rng.normal(0.0, 0.05, sh.shape)
+        rgb = np.empty((m, 3))
+        res = np.empty(m)
+        st = np.empty(m, dtype=np.int8)
+        ws = np.empty(m)
+        cnt = np.zeros((1, 2), dtype=np.int64)
+        K.render_rays(pos, off, nbr, sigma, sh, sa.background, origins, dirs, np.zeros(m),
+                      np.full(m, t_max), np.full(m, start), 1e-3, 4096, sa.width_floor, 1, rgb,
+                      res, st, ws, cnt)
+        ref = orc.render_rays(orc.SceneArrays(pos, off, nbr, sigma, sh, sa.background), origins,
+                              dirs, 0.0, t_max, start)
+        np.testing.assert_array_equal(st, ref["status"])
+        np.testing.assert_array_equal(cnt[0], ref["counters"].sum(0))
+        assert np.abs(rgb - ref["rgb"]).max() <= IMG_TOL

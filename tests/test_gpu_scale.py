@@ -86,12 +86,15 @@ def test_sharded_renderer_host_frame(cuda_ok, scene100k):
     W, H = 200, 120
     ds = dv.DeviceScene(scene100k)
     cams = [_cam(W, H, k) for k in range(2)]
-    full = [dv.render_image_device(ds, c).rgb.cpu() for c in cams]
+    full = [dv.render_image_device(ds, c, f64=True).rgb.cpu().numpy().reshape(H, W, 3)
+            for c in cams]
     sr = ShardedRenderer(ds, W, H)
     h0 = sr.render_to_host(cams[0])
     h1 = sr.render_to_host(cams[1])
-    assert h0.is_pinned() and h0.data_ptr() != h1.data_ptr()
-    assert torch.equal(h0, full[0]) and torch.equal(h1, full[1])
+    assert h0.dtype == np.float64 and h0.shape == (H, W, 3)
+    assert h0.ctypes.data != h1.ctypes.data
+    np.testing.assert_array_equal(h0, full[0])
+    np.testing.assert_array_equal(h1, full[1])
 
 
 def test_train_100k_gradients(cuda_ok, scene100k):

@@ -126,3 +126,52 @@ def test_device_training_loop_with_rebuilds(cuda_ok):
             np.testing.assert_array_equal(tr.ds.neighbors.cpu().numpy(), nbr)
             assert info["reverse_edges_added"] == 0
     assert losses[-1] < 0.7 * losses[0], losses
+
+
+def test_trainer_dc_only_scene_after_warmup(cuda_ok):
+    """A scene initialised with the DC band only (train.py:77 scene_from_sfm) gains
+    higher SH bands once the warm-up ends; the trainer's walk must then colour
+    with all 16 bands (the scene is pinned to SH degree 3) and its fp32 colour
+    bound must follow the grown coefficients (rfb_scene.sh_absmax_dev)."""
+    from paper_2502_01157_b200 import device as dv
+    from paper_2502_01157_b200.train import DeviceTrainer
+
+    g = load_golden("train_2k_deg3_q")
+    scene = golden_scene(g)
+    scene.sh_coeffs = scene.sh_coeffs.copy()
+    scene.sh_coeffs[:, 1:, :] = 0.0
+    n = scene.n_sites
+    m = len(g["origins"])
+    d = lambda a, dt=torch.float64: torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)  # noqa
+    tr = DeviceTrainer(scene)
+    assert tr.ds.sh_degree == 3
+    bound0 = float(tr.ds.sh_absmax_dev.item())
+    for _ in range(3):  # past the warm-up: bands 1..15 receive gradients
+        tr.step(d(g["origins"]), d(g["dirs"]), d(np.zeros(m)), d(g["t_max"]),
+                d(g["start"], torch.int32), d(g["targets"]), lr_position=0.0, lr_density=0.05,
+                lr_sh=0.5, sh_warmup=False)
+    torch.cuda.synchronize()
+    sh = tr.sh.cpu().numpy()
+    assert np.abs(sh.reshape(n, 16, 3)[:, 1:, :]).max() > 0.1
+    assert float(tr.ds.sh_absmax_dev.item()) >= np.abs(sh).max().astype(np.float32)
+    assert float(tr.ds.sh_absmax_dev.item()) > bound0
+    # the trainer's scene renders exactly what the oracle renders from the updated
+    # parameters (sigma read back from the device's site4)
+    res = dv.render_rays_device(tr.ds, d(g["origins"]), d(g["dirs"]), d(np.zeros(m)),
+                                d(g["t_max"]), d(g["start"], torch.int32), f64=True)
+    torch.cuda.synchronize()
+    s4 = tr.ds.site4.cpu().numpy()
+    sa = orc.SceneArrays(s4[:, :3], g["offsets"], g["neighbors"], s4[:, 3], sh,
+                         g["background"])
+    ref = orc.render_rays(sa, g["origins"], g["dirs"], 0.0, g["t_max"], g["start"])
+    np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
+    assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= 1e-4
+
+
+def test_trainer_rejects_moving_fixed_sites(cuda_ok):
+    from paper_2502_01157_b200.train import AdamHyper, DeviceTrainer
+
+    g = load_golden("train_2k_deg3_q")
+    tr = DeviceTrainer(golden_scene(g), update_positions=False)
+    with pytest.raises(ValueError):
+        tr.post_grad_adam(1e-4, 0.1, 5e-3, False, AdamHyper())

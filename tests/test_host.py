@@ -180,3 +180,16 @@ def test_effect_rays_host_match_reference():
         rd.EffectPlane(np.zeros(3), np.ones(3), kind="lens")
     with pytest.raises(ValueError):
         rd.intersect_face(rd.Ray(np.zeros(3), np.array([0.0, 0.0, 1.0])), np.ones(3), np.ones(3))
+
+
+def test_csr_sha1_of_qhull_fixture():
+    """synthetic.csr_sha1 over a Qhull CSR is deterministic and sensitive to one edge."""
+    from paper_2502_01157_b200.synthetic import csr_sha1, delaunay_csr, random_positions
+
+    pos = random_positions(3000, 9, "uniform")
+    off, nbr, _ = delaunay_csr(pos)
+    h = csr_sha1(off, nbr)
+    assert h == csr_sha1(off.astype(np.int32), nbr.astype(np.int32))
+    nbr2 = nbr.copy()
+    nbr2[5] += 1
+    assert csr_sha1(off, nbr2) != h
