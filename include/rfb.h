@@ -71,18 +71,26 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 10
+#define RFB_ABI_VERSION 11
+
+/* Capacity (records) of the packed edge arrays rfb_pack_scene fills: rows are
+ * padded to an even length, so E + n_sites slots suffice (+2 spare). */
+#define RFB_PACKED_EDGE_SLOTS(n_sites, n_edges) ((n_edges) + (n_sites) + 2)
 
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
  *  packed (packed != 0): per-site 32-byte cell headers {float x,y,z; int k0;
- *   double sigma; int k1; float n1max} and per-edge 16-byte records
- *   {float xj,yj,zj; int j} in CSR order, plus fp32 SH (sh32) with the fp64
- *   table kept for the exact clamp fallback.  With positions_f64 == 0 the
- *   fp32 coordinates are the sites themselves; with positions_f64 != 0 they
- *   are rounded copies, n1max carries the widened pre-filter bound and the
- *   exact phase reads site4 (rfb_pack_scene and rfb_refresh_scene derive both).
- *   The generic arrays are always present (backward, locate). */
+ *   double sigma; int k1; float n1max} and per-edge 16-byte face records
+ *   {float nx,ny,nz, c} (n = x_j - x_i of the fp32 copies, c = |n|^2 / 2: the
+ *   face plane relative to the cell's site) in CSR order, each row starting
+ *   at an even slot k0 and padded to an even length with an all-NaN record
+ *   (k1 = k0 + degree), the neighbour id of every slot in edge_nbr (-1 for a
+ *   pad), plus fp32 SH (sh32) with the fp64 table kept for the exact clamp
+ *   fallback.  With positions_f64 == 0 the fp32 coordinates are the sites
+ *   themselves; with positions_f64 != 0 they are rounded copies, n1max
+ *   carries the widened pre-filter bound and the exact phase reads site4
+ *   (rfb_pack_scene and rfb_refresh_scene derive both).  The generic arrays
+ *   are always present (backward, locate). */
 typedef struct rfb_scene {
     int64_t n_sites;
     int64_t n_edges;
@@ -91,13 +99,12 @@ typedef struct rfb_scene {
     const int32_t *neighbors; /* [n_edges] ascending per site */
     const double *sh;         /* [n_sites][48], index k*3 + ch (render.py:53) */
     const void *cells;        /* packed: [n_sites] 32-byte headers (nullable) */
-    const void *edges;        /* packed: [n_edges + 1] 16-byte records (nullable); the walk
-                                 reads 32-byte aligned pairs, so the record after the last
-                                 one must be readable (its value is ignored) */
-    const void *edge_meta;    /* packed, optional: [n_edges] int2 {k0, k1} of the edge's target */
+    const void *edges;        /* packed: [RFB_PACKED_EDGE_SLOTS] 16-byte face records
+                                 (nullable); read as 32-byte aligned pairs */
+    const int32_t *edge_nbr;  /* packed: [RFB_PACKED_EDGE_SLOTS] neighbour id per slot */
     const float *sh32;        /* packed: [n_sites][3][16] fp32 channel-major copy of sh (nullable)
                                  cells, edges and sh32 must be 32-byte aligned (EINVAL) */
-    int32_t packed;           /* 1: use cells/edges/sh32 for the walk */
+    int32_t packed;           /* 1: use cells/edges/edge_nbr/sh32 for the walk */
     float sh_absmax;          /* packed: >= max |sh| over the scene (fp32 colour bound) */
     int32_t sh_degree;        /* 0: read the DC band only (exact when bands 1..15 are
                                  all zero), 3: all 16 bands */
@@ -186,14 +193,16 @@ int rfb_host_device_pointer(void *host, void **device_ptr);
 /* Build the device layout from fp64/int64 device arrays:
  * positions [n][3], sigma [n], sh [n][48], offsets [n+1], neighbors [E]
  * -> site4 [n][4] f64, offsets32 [n+1], neighbors32 [E] and, when
- * cells/edges/sh32 are non-NULL, the packed layout.  positions_f64 must be
+ * cells/edges/edge_nbr/sh32 are non-NULL, the packed layout (edges and
+ * edge_nbr hold RFB_PACKED_EDGE_SLOTS(n, E) slots).  positions_f64 must be
  * nonzero unless every coordinate is exactly representable in fp32 (and
  * stays so: set it for scenes whose sites will move); the same value goes
- * into rfb_scene.positions_f64.  edge_meta (optional) is unused by the walk. */
+ * into rfb_scene.positions_f64.  Uses stream-ordered scratch
+ * (cudaMallocAsync) for the padded row starts: not a hot-path call. */
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
-                   void *cells, void *edges, void *edge_meta, float *sh32,
+                   void *cells, void *edges, int32_t *edge_nbr, float *sh32,
                    int32_t positions_f64, void *stream);
 
 /* sigma = softplus_10(raw) for device-resident training, written to out
@@ -222,8 +231,9 @@ int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positio
 /* After a parameter update: site4 = {positions, softplus(raw)}, packed
  * headers' sigma and, when refresh_sh32 is nonzero, the fp32 SH copy are
  * refreshed from scene->sh (pass 0 when rfb_post_grad_adam already wrote
- * scene->sh32).  (The packed edge records hold positions: a scene whose
- * positions moved must be re-packed, or used with packed = 0.) */
+ * scene->sh32).  A packed scene with positions_f64 != 0 also gets its fp32
+ * copies, face records and widened bounds re-derived from the moved sites;
+ * one with positions_f64 == 0 cannot take moved sites (re-pack it). */
 int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const double *raw_density,
                       int32_t refresh_sh32, void *stream);
 

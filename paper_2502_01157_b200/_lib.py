@@ -13,7 +13,7 @@ import threading
 
 from .errors import DeviceError, ExtensionMissing
 
-ABI_VERSION = 10  # include/rfb.h RFB_ABI_VERSION
+ABI_VERSION = 11  # include/rfb.h RFB_ABI_VERSION
 _lock = threading.Lock()
 _lib = None
 
@@ -30,7 +30,7 @@ class rfb_scene(ctypes.Structure):
         ("sh", ctypes.c_void_p),
         ("cells", ctypes.c_void_p),
         ("edges", ctypes.c_void_p),
-        ("edge_meta", ctypes.c_void_p),
+        ("edge_nbr", ctypes.c_void_p),
         ("sh32", ctypes.c_void_p),
         ("packed", ctypes.c_int32),
         ("sh_absmax", ctypes.c_float),

@@ -12,6 +12,8 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 #include "rfb_device.cuh"
 
 namespace rfb {
@@ -19,6 +21,9 @@ namespace rfb {
 constexpr unsigned kFull = 0xffffffffu;
 #ifndef RFB_SUBTILE_W
 #define RFB_SUBTILE_W 4  // a warp's 32 rays cover a 4 x 8 pixel patch (measured best)
+#endif
+#ifndef RFB_PF_SH
+#define RFB_PF_SH 0  // prefetch the cell's fp32 SH row into L1 at the start of each step
 #endif
 #ifndef RFB_F32_FILTER
 #define RFB_F32_FILTER 1
@@ -189,6 +194,12 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
             return RFB_STATUS_STEP_LIMIT;
         }
         const Cell c = S.cell(i);
+#if RFB_PF_SH
+        if (PACKED) {  // the segment's SH row (read after phase 2), 192 B = 2 lines
+            prefetch_l1(S.sh32 + (int64_t)i * 48);
+            prefetch_l1(S.sh32 + (int64_t)i * 48 + 32);
+        }
+#endif
         visits += c.k1 - c.k0;
         double best_t;
         int32_t best_j;
@@ -255,8 +266,12 @@ __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
 #ifndef RFB_FWD_MINB
 #define RFB_FWD_MINB 4
 #endif
+#ifndef RFB_CONST_ORIGIN
+#define RFB_CONST_ORIGIN 1  // shared-origin rays: origin / t-range from the constant bank
+#endif
 template <int G, int SHDEG, int PACKED, class Src>
-__global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> S, Src src, double epsilon,
+__global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> S,
+                                                const __grid_constant__ Src src, double epsilon,
                                                 double log_eps, double width_floor,
                                                 int32_t step_limit, FwdOut O,
                                                 unsigned long long *ray_counter) {
@@ -289,10 +304,18 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
         // the ray's fp64 constants and fp32 SH basis live in shared memory
         // (field-major, conflict-free) to keep registers for the walk: the
         // kernel is occupancy-bound
-        using RayS = typename std::conditional<Src::kUniform, RaySmemU<256>, RaySmem<256>>::type;
+        using RayU = typename std::conditional<RFB_CONST_ORIGIN, RaySmemP<256, Src>,
+                                               RaySmemU<256>>::type;
+        using RayS = typename std::conditional<Src::kUniform, RayU, RaySmem<256>>::type;
         RayS r;
         r.p = s_ray + threadIdx.x;
-        if constexpr (Src::kUniform) r.u = s_uni;
+        if constexpr (Src::kUniform) {
+#if RFB_CONST_ORIGIN
+            r.src = &src;
+#else
+            r.u = s_uni;
+#endif
+        }
         double *tol_p = s_ray + (kRayFields - 1) * 256 + threadIdx.x;  // color_tol
         {
             Ray rr;
@@ -322,7 +345,11 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                 double delta = t1 - t0;
                 const double alpha = (double)(-expm1f(-(float)(sigma * delta)));
                 double col[3];
+#ifdef RFB_NO_COLOR  // profiling knob: walk + compositing with a constant colour
+                col[0] = col[1] = col[2] = 0.5;
+#else
                 cell_color<SHDEG, PACKED, 256, 1>(S, cell, s_basis + threadIdx.x, r, *tol_p, col);
+#endif
                 const double w = T * alpha;
                 wsum += w;
                 const float wf = (float)w;
@@ -967,9 +994,53 @@ __device__ __forceinline__ float pos64_widen(double xabs) {
     return (float)(2.0 * fmax(xabs, 0.25)) * (1.0f + 0x1p-20f);
 }
 
+// One row of packed edge records (rfb_device.cuh, exit_face_f32): for each CSR
+// neighbour j of site i, {n = fl32(x_j) - fl32(x_i) (fp32 subtraction, the
+// values phase 1 used to compute itself), c = fl32(0.5 |n|^2) (from the fp32 n
+// in fp64)} (RFB_FACE_C; else {fl32(x_j), j}), the neighbour id in enbr, and
+// an all-NaN pad when the degree is odd.  Returns n1max (>= max |n|_1, rounded
+// up) and X (largest |coordinate|).
+__device__ __forceinline__ float pack_row(const double *pos, int64_t i, const int64_t *nbr64,
+                                          const int32_t *nbr32, int64_t kc0, int32_t deg,
+                                          int64_t kp0, float4 *edges, int32_t *enbr,
+                                          double &xabs) {
+    const float xi = (float)pos[3 * i], yi = (float)pos[3 * i + 1], zi = (float)pos[3 * i + 2];
+    float n1max = 0.f;
+    xabs = fmax(fabs(pos[3 * i]), fmax(fabs(pos[3 * i + 1]), fabs(pos[3 * i + 2])));
+    for (int32_t t = 0; t < deg; ++t) {
+        const int64_t j = nbr64 ? nbr64[kc0 + t] : (int64_t)nbr32[kc0 + t];
+        const float nx = (float)pos[3 * j] - xi, ny = (float)pos[3 * j + 1] - yi,
+                    nz = (float)pos[3 * j + 2] - zi;
+#if RFB_FACE_C
+        const double c = 0.5 * ((double)nx * nx + (double)ny * ny + (double)nz * nz);
+        edges[kp0 + t] = make_float4(nx, ny, nz, (float)c);
+#else
+        edges[kp0 + t] = make_float4((float)pos[3 * j], (float)pos[3 * j + 1],
+                                     (float)pos[3 * j + 2], __int_as_float((int32_t)j));
+#endif
+        enbr[kp0 + t] = (int32_t)j;
+        n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
+        xabs = fmax(xabs, fmax(fabs(pos[3 * j]), fmax(fabs(pos[3 * j + 1]), fabs(pos[3 * j + 2]))));
+    }
+    if (deg & 1) {  // pad to an even row: rejected as back-facing by every ray (NaN)
+        const float qnan = __int_as_float(0x7fffffff);
+        edges[kp0 + deg] = make_float4(qnan, qnan, qnan, qnan);
+        enbr[kp0 + deg] = -1;
+    }
+    return n1max * (1.0f + 0x1p-20f);
+}
+
+__global__ void k_odd_rows(const int64_t *off64, int64_t n, int32_t *odd) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) odd[i] = (int32_t)((off64[i + 1] - off64[i]) & 1);
+}
+
+// odd_before: exclusive prefix count of odd-degree rows (the padded row start
+// of site i is off64[i] + odd_before[i], always even).
 __global__ void k_pack_sites(const double *pos, const double *sigma, const double *sh, int64_t n,
-                             const int64_t *off64, const int64_t *nbr64, double4 *site4,
-                             int32_t *off32, CellHdr *cells, float *sh32, int pos64) {
+                             const int64_t *off64, const int64_t *nbr64, const int32_t *odd_before,
+                             double4 *site4, int32_t *off32, CellHdr *cells, float *sh32,
+                             float4 *edges, int32_t *enbr, int pos64) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n) return;
     off32[i] = (int32_t)off64[i];
@@ -979,40 +1050,26 @@ __global__ void k_pack_sites(const double *pos, const double *sigma, const doubl
         for (int k = 0; k < 16; ++k)
             for (int ch = 0; ch < 3; ++ch)
                 sh32[i * 48 + 16 * ch + k] = (float)sh[i * 48 + 3 * k + ch];  // channel-major
-        const float xi = (float)pos[3 * i], yi = (float)pos[3 * i + 1], zi = (float)pos[3 * i + 2];
-        float n1max = 0.f;
-        double xabs = fmax(fabs(pos[3 * i]), fmax(fabs(pos[3 * i + 1]), fabs(pos[3 * i + 2])));
-        for (int64_t k = off64[i]; k < off64[i + 1]; ++k) {  // same fp32 ops as exit_face_f32
-            const int64_t j = nbr64[k];
-            const float nx = (float)pos[3 * j] - xi, ny = (float)pos[3 * j + 1] - yi,
-                        nz = (float)pos[3 * j + 2] - zi;
-            n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
-            xabs = fmax(xabs, fmax(fabs(pos[3 * j]), fmax(fabs(pos[3 * j + 1]), fabs(pos[3 * j + 2]))));
-        }
+        const int32_t deg = (int32_t)(off64[i + 1] - off64[i]);
+        const int64_t kp0 = off64[i] + odd_before[i];
+        double xabs;
+        float n1max = pack_row(pos, i, nbr64, nullptr, off64[i], deg, kp0, edges, enbr, xabs);
         if (pos64) n1max += pos64_widen(xabs);
         CellHdr h;
-        h.x = xi;
-        h.y = yi;
-        h.z = zi;
-        h.k0 = (int32_t)off64[i];
+        h.x = (float)pos[3 * i];
+        h.y = (float)pos[3 * i + 1];
+        h.z = (float)pos[3 * i + 2];
+        h.k0 = (int32_t)kp0;
         h.sigma = sigma[i];
-        h.k1 = (int32_t)off64[i + 1];
-        h.n1max = n1max * (1.0f + 0x1p-20f);
+        h.k1 = (int32_t)(kp0 + deg);
+        h.n1max = n1max;
         cells[i] = h;
     }
 }
 
-__global__ void k_pack_edges(const int64_t *nbr64, const int64_t *off64, const double *pos,
-                             int64_t E, int32_t *nbr32, float4 *edges, int2 *emeta) {
+__global__ void k_pack_edges(const int64_t *nbr64, int64_t E, int32_t *nbr32) {
     int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= E) return;
-    int32_t j = (int32_t)nbr64[k];
-    nbr32[k] = j;
-    if (edges) {
-        edges[k] = make_float4((float)pos[3 * j], (float)pos[3 * j + 1], (float)pos[3 * j + 2],
-                               __int_as_float(j));
-        if (emeta) emeta[k] = make_int2((int32_t)off64[j], (int32_t)off64[j + 1]);
-    }
+    if (k < E) nbr32[k] = (int32_t)nbr64[k];
 }
 
 // foam.py:22-25 (device libm; may differ from numpy's log1p/exp by 1 ulp).
@@ -1293,35 +1350,27 @@ __global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double
 }
 
 // Refresh the kernel arrays from updated parameters (render.py:49-54 on
-// device): site4 = {pos, softplus(raw)}, packed headers' sigma, sh32.
-__global__ void k_refresh_scene(int64_t n, const double *pos, const double *raw,
-                                const double *sh, double4 *site4, CellHdr *cells, float *sh32,
-                                const int32_t *off, const float4 *edges, int pos64) {
+// device): site4 = {pos, softplus(raw)}, packed headers' sigma; for moved
+// fp64 sites also the fp32 copies, the row's edge records and the widened
+// bound (k_pack_sites' rules).
+__global__ void k_refresh_scene(int64_t n, const double *pos, const double *raw, double4 *site4,
+                                CellHdr *cells, const int32_t *off, const int32_t *nbr,
+                                float4 *edges, int32_t *enbr, int pos64) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double x = raw[i];
     const double sig = fmax(x, 0.0) + log1p(exp(-fabs(10.0 * x))) / 10.0;
     site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sig);
     if (cells) cells[i].sigma = sig;
-    if (cells && pos64) {  // moved sites: fp32 copies and the widened bound (k_pack_sites)
-        // reads the refreshed fp32 edge records (k_refresh_edges ran first): the
-        // same fp32 n as k_pack_sites; |x| <= |fl32(x)| (1 + 2^-23)
-        const float xi = (float)pos[3 * i], yi = (float)pos[3 * i + 1], zi = (float)pos[3 * i + 2];
-        float n1max = 0.f;
-        double xabs = fmax(fabs(pos[3 * i]), fmax(fabs(pos[3 * i + 1]), fabs(pos[3 * i + 2])));
-        float xabs_f = 0.f;
-        for (int32_t k = off[i]; k < off[i + 1]; ++k) {
-            const float4 e = __ldg(edges + k);
-            const float nx = e.x - xi, ny = e.y - yi, nz = e.z - zi;
-            n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
-            xabs_f = fmaxf(xabs_f, fmaxf(fabsf(e.x), fmaxf(fabsf(e.y), fabsf(e.z))));
-        }
-        xabs = fmax(xabs, (double)xabs_f * (1.0 + 0x1p-22));
+    if (cells && pos64) {
         CellHdr &h = cells[i];
-        h.x = xi;
-        h.y = yi;
-        h.z = zi;
-        h.n1max = n1max * (1.0f + 0x1p-20f) + pos64_widen(xabs);
+        double xabs;
+        const float n1max = pack_row(pos, i, nullptr, nbr, off[i], off[i + 1] - off[i], h.k0,
+                                     edges, enbr, xabs);
+        h.x = (float)pos[3 * i];
+        h.y = (float)pos[3 * i + 1];
+        h.z = (float)pos[3 * i + 2];
+        h.n1max = n1max + pos64_widen(xabs);
     }
 }
 
@@ -1344,7 +1393,7 @@ static SceneView<PACKED> view(const rfb_scene *s) {
     SceneView<PACKED> v;
     v.hdr = reinterpret_cast<const CellHdr *>(s->cells);
     v.edge = reinterpret_cast<const float4 *>(s->edges);
-    v.emeta = reinterpret_cast<const int2 *>(s->edge_meta);
+    v.enbr = s->edge_nbr;
     v.site4 = reinterpret_cast<const double4 *>(s->site4);
     v.off = s->offsets;
     v.nbr = s->neighbors;
@@ -1387,7 +1436,7 @@ static bool scene_ok(const rfb_scene *s) {
     if (!s || !s->site4 || !s->offsets || !s->neighbors || !s->sh || s->n_sites <= 0 ||
         s->n_sites >= (1 << 29) || (s->sh_degree != 0 && s->sh_degree != 3))
         return false;
-    if (s->packed && (!s->cells || !s->edges || !s->sh32)) return false;
+    if (s->packed && (!s->cells || !s->edges || !s->edge_nbr || !s->sh32)) return false;
     if (s->packed && ((reinterpret_cast<uintptr_t>(s->cells) | reinterpret_cast<uintptr_t>(s->edges) |
                        reinterpret_cast<uintptr_t>(s->sh32)) & 31u))
         return false;  // 256-bit loads
@@ -1674,20 +1723,35 @@ int rfb_host_device_pointer(void *host, void **device_ptr) {
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
-                   void *cells, void *edges, void *edge_meta, float *sh32,
+                   void *cells, void *edges, int32_t *edge_nbr, float *sh32,
                    int32_t positions_f64, void *stream) {
     if (!positions || !sigma || !offsets || !neighbors || !site4 || !offsets32 || !neighbors32 ||
-        n_sites <= 0 || n_edges < 0 || n_edges >= ((int64_t)1 << 31) ||
-        ((cells || edges || sh32) && (!cells || !edges || !sh32 || !sh)))
+        n_sites <= 0 || n_edges < 0 || n_edges + n_sites + 2 >= ((int64_t)1 << 31) ||
+        ((cells || edges || edge_nbr || sh32) && (!cells || !edges || !edge_nbr || !sh32 || !sh)))
         return RFB_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
+    int32_t *odd = nullptr;
+    void *tmp = nullptr;
+    if (cells) {  // padded row starts: exclusive count of odd-degree rows
+        size_t tmp_bytes = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, odd, odd, (int)n_sites, st);
+        // one allocation: [odd flags (n+1) | 256-byte aligned scan scratch]
+        const size_t head = ((sizeof(int32_t) * (n_sites + 1)) + 255) & ~(size_t)255;
+        cudaError_t e = cudaMallocAsync(&tmp, head + tmp_bytes, st);
+        if (e != cudaSuccess) return (int)e;
+        odd = reinterpret_cast<int32_t *>(tmp);
+        k_odd_rows<<<(unsigned)((n_sites + 255) / 256), 256, 0, st>>>(offsets, n_sites, odd);
+        cub::DeviceScan::ExclusiveSum(reinterpret_cast<char *>(tmp) + head, tmp_bytes, odd, odd,
+                                      (int)n_sites, st);
+    }
     k_pack_sites<<<(unsigned)((n_sites + 1 + 255) / 256), 256, 0, st>>>(
-        positions, sigma, sh, n_sites, offsets, neighbors, reinterpret_cast<double4 *>(site4),
-        offsets32, reinterpret_cast<CellHdr *>(cells), sh32, positions_f64 ? 1 : 0);
+        positions, sigma, sh, n_sites, offsets, neighbors, odd, reinterpret_cast<double4 *>(site4),
+        offsets32, reinterpret_cast<CellHdr *>(cells), sh32, reinterpret_cast<float4 *>(edges),
+        edge_nbr, positions_f64 ? 1 : 0);
     if (n_edges > 0)
-        k_pack_edges<<<(unsigned)((n_edges + 255) / 256), 256, 0, st>>>(
-            neighbors, offsets, positions, n_edges, neighbors32, reinterpret_cast<float4 *>(edges),
-            reinterpret_cast<int2 *>(edge_meta));
+        k_pack_edges<<<(unsigned)((n_edges + 255) / 256), 256, 0, st>>>(neighbors, n_edges,
+                                                                         neighbors32);
+    if (tmp) cudaFreeAsync(tmp, st);
     return (int)cudaGetLastError();
 }
 
@@ -1732,28 +1796,17 @@ __global__ void k_refresh_sh32(int64_t n, const double *sh, float *sh32) {
     sh32[o] = (float)sh[48 * i + 3 * k + ch];
 }
 
-__global__ void k_refresh_edges(const int32_t *nbr, const double *pos, int64_t E, float4 *edges) {
-    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= E) return;
-    const int32_t j = nbr[k];
-    edges[k] = make_float4((float)pos[3 * j], (float)pos[3 * j + 1], (float)pos[3 * j + 2],
-                           __int_as_float(j));
-}
-
 int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const double *raw_density,
                       int32_t refresh_sh32, void *stream) {
     if (!scene_ok(scene) || !positions || !raw_density) return RFB_EINVAL;
     // a packed scene with fp32-exact positions cannot take moved sites in place
     const bool pos64 = scene->packed && scene->positions_f64;
     cudaStream_t st = (cudaStream_t)stream;
-    if (pos64 && scene->n_edges > 0)  // first: k_refresh_scene reads the new records
-        k_refresh_edges<<<(unsigned)((scene->n_edges + 255) / 256), 256, 0, st>>>(
-            scene->neighbors, positions, scene->n_edges,
-            reinterpret_cast<float4 *>(const_cast<void *>(scene->edges)));
     k_refresh_scene<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, st>>>(
-        scene->n_sites, positions, raw_density, scene->sh, (double4 *)scene->site4,
-        scene->packed ? (CellHdr *)scene->cells : nullptr,
-        nullptr, scene->offsets, reinterpret_cast<const float4 *>(scene->edges), pos64 ? 1 : 0);
+        scene->n_sites, positions, raw_density, (double4 *)scene->site4,
+        scene->packed ? (CellHdr *)scene->cells : nullptr, scene->offsets, scene->neighbors,
+        reinterpret_cast<float4 *>(const_cast<void *>(scene->edges)),
+        const_cast<int32_t *>(scene->edge_nbr), pos64 ? 1 : 0);
     if (refresh_sh32 && scene->packed && scene->sh32)
         k_refresh_sh32<<<(unsigned)((48 * scene->n_sites + 255) / 256), 256, 0, st>>>(
             scene->n_sites, scene->sh, (float *)scene->sh32);

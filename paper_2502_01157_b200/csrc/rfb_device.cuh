@@ -27,6 +27,12 @@
 #ifndef RFB_HDR256
 #define RFB_HDR256 0  // one 256-bit load per cell header
 #endif
+#ifndef RFB_SH_PIPE
+#define RFB_SH_PIPE 1  // SH colour: the next channel's row loads overlap this channel's sum
+#endif
+#ifndef RFB_EDGE_PIPE
+#define RFB_EDGE_PIPE 0  // phase 1: the next edge pair's load overlaps this pair's visit
+#endif
 #ifndef RFB_CHECK
 #define RFB_CHECK 0  // 1: device-side bounds asserts on every scene gather / record (debug build)
 #endif
@@ -127,7 +133,7 @@ template <int PACKED>
 struct SceneView {
     const CellHdr *hdr;     // PACKED
     const float4 *edge;     // PACKED
-    const int2 *emeta;      // PACKED: [E] {k0_j, k1_j} of the edge's target site
+    const int32_t *enbr;    // PACKED: neighbour id per packed edge slot (-1: row pad)
     const double4 *site4;   // both (backward gradients use fp64 positions)
     const int32_t *off;     // generic
     const int32_t *nbr;     // generic
@@ -180,16 +186,26 @@ struct SceneView {
         return c.sigma;
     }
 
+    // CSR slot k's neighbour (generic) or packed slot k's (packed layout)
     __device__ __forceinline__ void edge_at(int32_t k, double &x, double &y, double &z,
                                             int32_t &j) const {
-        RFB_BOUND(k, n_edges);
         if (PACKED) {
-            float4 e = __ldg(edge + k);
-            x = e.x;
-            y = e.y;
-            z = e.z;
-            j = __float_as_int(e.w);
+            RFB_BOUND(k, n_edges + n_sites + 2);
+            j = __ldg(enbr + k);
+            RFB_BOUND(j, n_sites);
+            if (PACKED == 2) {
+                const double4 s = ld_site(site4 + j);
+                x = s.x;
+                y = s.y;
+                z = s.z;
+            } else {
+                const float4 h = __ldg(reinterpret_cast<const float4 *>(hdr + j));
+                x = h.x;
+                y = h.y;
+                z = h.z;
+            }
         } else {
+            RFB_BOUND(k, n_edges);
             j = __ldg(nbr + k);
             RFB_BOUND(j, n_sites);
             double4 s = ld_site(site4 + j);
@@ -255,6 +271,30 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
 #pragma unroll
             for (int ch = 0; ch < 3; ++ch)
                 acc[ch] = (double)__fmaf_rn(bk(0), __ldg(row + 16 * ch), 0.5f);
+        } else if (RFB_SH_PIPE) {
+            // two channels' loads in flight: channel ch+1's 64 B arrive while ch is summed
+            const float4 *r4 = reinterpret_cast<const float4 *>(row);
+            float4 va[4], vb[4];
+            ldg256(r4, va[0], va[1]);
+            ldg256(r4 + 2, va[2], va[3]);
+            ldg256(r4 + 4, vb[0], vb[1]);
+            ldg256(r4 + 6, vb[2], vb[3]);
+            auto dot = [&](const float4 *v) {
+                float a = 0.5f;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    a = __fmaf_rn(bk(4 * q), v[q].x, a);
+                    a = __fmaf_rn(bk(4 * q + 1), v[q].y, a);
+                    a = __fmaf_rn(bk(4 * q + 2), v[q].z, a);
+                    a = __fmaf_rn(bk(4 * q + 3), v[q].w, a);
+                }
+                return (double)a;
+            };
+            acc[0] = dot(va);
+            ldg256(r4 + 8, va[0], va[1]);
+            ldg256(r4 + 10, va[2], va[3]);
+            acc[1] = dot(vb);
+            acc[2] = dot(va);
         } else {
 #pragma unroll 1
             for (int ch = 0; ch < 3; ++ch) {  // one channel (4 x 16 B) in flight: registers
@@ -336,6 +376,28 @@ struct RaySmemU {
     __device__ __forceinline__ double dz() const { return p[2 * NT]; }
     __device__ __forceinline__ double t_min() const { return u[3]; }
     __device__ __forceinline__ double t_max() const { return u[4]; }
+    __device__ __forceinline__ void store(const Ray &r) {
+        p[0 * NT] = r.dx_;
+        p[1 * NT] = r.dy_;
+        p[2 * NT] = r.dz_;
+    }
+};
+
+// ... or, for a shared-origin camera source passed as a __grid_constant__
+// kernel parameter, the direction per thread in shared memory and the origin /
+// t-range read straight from the parameter (constant bank: no data-pipe traffic).
+template <int NT, class Src>
+struct RaySmemP {
+    double *p;       // &s_dir[0][threadIdx.x]
+    const Src *src;  // address of the __grid_constant__ parameter
+    __device__ __forceinline__ double ox() const { return src->cam.o[0]; }
+    __device__ __forceinline__ double oy() const { return src->cam.o[1]; }
+    __device__ __forceinline__ double oz() const { return src->cam.o[2]; }
+    __device__ __forceinline__ double dx() const { return p[0 * NT]; }
+    __device__ __forceinline__ double dy() const { return p[1 * NT]; }
+    __device__ __forceinline__ double dz() const { return p[2 * NT]; }
+    __device__ __forceinline__ double t_min() const { return src->t_min; }
+    __device__ __forceinline__ double t_max() const { return src->t_max; }
     __device__ __forceinline__ void store(const Ray &r) {
         p[0 * NT] = r.dx_;
         p[1 * NT] = r.dy_;
@@ -448,50 +510,71 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 
 
 // ---------------------------------------------------------------------------
-// Packed-layout exit face with an fp32 pre-filter (DESIGN.md §4.2).
+// Packed-layout exit face with an fp32 pre-filter (DESIGN.md §4.1).
 //
-// Phase 1 (fp32 FMA, no conversions): for every neighbour compute, relative
-// to q = o + entry*d (fp64, rounded once to fp32), the shifted depth
-// s = ((m - q).n) / (d.n) and a rigorous bound on |s - s_exact|:
-//   den:  |den_f - d.n|  <= Ed = 8u |n|_1                       (u = 2^-24)
-//   num:  |num_f - (m-q).n| <= En = u |n|_1 (|q|_inf + 8|h|_inf + 2|n|_1)
+// Edge records (packed layout): row i holds, for each neighbour j in CSR
+// order, {n = fl32(x_j - x_i) (fp32 copies), c = fl32(0.5 |n|^2)} -- the face
+// plane n.(x - x_i) = c relative to the cell's own site -- and rows are padded
+// to an even length (start index even) with an all-NaN record, so a row is
+// read as whole 32-byte pairs (one LDG.256 per two neighbours) and a pad is
+// rejected by the back-facing test like any back face (NaN compares false).
+// The neighbour ids live in a parallel int32 array (edge_nbr) that only
+// phase 2 reads.
+//
+// Phase 1 (fp32 FMA): for every neighbour, relative to q = o + entry*d (fp64,
+// rounded once to fp32) and p = x_i - q, the shifted depth s = num / den with
+//   den = d.n (3 FMA-chain ops),  num = c + p.n (3),
+// and a rigorous bound on |s - s_exact| (u = 2^-24, N >= |n|_1 = n1max,
+// P = |p|_inf, Q = |q|_inf):
+//   den:  |den_f - d.n|      <= 5u N                      <= Ed = 8u N
+//   num:  |num_f - (m-q).n|  <= u N (Q + 5P + 3N)         <= En = u N (Q + 8 Hm + 2N),
+//         Hm = (P + N/2)(1 + 4u)   (the bound of the earlier (p + n/2).n form,
+//         kept: it dominates this form's)
 //   s:    es = 2.2 (En + |s| Ed) / den_f + 8u |s| + 2^-40 (|entry| + |s| + 1)
-// (first-order roundings of the inputs, the differences, the FMA chains and
-// the fast division, with margin; the last term covers the reference's own
-// fp64 rounding).  A neighbour is certainly back-facing if den_f < -Ed, and
-// certainly front-facing if den_f > 2 Ed; anything in between is
-// "uncertain".  Front-facing neighbours with s - es > U, U the running
-// minimum of s + es, cannot be the reference's first minimum (their fp64
-// t is strictly larger than some other neighbour's).
-// Phase 2 (fp64, exactly the reference's expressions): every uncertain
-// neighbour and every front-facing one that was within the running band
-// when it was seen (a superset of the final band) is re-evaluated in CSR
-// order with `denom <= 0 -> skip`, `t < best_t` -- so best_t / best_j are
-// bit-identical to kernels.py:116-133.  Rows longer than 64 neighbours
-// evaluate the tail exactly.
+// (c's own rounding and the n rounding enter num as 1.5uN^2, p's as
+// u(Q + P)N, the FMA chain as 3u(N^2/2 + PN); the last term of es covers the
+// reference's own fp64 rounding).  For fp64 sites (PK = 2) the fp32 copies
+// add <= 2uX per n component and uX per p component (X = largest |coordinate|
+// of the cell and its neighbours): <= u(3XN + 6XP) to num and <= 6uX to den,
+// covered by storing n1max = N + w with w = 2 max(X, 1/4) >= X (the bound's
+// terms grow by >= uw(8P + 6N) and 8uw).  A neighbour is certainly
+// back-facing unless den_f >= -Ed (NaN pads included), certainly front-facing
+// if den_f > 2 Ed; anything in between is "uncertain".  Front-facing
+// neighbours with s - es > U, U the running minimum of s + es, cannot be the
+// reference's first minimum (their fp64 t is strictly larger than some other
+// neighbour's).
+// Phase 2 (fp64, exactly the reference's expressions on the exact sites):
+// every uncertain neighbour and every front-facing one that was within the
+// running band when it was seen (a superset of the final band) is
+// re-evaluated in CSR order with `denom <= 0 -> skip`, `t < best_t` -- so
+// best_t / best_j are bit-identical to kernels.py:116-133.  With the final-
+// band filter (below) usually only one neighbour is.  Rows longer than 32
+// slots are evaluated exactly in full.
 // ---------------------------------------------------------------------------
-#ifndef RFB_MASK32
-#define RFB_MASK32 1
-#endif
-#ifndef RFB_FAST_BOUND
-#define RFB_FAST_BOUND 1
-#endif
-#ifndef RFB_BRANCHFREE
-#define RFB_BRANCHFREE 1
-#endif
 #ifndef RFB_F32_UNROLL
 #define RFB_F32_UNROLL 4
 #endif
 #ifndef RFB_PAIR_UNROLL
 #define RFB_PAIR_UNROLL 2  // edge pairs per unrolled phase-1 iteration (LDG.256 path)
 #endif
-#if RFB_MASK32
+#ifndef RFB_FINAL_BAND
+#define RFB_FINAL_BAND 1  // drop candidates the final band excludes (one exact evaluation)
+#endif
+#ifndef RFB_FACE_C
+#define RFB_FACE_C 0  // edge records {n, c} (1) or {x_j (fp32 copy), j} (0)
+#endif
+#ifndef RFB_PF_NBR
+#define RFB_PF_NBR 1  // RFB_FACE_C: prefetch the row's neighbour ids into L1 for phase 2
+#endif
+#ifndef RFB_PF_NEXT
+#define RFB_PF_NEXT 0  // prefetch the next cell's header as soon as phase 1 decides it
+#endif
+
+__device__ __forceinline__ void prefetch_l1(const void *p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 typedef unsigned int cand_mask_t;
 constexpr int kMaskBits = 32;
-#else
-typedef unsigned long long cand_mask_t;
-constexpr int kMaskBits = 64;
-#endif
 
 // PK: 1 = packed with fp32-exact sites, 2 = packed with fp64 sites (positions_f64)
 template <int G, int PK, class RayT>
@@ -506,191 +589,210 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     const float Q = fmaxf(fabsf(qxf), fmaxf(fabsf(qyf), fabsf(qzf))) * (1.0f + 4.0f * u);
     const float px = hdr_f.x - qxf, py = hdr_f.y - qyf, pz = hdr_f.z - qzf;
     const float slack = (float)(0x1p-40 * (fabs(entry) + 1.0));
-#if RFB_FAST_BOUND
     const float N = c.n1max;
     const float Ed = 8.0f * u * N;
+    const float thr = fmaxf(2.0f * Ed, 0x1p-100f);  // certainly front-facing above
     const float P = fmaxf(fabsf(px), fmaxf(fabsf(py), fabsf(pz)));
     const float Hm = (P + 0.5f * N) * (1.0f + 4.0f * u);
     const float K1 = 2.2f * u * N * (Q + 8.0f * Hm + 2.0f * N);
     const float K2 = 2.2f * Ed;
     constexpr float K3 = 8.0f * u + 0x1p-40f;
-#endif
-    float U = __int_as_float(0x7f800000);  // +inf
+    const float kInf = __int_as_float(0x7f800000);
+    float U = kInf;
     cand_mask_t mask = 0;
-    const int32_t k0 = c.k0 + gl;
-    int32_t nk = 0;
-#if RFB_LDG256 && RFB_BRANCHFREE && RFB_FAST_BOUND
-    if (G == 1) {
-        // Edge records are read as 32-byte aligned pairs starting at k0 & ~1
-        // (one LDG.256 per two neighbours); slots outside [k0, k1) -- the
-        // previous row's last edge, the next row's first, or the record
-        // after the array -- are predicated off.
-        auto visit = [&](const float4 &e, int32_t idx, bool valid) {
-            const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
-            const float den = __fmaf_rn(df[2], nz, __fmaf_rn(df[1], ny, df[0] * nx));
-            const cand_mask_t bit =
-                (valid && idx < kMaskBits) ? ((cand_mask_t)1 << idx) : (cand_mask_t)0;
-            const bool back = !valid || den < -Ed;
-            const bool sure = valid && den > 2.0f * Ed && den >= 0x1p-100f;
-            const float hx = __fmaf_rn(0.5f, nx, px), hy = __fmaf_rn(0.5f, ny, py),
-                        hz = __fmaf_rn(0.5f, nz, pz);
-            const float num = __fmaf_rn(hz, nz, __fmaf_rn(hy, ny, hx * nx));
-            float rinv;
-            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rinv) : "f"(sure ? den : 1.0f));
-            const float s = num * rinv;
-            const float as = fabsf(s);
-            const float es = __fmaf_rn(K3, as, __fmaf_rn(__fmaf_rn(K2, as, K1), rinv, slack));
-            const bool cand = !back && (!sure || s - es <= U);
-            mask |= cand ? bit : (cand_mask_t)0;
-            U = sure ? fminf(U, s + es) : U;
-        };
-        RFB_PRAGMA_UNROLL(RFB_PAIR_UNROLL)
-        for (int32_t kp = c.k0 & ~1; kp < c.k1; kp += 2) {
-            float4 e0, e1;
-            RFB_BOUND(kp + 1, S.n_edges + 1);  // the pad record after the array
-#if RFB_CHECK
-            assert((reinterpret_cast<uintptr_t>(S.edge + kp) & 31) == 0);
-#endif
-            ldg256(S.edge + kp, e0, e1);
-            visit(e0, kp - k0, kp >= k0);
-            visit(e1, kp + 1 - k0, kp + 1 < c.k1);
-        }
-        nk = c.k1 - k0;
-    } else
-#endif
-    RFB_PRAGMA_UNROLL(RFB_F32_UNROLL)
-    for (int32_t k = k0; k < c.k1; k += G, ++nk) {
-        RFB_BOUND(k, S.n_edges);
-        const float4 e = __ldg(S.edge + k);
-        const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
-        const float den = __fmaf_rn(df[2], nz, __fmaf_rn(df[1], ny, df[0] * nx));
-#if !RFB_FAST_BOUND
-        const float n1 = fabsf(nx) + fabsf(ny) + fabsf(nz);
-        const float Ed = 8.0f * u * n1;
-#endif
-#if RFB_BRANCHFREE && RFB_FAST_BOUND
-        // predicated form: every lane evaluates the same instruction stream
-        // (no per-neighbour divergence); back-facing values are computed and
-        // discarded.  Same decisions as the branchy form below.
-        const cand_mask_t bit = nk < kMaskBits ? ((cand_mask_t)1 << nk) : (cand_mask_t)0;
-        const bool back = den < -Ed;
-        const bool sure = den > 2.0f * Ed && den >= 0x1p-100f;
-        const float hx = __fmaf_rn(0.5f, nx, px), hy = __fmaf_rn(0.5f, ny, py),
-                    hz = __fmaf_rn(0.5f, nz, pz);
-        const float num = __fmaf_rn(hz, nz, __fmaf_rn(hy, ny, hx * nx));
-        float rinv;
-        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rinv) : "f"(sure ? den : 1.0f));
-        const float s = num * rinv;
-        const float as = fabsf(s);
-        const float es = __fmaf_rn(K3, as, __fmaf_rn(__fmaf_rn(K2, as, K1), rinv, slack));
-        const bool cand = !back && (!sure || s - es <= U);
-        mask |= cand ? bit : (cand_mask_t)0;
-        U = sure ? fminf(U, s + es) : U;
+    // one neighbour record -> (lower bound, upper bound, back, sure)
+    auto bounds = [&](const float4 &e, float &lb, float &ub, bool &front, bool &sure) {
+#if RFB_FACE_C
+        const float nx = e.x, ny = e.y, nz = e.z;
+        const float num = __fmaf_rn(pz, nz, __fmaf_rn(py, ny, __fmaf_rn(px, nx, e.w)));
 #else
-        if (den < -Ed) continue;                       // certainly back-facing
-        const cand_mask_t bit = nk < kMaskBits ? ((cand_mask_t)1 << nk) : (cand_mask_t)0;
-        if (den <= 2.0f * Ed || den < 0x1p-100f) {     // uncertain: exact path
-            mask |= bit;
-            continue;
-        }
+        const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
         const float hx = __fmaf_rn(0.5f, nx, px), hy = __fmaf_rn(0.5f, ny, py),
                     hz = __fmaf_rn(0.5f, nz, pz);
         const float num = __fmaf_rn(hz, nz, __fmaf_rn(hy, ny, hx * nx));
-        float rinv;  // MUFU reciprocal, <= 1 ulp (normal den guaranteed above)
+#endif
+        const float den = __fmaf_rn(df[2], nz, __fmaf_rn(df[1], ny, df[0] * nx));
+        front = den >= -Ed;  // not certainly back-facing (NaN pad records: false)
+        sure = den > thr;
+        float rinv;  // MUFU reciprocal (<= 1 ulp for the `sure` ones; others are discarded)
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rinv) : "f"(den));
         const float s = num * rinv;
         const float as = fabsf(s);
-#if RFB_FAST_BOUND
-        // per-cell constants: |n|_1 <= N, |h|_inf <= P + N/2
         const float es = __fmaf_rn(K3, as, __fmaf_rn(__fmaf_rn(K2, as, K1), rinv, slack));
-#else
-        const float H = fmaxf(fabsf(hx), fmaxf(fabsf(hy), fabsf(hz)));
-        const float En = u * n1 * (Q + 8.0f * H + 2.0f * n1);
-        const float es = 2.2f * (En + as * Ed) * rinv + 8.0f * u * as + slack + 0x1p-40f * as;
-#endif
-        if (s - es <= U) mask |= bit;
-        U = fminf(U, s + es);
-#endif
-    }
-    double cx = hdr_f.x, cy = hdr_f.y, cz = hdr_f.z;  // exact widening (fp32-exact sites)
+        lb = s - es;
+        ub = s + es;
+    };
+    // neighbour j's exact coordinates: the cell header's fp32 copy (fp32-exact
+    // sites) or the fp64 site
+    double cx = hdr_f.x, cy = hdr_f.y, cz = hdr_f.z;
     constexpr bool pos64 = PK == 2;
-    if (pos64) {  // the sites themselves (the fp32 copies are rounded)
+    if (pos64) {
         const double4 si = ld_site(S.site4 + ci);
         cx = si.x;
         cy = si.y;
         cz = si.z;
     }
-    // neighbour j's exact coordinates: the widened fp32 record, or site4
-    auto site_of = [&](const float4 &e, double &x, double &y, double &z) {
-        RFB_BOUND(__float_as_int(e.w), S.n_sites);
-        if (pos64) {
-            const double4 sj = ld_site(S.site4 + __float_as_int(e.w));
-            x = sj.x;
-            y = sj.y;
-            z = sj.z;
-        } else {
-            x = e.x;
-            y = e.y;
-            z = e.z;
-        }
-    };
-    // phase 2: exact fp64 re-evaluation of the candidates, CSR order
     best_t = dinf();
     best_j = -1;
     int32_t best_k = 0x7fffffff;
-    const int32_t nexact = nk;
-    for (;;) {
-        int32_t idx;
-        if (mask) {
-            idx = (kMaskBits == 32 ? __ffs((int)mask) : __ffsll((long long)mask)) - 1;
-            mask &= mask - 1;
-        } else {
-            break;
-        }
-        const int32_t k = k0 + idx * G;
-        RFB_BOUND(k, S.n_edges);
-        const float4 e = __ldg(S.edge + k);
+    // phase 2 on slot k: kernels.py:116-133 in fp64
+    auto exact = [&](int32_t k) {
+        RFB_BOUND(k, S.n_edges + S.n_sites + 2);
         double xj, yj, zj;
-        site_of(e, xj, yj, zj);
+#if RFB_FACE_C
+        const int32_t j = __ldg(S.enbr + k);
+        RFB_BOUND(j, S.n_sites);
+        if (!pos64) {
+            const float4 hj = __ldg(reinterpret_cast<const float4 *>(S.hdr + j));
+            xj = hj.x;
+            yj = hj.y;
+            zj = hj.z;
+        }
+#else
+        const float4 ej = __ldg(S.edge + k);  // {x_j (fp32 copy), j}
+        const int32_t j = __float_as_int(ej.w);
+        RFB_BOUND(j, S.n_sites);
+        xj = ej.x;
+        yj = ej.y;
+        zj = ej.z;
+#endif
+        if (pos64) {
+            const double4 sj = ld_site(S.site4 + j);
+            xj = sj.x;
+            yj = sj.y;
+            zj = sj.z;
+        }
         const double nx = xj - cx, ny = yj - cy, nz = zj - cz;
         const double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
-        if (denom <= 0.0) continue;
+        if (denom <= 0.0) return;
         const double mx = 0.5 * (xj + cx), my = 0.5 * (yj + cy), mz = 0.5 * (zj + cz);
         const double t = ((mx - r.ox()) * nx + (my - r.oy()) * ny + (mz - r.oz()) * nz) / denom;
         if (t < best_t) {
             best_t = t;
-            best_j = __float_as_int(e.w);
+            best_j = j;
             best_k = k;
         }
-    }
-    for (int32_t idx = kMaskBits; idx < nexact; ++idx) {  // rows longer than the mask
-        const int32_t k = k0 + idx * G;
-        RFB_BOUND(k, S.n_edges);
-        const float4 e = __ldg(S.edge + k);
-        double xj, yj, zj;
-        site_of(e, xj, yj, zj);
-        const double nx = xj - cx, ny = yj - cy, nz = zj - cz;
-        const double denom = r.dx() * nx + r.dy() * ny + r.dz() * nz;
-        if (denom <= 0.0) continue;
-        const double mx = 0.5 * (xj + cx), my = 0.5 * (yj + cy), mz = 0.5 * (zj + cz);
-        const double t = ((mx - r.ox()) * nx + (my - r.oy()) * ny + (mz - r.oz()) * nz) / denom;
-        if (t < best_t) {
-            best_t = t;
-            best_j = __float_as_int(e.w);
-            best_k = k;
+    };
+    if (G == 1) {
+        // Rows start at even slots: one LDG.256 per two neighbours; slot t of
+        // the row ends up as bit (nslots - 1 - t) of `mask`.
+        const int32_t nslots = (c.k1 - c.k0 + 1) & ~1;
+#if RFB_FACE_C && RFB_PF_NBR
+        prefetch_l1(S.enbr + c.k0);  // phase 2's neighbour ids (<= 2 lines for 32 slots)
+        prefetch_l1(S.enbr + c.k1 - 1);
+#endif
+        // Final-band filter: the running band admits every neighbour whose lower
+        // bound beats the upper bound seen SO FAR, so a row visited in CSR order
+        // keeps each new running minimum (~ln(front-facing) + 0.6 ~ 2.7 per
+        // step).  Track the best upper bound's slot (t_best, its lower bound
+        // lb_best) and the smallest lower bound of every other candidate
+        // (lb_other; -inf for an uncertain-facing one): if lb_other > U at the
+        // end, every other neighbour's fp64 t is strictly larger than the
+        // best's, so phase 2 evaluates the best alone -- the same first
+        // minimum, bit for bit.
+        // (Tracked as the two smallest candidate lower bounds L1 <= L2 and L1's
+        // slot: if L2 > U_final, only L1's neighbour can beat the final band,
+        // and it is the best upper bound's (lb <= ub = U_final); folding in a
+        // non-candidate's lower bound (> U_running >= U_final) only makes the
+        // test more conservative.)
+        float L1 = kInf, L2 = kInf;
+        int32_t t1 = -1, slot = 0;
+        auto visit = [&](const float4 &e) {
+            float lb, ub;
+            bool front, sure;
+            bounds(e, lb, ub, front, sure);
+            const float lbm = sure ? lb : -kInf;  // uncertain facing: always a candidate
+            const bool cand = front && lbm <= U;
+            mask = (mask << 1) | (cand ? 1u : 0u);
+#if RFB_FINAL_BAND
+            const float lbc = front ? lbm : kInf;
+            t1 = lbc < L1 ? slot : t1;
+            L2 = fminf(L2, fmaxf(L1, lbc));
+            L1 = fminf(L1, lbc);
+#endif
+            U = sure ? fminf(U, ub) : U;
+            ++slot;
+        };
+#if RFB_EDGE_PIPE
+        // software-pipelined: pair kp + 2 is in flight while pair kp is visited
+        float4 e0, e1;
+        if (c.k0 < c.k1) ldg256(S.edge + c.k0, e0, e1);
+        RFB_PRAGMA_UNROLL(RFB_PAIR_UNROLL)
+        for (int32_t kp = c.k0; kp < c.k1; kp += 2) {
+            RFB_BOUND(kp + 1, S.n_edges + S.n_sites + 2);
+            float4 f0, f1;
+            if (kp + 2 < c.k1) ldg256(S.edge + kp + 2, f0, f1);
+            visit(e0);
+            visit(e1);
+            e0 = f0;
+            e1 = f1;
         }
-    }
-    if (G > 1) {
-#pragma unroll
-        for (int off = G / 2; off > 0; off >>= 1) {
-            double ot = __shfl_xor_sync(gmask, best_t, off, G);
-            int32_t oj = __shfl_xor_sync(gmask, best_j, off, G);
-            int32_t ok = __shfl_xor_sync(gmask, best_k, off, G);
-            if (ot < best_t || (ot == best_t && ok < best_k)) {
-                best_t = ot;
-                best_j = oj;
-                best_k = ok;
+#else
+        RFB_PRAGMA_UNROLL(RFB_PAIR_UNROLL)
+        for (int32_t kp = c.k0; kp < c.k1; kp += 2) {
+            float4 e0, e1;
+            RFB_BOUND(kp + 1, S.n_edges + S.n_sites + 2);
+#if RFB_CHECK
+            assert((reinterpret_cast<uintptr_t>(S.edge + kp) & 31) == 0);
+#endif
+            ldg256(S.edge + kp, e0, e1);
+            visit(e0);
+            visit(e1);
+        }
+#endif
+        if (nslots > kMaskBits) {  // rare: the mask lost bits -- every neighbour exactly
+            for (int32_t k = c.k0; k < c.k1; ++k) exact(k);
+            return;
+        }
+#if RFB_FINAL_BAND
+        if (t1 >= 0 && L2 > U && L1 <= U) {  // only L1's neighbour can be the first minimum
+#if RFB_PF_NEXT && !RFB_FACE_C
+            {  // the next cell is decided: start its header load under phase 2
+                const int32_t jn = __float_as_int(__ldg(S.edge + c.k0 + t1).w);
+                prefetch_l1(S.hdr + jn);
             }
+#endif
+            exact(c.k0 + t1);
+            return;
+        }
+#endif
+        while (mask) {  // highest bit = lowest slot: CSR order
+            const int b = 31 - __clz((int)mask);
+            mask &= ~(1u << b);
+            exact(c.k0 + (nslots - 1 - b));
+        }
+        return;
+    }
+    // G > 1 lanes per ray: lane gl takes slots gl, gl + G, ... (real neighbours only)
+    const int32_t k0 = c.k0 + gl;
+    int32_t nk = 0;
+    RFB_PRAGMA_UNROLL(RFB_F32_UNROLL)
+    for (int32_t k = k0; k < c.k1; k += G, ++nk) {
+        RFB_BOUND(k, S.n_edges + S.n_sites + 2);
+        const float4 e = __ldg(S.edge + k);
+        float lb, ub;
+        bool front, sure;
+        bounds(e, lb, ub, front, sure);
+        const cand_mask_t bit = nk < kMaskBits ? ((cand_mask_t)1 << nk) : (cand_mask_t)0;
+        const bool cand = front && (!sure || lb <= U);
+        mask |= cand ? bit : (cand_mask_t)0;
+        U = sure ? fminf(U, ub) : U;
+    }
+    while (mask) {  // this lane's candidates, CSR order
+        const int idx = __ffs((int)mask) - 1;
+        mask &= mask - 1;
+        exact(k0 + idx * G);
+    }
+    for (int32_t idx = kMaskBits; idx < nk; ++idx) exact(k0 + idx * G);  // beyond the mask
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        double ot = __shfl_xor_sync(gmask, best_t, off, G);
+        int32_t oj = __shfl_xor_sync(gmask, best_j, off, G);
+        int32_t ok = __shfl_xor_sync(gmask, best_k, off, G);
+        if (ot < best_t || (ot == best_t && ok < best_k)) {
+            best_t = ot;
+            best_j = oj;
+            best_k = ok;
         }
     }
 }

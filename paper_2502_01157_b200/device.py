@@ -109,12 +109,10 @@ class DeviceScene:
             self.sh_absmax_dev = torch.tensor([self.sh_absmax], dtype=torch.float32, device=dev)
             if self.packed:
                 self.cells = torch.empty((n, 8), dtype=torch.int32, device=dev)      # 32 B headers
-                # 16 B records + one readable pad record (the walk loads aligned pairs)
-                self.edges = torch.zeros((self.n_edges + 1, 4), dtype=torch.float32, device=dev)
-                self.edge_meta = None  # optional {k0, k1} per edge (unused by the walk)
+                self._alloc_edges(n, self.n_edges, dev)
                 self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
             else:
-                self.cells = self.edges = self.edge_meta = self.sh32 = None
+                self.cells = self.edges = self.edge_nbr = self.sh32 = None
             pos_d = torch.from_numpy(pos).to(dev)
             sig_d = torch.from_numpy(sigma).to(dev)
             off_d = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
@@ -122,7 +120,7 @@ class DeviceScene:
             _lib.check(self.lib.rfb_pack_scene(
                 _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
                 self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
-                _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_meta), _ptr(self.sh32),
+                _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_nbr), _ptr(self.sh32),
                 1 if self.positions_f64 else 0, _stream()),
                 "rfb_pack_scene")
             torch.cuda.current_stream().synchronize()
@@ -171,10 +169,17 @@ class DeviceScene:
             _lib.check(self.lib.rfb_pack_scene(
                 _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
                 self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
-                _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_meta), _ptr(self.sh32),
+                _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_nbr), _ptr(self.sh32),
                 1 if self.positions_f64 else 0, _stream()), "rfb_pack_scene")
         self._refresh_struct()
         self._build_locate_grid()
+
+    def _alloc_edges(self, n, n_edges, dev):
+        """Packed face records (16 B, rows padded to even length) and the
+        neighbour id of every slot: RFB_PACKED_EDGE_SLOTS(n, E) = E + n + 2."""
+        slots = n_edges + n + 2
+        self.edges = torch.zeros((slots, 4), dtype=torch.float32, device=dev)
+        self.edge_nbr = torch.full((slots,), -1, dtype=torch.int32, device=dev)
 
     LOCATE_GRID_RES = 64  # cells along the longest bounding-box axis
 
@@ -204,7 +209,7 @@ class DeviceScene:
         c.sh = self.sh.data_ptr()
         c.cells = self.cells.data_ptr() if self.packed else None
         c.edges = self.edges.data_ptr() if self.packed else None
-        c.edge_meta = None
+        c.edge_nbr = self.edge_nbr.data_ptr() if self.packed else None
         c.sh32 = self.sh32.data_ptr() if self.packed else None
         c.packed = 1 if self.packed else 0
         c.positions_f64 = 1 if (self.packed and self.positions_f64) else 0
@@ -250,15 +255,15 @@ class DeviceScene:
             self.neighbors = torch.empty(max(self.n_edges, 1), dtype=torch.int32, device=dev)
             if self.packed:
                 self.cells = torch.empty((n, 8), dtype=torch.int32, device=dev)
-                self.edges = torch.zeros((self.n_edges + 1, 4), dtype=torch.float32, device=dev)
+                self._alloc_edges(n, self.n_edges, dev)
                 self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
             else:
-                self.cells = self.edges = self.sh32 = None
-            self.edge_meta = None
+                self.cells = self.edges = self.edge_nbr = self.sh32 = None
             _lib.check(self.lib.rfb_pack_scene(
                 _ptr(pos), _ptr(sig), _ptr(self.sh), _ptr(off), _ptr(nbr), n, self.n_edges,
                 _ptr(site4), _ptr(self.offsets), _ptr(self.neighbors), _ptr(self.cells),
-                _ptr(self.edges), None, _ptr(self.sh32), 1 if self.positions_f64 else 0,
+                _ptr(self.edges), _ptr(self.edge_nbr), _ptr(self.sh32),
+                1 if self.positions_f64 else 0,
                 _stream(stream)), "rfb_pack_scene")
             self.site4 = site4
         self.hull = hull

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import hashlib
 import os
+import sys
 import time
 from dataclasses import dataclass
 
@@ -148,7 +149,7 @@ def cached_adjacency(positions: np.ndarray, tag: str, cache_dir: str | None = No
             raise RuntimeError(f"{builder} CSR for {tag} differs from the committed Qhull digest")
     if verbose:
         print(f"[synthetic] {builder} CSR for {tag}: {build_s:.1f}s"
-              + ("" if matches is None else " (== Qhull sha1)"), flush=True)
+              + ("" if matches is None else " (== Qhull sha1)"), file=sys.stderr, flush=True)
     try:
         os.makedirs(cache_dir, exist_ok=True)
         tmp = path + f".tmp{os.getpid()}.npz"

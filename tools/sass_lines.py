@@ -39,12 +39,32 @@ hdr = rows[s]
 data = [r for r in rows[s + 1:] if len(r) == len(hdr) and r[0].startswith("0x")]
 a0 = int(data[0][0], 16)
 ie, st = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
+extra = [k for k in ("Thread Instructions Executed", "L1 Tag Requests Global",
+                     "L2 Theoretical Sectors Global", "L1 Wavefronts Shared") if k in hdr]
 agg, aggi = collections.Counter(), collections.Counter()
+aggx = {k: collections.Counter() for k in extra}
+
+
+def num(v):
+    try:
+        return float(v.replace(",", ""))
+    except (ValueError, AttributeError):
+        return 0.0
+
+
 for r in data:
     ln = a2l.get(int(r[0], 16) - a0)
     agg[ln] += int(r[st] or 0)
     aggi[ln] += int(r[ie] or 0)
+    for k in extra:
+        aggx[k][ln] += num(r[hdr.index(k)])
 tot, toti = sum(agg.values()) or 1, sum(aggi.values()) or 1
+totx = {k: sum(aggx[k].values()) or 1 for k in extra}
+print("totals: stall samples %d, warp instr %.4g, " % (tot, toti)
+      + ", ".join(f"{k} {totx[k]:.4g}" for k in extra))
+short = {"Thread Instructions Executed": "thr", "L1 Tag Requests Global": "l1req",
+         "L2 Theoretical Sectors Global": "l2sec", "L1 Wavefronts Shared": "shwf"}
+print(f"{'line':24s} {'stall':>6s} {'instr':>6s} " + " ".join(f"{short[k]:>6s}" for k in extra))
 src_cache = {}
 for ln, v in agg.most_common(int(os.environ.get("TOP", "40"))):
     text = ""
@@ -53,5 +73,6 @@ for ln, v in agg.most_common(int(os.environ.get("TOP", "40"))):
         path = os.path.join("paper_2502_01157_b200/csrc", f)
         if os.path.exists(path):
             lines_ = src_cache.setdefault(path, open(path).read().split("\n"))
-            text = lines_[int(n) - 1].strip()[:70] if int(n) <= len(lines_) else ""
-    print(f"{str(ln):24s} stall {100 * v / tot:5.1f}%  instr {100 * aggi[ln] / toti:5.1f}%  {text}")
+            text = lines_[int(n) - 1].strip()[:60] if int(n) <= len(lines_) else ""
+    print(f"{str(ln):24s} {100 * v / tot:5.1f}% {100 * aggi[ln] / toti:5.1f}% "
+          + " ".join(f"{100 * aggx[k][ln] / totx[k]:5.1f}%" for k in extra) + f"  {text}")

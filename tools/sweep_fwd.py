@@ -30,6 +30,9 @@ ap.add_argument("--once", action="store_true")
 ap.add_argument("--view", type=int, default=0)
 ap.add_argument("--packed", type=int, default=-1)
 ap.add_argument("--quantile", action="store_true")
+ap.add_argument("--morton", action="store_true", help="renumber sites in Morton order")
+ap.add_argument("--force-deg0", action="store_true",
+                help="timing probe: colour from the DC band only (walk unchanged)")
 ap.add_argument("--fp64", action="store_true",
                 help="perturb the sites by 1e-12 (not fp32-exact; same Delaunay graph)")
 args = ap.parse_args()
@@ -40,7 +43,33 @@ if args.fp64:
     import numpy as np
     scene.adjacency.positions += np.random.default_rng(0).normal(0, 1e-12, scene.adjacency.positions.shape)
     scene.positions = scene.adjacency.positions
-ds = dv.DeviceScene(scene, packed=None if args.packed < 0 else bool(args.packed))
+if args.morton:  # experiment: renumber the sites along a Morton curve (same geometry)
+    from paper_2502_01157_b200.scene import AdjacencyGraph, FoamScene
+    adj = scene.adjacency
+    q = np.clip(((adj.positions - adj.positions.min(0)) / np.ptp(adj.positions, 0).max()
+                 * 1023).astype(np.int64), 0, 1023)
+    def spread(x):
+        x = x & 0x3FF
+        x = (x | (x << 16)) & 0x30000FF
+        x = (x | (x << 8)) & 0x300F00F
+        x = (x | (x << 4)) & 0x30C30C3
+        x = (x | (x << 2)) & 0x9249249
+        return x
+    key = spread(q[:, 0]) | (spread(q[:, 1]) << 1) | (spread(q[:, 2]) << 2)
+    perm = np.argsort(key, kind="stable")      # new id -> old id
+    inv = np.empty_like(perm); inv[perm] = np.arange(len(perm))
+    deg = np.diff(adj.offsets)[perm]
+    off = np.concatenate([[0], np.cumsum(deg)])
+    E = int(off[-1])
+    rid = np.repeat(np.arange(len(perm)), deg)
+    src = np.repeat(adj.offsets[perm] - off[:-1], deg) + np.arange(E)
+    vals = inv[adj.neighbors[src]]
+    nbr = vals[np.lexsort((vals, rid))]
+    a2 = AdjacencyGraph(adj.positions[perm], off, nbr)
+    scene = FoamScene(adj.positions[perm], scene.raw_density[perm], scene.sh_coeffs[perm],
+                      scene.background, a2)
+ds = dv.DeviceScene(scene, packed=None if args.packed < 0 else bool(args.packed),
+                    sh_degree=0 if args.force_deg0 else None)
 print("packed", ds.packed, "positions_f64", getattr(ds, "positions_f64", None), flush=True)
 cam = make_views(args.view + 1, args.width, args.height)[args.view]
 ws = dv.Workspace(ds.device)
@@ -75,7 +104,10 @@ for lanes in [int(x) for x in args.lanes.split(",")]:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     m = args.width * args.height
-    print(f"fwd lanes={lanes:2d}: {ms:8.2f} ms/frame  {m / ms / 1e3:8.2f} Mrays/s", flush=True)
+    import hashlib
+    h = hashlib.sha1(out.rgb.cpu().numpy().tobytes()).hexdigest()[:12]
+    print(f"fwd lanes={lanes:2d}: {ms:8.2f} ms/frame  {m / ms / 1e3:8.2f} Mrays/s  rgb sha1 {h}",
+          flush=True)
 
 if args.train:
     perm = torch.from_numpy(dv.tile_order(args.width, args.height)).cuda()
@@ -106,4 +138,5 @@ if args.train:
                                   rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo, order=None)
     torch.cuda.synchronize()
     ms = (time.perf_counter() - t0) * 1e3 / reps
-    print(f"train: {ms:8.2f} ms/step  {m / ms / 1e3:8.2f} Mrays/s", flush=True)
+    print(f"train: {ms:8.2f} ms/step  {m / ms / 1e3:8.2f} Mrays/s  loss {float(loss[0]):.12g}",
+          flush=True)
