@@ -347,7 +347,8 @@ int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb
                      void *workspace, size_t workspace_bytes, void *stream);
 
 /* Workspace bytes needed by the calls above for m rays (kind: 0 forward,
- * 1 backward/train). */
+ * 1 backward/train with any loss, 2 backward / train without the quantile
+ * term: 8-byte segment records instead of 32). */
 size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind);
 
 /* Forward + reverse pass for arbitrary colour adjoints [m][3] f64.  out.rgb

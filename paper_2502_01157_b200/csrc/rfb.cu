@@ -187,13 +187,16 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
     nseg = 0;
     cells = 0;
     visits = 0;  // cells stepped == steps taken (kernels.py:111), set on return
+    Cell cn;
+    bool have_next = false;
     for (;;) {
         steps += 1;
         if (steps > step_limit) {
             cells = step_limit;
             return RFB_STATUS_STEP_LIMIT;
         }
-        const Cell c = S.cell(i);
+        const Cell c = have_next ? cn : S.cell(i);
+        have_next = false;
 #if RFB_PF_SH
         if (PACKED) {  // the segment's SH row (read after phase 2), 192 B = 2 lines
             prefetch_l1(S.sh32 + (int64_t)i * 48);
@@ -204,7 +207,8 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
         double best_t;
         int32_t best_j;
         if constexpr (PACKED && kUseF32Filter)
-            exit_face_f32<G, PACKED>(S, i, c, c.hf, r, entry, df, gl, gmask, best_t, best_j);
+            exit_face_f32<G, PACKED>(S, i, c, c.hf, r, entry, df, gl, gmask, best_t, best_j, cn,
+                                     have_next);
         else
             exit_face<G, PACKED>(S, c, r, gl, gmask, best_t, best_j);
         if (best_j < 0 || best_t >= r.t_max()) {  // hull exit or far plane
@@ -404,12 +408,22 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
 // fp32 accumulators changes.
 // ---------------------------------------------------------------------------
 struct Scratch {
-    // one 32-byte record per segment in two 16-byte halves (one vector store each):
+    // quantile variant: one 32-byte record per segment in two 16-byte halves:
     float4 *a;      // [cap][slots]: {cell id | clamp mask << 29 (int bits), clamped colour rgb}
     double2 *b;     // [cap][slots]: {exit depth t1 (the entry of s+1),
                     //                T_before[s+1] = prod exp(-sigma*delta) (kernels.py:270-275)}
+    // L2 / adjoint variants: one 8-byte record per segment, {cell id, fp32 exit
+    // depth}; the reverse pass recomputes the colour (same fp32 arithmetic, so
+    // the same values and clamp mask) and the transmittance from the log
+    uint2 *c;       // [cap][slots]
     int64_t slots;
 };
+
+#ifndef RFB_COMPACT_REC
+#define RFB_COMPACT_REC 0  // 1: 8-byte records (4x less scratch, measured 33.4 -> 37.6 ms: colour recompute)
+#endif
+constexpr int kCompactRecBytes = 8;
+constexpr int kFullRecBytes = 32;
 
 struct Grads {
     float *g4;  // [n][4] dpos xyz, dsigma
@@ -547,8 +561,10 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
     // s_t1 / s_tb step SL doubles (the two halves of rec_b are interleaved)
     const int64_t SL4 = scr.slots;             // records per segment row
     const int64_t SLa = 4 * SL4, SL = 2 * SL4;
+    constexpr bool kCompact = !QUANT && RFB_COMPACT_REC;
     float4 *rec_a = scr.a + slot;
     double2 *rec_b = scr.b + slot;
+    uint2 *rec_c = scr.c + slot;
     const int32_t *s_cell = reinterpret_cast<const int32_t *>(rec_a);
     const double *s_t1 = reinterpret_cast<const double *>(rec_b);
     const double *s_tb = s_t1 + 1;
@@ -582,11 +598,11 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
         int status = RFB_STATUS_OK;
         float ar = 0.f, ag = 0.f, ab = 0.f;
         bool grad_ok = false;
-        double Tb = 1.0, wsum = 0.0;
+        double Tb = 1.0, wsum = 0.0, lt = 0.0;  // lt: log T (the walk's log_T)
         float cr = 0.f, cg = 0.f, cb = 0.f;
         int32_t cells = 0, visits = 0;
+        double ctol = 0.0;
         if (have_ray) {
-            double ctol;
             int32_t start;
             {
                 Ray rr;
@@ -614,9 +630,15 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                     if (G == 1 || gl == 0) {
                         RFB_BOUND(s, step_limit);
                         RFB_BOUND(slot, SL4);
-                        rec_a[s * SL4] = make_float4(__int_as_float(cell | (mask << 29)),
-                                                     (float)col[0], (float)col[1], (float)col[2]);
-                        rec_b[s * SL4] = make_double2(t1, Tn);
+                        if constexpr (kCompact) {
+                            lt -= sigma * (t1 - t0);
+                            rec_c[s * SL4] = make_uint2((unsigned)cell, __float_as_uint((float)t1));
+                        } else {
+                            rec_a[s * SL4] = make_float4(__int_as_float(cell | (mask << 29)),
+                                                         (float)col[0], (float)col[1],
+                                                         (float)col[2]);
+                            rec_b[s * SL4] = make_double2(t1, Tn);
+                        }
                     }
                 });
         }
@@ -704,7 +726,17 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
 #if RFB_REV_COLREG
         float cc0 = 0.f, cc1 = 0.f, cc2 = 0.f;  // colour of the current segment
 #endif
+        float lt1 = 0.f, lt0 = 0.f;  // compact: log T after / before segment s
         auto load_seg = [&]() {
+            if constexpr (kCompact) {
+                const uint2 rc = rec_c[s * SL4];
+                ci = (int32_t)rc.x;
+                t1 = __uint_as_float(rc.y);
+                t0 = s > 0 ? (double)__uint_as_float(rec_c[(s - 1) * SL4].y) : r.t_min();
+                tb1 = (float)Tb;  // T_end of the forward (fp64 product)
+                lt1 = (float)lt;
+                return;
+            }
 #if RFB_REV_COLREG
             const float4 ra = rec_a[s * SL4];
             const int32_t cm = __float_as_int(ra.x);
@@ -737,7 +769,10 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
             // coherence probe: the cell at the middle of each lane's path (the
             // first and last cells are shared by any rays with a common origin
             // or exit)
-            const int32_t mid = s >= 0 ? (s_cell[(s / 2) * SLa] & 0x1fffffff) : -1 - lane;
+            int32_t mid = -1 - lane;
+            if (s >= 0)
+                mid = kCompact ? (int32_t)rec_c[(s / 2) * SL4].x
+                               : (s_cell[(s / 2) * SLa] & 0x1fffffff);
             const unsigned peers = __match_any_sync(kFull, mid);
             const bool first = (__ffs(peers) - 1) == lane;
             const int groups = __popc(__ballot_sync(kFull, first && s >= 0));
@@ -768,13 +803,30 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 const double sig_d = ld_sigma(S.site4 + ci);
                 const float sig = (float)sig_d;
                 const float delta = (float)(t1 - t0);
-                const float w = tb0 - tb1;
+                float c0, c1, c2;
+                if constexpr (kCompact) {
+                    // T before s from the log (exact 1 for the first segment); the
+                    // colour as the forward computed it (kernels.py:61-73)
+                    lt0 = lt1 + sig * delta;
+                    tb0 = s > 0 ? exp2f(lt0 * 1.4426950408889634f) : 1.f;
+                    double col[3];
+                    cmask = cell_color<SHDEG, PACKED>(S, ci, bas, r, ctol, col);
+                    c0 = (float)col[0];
+                    c1 = (float)col[1];
+                    c2 = (float)col[2];
+                } else {
 #if RFB_REV_COLREG
-                const float c0 = cc0, c1 = cc1, c2 = cc2;
+                    c0 = cc0;
+                    c1 = cc1;
+                    c2 = cc2;
 #else
-                const float4 ra = rec_a[s * SL4];  // one 16-byte load: cell bits + colour
-                const float c0 = ra.y, c1 = ra.z, c2 = ra.w;
+                    const float4 ra = rec_a[s * SL4];  // one 16-byte load: cell bits + colour
+                    c0 = ra.y;
+                    c1 = ra.z;
+                    c2 = ra.w;
 #endif
+                }
+                const float w = tb0 - tb1;
                 const float common =
                     ar * (tb1 * c0 - Sr) + ag * (tb1 * c1 - Sg) + ab * (tb1 * c2 - Sb);
                 v[6] = delta * common;
@@ -819,7 +871,13 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 d_next = dd;
                 next_cell = ci;
                 s -= 1;
-                if (s >= 0) {  // segment s's end is segment s+1's start: reuse it
+                if (kCompact && s >= 0) {
+                    ci = (int32_t)rec_c[s * SL4].x;
+                    t1 = t0;
+                    t0 = s > 0 ? (double)__uint_as_float(rec_c[(s - 1) * SL4].y) : r.t_min();
+                    tb1 = tb0;
+                    lt1 = lt0;
+                } else if (s >= 0) {  // segment s's end is segment s+1's start: reuse it
 #if RFB_REV_COLREG
                     const float4 ra = rec_a[s * SL4];
                     const int32_t cm = __float_as_int(ra.x);
@@ -994,20 +1052,24 @@ __device__ __forceinline__ float pos64_widen(double xabs) {
     return (float)(2.0 * fmax(xabs, 0.25)) * (1.0f + 0x1p-20f);
 }
 
-// One row of packed edge records (rfb_device.cuh, exit_face_f32): for each CSR
-// neighbour j of site i, {n = fl32(x_j) - fl32(x_i) (fp32 subtraction, the
-// values phase 1 used to compute itself), c = fl32(0.5 |n|^2) (from the fp32 n
-// in fp64)} (RFB_FACE_C; else {fl32(x_j), j}), the neighbour id in enbr, and
-// an all-NaN pad when the degree is odd.  Returns n1max (>= max |n|_1, rounded
-// up) and X (largest |coordinate|).
-__device__ __forceinline__ float pack_row(const double *pos, int64_t i, const int64_t *nbr64,
-                                          const int32_t *nbr32, int64_t kc0, int32_t deg,
-                                          int64_t kp0, float4 *edges, int32_t *enbr,
-                                          double &xabs) {
+// Packed edge rows (rfb_device.cuh, exit_face_f32), one row per 16-lane
+// group so the record stores coalesce: for each CSR neighbour j of site i,
+// {n = fl32(x_j) - fl32(x_i) (fp32 subtraction, the values phase 1 would
+// compute itself), c = fl32(0.5 |n|^2) (from the fp32 n in fp64)}
+// (RFB_FACE_C; else {fl32(x_j), j}), the neighbour id in enbr, and an all-NaN
+// pad when the degree is odd; then the header (k0 = kp0 padded start, k1 =
+// kp0 + degree, n1max >= max |n|_1 rounded up, widened for fp64 sites).
+// kc0: the row's start in the CSR (nbr64 or nbr32).
+constexpr int kRowLanes = 16;
+__device__ __forceinline__ void pack_row(const double *pos, int64_t i, const int64_t *nbr64,
+                                         const int32_t *nbr32, int64_t kc0, int32_t deg,
+                                         int64_t kp0, float4 *edges, int32_t *enbr,
+                                         CellHdr *cells, const double *sigma, int pos64, int gl) {
+    const unsigned gmask = 0xffffu << (threadIdx.x & 16);
     const float xi = (float)pos[3 * i], yi = (float)pos[3 * i + 1], zi = (float)pos[3 * i + 2];
     float n1max = 0.f;
-    xabs = fmax(fabs(pos[3 * i]), fmax(fabs(pos[3 * i + 1]), fabs(pos[3 * i + 2])));
-    for (int32_t t = 0; t < deg; ++t) {
+    double xabs = fmax(fabs(pos[3 * i]), fmax(fabs(pos[3 * i + 1]), fabs(pos[3 * i + 2])));
+    for (int32_t t = gl; t < deg; t += kRowLanes) {
         const int64_t j = nbr64 ? nbr64[kc0 + t] : (int64_t)nbr32[kc0 + t];
         const float nx = (float)pos[3 * j] - xi, ny = (float)pos[3 * j + 1] - yi,
                     nz = (float)pos[3 * j + 2] - zi;
@@ -1022,12 +1084,28 @@ __device__ __forceinline__ float pack_row(const double *pos, int64_t i, const in
         n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
         xabs = fmax(xabs, fmax(fabs(pos[3 * j]), fmax(fabs(pos[3 * j + 1]), fabs(pos[3 * j + 2]))));
     }
+#pragma unroll
+    for (int off = kRowLanes / 2; off > 0; off >>= 1) {
+        n1max = fmaxf(n1max, __shfl_xor_sync(gmask, n1max, off, kRowLanes));
+        xabs = fmax(xabs, __shfl_xor_sync(gmask, xabs, off, kRowLanes));
+    }
+    if (gl != 0) return;
     if (deg & 1) {  // pad to an even row: rejected as back-facing by every ray (NaN)
         const float qnan = __int_as_float(0x7fffffff);
         edges[kp0 + deg] = make_float4(qnan, qnan, qnan, qnan);
         enbr[kp0 + deg] = -1;
     }
-    return n1max * (1.0f + 0x1p-20f);
+    n1max *= 1.0f + 0x1p-20f;
+    if (pos64) n1max += pos64_widen(xabs);
+    CellHdr h;
+    h.x = xi;
+    h.y = yi;
+    h.z = zi;
+    h.k0 = (int32_t)kp0;
+    h.sigma = sigma ? sigma[i] : cells[i].sigma;
+    h.k1 = (int32_t)(kp0 + deg);
+    h.n1max = n1max;
+    cells[i] = h;
 }
 
 __global__ void k_odd_rows(const int64_t *off64, int64_t n, int32_t *odd) {
@@ -1035,36 +1113,29 @@ __global__ void k_odd_rows(const int64_t *off64, int64_t n, int32_t *odd) {
     if (i < n) odd[i] = (int32_t)((off64[i + 1] - off64[i]) & 1);
 }
 
-// odd_before: exclusive prefix count of odd-degree rows (the padded row start
-// of site i is off64[i] + odd_before[i], always even).
 __global__ void k_pack_sites(const double *pos, const double *sigma, const double *sh, int64_t n,
-                             const int64_t *off64, const int64_t *nbr64, const int32_t *odd_before,
-                             double4 *site4, int32_t *off32, CellHdr *cells, float *sh32,
-                             float4 *edges, int32_t *enbr, int pos64) {
+                             const int64_t *off64, double4 *site4, int32_t *off32, float *sh32) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i > n) return;
     off32[i] = (int32_t)off64[i];
     if (i == n) return;
     site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sigma[i]);
-    if (cells) {
+    if (sh32)
         for (int k = 0; k < 16; ++k)
             for (int ch = 0; ch < 3; ++ch)
                 sh32[i * 48 + 16 * ch + k] = (float)sh[i * 48 + 3 * k + ch];  // channel-major
-        const int32_t deg = (int32_t)(off64[i + 1] - off64[i]);
-        const int64_t kp0 = off64[i] + odd_before[i];
-        double xabs;
-        float n1max = pack_row(pos, i, nbr64, nullptr, off64[i], deg, kp0, edges, enbr, xabs);
-        if (pos64) n1max += pos64_widen(xabs);
-        CellHdr h;
-        h.x = (float)pos[3 * i];
-        h.y = (float)pos[3 * i + 1];
-        h.z = (float)pos[3 * i + 2];
-        h.k0 = (int32_t)kp0;
-        h.sigma = sigma[i];
-        h.k1 = (int32_t)(kp0 + deg);
-        h.n1max = n1max;
-        cells[i] = h;
-    }
+}
+
+// odd_before: exclusive prefix count of odd-degree rows (the padded row start
+// of site i is off64[i] + odd_before[i], always even).  One row per 16 lanes.
+__global__ void k_pack_rows(const double *pos, const double *sigma, int64_t n,
+                            const int64_t *off64, const int64_t *nbr64, const int32_t *odd_before,
+                            CellHdr *cells, float4 *edges, int32_t *enbr, int pos64) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kRowLanes;
+    if (i >= n) return;
+    pack_row(pos, i, nbr64, nullptr, off64[i], (int32_t)(off64[i + 1] - off64[i]),
+             off64[i] + odd_before[i], edges, enbr, cells, sigma, pos64,
+             threadIdx.x & (kRowLanes - 1));
 }
 
 __global__ void k_pack_edges(const int64_t *nbr64, int64_t E, int32_t *nbr32) {
@@ -1350,28 +1421,25 @@ __global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double
 }
 
 // Refresh the kernel arrays from updated parameters (render.py:49-54 on
-// device): site4 = {pos, softplus(raw)}, packed headers' sigma; for moved
-// fp64 sites also the fp32 copies, the row's edge records and the widened
-// bound (k_pack_sites' rules).
+// device): site4 = {pos, softplus(raw)}, packed headers' sigma.
 __global__ void k_refresh_scene(int64_t n, const double *pos, const double *raw, double4 *site4,
-                                CellHdr *cells, const int32_t *off, const int32_t *nbr,
-                                float4 *edges, int32_t *enbr, int pos64) {
+                                CellHdr *cells) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const double x = raw[i];
     const double sig = fmax(x, 0.0) + log1p(exp(-fabs(10.0 * x))) / 10.0;
     site4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], sig);
     if (cells) cells[i].sigma = sig;
-    if (cells && pos64) {
-        CellHdr &h = cells[i];
-        double xabs;
-        const float n1max = pack_row(pos, i, nullptr, nbr, off[i], off[i + 1] - off[i], h.k0,
-                                     edges, enbr, xabs);
-        h.x = (float)pos[3 * i];
-        h.y = (float)pos[3 * i + 1];
-        h.z = (float)pos[3 * i + 2];
-        h.n1max = n1max + pos64_widen(xabs);
-    }
+}
+
+// Moved fp64 sites: the fp32 copies, the rows' records and the widened bounds
+// (k_pack_rows' rules; the row starts are unchanged), one row per 16 lanes.
+__global__ void k_refresh_rows(int64_t n, const double *pos, CellHdr *cells, const int32_t *off,
+                               const int32_t *nbr, float4 *edges, int32_t *enbr) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kRowLanes;
+    if (i >= n) return;
+    pack_row(pos, i, nullptr, nbr, off[i], off[i + 1] - off[i], cells[i].k0, edges, enbr, cells,
+             nullptr, 1, threadIdx.x & (kRowLanes - 1));
 }
 
 // ---------------------------------------------------------------------------
@@ -1565,8 +1633,9 @@ static int launch_render(const rfb_scene *scene, const Src &src, const rfb_param
     return (int)cudaGetLastError();
 }
 
-static int64_t bwd_slot_bytes(int32_t step_limit) {
-    return (int64_t)step_limit * (4 + 8 + 8 + 12);
+static int64_t bwd_slot_bytes(int32_t step_limit, bool quant) {
+    const bool compact = !quant && RFB_COMPACT_REC;
+    return (int64_t)step_limit * (compact ? kCompactRecBytes : kFullRecBytes);
 }
 
 static int64_t bwd_slots_max(bool quant) {
@@ -1629,10 +1698,10 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
         return RFB_EINVAL;
     if (train && (!targets || (q_scale > 0.0 && (!u_pairs || n_pairs <= 0)))) return RFB_EINVAL;
     if (!train && !adjoints) return RFB_EINVAL;
-    const int64_t per = bwd_slot_bytes(p->step_limit);
+    const bool quant = train && q_scale > 0.0;
+    const int64_t per = bwd_slot_bytes(p->step_limit, quant);
     if (!ws || ws_bytes < 256 + (size_t)per * kTrainBlock) return RFB_EINVAL;
     int64_t slots = (int64_t)((ws_bytes - 256) / (size_t)per);
-    const bool quant = train && q_scale > 0.0;
     if (p->lanes_per_ray < 0 || p->lanes_per_ray > 2) return RFB_EINVAL;
     const int lanes = p->lanes_per_ray > 0 ? p->lanes_per_ray : train_lanes(rays->m, quant);
     slots = std::min<int64_t>(slots, bwd_slots_max(quant));
@@ -1646,6 +1715,7 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     const int64_t cap = p->step_limit;
     char *c = base + 256;
     scr.a = reinterpret_cast<float4 *>(c);
+    scr.c = reinterpret_cast<uint2 *>(c);  // (compact and full records share the space)
     c += cap * slots * 16;
     scr.b = reinterpret_cast<double2 *>(c);
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
@@ -1745,9 +1815,12 @@ int rfb_pack_scene(const double *positions, const double *sigma, const double *s
                                       (int)n_sites, st);
     }
     k_pack_sites<<<(unsigned)((n_sites + 1 + 255) / 256), 256, 0, st>>>(
-        positions, sigma, sh, n_sites, offsets, neighbors, odd, reinterpret_cast<double4 *>(site4),
-        offsets32, reinterpret_cast<CellHdr *>(cells), sh32, reinterpret_cast<float4 *>(edges),
-        edge_nbr, positions_f64 ? 1 : 0);
+        positions, sigma, sh, n_sites, offsets, reinterpret_cast<double4 *>(site4), offsets32,
+        cells ? sh32 : nullptr);
+    if (cells)
+        k_pack_rows<<<(unsigned)((n_sites * kRowLanes + 255) / 256), 256, 0, st>>>(
+            positions, sigma, n_sites, offsets, neighbors, odd, reinterpret_cast<CellHdr *>(cells),
+            reinterpret_cast<float4 *>(edges), edge_nbr, positions_f64 ? 1 : 0);
     if (n_edges > 0)
         k_pack_edges<<<(unsigned)((n_edges + 255) / 256), 256, 0, st>>>(neighbors, n_edges,
                                                                          neighbors32);
@@ -1804,9 +1877,12 @@ int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const dou
     cudaStream_t st = (cudaStream_t)stream;
     k_refresh_scene<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, st>>>(
         scene->n_sites, positions, raw_density, (double4 *)scene->site4,
-        scene->packed ? (CellHdr *)scene->cells : nullptr, scene->offsets, scene->neighbors,
-        reinterpret_cast<float4 *>(const_cast<void *>(scene->edges)),
-        const_cast<int32_t *>(scene->edge_nbr), pos64 ? 1 : 0);
+        scene->packed ? (CellHdr *)scene->cells : nullptr);
+    if (pos64)  // after k_refresh_scene: the headers' sigma is read back
+        k_refresh_rows<<<(unsigned)((scene->n_sites * kRowLanes + 255) / 256), 256, 0, st>>>(
+            scene->n_sites, positions, (CellHdr *)scene->cells, scene->offsets,
+            scene->neighbors, reinterpret_cast<float4 *>(const_cast<void *>(scene->edges)),
+            const_cast<int32_t *>(scene->edge_nbr));
     if (refresh_sh32 && scene->packed && scene->sh32)
         k_refresh_sh32<<<(unsigned)((48 * scene->n_sites + 255) / 256), 256, 0, st>>>(
             scene->n_sites, scene->sh, (float *)scene->sh32);
@@ -1890,10 +1966,12 @@ int rfb_locate_seeded(const rfb_scene *scene, const double *queries, int64_t m,
 
 size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind) {
     if (kind == 0) return 256;
-    int64_t slots = std::min<int64_t>(std::max(bwd_slots_max(false), bwd_slots_max(true)),
+    const bool quant = kind != 2;  // 2: no quantile term (compact records)
+    int64_t slots = std::min<int64_t>(quant ? std::max(bwd_slots_max(false), bwd_slots_max(true))
+                                            : bwd_slots_max(false),
                                       ((2 * m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
     slots = std::max<int64_t>(slots, kTrainBlock);
-    return 256 + (size_t)slots * (size_t)bwd_slot_bytes(step_limit);
+    return 256 + (size_t)slots * (size_t)bwd_slot_bytes(step_limit, quant);
 }
 
 int rfb_render_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,

@@ -155,8 +155,9 @@ struct SceneView {
             const float4 *p = reinterpret_cast<const float4 *>(hdr + i);
 #if RFB_HDR256
             float4 a, b4;
-            ldg256(p, a, b4);  // whole 32-byte header in one request (sigma unused here)
+            ldg256(p, a, b4);  // whole 32-byte header in one request, sigma included
             const float2 b = make_float2(b4.z, b4.w);
+            c.sigma = __hiloint2double(__float_as_int(b4.y), __float_as_int(b4.x));
 #else
             float4 a = __ldg(p);
             const float2 b = __ldg(reinterpret_cast<const float2 *>(p + 1) + 1);
@@ -182,7 +183,7 @@ struct SceneView {
 
     __device__ __forceinline__ double sigma_of(int32_t i, const Cell &c) const {
         RFB_BOUND(i, n_sites);
-        if (PACKED) return __ldg(&hdr[i].sigma);
+        if (PACKED && !RFB_HDR256) return __ldg(&hdr[i].sigma);
         return c.sigma;
     }
 
@@ -566,8 +567,8 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #ifndef RFB_PF_NBR
 #define RFB_PF_NBR 1  // RFB_FACE_C: prefetch the row's neighbour ids into L1 for phase 2
 #endif
-#ifndef RFB_PF_NEXT
-#define RFB_PF_NEXT 0  // prefetch the next cell's header as soon as phase 1 decides it
+#ifndef RFB_NEXT_EARLY
+#define RFB_NEXT_EARLY 0  // load the next cell's header as soon as phase 1 decides it
 #endif
 
 __device__ __forceinline__ void prefetch_l1(const void *p) {
@@ -581,7 +582,8 @@ template <int G, int PK, class RayT>
 __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci, const Cell &c,
                                               const float4 &hdr_f, const RayT &r, double entry,
                                               const float *df, int gl, unsigned gmask,
-                                              double &best_t, int32_t &best_j) {
+                                              double &best_t, int32_t &best_j, Cell &next,
+                                              bool &have_next) {
     constexpr float u = 0x1p-24f;
     // q = o + entry * d in fp64 (once per step), rounded to fp32
     const double qx = r.ox() + entry * r.dx(), qy = r.oy() + entry * r.dy(), qz = r.oz() + entry * r.dz();
@@ -746,10 +748,12 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
         }
 #if RFB_FINAL_BAND
         if (t1 >= 0 && L2 > U && L1 <= U) {  // only L1's neighbour can be the first minimum
-#if RFB_PF_NEXT && !RFB_FACE_C
-            {  // the next cell is decided: start its header load under phase 2
+#if RFB_NEXT_EARLY && !RFB_FACE_C
+            {  // the next cell is decided: its header loads run under phase 2 and the
+               // segment's colour (the walk takes it instead of loading it again)
                 const int32_t jn = __float_as_int(__ldg(S.edge + c.k0 + t1).w);
-                prefetch_l1(S.hdr + jn);
+                next = S.cell(jn);
+                have_next = true;
             }
 #endif
             exact(c.k0 + t1);

@@ -564,8 +564,9 @@ class GradBuffers:
         return self.g4[:, 3]
 
 
-def backward_workspace_bytes(ds: DeviceScene, m: int, step_limit: int) -> int:
-    return int(ds.lib.rfb_workspace_bytes(int(m), int(step_limit), 1))
+def backward_workspace_bytes(ds: DeviceScene, m: int, step_limit: int, quantile=True) -> int:
+    """rfb_workspace_bytes: kind 1 (any loss) or 2 (no quantile term: compact records)."""
+    return int(ds.lib.rfb_workspace_bytes(int(m), int(step_limit), 1 if quantile else 2))
 
 
 def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start, adjoints,
@@ -577,7 +578,8 @@ def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, sta
     ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
-    ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
+    ws = (workspace or Workspace(ds.device)).get(
+        backward_workspace_bytes(ds, m, step_limit, quantile=False))
     p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
     order = _order32(order, m, ds.device, origins, directions)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
@@ -601,7 +603,8 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
     ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
-    ws = (workspace or Workspace(ds.device)).get(backward_workspace_bytes(ds, m, step_limit))
+    ws = (workspace or Workspace(ds.device)).get(
+        backward_workspace_bytes(ds, m, step_limit, quantile=quantile_scale > 0.0))
     p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
     order = _order32(order, m, ds.device, origins, directions)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
