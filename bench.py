@@ -859,7 +859,7 @@ def main():
             parity = {"tolerances": {"rgb_abs": IMG_TOL, "grad_rel": GRAD_RTOL,
                                      "cells_counters_status": "bit-exact"},
                       "forward": frame_parity(ds, views[0], probe, ref, args)}
-            if fb is not None and args.config in (1, 2):
+            if fb is not None:
                 parity["fwd_bwd"] = grad_parity(ds, sa, train_views[0], args, threads)
             parity["ok"] = all(v.get("ok", True) for v in parity.values() if isinstance(v, dict)
                                and "ok" in v)
