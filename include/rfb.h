@@ -71,7 +71,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 11
+#define RFB_ABI_VERSION 12
 
 /* Capacity (records) of the packed edge arrays rfb_pack_scene fills: rows are
  * padded to an even length, so E + n_sites slots suffice (+2 spare). */
@@ -80,12 +80,12 @@ extern "C" {
 /* Device-resident scene, produced by rfb_pack_scene.  Two layouts:
  *  generic: site4 + offsets + neighbors (+ sh), any fp64 positions;
  *  packed (packed != 0): per-site 32-byte cell headers {float x,y,z; int k0;
- *   double sigma; int k1; float n1max} and per-edge 16-byte face records
- *   {float nx,ny,nz, c} (n = x_j - x_i of the fp32 copies, c = |n|^2 / 2: the
- *   face plane relative to the cell's site) in CSR order, each row starting
- *   at an even slot k0 and padded to an even length with an all-NaN record
- *   (k1 = k0 + degree), the neighbour id of every slot in edge_nbr (-1 for a
- *   pad), plus fp32 SH (sh32) with the fp64 table kept for the exact clamp
+ *   double sigma; int k1; float n1max} and per-edge 16-byte records
+ *   {float xj,yj,zj; int j} (the neighbour's fp32 site copy and id) in CSR
+ *   order, each row starting at an even slot k0 and padded to an even length
+ *   with an all-NaN record (k1 = k0 + degree), so rows are read as whole
+ *   32-byte pairs; edge_nbr holds every slot's neighbour id (-1 for a pad);
+ *   plus fp32 SH (sh32) with the fp64 table kept for the exact clamp
  *   fallback.  With positions_f64 == 0 the fp32 coordinates are the sites
  *   themselves; with positions_f64 != 0 they are rounded copies, n1max
  *   carries the widened pre-filter bound and the exact phase reads site4
@@ -99,8 +99,7 @@ typedef struct rfb_scene {
     const int32_t *neighbors; /* [n_edges] ascending per site */
     const double *sh;         /* [n_sites][48], index k*3 + ch (render.py:53) */
     const void *cells;        /* packed: [n_sites] 32-byte headers (nullable) */
-    const void *edges;        /* packed: [RFB_PACKED_EDGE_SLOTS] 16-byte face records
-                                 (nullable); read as 32-byte aligned pairs */
+    const void *edges;        /* packed: [RFB_PACKED_EDGE_SLOTS] 16-byte records (nullable) */
     const int32_t *edge_nbr;  /* packed: [RFB_PACKED_EDGE_SLOTS] neighbour id per slot */
     const float *sh32;        /* packed: [n_sites][3][16] fp32 channel-major copy of sh (nullable)
                                  cells, edges and sh32 must be 32-byte aligned (EINVAL) */

@@ -13,7 +13,7 @@ import threading
 
 from .errors import DeviceError, ExtensionMissing
 
-ABI_VERSION = 11  # include/rfb.h RFB_ABI_VERSION
+ABI_VERSION = 12  # include/rfb.h RFB_ABI_VERSION
 _lock = threading.Lock()
 _lib = None
 

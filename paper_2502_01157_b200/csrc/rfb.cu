@@ -22,9 +22,6 @@ constexpr unsigned kFull = 0xffffffffu;
 #ifndef RFB_SUBTILE_W
 #define RFB_SUBTILE_W 4  // a warp's 32 rays cover a 4 x 8 pixel patch (measured best)
 #endif
-#ifndef RFB_PF_SH
-#define RFB_PF_SH 0  // prefetch the cell's fp32 SH row into L1 at the start of each step
-#endif
 #ifndef RFB_F32_FILTER
 #define RFB_F32_FILTER 1
 #endif
@@ -187,28 +184,18 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
     nseg = 0;
     cells = 0;
     visits = 0;  // cells stepped == steps taken (kernels.py:111), set on return
-    Cell cn;
-    bool have_next = false;
     for (;;) {
         steps += 1;
         if (steps > step_limit) {
             cells = step_limit;
             return RFB_STATUS_STEP_LIMIT;
         }
-        const Cell c = have_next ? cn : S.cell(i);
-        have_next = false;
-#if RFB_PF_SH
-        if (PACKED) {  // the segment's SH row (read after phase 2), 192 B = 2 lines
-            prefetch_l1(S.sh32 + (int64_t)i * 48);
-            prefetch_l1(S.sh32 + (int64_t)i * 48 + 32);
-        }
-#endif
+        const Cell c = S.cell(i);
         visits += c.k1 - c.k0;
         double best_t;
         int32_t best_j;
         if constexpr (PACKED && kUseF32Filter)
-            exit_face_f32<G, PACKED>(S, i, c, c.hf, r, entry, df, gl, gmask, best_t, best_j, cn,
-                                     have_next);
+            exit_face_f32<G, PACKED>(S, i, c, c.hf, r, entry, df, gl, gmask, best_t, best_j);
         else
             exit_face<G, PACKED>(S, c, r, gl, gmask, best_t, best_j);
         if (best_j < 0 || best_t >= r.t_max()) {  // hull exit or far plane
@@ -1054,11 +1041,9 @@ __device__ __forceinline__ float pos64_widen(double xabs) {
 
 // Packed edge rows (rfb_device.cuh, exit_face_f32), one row per 16-lane
 // group so the record stores coalesce: for each CSR neighbour j of site i,
-// {n = fl32(x_j) - fl32(x_i) (fp32 subtraction, the values phase 1 would
-// compute itself), c = fl32(0.5 |n|^2) (from the fp32 n in fp64)}
-// (RFB_FACE_C; else {fl32(x_j), j}), the neighbour id in enbr, and an all-NaN
-// pad when the degree is odd; then the header (k0 = kp0 padded start, k1 =
-// kp0 + degree, n1max >= max |n|_1 rounded up, widened for fp64 sites).
+// {fl32(x_j), j}, the neighbour id in enbr, and an all-NaN pad when the degree is odd; then
+// the header (k0 = kp0 padded start, k1 = kp0 + degree, n1max >= max |n|_1
+// of the fp32 n = fl32(x_j) - fl32(x_i) rounded up, widened for fp64 sites).
 // kc0: the row's start in the CSR (nbr64 or nbr32).
 constexpr int kRowLanes = 16;
 __device__ __forceinline__ void pack_row(const double *pos, int64_t i, const int64_t *nbr64,
@@ -1073,13 +1058,8 @@ __device__ __forceinline__ void pack_row(const double *pos, int64_t i, const int
         const int64_t j = nbr64 ? nbr64[kc0 + t] : (int64_t)nbr32[kc0 + t];
         const float nx = (float)pos[3 * j] - xi, ny = (float)pos[3 * j + 1] - yi,
                     nz = (float)pos[3 * j + 2] - zi;
-#if RFB_FACE_C
-        const double c = 0.5 * ((double)nx * nx + (double)ny * ny + (double)nz * nz);
-        edges[kp0 + t] = make_float4(nx, ny, nz, (float)c);
-#else
         edges[kp0 + t] = make_float4((float)pos[3 * j], (float)pos[3 * j + 1],
-                                     (float)pos[3 * j + 2], __int_as_float((int32_t)j));
-#endif
+                                                (float)pos[3 * j + 2], __int_as_float((int32_t)j));
         enbr[kp0 + t] = (int32_t)j;
         n1max = fmaxf(n1max, fabsf(nx) + fabsf(ny) + fabsf(nz));
         xabs = fmax(xabs, fmax(fabs(pos[3 * j]), fmax(fabs(pos[3 * j + 1]), fabs(pos[3 * j + 2]))));
@@ -1817,10 +1797,11 @@ int rfb_pack_scene(const double *positions, const double *sigma, const double *s
     k_pack_sites<<<(unsigned)((n_sites + 1 + 255) / 256), 256, 0, st>>>(
         positions, sigma, sh, n_sites, offsets, reinterpret_cast<double4 *>(site4), offsets32,
         cells ? sh32 : nullptr);
-    if (cells)
+    if (cells) {
         k_pack_rows<<<(unsigned)((n_sites * kRowLanes + 255) / 256), 256, 0, st>>>(
             positions, sigma, n_sites, offsets, neighbors, odd, reinterpret_cast<CellHdr *>(cells),
             reinterpret_cast<float4 *>(edges), edge_nbr, positions_f64 ? 1 : 0);
+    }
     if (n_edges > 0)
         k_pack_edges<<<(unsigned)((n_edges + 255) / 256), 256, 0, st>>>(neighbors, n_edges,
                                                                          neighbors32);
@@ -1878,11 +1859,12 @@ int rfb_refresh_scene(const rfb_scene *scene, const double *positions, const dou
     k_refresh_scene<<<(unsigned)((scene->n_sites + 255) / 256), 256, 0, st>>>(
         scene->n_sites, positions, raw_density, (double4 *)scene->site4,
         scene->packed ? (CellHdr *)scene->cells : nullptr);
-    if (pos64)  // after k_refresh_scene: the headers' sigma is read back
+    if (pos64) {  // after k_refresh_scene: the headers' sigma is read back
         k_refresh_rows<<<(unsigned)((scene->n_sites * kRowLanes + 255) / 256), 256, 0, st>>>(
             scene->n_sites, positions, (CellHdr *)scene->cells, scene->offsets,
             scene->neighbors, reinterpret_cast<float4 *>(const_cast<void *>(scene->edges)),
             const_cast<int32_t *>(scene->edge_nbr));
+    }
     if (refresh_sh32 && scene->packed && scene->sh32)
         k_refresh_sh32<<<(unsigned)((48 * scene->n_sites + 255) / 256), 256, 0, st>>>(
             scene->n_sites, scene->sh, (float *)scene->sh32);

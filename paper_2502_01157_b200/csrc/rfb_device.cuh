@@ -24,14 +24,8 @@
 #ifndef RFB_LDG256
 #define RFB_LDG256 1  // 256-bit loads for edge pairs and SH rows (packed layout)
 #endif
-#ifndef RFB_HDR256
-#define RFB_HDR256 0  // one 256-bit load per cell header
-#endif
 #ifndef RFB_SH_PIPE
 #define RFB_SH_PIPE 1  // SH colour: the next channel's row loads overlap this channel's sum
-#endif
-#ifndef RFB_EDGE_PIPE
-#define RFB_EDGE_PIPE 0  // phase 1: the next edge pair's load overlaps this pair's visit
 #endif
 #ifndef RFB_CHECK
 #define RFB_CHECK 0  // 1: device-side bounds asserts on every scene gather / record (debug build)
@@ -153,15 +147,8 @@ struct SceneView {
         Cell c;
         if (PACKED) {
             const float4 *p = reinterpret_cast<const float4 *>(hdr + i);
-#if RFB_HDR256
-            float4 a, b4;
-            ldg256(p, a, b4);  // whole 32-byte header in one request, sigma included
-            const float2 b = make_float2(b4.z, b4.w);
-            c.sigma = __hiloint2double(__float_as_int(b4.y), __float_as_int(b4.x));
-#else
             float4 a = __ldg(p);
             const float2 b = __ldg(reinterpret_cast<const float2 *>(p + 1) + 1);
-#endif
             c.hf = a;
             c.k0 = __float_as_int(a.w);
             c.k1 = __float_as_int(b.x);
@@ -183,7 +170,7 @@ struct SceneView {
 
     __device__ __forceinline__ double sigma_of(int32_t i, const Cell &c) const {
         RFB_BOUND(i, n_sites);
-        if (PACKED && !RFB_HDR256) return __ldg(&hdr[i].sigma);
+        if (PACKED) return __ldg(&hdr[i].sigma);
         return c.sigma;
     }
 
@@ -556,34 +543,23 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #define RFB_F32_UNROLL 4
 #endif
 #ifndef RFB_PAIR_UNROLL
-#define RFB_PAIR_UNROLL 2  // edge pairs per unrolled phase-1 iteration (LDG.256 path)
+#define RFB_PAIR_UNROLL 2  // edge pairs per unrolled phase-1 iteration (16-byte records)
 #endif
 #ifndef RFB_FINAL_BAND
 #define RFB_FINAL_BAND 1  // drop candidates the final band excludes (one exact evaluation)
 #endif
-#ifndef RFB_FACE_C
-#define RFB_FACE_C 0  // edge records {n, c} (1) or {x_j (fp32 copy), j} (0)
-#endif
-#ifndef RFB_PF_NBR
-#define RFB_PF_NBR 1  // RFB_FACE_C: prefetch the row's neighbour ids into L1 for phase 2
-#endif
-#ifndef RFB_NEXT_EARLY
-#define RFB_NEXT_EARLY 0  // load the next cell's header as soon as phase 1 decides it
-#endif
-
-__device__ __forceinline__ void prefetch_l1(const void *p) {
-    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
 typedef unsigned int cand_mask_t;
 constexpr int kMaskBits = 32;
 
-// PK: 1 = packed with fp32-exact sites, 2 = packed with fp64 sites (positions_f64)
+// Packed edge slot k: {fp32 copy of x_j, j}.
+__device__ __forceinline__ float4 rec_site(const float4 *edge, int32_t k) { return __ldg(edge + k); }
+
+// PK: 1 = packed with fp32-exact sites, 2 = packed with fp64 sites (positions_f64).
 template <int G, int PK, class RayT>
 __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci, const Cell &c,
                                               const float4 &hdr_f, const RayT &r, double entry,
                                               const float *df, int gl, unsigned gmask,
-                                              double &best_t, int32_t &best_j, Cell &next,
-                                              bool &have_next) {
+                                              double &best_t, int32_t &best_j) {
     constexpr float u = 0x1p-24f;
     // q = o + entry * d in fp64 (once per step), rounded to fp32
     const double qx = r.ox() + entry * r.dx(), qy = r.oy() + entry * r.dy(), qz = r.oz() + entry * r.dz();
@@ -602,17 +578,12 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     const float kInf = __int_as_float(0x7f800000);
     float U = kInf;
     cand_mask_t mask = 0;
-    // one neighbour record -> (lower bound, upper bound, back, sure)
+    // one neighbour record {fp32 x_j, j} -> (lower bound, upper bound, front, sure)
     auto bounds = [&](const float4 &e, float &lb, float &ub, bool &front, bool &sure) {
-#if RFB_FACE_C
-        const float nx = e.x, ny = e.y, nz = e.z;
-        const float num = __fmaf_rn(pz, nz, __fmaf_rn(py, ny, __fmaf_rn(px, nx, e.w)));
-#else
         const float nx = e.x - hdr_f.x, ny = e.y - hdr_f.y, nz = e.z - hdr_f.z;
         const float hx = __fmaf_rn(0.5f, nx, px), hy = __fmaf_rn(0.5f, ny, py),
                     hz = __fmaf_rn(0.5f, nz, pz);
         const float num = __fmaf_rn(hz, nz, __fmaf_rn(hy, ny, hx * nx));
-#endif
         const float den = __fmaf_rn(df[2], nz, __fmaf_rn(df[1], ny, df[0] * nx));
         front = den >= -Ed;  // not certainly back-facing (NaN pad records: false)
         sure = den > thr;
@@ -624,8 +595,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
         lb = s - es;
         ub = s + es;
     };
-    // neighbour j's exact coordinates: the cell header's fp32 copy (fp32-exact
-    // sites) or the fp64 site
+    // the cell's exact site: its fp32 header copy (fp32-exact sites) or the fp64 site
     double cx = hdr_f.x, cy = hdr_f.y, cz = hdr_f.z;
     constexpr bool pos64 = PK == 2;
     if (pos64) {
@@ -640,24 +610,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     // phase 2 on slot k: kernels.py:116-133 in fp64
     auto exact = [&](int32_t k) {
         RFB_BOUND(k, S.n_edges + S.n_sites + 2);
-        double xj, yj, zj;
-#if RFB_FACE_C
-        const int32_t j = __ldg(S.enbr + k);
-        RFB_BOUND(j, S.n_sites);
-        if (!pos64) {
-            const float4 hj = __ldg(reinterpret_cast<const float4 *>(S.hdr + j));
-            xj = hj.x;
-            yj = hj.y;
-            zj = hj.z;
-        }
-#else
-        const float4 ej = __ldg(S.edge + k);  // {x_j (fp32 copy), j}
+        const float4 ej = rec_site(S.edge, k);  // (in L1: phase 1 just read it)
         const int32_t j = __float_as_int(ej.w);
         RFB_BOUND(j, S.n_sites);
-        xj = ej.x;
-        yj = ej.y;
-        zj = ej.z;
-#endif
+        double xj = ej.x, yj = ej.y, zj = ej.z;
         if (pos64) {
             const double4 sj = ld_site(S.site4 + j);
             xj = sj.x;
@@ -676,29 +632,19 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
         }
     };
     if (G == 1) {
-        // Rows start at even slots: one LDG.256 per two neighbours; slot t of
-        // the row ends up as bit (nslots - 1 - t) of `mask`.
-        const int32_t nslots = (c.k1 - c.k0 + 1) & ~1;
-#if RFB_FACE_C && RFB_PF_NBR
-        prefetch_l1(S.enbr + c.k0);  // phase 2's neighbour ids (<= 2 lines for 32 slots)
-        prefetch_l1(S.enbr + c.k1 - 1);
-#endif
         // Final-band filter: the running band admits every neighbour whose lower
         // bound beats the upper bound seen SO FAR, so a row visited in CSR order
         // keeps each new running minimum (~ln(front-facing) + 0.6 ~ 2.7 per
-        // step).  Track the best upper bound's slot (t_best, its lower bound
-        // lb_best) and the smallest lower bound of every other candidate
-        // (lb_other; -inf for an uncertain-facing one): if lb_other > U at the
-        // end, every other neighbour's fp64 t is strictly larger than the
-        // best's, so phase 2 evaluates the best alone -- the same first
-        // minimum, bit for bit.
-        // (Tracked as the two smallest candidate lower bounds L1 <= L2 and L1's
-        // slot: if L2 > U_final, only L1's neighbour can beat the final band,
-        // and it is the best upper bound's (lb <= ub = U_final); folding in a
-        // non-candidate's lower bound (> U_running >= U_final) only makes the
-        // test more conservative.)
+        // step).  Only the neighbours whose lower bound beats the FINAL band can
+        // be the reference's first minimum; tracked as the two smallest
+        // candidate lower bounds L1 <= L2 and L1's slot: if L2 > U_final, only
+        // L1's neighbour can beat the final band, and it is the best upper
+        // bound's (lb <= ub = U_final), so phase 2 evaluates it alone -- the
+        // same first minimum, bit for bit.  (Folding in a non-candidate's lower
+        // bound, > U_running >= U_final, only makes the test more conservative.)
         float L1 = kInf, L2 = kInf;
         int32_t t1 = -1, slot = 0;
+        // slot t of the row ends up as bit (nslots - 1 - t) of `mask`
         auto visit = [&](const float4 &e) {
             float lb, ub;
             bool front, sure;
@@ -715,21 +661,8 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
             U = sure ? fminf(U, ub) : U;
             ++slot;
         };
-#if RFB_EDGE_PIPE
-        // software-pipelined: pair kp + 2 is in flight while pair kp is visited
-        float4 e0, e1;
-        if (c.k0 < c.k1) ldg256(S.edge + c.k0, e0, e1);
-        RFB_PRAGMA_UNROLL(RFB_PAIR_UNROLL)
-        for (int32_t kp = c.k0; kp < c.k1; kp += 2) {
-            RFB_BOUND(kp + 1, S.n_edges + S.n_sites + 2);
-            float4 f0, f1;
-            if (kp + 2 < c.k1) ldg256(S.edge + kp + 2, f0, f1);
-            visit(e0);
-            visit(e1);
-            e0 = f0;
-            e1 = f1;
-        }
-#else
+        // rows start at even slots: one LDG.256 per two neighbours (NaN pads)
+        const int32_t nslots = (c.k1 - c.k0 + 1) & ~1;
         RFB_PRAGMA_UNROLL(RFB_PAIR_UNROLL)
         for (int32_t kp = c.k0; kp < c.k1; kp += 2) {
             float4 e0, e1;
@@ -741,29 +674,20 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
             visit(e0);
             visit(e1);
         }
-#endif
         if (nslots > kMaskBits) {  // rare: the mask lost bits -- every neighbour exactly
             for (int32_t k = c.k0; k < c.k1; ++k) exact(k);
-            return;
         }
 #if RFB_FINAL_BAND
-        if (t1 >= 0 && L2 > U && L1 <= U) {  // only L1's neighbour can be the first minimum
-#if RFB_NEXT_EARLY && !RFB_FACE_C
-            {  // the next cell is decided: its header loads run under phase 2 and the
-               // segment's colour (the walk takes it instead of loading it again)
-                const int32_t jn = __float_as_int(__ldg(S.edge + c.k0 + t1).w);
-                next = S.cell(jn);
-                have_next = true;
-            }
-#endif
+        else if (t1 >= 0 && L2 > U && L1 <= U) {  // only L1's neighbour can be the first minimum
             exact(c.k0 + t1);
-            return;
         }
 #endif
-        while (mask) {  // highest bit = lowest slot: CSR order
-            const int b = 31 - __clz((int)mask);
-            mask &= ~(1u << b);
-            exact(c.k0 + (nslots - 1 - b));
+        else {
+            while (mask) {  // highest bit = lowest slot: CSR order
+                const int b = 31 - __clz((int)mask);
+                mask &= ~(1u << b);
+                exact(c.k0 + (nslots - 1 - b));
+            }
         }
         return;
     }
@@ -773,7 +697,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     RFB_PRAGMA_UNROLL(RFB_F32_UNROLL)
     for (int32_t k = k0; k < c.k1; k += G, ++nk) {
         RFB_BOUND(k, S.n_edges + S.n_sites + 2);
-        const float4 e = __ldg(S.edge + k);
+        const float4 e = rec_site(S.edge, k);
         float lb, ub;
         bool front, sure;
         bounds(e, lb, ub, front, sure);

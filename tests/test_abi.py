@@ -41,7 +41,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_errors(lib):
-    assert lib.rfb_abi_version() == 11
+    assert lib.rfb_abi_version() == 12
     assert lib.rfb_error_string(0) == b"ok"
     assert lib.rfb_error_string(-1) == b"invalid argument"
 
