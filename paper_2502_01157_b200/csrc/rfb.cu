@@ -1382,7 +1382,10 @@ __global__ void k_post_adam(int64_t n, const float *g4, const float *gsh, double
             const unsigned bits = __float_as_uint(__double2float_ru(fabs(sh[t])));
             const unsigned am = __activemask();
             const unsigned mx = __reduce_max_sync(am, bits);
-            if ((int)(threadIdx.x & 31) == __ffs(am) - 1) atomicMax(absmax_bits, mx);
+            // the bound only grows, and rarely: skip the (single-address) atomic
+            // unless this warp's maximum exceeds the value already stored
+            if ((int)(threadIdx.x & 31) == __ffs(am) - 1 && mx > __ldcg(absmax_bits))
+                atomicMax(absmax_bits, mx);
         }
         return;
     }
