@@ -71,7 +71,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 12
+#define RFB_ABI_VERSION 13
 
 /* Capacity (records) of the packed edge arrays rfb_pack_scene fills: rows are
  * padded to an even length, so E + n_sites slots suffice (+2 spare). */
@@ -114,6 +114,10 @@ typedef struct rfb_scene {
     const float *sh_absmax_dev; /* nullable device scalar; when set the kernels read the colour
                                  bound from it instead of sh_absmax (rfb_post_grad_adam raises it
                                  after every update, so a training scene needs no host refresh) */
+    const int32_t *pk_of;     /* packed, nullable: [n_sites] packed index of each site (the
+                                 packed arrays cells/edges/edge_nbr/sh32 are in the internal
+                                 Morton order rfb_pack_scene chose; NULL = site order) */
+    const int32_t *pk_id;     /* packed, nullable: [n_sites] site id of each packed index */
 } rfb_scene;
 
 /* Walk parameters (tracer/rays.py:12-14). */
@@ -196,18 +200,23 @@ int rfb_host_device_pointer(void *host, void **device_ptr);
  * edge_nbr hold RFB_PACKED_EDGE_SLOTS(n, E) slots).  positions_f64 must be
  * nonzero unless every coordinate is exactly representable in fp32 (and
  * stays so: set it for scenes whose sites will move); the same value goes
- * into rfb_scene.positions_f64.  Uses stream-ordered scratch
- * (cudaMallocAsync) for the padded row starts: not a hot-path call. */
+ * into rfb_scene.positions_f64.  pk_of / pk_id (nullable, both or neither,
+ * [n] each): when given, the packed arrays are laid out in a Morton order of
+ * the sites (cells a ray visits in turn sit near each other) and the two
+ * permutations are written there; every row keeps its site's CSR order, and
+ * all inputs and outputs of the other calls stay in site ids.  Uses
+ * stream-ordered scratch (cudaMallocAsync): not a hot-path call. */
 int rfb_pack_scene(const double *positions, const double *sigma, const double *sh,
                    const int64_t *offsets, const int64_t *neighbors, int64_t n_sites,
                    int64_t n_edges, double *site4, int32_t *offsets32, int32_t *neighbors32,
-                   void *cells, void *edges, int32_t *edge_nbr, float *sh32,
-                   int32_t positions_f64, void *stream);
+                   void *cells, void *edges, int32_t *edge_nbr, float *sh32, int32_t *pk_of,
+                   int32_t *pk_id, int32_t positions_f64, void *stream);
 
 /* sigma = softplus_10(raw) for device-resident training, written to out
- * (nullable), site4[:,3] (nullable) and the packed headers (nullable). */
+ * (nullable), site4[:,3] (nullable) and the packed headers (nullable; rows
+ * permuted by pk_of when given). */
 int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void *cells,
-                 void *stream);
+                 const int32_t *pk_of, void *stream);
 
 /* Fused gradient post-processing + Adam after the gradient all-reduce
  * (optim/train.py:195-209 + optim/adam.py:15-31).  grads_flat is the [n*52]
@@ -221,11 +230,12 @@ int rfb_softplus(const double *raw, int64_t n, double *out, double *site4, void 
  * from the updated coefficients in the same pass.  sh_absmax_dev (nullable):
  * the scene's device colour bound (rfb_scene.sh_absmax_dev), raised to at
  * least max |sh| of the updated coefficients (a running maximum: never
- * lowered, so it stays an upper bound of every coefficient). */
+ * lowered, so it stays an upper bound of every coefficient).  pk_of: the
+ * scene's packed order (rfb_scene.pk_of) for the sh32 rows, nullable. */
 int rfb_post_grad_adam(int64_t n_sites, const float *grads_flat, double *positions,
                        double *raw_density, double *sh, double *adam_state, double clip,
                        int32_t sh_warmup, int32_t update_positions, const double *hyper,
-                       float *sh32, float *sh_absmax_dev, void *stream);
+                       float *sh32, float *sh_absmax_dev, const int32_t *pk_of, void *stream);
 
 /* After a parameter update: site4 = {positions, softplus(raw)}, packed
  * headers' sigma and, when refresh_sh32 is nonzero, the fp32 SH copy are

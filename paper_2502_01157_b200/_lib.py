@@ -13,7 +13,7 @@ import threading
 
 from .errors import DeviceError, ExtensionMissing
 
-ABI_VERSION = 12  # include/rfb.h RFB_ABI_VERSION
+ABI_VERSION = 13  # include/rfb.h RFB_ABI_VERSION
 _lock = threading.Lock()
 _lib = None
 
@@ -38,6 +38,8 @@ class rfb_scene(ctypes.Structure):
         ("positions_f64", ctypes.c_int32),
         ("background", ctypes.c_double * 3),
         ("sh_absmax_dev", ctypes.c_void_p),
+        ("pk_of", ctypes.c_void_p),
+        ("pk_id", ctypes.c_void_p),
     ]
 
 
@@ -122,10 +124,10 @@ SIGNATURES = {
     "rfb_device_ok": (ctypes.c_int, []),
     "rfb_host_device_pointer": (ctypes.c_int, [VP, P(VP)]),
     "rfb_pack_scene": (ctypes.c_int, [VP, VP, VP, VP, VP, I64, I64, VP, VP, VP, VP, VP, VP, VP,
-                                      I32, VP]),
-    "rfb_softplus": (ctypes.c_int, [VP, I64, VP, VP, VP, VP]),
+                                      VP, VP, I32, VP]),
+    "rfb_softplus": (ctypes.c_int, [VP, I64, VP, VP, VP, VP, VP]),
     "rfb_camera_rays": (ctypes.c_int, [P(rfb_camera), I64, I64, VP, VP]),
-    "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP, VP, VP]),
+    "rfb_post_grad_adam": (ctypes.c_int, [I64, VP, VP, VP, VP, VP, F64, I32, I32, VP, VP, VP, VP, VP]),
     "rfb_refresh_scene": (ctypes.c_int, [P(rfb_scene), VP, VP, I32, VP]),
     "rfb_locate": (ctypes.c_int, [P(rfb_scene), VP, I64, I32, VP, VP]),
     "rfb_build_locate_grid": (ctypes.c_int, [P(rfb_scene), P(rfb_locate_grid), VP]),

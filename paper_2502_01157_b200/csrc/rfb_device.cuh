@@ -128,6 +128,9 @@ struct SceneView {
     const CellHdr *hdr;     // PACKED
     const float4 *edge;     // PACKED
     const int32_t *enbr;    // PACKED: neighbour id per packed edge slot (-1: row pad)
+    // PACKED: the packed arrays are in the scene's internal (Morton) order; pk_of maps
+    // a site id to its packed index, pk_id back (nullable: identity)
+    const int32_t *pk_of, *pk_id;
     const double4 *site4;   // both (backward gradients use fp64 positions)
     const int32_t *off;     // generic
     const int32_t *nbr;     // generic
@@ -137,6 +140,14 @@ struct SceneView {
     const float *absmax_p;  // nullable device copy of the bound (training: raised by Adam)
     double bg[3];
     int64_t n_sites, n_edges;  // extents (RFB_CHECK builds assert every index against them)
+
+    // site id <-> packed index (identity for the generic layout)
+    __device__ __forceinline__ int32_t to_pk(int32_t i) const {
+        return (PACKED && pk_of) ? __ldg(pk_of + i) : i;
+    }
+    __device__ __forceinline__ int32_t to_id(int32_t u) const {
+        return (PACKED && pk_id) ? __ldg(pk_id + u) : u;
+    }
 
     // Per-step cell record.  PACKED: only the fp32 header fields (the walk
     // widens x,y,z exactly where the fp64 path needs them and fetches sigma
@@ -182,7 +193,7 @@ struct SceneView {
             j = __ldg(enbr + k);
             RFB_BOUND(j, n_sites);
             if (PACKED == 2) {
-                const double4 s = ld_site(site4 + j);
+                const double4 s = ld_site(site4 + to_id(j));
                 x = s.x;
                 y = s.y;
                 z = s.z;
@@ -325,7 +336,8 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
     for (int ch = 0; ch < 3; ++ch) {
         double a = acc[ch];
         if (PACKED && fabs(a) <= tol)  // ambiguous clamp: redo in fp64 (exact)
-            a = exact_channel(S.sh + (int64_t)i * 48, ch, NB, ray.dx(), ray.dy(), ray.dz());
+            a = exact_channel(S.sh + (int64_t)S.to_id(i) * 48, ch, NB, ray.dx(), ray.dy(),
+                              ray.dz());
         if (a < 0.0) {
             a = 0.0;
             mask |= 1 << ch;
@@ -599,7 +611,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     double cx = hdr_f.x, cy = hdr_f.y, cz = hdr_f.z;
     constexpr bool pos64 = PK == 2;
     if (pos64) {
-        const double4 si = ld_site(S.site4 + ci);
+        const double4 si = ld_site(S.site4 + S.to_id(ci));
         cx = si.x;
         cy = si.y;
         cz = si.z;
@@ -615,7 +627,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
         RFB_BOUND(j, S.n_sites);
         double xj = ej.x, yj = ej.y, zj = ej.z;
         if (pos64) {
-            const double4 sj = ld_site(S.site4 + j);
+            const double4 sj = ld_site(S.site4 + S.to_id(j));
             xj = sj.x;
             yj = sj.y;
             zj = sj.z;

@@ -17,6 +17,7 @@ in the sm_100a kernels behind the C ABI (include/rfb.h).  Layout in HBM
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -113,6 +114,7 @@ class DeviceScene:
                 self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
             else:
                 self.cells = self.edges = self.edge_nbr = self.sh32 = None
+                self.pk_of = self.pk_id = None
             pos_d = torch.from_numpy(pos).to(dev)
             sig_d = torch.from_numpy(sigma).to(dev)
             off_d = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
@@ -121,7 +123,7 @@ class DeviceScene:
                 _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
                 self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
                 _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_nbr), _ptr(self.sh32),
-                1 if self.positions_f64 else 0, _stream()),
+                _ptr(self.pk_of), _ptr(self.pk_id), 1 if self.positions_f64 else 0, _stream()),
                 "rfb_pack_scene")
             torch.cuda.current_stream().synchronize()
             self._csr64 = (off_d, nbr_d) if keep_csr64 else None
@@ -170,16 +172,26 @@ class DeviceScene:
                 _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
                 self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
                 _ptr(self.cells), _ptr(self.edges), _ptr(self.edge_nbr), _ptr(self.sh32),
-                1 if self.positions_f64 else 0, _stream()), "rfb_pack_scene")
+                _ptr(self.pk_of), _ptr(self.pk_id), 1 if self.positions_f64 else 0, _stream()),
+                "rfb_pack_scene")
         self._refresh_struct()
         self._build_locate_grid()
 
+    # the packed arrays in a Morton order of the sites (rfb_pack_scene pk_of/pk_id):
+    # cells a ray visits in turn sit near each other; ids outside stay site ids
+    PACKED_ORDER = os.environ.get("RFB_PACKED_ORDER", "1") != "0"
+
     def _alloc_edges(self, n, n_edges, dev):
-        """Packed face records (16 B, rows padded to even length) and the
-        neighbour id of every slot: RFB_PACKED_EDGE_SLOTS(n, E) = E + n + 2."""
+        """Packed records (16 B, rows padded to even length), the neighbour of
+        every slot (RFB_PACKED_EDGE_SLOTS(n, E) = E + n + 2) and the packed order."""
         slots = n_edges + n + 2
         self.edges = torch.zeros((slots, 4), dtype=torch.float32, device=dev)
         self.edge_nbr = torch.full((slots,), -1, dtype=torch.int32, device=dev)
+        if self.PACKED_ORDER:
+            self.pk_of = torch.empty(n, dtype=torch.int32, device=dev)
+            self.pk_id = torch.empty(n, dtype=torch.int32, device=dev)
+        else:
+            self.pk_of = self.pk_id = None
 
     LOCATE_GRID_RES = 64  # cells along the longest bounding-box axis
 
@@ -210,6 +222,8 @@ class DeviceScene:
         c.cells = self.cells.data_ptr() if self.packed else None
         c.edges = self.edges.data_ptr() if self.packed else None
         c.edge_nbr = self.edge_nbr.data_ptr() if self.packed else None
+        c.pk_of = self.pk_of.data_ptr() if (self.packed and self.pk_of is not None) else None
+        c.pk_id = self.pk_id.data_ptr() if (self.packed and self.pk_id is not None) else None
         c.sh32 = self.sh32.data_ptr() if self.packed else None
         c.packed = 1 if self.packed else 0
         c.positions_f64 = 1 if (self.packed and self.positions_f64) else 0
@@ -259,11 +273,12 @@ class DeviceScene:
                 self.sh32 = torch.empty((n, 48), dtype=torch.float32, device=dev)
             else:
                 self.cells = self.edges = self.edge_nbr = self.sh32 = None
+                self.pk_of = self.pk_id = None
             _lib.check(self.lib.rfb_pack_scene(
                 _ptr(pos), _ptr(sig), _ptr(self.sh), _ptr(off), _ptr(nbr), n, self.n_edges,
                 _ptr(site4), _ptr(self.offsets), _ptr(self.neighbors), _ptr(self.cells),
-                _ptr(self.edges), _ptr(self.edge_nbr), _ptr(self.sh32),
-                1 if self.positions_f64 else 0,
+                _ptr(self.edges), _ptr(self.edge_nbr), _ptr(self.sh32), _ptr(self.pk_of),
+                _ptr(self.pk_id), 1 if self.positions_f64 else 0,
                 _stream(stream)), "rfb_pack_scene")
             self.site4 = site4
         self.hull = hull
@@ -275,7 +290,8 @@ class DeviceScene:
     def set_raw_density(self, raw: torch.Tensor, stream=None):
         raw = raw.to(self.device, torch.float64).contiguous()
         _lib.check(self.lib.rfb_softplus(_ptr(raw), self.n_sites, None, _ptr(self.site4),
-                                         _ptr(self.cells), _stream(stream)), "rfb_softplus")
+                                         _ptr(self.cells), _ptr(self.pk_of), _stream(stream)),
+                   "rfb_softplus")
 
     def default_t_max(self, origins: np.ndarray) -> float:
         """Batch fallback t_max (render.py:72-76)."""

@@ -99,7 +99,7 @@ class DeviceTrainer:
             dv._ptr(self.sh), dv._ptr(self.adam_state), float(hyper.grad_clip),
             1 if sh_warmup else 0, 1 if do_pos else 0,
             hp.ctypes.data_as(ctypes.c_void_p), sh32, dv._ptr(self.ds.sh_absmax_dev),
-            dv._stream(stream)), "rfb_post_grad_adam")
+            dv._ptr(self.ds.pk_of), dv._stream(stream)), "rfb_post_grad_adam")
         _lib.check(self.lib.rfb_refresh_scene(self.ds.c, dv._ptr(self.positions),
                                               dv._ptr(self.raw), 0 if fuse else 1,
                                               dv._stream(stream)),

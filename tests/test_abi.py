@@ -41,7 +41,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_errors(lib):
-    assert lib.rfb_abi_version() == 12
+    assert lib.rfb_abi_version() == 13
     assert lib.rfb_error_string(0) == b"ok"
     assert lib.rfb_error_string(-1) == b"invalid argument"
 
@@ -97,6 +97,6 @@ def test_argument_validation_without_device(lib):
     cam = _lib.rfb_camera()
     assert lib.rfb_camera_rays(ctypes.byref(cam), 0, 1, None, None) == -1
     assert lib.rfb_pack_scene(None, None, None, None, None, 0, 0, None, None, None, None, None,
-                              None, None, 0, None) == -1
-    assert lib.rfb_softplus(None, 1, None, None, None, None) == -1
+                              None, None, None, None, 0, None) == -1
+    assert lib.rfb_softplus(None, 1, None, None, None, None, None) == -1
     assert lib.rfb_host_device_pointer(None, None) == -1

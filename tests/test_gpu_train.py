@@ -40,6 +40,8 @@ def test_post_grad_adam_matches_reference(cuda_ok):
     np.testing.assert_allclose(s4[:, 3], softplus(g["raw2"]), rtol=1e-13)
     if tr.ds.sh32 is not None:  # fp32 channel-major copy written by the Adam pass
         sh32 = tr.ds.sh32.cpu().numpy().reshape(n, 3, 16)
+        if tr.ds.pk_of is not None:  # rows in the packed (Morton) order
+            sh32 = sh32[tr.ds.pk_of.cpu().numpy()]
         np.testing.assert_array_equal(sh32, g["sh2"].astype(np.float32).transpose(0, 2, 1))
 
 
