@@ -89,22 +89,35 @@ class DeviceScene:
         self.width_floor = WIDTH_FLOOR_SCALE * self.diagonal
         self.background = np.asarray(background, dtype=np.float64).copy()
         sh = np.ascontiguousarray(np.asarray(sh_flat, dtype=np.float64).reshape(n, 48))
-        self.sh_degree = sh_degree_of(sh) if sh_degree is None else int(sh_degree)
-        # fp32 upper bound of max |coefficient| (colour rounding bound, packed layout)
-        self.sh_absmax = float(np.float32(np.abs(sh).max() if sh.size else 0.0) * np.float32(1.0001))
         sigma = np.ascontiguousarray(sigma, dtype=np.float64)
-        # packed layout by default; positions that do not survive an fp32 round trip
-        # (or that will move, positions_f64=True) use the widened pre-filter bound
-        # and exact phase from site4 (rfb_scene.positions_f64)
         self.packed = True if packed is None else bool(packed)
-        exact32 = bool(np.array_equal(pos.astype(np.float32).astype(np.float64), pos))
-        self.positions_f64 = (not exact32) if positions_f64 is None else bool(positions_f64)
         dev = self.device
         with torch.cuda.device(dev):
+            # upload first; the scene statistics the layout needs are reductions on
+            # the device (one sync) instead of host passes over the 384 MB SH table
+            self.sh = torch.from_numpy(sh).to(dev)
+            pos_d = torch.from_numpy(pos).to(dev)
+            sig_d = torch.from_numpy(sigma).to(dev)
+            off_d = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
+            nbr_d = torch.from_numpy(np.ascontiguousarray(neighbors, dtype=np.int64)).to(dev)
+            if n:
+                st = torch.stack([self.sh.abs().max(),
+                                  (self.sh.view(n, 16, 3)[:, 1:, :] != 0).any().double(),
+                                  (pos_d.float().double() != pos_d).any().double()]).cpu()
+                absmax, any_hi, not_exact32 = float(st[0]), bool(st[1] > 0), bool(st[2] > 0)
+            else:
+                absmax, any_hi, not_exact32 = 0.0, False, False
+            # SH degree 0 when bands 1..15 are all zero (sh_degree_of), else 3
+            self.sh_degree = (3 if any_hi else 0) if sh_degree is None else int(sh_degree)
+            # fp32 upper bound of max |coefficient| (colour rounding bound, packed layout)
+            self.sh_absmax = float(np.float32(absmax) * np.float32(1.0001))
+            # packed layout by default; positions that do not survive an fp32 round trip
+            # (or that will move, positions_f64=True) use the widened pre-filter bound
+            # and exact phase from site4 (rfb_scene.positions_f64)
+            self.positions_f64 = not_exact32 if positions_f64 is None else bool(positions_f64)
             self.site4 = torch.empty((n, 4), dtype=torch.float64, device=dev)
             self.offsets = torch.empty(n + 1, dtype=torch.int32, device=dev)
             self.neighbors = torch.empty(max(self.n_edges, 1), dtype=torch.int32, device=dev)
-            self.sh = torch.from_numpy(sh).to(dev)
             # device copy of the colour bound: rfb_post_grad_adam raises it when a
             # training step grows a coefficient (the kernels read this copy)
             self.sh_absmax_dev = torch.tensor([self.sh_absmax], dtype=torch.float32, device=dev)
@@ -115,10 +128,6 @@ class DeviceScene:
             else:
                 self.cells = self.edges = self.edge_nbr = self.sh32 = None
                 self.pk_of = self.pk_id = None
-            pos_d = torch.from_numpy(pos).to(dev)
-            sig_d = torch.from_numpy(sigma).to(dev)
-            off_d = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
-            nbr_d = torch.from_numpy(np.ascontiguousarray(neighbors, dtype=np.int64)).to(dev)
             _lib.check(self.lib.rfb_pack_scene(
                 _ptr(pos_d), _ptr(sig_d), _ptr(self.sh), _ptr(off_d), _ptr(nbr_d), n,
                 self.n_edges, _ptr(self.site4), _ptr(self.offsets), _ptr(self.neighbors),
