@@ -896,7 +896,6 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 if (in) {
                     const float *b = &s_basis[warp][lane][0];
                     RFB_BOUND(lc, S.n_sites);
-                    RFB_BOUND(lc, S.n_sites);
             float *row = gr.sh + 48 * (int64_t)lc;
                     if (v[0] != 0.f || v[1] != 0.f || v[2] != 0.f) {
 #pragma unroll

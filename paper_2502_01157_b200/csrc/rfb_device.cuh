@@ -165,7 +165,8 @@ struct SceneView {
             c.k1 = __float_as_int(b.x);
             c.n1max = b.y;
             RFB_BOUND(c.k0, c.k1 + 1);
-            RFB_BOUND(c.k1, n_edges + 1);
+            RFB_BOUND(c.k1, n_edges + n_sites + 3);  // padded rows (RFB_PACKED_EDGE_SLOTS)
+            RFB_BOUND(c.k0 & 1, 1);                  // rows start at even slots
         } else {
             double4 s = ld_site(site4 + i);
             c.x = s.x;
