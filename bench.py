@@ -452,7 +452,8 @@ def grad_parity(ds, sa, cam, args, threads):
     loss = torch.zeros(2, dtype=torch.float64, device=ds.device)
     res = dv.train_batch_device(ds, d(o), d(dirs), d(np.zeros(m)), d(np.full(m, t_max)),
                                 d(np.full(m, start), torch.int32), d(targets), gb, loss,
-                                rgb_scale=1.0 / (3 * m), f64=True, order=None)
+                                rgb_scale=1.0 / (3 * m), f64=True, order=None,
+                                view_dirs=dv.view_cone(cam))
     torch.cuda.synchronize()
 
     def rel(a, b):
@@ -552,7 +553,19 @@ def main():
     failed = int((probe.status != 0).sum().item())
     m0 = W * H
     sh_bytes = 192 if ds.sh_degree == 3 else 12
-    bytes_per_frame = algorithmic_bytes(C_tot, V_tot, N_tot, m0, sh_bytes)
+    # records the walk actually reads: the view-culled rows leave out the faces that are
+    # back-facing for the whole frame (rfb_cull_scene); the visit counter adds them back
+    # (n1max's low bits), so count them once more on the view with those bits cleared
+    V_walk = V_tot
+    if ds.packed and dv.view_cone(views[0]) is not None and ds.VIEW_CULL:
+        ds.view(dv.view_cone(views[0]))
+        ds._view_cells[:, 7].bitwise_and_(~31)
+        diag = dv.render_image_device(ds, views[0], per_ray=False, lanes_per_ray=lanes,
+                                      workspace=ws, cull="last")
+        torch.cuda.synchronize()
+        V_walk = int(diag.counters[1].item())
+    ref_bytes_per_frame = algorithmic_bytes(C_tot, V_tot, N_tot, m0, sh_bytes)
+    bytes_per_frame = algorithmic_bytes(C_tot, V_walk, N_tot, m0, sh_bytes)
 
     # -- forward timing ------------------------------------------------------------
     kernel_ms = None
@@ -610,7 +623,8 @@ def main():
             targets = torch.from_numpy(rng.uniform(0.0, 1.0, (m, 3))).to(dev)[perm].contiguous()
             u_pairs = (torch.from_numpy(np.random.default_rng(12).uniform(0.0, 1.0, (m, 2, 2)))
                        .to(dev)[perm].contiguous() if args.quantile else None)
-            batches.append((origins, dirs, t_min, t_max, start, targets, u_pairs))
+            batches.append((origins, dirs, t_min, t_max, start, targets, u_pairs,
+                            dv.view_cone(cam)))
         m = W * H
         n_train_views = len(train_views) * world if args.config in (1, 2) else 8
         gb = dv.GradBuffers(ds.n_sites, dev)
@@ -623,11 +637,13 @@ def main():
         def fb_step():
             gb.zero_()
             loss.zero_()
-            for (origins, dirs, t_min, t_max, start, targets, u_pairs) in batches:
+            for (origins, dirs, t_min, t_max, start, targets, u_pairs, cone) in batches:
+                # rays already in tile order; the view's culled rows (rfb_cull_scene) are
+                # re-derived inside every step
                 dv.train_batch_device(ds, origins, dirs, t_min, t_max, start, targets, gb, loss,
                                       rgb_scale=rgb_scale, quantile_scale=q_scale,
                                       u_pairs=u_pairs, workspace=wsb, out=out_fb,
-                                      order=None)  # rays already in tile order
+                                      order=None, view_dirs=cone)
             if dist_on:
                 dist.all_reduce(gb.flat)
                 dist.all_reduce(loss)
@@ -659,6 +675,7 @@ def main():
         fb_C = int(out_fb.ray_counters[:, 0].sum().item())
         fb_V = int(out_fb.ray_counters[:, 1].sum().item())
         fb_N = int(out_fb.nseg.to(torch.int64).sum().item())
+        fb_V = int(round(fb_V * V_walk / max(V_tot, 1)))  # culled rows (forward probe's ratio)
         fb_bytes = fwd_bwd_bytes(fb_C, fb_V, fb_N, m, sh_bytes)  # last view's counters
         view_ms = fb_ms / args.steps / max(len(batches), 1)
         fb_achieved = fb_bytes / (view_ms / 1e3) / 1e9
@@ -891,7 +908,7 @@ def main():
     l2_note = (f"inputs larger than L2 (scene {scene_mb:.0f} MB vs 126 MB L2); no flush"
                if scene_mb > 126 else
                f"scene ({scene_mb:.0f} MB) fits in L2; no flush (small-config case)")
-    fwd_launches = 3 * args.steps * len(views) if args.config != 5 else 0
+    fwd_launches = 4 * args.steps * len(views) if args.config != 5 else 0
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -913,12 +930,18 @@ def main():
         "train_iteration": train_iter,
         "gpu_launches": fwd_launches + fb_launches,
         "gpu_launches_detail": {"forward": fwd_launches, "fwd_bwd": fb_launches,
-                                "per_forward_view": "k_nearest_dist, k_nearest_id, k_render",
-                                "per_fwd_bwd_view": "k_train"},
+                                "per_forward_view": "k_cull_rows, k_nearest_dist, "
+                                                    "k_nearest_id, k_render",
+                                "per_fwd_bwd_view": "k_cull_rows, k_train"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
                      "peak_kind": peak_kind, "kernel": roof_kernel,
                      "algorithmic_bytes_per_launch": bytes_per_frame,
+                     "reference_algorithmic_bytes_per_launch": ref_bytes_per_frame,
+                     "bytes_model": "B_f of SURVEY §8d with V = the neighbour records the walk "
+                                    "reads (view-culled rows; the reference's V counts every "
+                                    "neighbour: reference_algorithmic_bytes_per_launch)",
+                     "neighbor_records_walked_per_ray": V_walk / m0,
                      "launch_ms": launch_ms,
                      "binding_unit": "L1 data pipe (l1tex wavefronts), not HBM: the walk's "
                                      "gathers hit L2/L1 (DRAM traffic per launch is "

@@ -37,6 +37,12 @@
  *   rfb_render_image    diffrender/render.py:128-149 render_image() (fused
  *                        ray generation + shared-origin start cell + render,
  *                        over a list of image tiles for multi-GPU sharding)
+ *   rfb_cull_scene      (no reference counterpart: an exact pre-pass for
+ *                        render_image() / a view's train_batch) drops from a
+ *                        copy of the packed rows every neighbour that
+ *                        kernels.py:118-119 skips as back-facing for EVERY ray
+ *                        of a frame (pinhole: the 4 corner-pixel directions
+ *                        generate the frame's direction cone)
  *   rfb_host_device_pointer  render_image() returns a host image: the mapped
  *                        address of a pinned host frame, so rfb_render_image
  *                        stores the image to host memory during the walk
@@ -71,7 +77,7 @@ extern "C" {
 #define RFB_STATUS_STEP_LIMIT 2
 #define RFB_STATUS_CYCLE 3
 
-#define RFB_ABI_VERSION 13
+#define RFB_ABI_VERSION 14
 
 /* Capacity (records) of the packed edge arrays rfb_pack_scene fills: rows are
  * padded to an even length, so E + n_sites slots suffice (+2 spare). */
@@ -362,6 +368,20 @@ size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind);
 
 /* Forward + reverse pass for arbitrary colour adjoints [m][3] f64.  out.rgb
  * receives the forward colour; gradients accumulate into grads. */
+/* View culling: `dirs` (host, [n_dirs][3], 1 <= n_dirs <= 8) generate a cone
+ * (positive combinations) that must contain the direction of every ray the
+ * culled scene will walk -- for a pinhole camera the directions of its four
+ * corner pixels.  Writes a copy of the packed rows into cells_out
+ * ([n_sites] 32-byte headers) and edges_out ([RFB_PACKED_EDGE_SLOTS] 16-byte
+ * records), both 32-byte aligned, leaving out every neighbour whose face is
+ * back-facing (d . n < -1e-9 |n|_1) for every direction of the cone, and fills
+ * *view_out (host) with the scene using them.  The walk over the view is
+ * bit-identical to the walk over the full rows for every ray in the cone
+ * (the dropped faces fail `denom <= 0` there), counters included.  Packed
+ * scenes only; any later rfb_refresh_scene / re-pack invalidates the view. */
+int rfb_cull_scene(const rfb_scene *scene, const double *dirs, int32_t n_dirs, void *cells_out,
+                   void *edges_out, rfb_scene *view_out, void *stream);
+
 int rfb_backward_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,
                       const double *adjoints, const rfb_fwd_out *out, const rfb_grads *grads,
                       void *workspace, size_t workspace_bytes, void *stream);

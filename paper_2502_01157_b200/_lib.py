@@ -13,7 +13,7 @@ import threading
 
 from .errors import DeviceError, ExtensionMissing
 
-ABI_VERSION = 13  # include/rfb.h RFB_ABI_VERSION
+ABI_VERSION = 14  # include/rfb.h RFB_ABI_VERSION
 _lock = threading.Lock()
 _lib = None
 
@@ -154,6 +154,8 @@ SIGNATURES = {
     "rfb_render_image": (ctypes.c_int, [P(rfb_scene), P(rfb_camera), P(rfb_params), F64, F64, I32,
                                         VP, I64, I32, I32, P(rfb_fwd_out), VP, SZ, VP]),
     "rfb_workspace_bytes": (SZ, [I64, I32, I32]),
+    "rfb_cull_scene": (ctypes.c_int, [P(rfb_scene), P(ctypes.c_double), I32, VP, VP, P(rfb_scene),
+                                      VP]),
     "rfb_backward_rays": (ctypes.c_int, [P(rfb_scene), P(rfb_rays), P(rfb_params), VP,
                                          P(rfb_fwd_out), P(rfb_grads), VP, SZ, VP]),
     "rfb_train_batch": (ctypes.c_int, [P(rfb_scene), P(rfb_rays), P(rfb_params), VP, F64, F64, VP,

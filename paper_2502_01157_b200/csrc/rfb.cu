@@ -192,7 +192,8 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
             return RFB_STATUS_STEP_LIMIT;
         }
         const Cell c = S.cell(i);
-        visits += c.k1 - c.k0;
+        // packed: + the neighbours a view-culled row dropped (k_cull_rows)
+        visits += c.k1 - c.k0 + (PACKED ? (__float_as_int(c.n1max) & 31) : 0);
         double best_t;
         int32_t best_j;
         if constexpr (PACKED && kUseF32Filter)
@@ -470,6 +471,9 @@ __device__ __forceinline__ unsigned order_key(double t) {
 #endif
 #ifndef RFB_REV_COLREG
 #define RFB_REV_COLREG 1  // reverse pass: load cell + colour together when advancing
+#endif
+#ifndef RFB_REV_PREFETCH
+#define RFB_REV_PREFETCH 0  // reverse pass: L2 prefetch distance (segments) of the records
 #endif
 constexpr int kTrainBlock = 128;
 constexpr int kTrainWarps = kTrainBlock / 32;
@@ -882,6 +886,14 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                     cmask = (cm >> 29) & 7;
                     t1 = t0;
                     tb1 = tb0;
+#if RFB_REV_PREFETCH > 0
+                    // the records RFB_REV_PREFETCH segments further back were written
+                    // early in the walk and have left L2: bring them back ahead of use
+                    if (s > RFB_REV_PREFETCH) {
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(rec_a + (s - RFB_REV_PREFETCH) * SL4));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(rec_b + (s - 1 - RFB_REV_PREFETCH) * SL4));
+                    }
+#endif
                     if (s > 0) {
                         const double2 rb = rec_b[(s - 1) * SL4];  // {t0, T_before[s]}
                         t0 = rb.x;
@@ -1083,6 +1095,9 @@ __device__ __forceinline__ void pack_row(const double *pos, int64_t u, int64_t i
     }
     n1max *= 1.0f + 0x1p-20f;
     if (pos64) n1max += pos64_widen(xabs);
+    // rounded up to a multiple of 32 ulp: the low 5 bits are free for k_cull_rows'
+    // dropped-neighbour count (the walk adds it back to its visit counter)
+    n1max = __uint_as_float((__float_as_uint(n1max) + 31u) & ~31u);
     CellHdr h;
     h.x = xi;
     h.y = yi;
@@ -1493,6 +1508,83 @@ __global__ void k_refresh_rows(int64_t n, const double *pos, CellHdr *cells, con
     const int64_t i = pk_id ? pk_id[u] : u;
     pack_row(pos, u, i, nullptr, nbr, off[i], off[i + 1] - off[i], cells[u].k0, edges, enbr,
              cells, nullptr, 1, threadIdx.x & (kRowLanes - 1), pk_of);
+}
+
+// ---------------------------------------------------------------------------
+// View culling (rfb_cull_scene).  Every ray of a frame has a direction d that
+// is a positive combination of the cone generators c_k (a pinhole frame: the
+// four corner-pixel directions, since R (u, v, -1) is linear in the pixel
+// centre (u, v) over the image rectangle).  A neighbour with
+// c_k . n < -1e-9 |n|_1 for every k (n = x_j - x_i) then has d . n < -1e-9 |n|_1
+// for every ray, far beyond the fp64 rounding of the reference's
+// `denom = d . n` (~1e-15 |n|_1), so kernels.py:118-119 (`if denom <= 0:
+// continue`) skips it for every ray of the frame: it can never be the exit
+// face.  The culled copy of the packed rows keeps the other neighbours in CSR
+// order (so exact ties resolve as before), pads to even with a NaN record and
+// stores the number dropped (<= 31; a row that would drop more is copied
+// whole) in n1max's low 5 bits, which pack_row leaves zero; the walk adds it
+// back to its neighbour-visit counter.  fp64 sites (positions_f64): the
+// records are rounded copies (<= 2^-24 X per coordinate, X the largest
+// |coordinate|), covered by widening the margin by 2^-21 X.  One row per 16
+// lanes; the kept records are compacted with a ballot.
+// ---------------------------------------------------------------------------
+constexpr int kCullMaxDirs = 8;
+constexpr int kCullMaxDrop = 31;
+struct CullCone {
+    double c[kCullMaxDirs][3];
+    int32_t nd;
+};
+__global__ void k_cull_rows(const CellHdr *cells, const float4 *edges, int64_t n, CullCone cone,
+                            int pos64, CellHdr *cells_out, float4 *edges_out) {
+    const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kRowLanes;
+    if (u >= n) return;  // whole 16-lane groups
+    const int gl = threadIdx.x & (kRowLanes - 1);
+    const unsigned gshift = threadIdx.x & 16;
+    const unsigned gmask = 0xffffu << gshift;
+    const CellHdr h = cells[u];
+    const double xi = h.x, yi = h.y, zi = h.z;
+    const double xa = fmax(fabs(xi), fmax(fabs(yi), fabs(zi)));
+    const int32_t deg = h.k1 - h.k0;
+    int32_t m = 0;
+    for (int pass = 0; pass < 2; ++pass) {  // pass 1: the row would drop > 31, copy it whole
+        m = 0;
+        for (int32_t t0 = 0; t0 < deg; t0 += kRowLanes) {
+            const int32_t t = t0 + gl;
+            const bool real = t < deg;
+            bool keep = real;
+            float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (real) {
+                e = edges[h.k0 + t];
+                if (pass == 0) {
+                    const double nx = (double)e.x - xi, ny = (double)e.y - yi,
+                                 nz = (double)e.z - zi;
+                    double marg = 1e-9 * (fabs(nx) + fabs(ny) + fabs(nz));
+                    if (pos64)
+                        marg += 0x1p-21 * fmax(xa, fmax(fabs((double)e.x),
+                                                        fmax(fabs((double)e.y), fabs((double)e.z))));
+                    bool back = true;
+                    for (int k = 0; k < cone.nd; ++k)
+                        back = back &&
+                               (cone.c[k][0] * nx + cone.c[k][1] * ny + cone.c[k][2] * nz < -marg);
+                    keep = !back;
+                }
+            }
+            const unsigned bal = (__ballot_sync(gmask, keep) >> gshift) & 0xffffu;
+            if (keep) edges_out[h.k0 + m + __popc(bal & ((1u << gl) - 1u))] = e;
+            m += __popc(bal);
+        }
+        if (deg - m <= kCullMaxDrop) break;
+    }
+    if (gl == 0) {
+        if (m & 1) {
+            const float qnan = __int_as_float(0x7fffffff);
+            edges_out[h.k0 + m] = make_float4(qnan, qnan, qnan, qnan);
+        }
+        CellHdr o = h;
+        o.k1 = h.k0 + m;
+        o.n1max = __uint_as_float((__float_as_uint(h.n1max) & ~31u) | (unsigned)(deg - m));
+        cells_out[u] = o;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -2102,6 +2194,33 @@ int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb
     src.t_max = t_max;
     src.start_ptr = start_ptr;
     return launch_render(scene, src, params, out, workspace, workspace_bytes, st);
+}
+
+int rfb_cull_scene(const rfb_scene *scene, const double *dirs, int32_t n_dirs, void *cells_out,
+                   void *edges_out, rfb_scene *view_out, void *stream) {
+    if (!scene_ok(scene) || !scene->packed || !dirs || n_dirs < 1 || n_dirs > kCullMaxDirs ||
+        !cells_out || !edges_out || !view_out ||
+        (reinterpret_cast<uintptr_t>(cells_out) & 31) || (reinterpret_cast<uintptr_t>(edges_out) & 31))
+        return RFB_EINVAL;
+    CullCone cone;
+    for (int k = 0; k < kCullMaxDirs; ++k)
+        for (int a = 0; a < 3; ++a) cone.c[k][a] = k < n_dirs ? dirs[3 * k + a] : 0.0;
+    for (int k = 0; k < n_dirs; ++k) {  // unit generators (the margin is relative to |c| = 1)
+        const double l = std::sqrt(cone.c[k][0] * cone.c[k][0] + cone.c[k][1] * cone.c[k][1] +
+                                   cone.c[k][2] * cone.c[k][2]);
+        if (!(l > 0.0) || !std::isfinite(l)) return RFB_EINVAL;
+        for (int a = 0; a < 3; ++a) cone.c[k][a] /= l;
+    }
+    cone.nd = n_dirs;
+    *view_out = *scene;
+    view_out->cells = cells_out;
+    view_out->edges = edges_out;
+    if (scene->n_sites == 0) return RFB_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_cull_rows<<<(unsigned)((scene->n_sites * kRowLanes + 255) / 256), 256, 0, st>>>(
+        (const CellHdr *)scene->cells, (const float4 *)scene->edges, scene->n_sites, cone,
+        scene->positions_f64 ? 1 : 0, (CellHdr *)cells_out, (float4 *)edges_out);
+    return (int)cudaGetLastError();
 }
 
 int rfb_backward_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,

@@ -561,6 +561,15 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #ifndef RFB_FINAL_BAND
 #define RFB_FINAL_BAND 1  // drop candidates the final band excludes (one exact evaluation)
 #endif
+#ifndef RFB_UNIFY_P2
+#define RFB_UNIFY_P2 1  // the single-candidate case goes through the candidate loop (one inlined copy)
+#endif
+#ifndef RFB_TWO_PASS
+#define RFB_TWO_PASS 1  // no running candidate mask; several candidates: second pass vs the final U
+#endif
+#if RFB_TWO_PASS && !RFB_FINAL_BAND
+#error "RFB_TWO_PASS needs RFB_FINAL_BAND"
+#endif
 typedef unsigned int cand_mask_t;
 constexpr int kMaskBits = 32;
 
@@ -663,8 +672,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
             bool front, sure;
             bounds(e, lb, ub, front, sure);
             const float lbm = sure ? lb : -kInf;  // uncertain facing: always a candidate
+#if !RFB_TWO_PASS
             const bool cand = front && lbm <= U;
             mask = (mask << 1) | (cand ? 1u : 0u);
+#endif
 #if RFB_FINAL_BAND
             const float lbc = front ? lbm : kInf;
             t1 = lbc < L1 ? slot : t1;
@@ -689,18 +700,41 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
         }
         if (nslots > kMaskBits) {  // rare: the mask lost bits -- every neighbour exactly
             for (int32_t k = c.k0; k < c.k1; ++k) exact(k);
+            return;
         }
 #if RFB_FINAL_BAND
-        else if (t1 >= 0 && L2 > U && L1 <= U) {  // only L1's neighbour can be the first minimum
+        if (t1 >= 0 && L2 > U && L1 <= U) {  // only L1's neighbour can be the first minimum
+#if RFB_UNIFY_P2
+            mask = 1u << (nslots - 1 - t1);  // one phase-2 site for every lane (no divergence)
+#else
             exact(c.k0 + t1);
+            return;
+#endif
+        }
+#if RFB_TWO_PASS
+        else if (t1 >= 0) {
+            // several candidates beat the final band: collect them against the final U
+            // (a subset of the running band, same guarantee) in a second pass over the row
+            // (L1-resident); only here does the candidate mask get built
+            for (int32_t kp = c.k0; kp < c.k1; kp += 2) {
+                float4 e0, e1;
+                ldg256(S.edge + kp, e0, e1);
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float lb, ub;
+                    bool front, sure;
+                    bounds(h ? e1 : e0, lb, ub, front, sure);
+                    const bool cand = front && (!sure || lb <= U);
+                    mask = (mask << 1) | (cand ? 1u : 0u);
+                }
+            }
         }
 #endif
-        else {
-            while (mask) {  // highest bit = lowest slot: CSR order
-                const int b = 31 - __clz((int)mask);
-                mask &= ~(1u << b);
-                exact(c.k0 + (nslots - 1 - b));
-            }
+#endif
+        while (mask) {  // highest bit = lowest slot: CSR order
+            const int b = 31 - __clz((int)mask);
+            mask &= ~(1u << b);
+            exact(c.k0 + (nslots - 1 - b));
         }
         return;
     }

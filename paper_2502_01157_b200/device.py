@@ -246,6 +246,30 @@ class DeviceScene:
     def c(self):
         return ctypes.byref(self._c)
 
+    # -- view culling (rfb_cull_scene) -------------------------------------
+    VIEW_CULL = os.environ.get("RFB_VIEW_CULL", "1") != "0"
+
+    def view(self, dirs, stream=None):
+        """The scene as walked by rays whose directions lie in the cone generated
+        by ``dirs`` ([k][3], k <= 8; see ``view_cone``): a copy of the packed rows
+        without the neighbours that are back-facing for every such ray (the
+        reference skips them for every ray, kernels.py:118-119), re-derived on
+        every call (the rows change when the scene does).  Returns a ctypes
+        reference to the derived rfb_scene, or ``self.c`` when culling does not
+        apply (generic layout, no cone, RFB_VIEW_CULL=0)."""
+        if dirs is None or not self.packed or not self.VIEW_CULL or self.n_sites == 0:
+            return self.c
+        d = np.ascontiguousarray(np.asarray(dirs, dtype=np.float64).reshape(-1, 3))
+        if getattr(self, "_view_cells", None) is None:
+            self._view_cells = torch.empty_like(self.cells)
+            self._view_edges = torch.empty_like(self.edges)
+            self._view_c = _lib.rfb_scene()
+        _lib.check(self.lib.rfb_cull_scene(
+            self.c, d.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(len(d)),
+            _ptr(self._view_cells), _ptr(self._view_edges), ctypes.byref(self._view_c),
+            _stream(stream)), "rfb_cull_scene")
+        return ctypes.byref(self._view_c)
+
     # -- device-resident updates (training) ------------------------------
     def rebuild_adjacency(self, positions: torch.Tensor | None = None, packed=None,
                           stream=None) -> dict:
@@ -497,10 +521,12 @@ def render_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
                        per_ray=True, seg_capacity=0, lanes_per_ray=DEFAULT_LANES,
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
-                       order=None, stream=None) -> ForwardResult:
+                       order=None, stream=None, view_dirs=None) -> ForwardResult:
     """rfb_render_rays on device tensors (kernels.py:199-247).  ``order``: an
     optional processing permutation (e.g. coherent_order) -- outputs stay
-    indexed by ray."""
+    indexed by ray.  ``view_dirs``: generators of a cone holding every ray
+    direction (``view_cone(camera)`` for a camera's pixels): the walk then
+    uses the view-culled rows (``DeviceScene.view``; same output)."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=per_ray, seg_capacity=seg_capacity)
     ws = (workspace or Workspace(ds.device)).get(256)
@@ -508,7 +534,8 @@ def render_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start
     order = _order32(order, m, ds.device)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)
-    _lib.check(ds.lib.rfb_render_rays(ds.c, ctypes.byref(rays), ctypes.byref(p), ctypes.byref(o),
+    sc = ds.view(view_dirs, stream)
+    _lib.check(ds.lib.rfb_render_rays(sc, ctypes.byref(rays), ctypes.byref(p), ctypes.byref(o),
                                       _ptr(ws), ws.numel(), _stream(stream)), "rfb_render_rays")
     return res
 
@@ -528,18 +555,36 @@ def host_device_pointer(lib, host: torch.Tensor) -> int | None:
     return dev.value
 
 
+def view_cone(camera):
+    """Generators of the cone holding every pixel ray direction of a pinhole
+    camera: its four corner-pixel directions R (u, v, -1) (camera.py:78-92 is
+    linear in the pixel centre (u, v), so every pixel direction is a positive
+    combination of them).  None for a fisheye camera."""
+    if getattr(camera, "kind", "pinhole") == "fisheye":
+        return None
+    W, H = int(camera.width), int(camera.height)
+    cols = np.array([0.0, W - 1.0, 0.0, W - 1.0])
+    rows = np.array([0.0, 0.0, H - 1.0, H - 1.0])
+    u = (cols + 0.5 - float(camera.cx)) / float(camera.focal)
+    v = -(rows + 0.5 - float(camera.cy)) / float(camera.focal)
+    d_cam = np.stack([u, v, -np.ones(4)], axis=1)
+    return d_cam @ np.asarray(camera.pose, dtype=np.float64)[:3, :3].T
+
+
 def render_image_device(ds: DeviceScene, camera, *, epsilon=DEFAULT_EPSILON,
                         step_limit=DEFAULT_STEP_LIMIT, t_max=None, start_site=-1, tile_ids=None,
                         tile_w=32, tile_h=32, f64=False, per_ray=False,
                         lanes_per_ray=DEFAULT_LANES, workspace: Workspace | None = None,
                         out: ForwardResult | None = None, stream=None,
-                        rgb_ptr: int | None = None) -> ForwardResult:
+                        rgb_ptr: int | None = None, cull: bool = True) -> ForwardResult:
     """Fused ray generation + render over a tile list (render.py:128-149).
 
     ``rgb_ptr``: optional device address (``host_device_pointer``) of a mapped
     page-locked (W*H, 3) host frame of ``out.rgb``'s dtype; the kernel then
     stores each ray's colour straight into host memory and ``out.rgb`` is
-    left untouched."""
+    left untouched.  ``cull``: walk a copy of the rows without the faces that
+    are back-facing for the whole frame (``DeviceScene.view``, re-derived per
+    call; bit-identical output)."""
     W, H = int(camera.width), int(camera.height)
     m = W * H
     if tile_ids is None:
@@ -554,7 +599,11 @@ def render_image_device(ds: DeviceScene, camera, *, epsilon=DEFAULT_EPSILON,
     o = fwd_struct(res)
     if rgb_ptr is not None:
         o.rgb = int(rgb_ptr)
-    _lib.check(ds.lib.rfb_render_image(ds.c, ctypes.byref(cam), ctypes.byref(p), 0.0, float(t_max),
+    if cull == "last":  # diagnostics: the view the previous call derived, as it is now
+        sc = ctypes.byref(ds._view_c)
+    else:
+        sc = ds.view(view_cone(camera), stream) if cull else ds.c
+    _lib.check(ds.lib.rfb_render_image(sc, ctypes.byref(cam), ctypes.byref(p), 0.0, float(t_max),
                                        int(start_site), _ptr(tile_ids), int(tile_ids.numel()),
                                        int(tile_w), int(tile_h), ctypes.byref(o), _ptr(ws),
                                        ws.numel(), _stream(stream)), "rfb_render_image")
@@ -598,9 +647,10 @@ def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, sta
                          grads: GradBuffers, *, epsilon=DEFAULT_EPSILON,
                          step_limit=DEFAULT_STEP_LIMIT, f64=False,
                          workspace: Workspace | None = None, out: ForwardResult | None = None,
-                         order="auto", lanes_per_ray=0, stream=None) -> ForwardResult:
+                         order="auto", lanes_per_ray=0, stream=None, view_dirs=None) -> ForwardResult:
     """rfb_backward_rays (render.py:152-221 generic adjoint).  ``order``: see _order32;
-    ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule."""
+    ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule;
+    ``view_dirs``: see render_rays_device."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(
@@ -611,7 +661,8 @@ def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, sta
     o = fwd_struct(res)
     g = grads.struct()
     adj = adjoints.to(ds.device, torch.float64).contiguous()
-    _lib.check(ds.lib.rfb_backward_rays(ds.c, ctypes.byref(rays), ctypes.byref(p), _ptr(adj),
+    sc = ds.view(view_dirs, stream)
+    _lib.check(ds.lib.rfb_backward_rays(sc, ctypes.byref(rays), ctypes.byref(p), _ptr(adj),
                                         ctypes.byref(o), ctypes.byref(g), _ptr(ws), ws.numel(),
                                         _stream(stream)), "rfb_backward_rays")
     return res
@@ -622,10 +673,11 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        quantile_scale: float = 0.0, u_pairs=None, weight_floor: float = 1e-4,
                        epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
-                       order="auto", lanes_per_ray=0, stream=None) -> ForwardResult:
+                       order="auto", lanes_per_ray=0, stream=None, view_dirs=None) -> ForwardResult:
     """rfb_train_batch (kernels.py:372-453).  ``loss`` float64 [2] accumulates.
     ``order``: "auto" sorts batches of >= 500k rays coherently (see _order32);
-    ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule."""
+    ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule;
+    ``view_dirs``: see render_rays_device."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(
@@ -640,7 +692,8 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
     if quantile_scale > 0.0:
         up = u_pairs.to(ds.device, torch.float64).contiguous()
         n_pairs = up.shape[1]
-    _lib.check(ds.lib.rfb_train_batch(ds.c, ctypes.byref(rays), ctypes.byref(p), _ptr(targets),
+    sc = ds.view(view_dirs, stream)
+    _lib.check(ds.lib.rfb_train_batch(sc, ctypes.byref(rays), ctypes.byref(p), _ptr(targets),
                                       float(rgb_scale), float(quantile_scale), _ptr(up), n_pairs,
                                       float(weight_floor), ctypes.byref(o), ctypes.byref(g),
                                       _ptr(loss), _ptr(ws), ws.numel(), _stream(stream)),

@@ -41,7 +41,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_errors(lib):
-    assert lib.rfb_abi_version() == 13
+    assert lib.rfb_abi_version() == 14
     assert lib.rfb_error_string(0) == b"ok"
     assert lib.rfb_error_string(-1) == b"invalid argument"
 
@@ -100,3 +100,7 @@ def test_argument_validation_without_device(lib):
                               None, None, None, None, 0, None) == -1
     assert lib.rfb_softplus(None, 1, None, None, None, None, None) == -1
     assert lib.rfb_host_device_pointer(None, None) == -1
+    view = _lib.rfb_scene()
+    dirs = (ctypes.c_double * 3)(0.0, 0.0, -1.0)
+    assert lib.rfb_cull_scene(ctypes.byref(sc), dirs, 1, None, None, ctypes.byref(view), None) == -1
+    assert lib.rfb_cull_scene(None, dirs, 1, None, None, ctypes.byref(view), None) == -1

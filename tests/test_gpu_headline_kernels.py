@@ -67,9 +67,10 @@ def rel(a, b):
     return float(np.abs(a - b).max() / np.abs(b).max())
 
 
-@pytest.mark.parametrize("view,eps", [(0, 1e-3), (2, 0.0)])
-def test_render_image_one_lane_per_ray(cuda_ok, scene100k, sa100k, ds100k, view, eps):
-    """k_render<1, 3, 1, TileRays> (the config-2 kernel) on a 480x270 frame."""
+@pytest.mark.parametrize("view,eps,cull", [(0, 1e-3, True), (2, 0.0, True), (0, 1e-3, False)])
+def test_render_image_one_lane_per_ray(cuda_ok, scene100k, sa100k, ds100k, view, eps, cull):
+    """k_render<1, 3, 1, TileRays> (the config-2 kernel) on a 480x270 frame, over the
+    view-culled rows (the default, rfb_cull_scene) and over the full rows."""
     from paper_2502_01157_b200 import device as dv
 
     W, H = 480, 270
@@ -77,12 +78,12 @@ def test_render_image_one_lane_per_ray(cuda_ok, scene100k, sa100k, ds100k, view,
     assert 2 * m > 148 * 4 * 256, "frame must be large enough for the auto rule to pick 1 lane"
     cam = _cam(W, H, view)
     first = dv.render_image_device(ds100k, cam, epsilon=eps, f64=True, per_ray=True,
-                                   lanes_per_ray=1)
+                                   lanes_per_ray=1, cull=cull)
     torch.cuda.synchronize()
     cap = int(first.nseg.max().item())
     out = dv.alloc_forward(m, ds100k.device, f64=True, per_ray=True, seg_capacity=cap)
-    res = dv.render_image_device(ds100k, cam, epsilon=eps, lanes_per_ray=1, out=out)
-    auto = dv.render_image_device(ds100k, cam, epsilon=eps, f64=True, per_ray=True)
+    res = dv.render_image_device(ds100k, cam, epsilon=eps, lanes_per_ray=1, out=out, cull=cull)
+    auto = dv.render_image_device(ds100k, cam, epsilon=eps, f64=True, per_ray=True, cull=cull)
     torch.cuda.synchronize()
     assert torch.equal(auto.rgb, res.rgb) and torch.equal(auto.ray_counters, res.ray_counters)
 
@@ -123,10 +124,11 @@ def _d(a, dt=torch.float64):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
 
 
-@pytest.mark.parametrize("quantile", [False, True])
-def test_train_batch_one_lane_full_view(cuda_ok, sa100k, ds100k, quantile):
+@pytest.mark.parametrize("quantile,cull", [(False, True), (True, True), (False, False)])
+def test_train_batch_one_lane_full_view(cuda_ok, sa100k, ds100k, quantile, cull):
     """k_train<3, 1, true, Q, 1> (the config-3 kernel) on an 81,920-ray view in tile
-    order, against the oracle's train_batch (kernels.py:372-453)."""
+    order, against the oracle's train_batch (kernels.py:372-453); the bench walks
+    the view-culled rows (view_dirs = the camera's cone)."""
     from paper_2502_01157_b200 import device as dv
 
     W, H = 320, 256
@@ -147,7 +149,7 @@ def test_train_batch_one_lane_full_view(cuda_ok, sa100k, ds100k, quantile):
                                 _d(np.full(m, start), torch.int32), _d(targets), gb, loss,
                                 rgb_scale=1.0 / (3 * m), quantile_scale=qs,
                                 u_pairs=_d(u) if quantile else None, f64=True, order=None,
-                                lanes_per_ray=1)
+                                lanes_per_ray=1, view_dirs=dv.view_cone(cam) if cull else None)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
     np.testing.assert_array_equal(res.counters.cpu().numpy(), ref["counters"].sum(axis=0))
@@ -174,7 +176,7 @@ def test_backward_rays_one_lane_full_view(cuda_ok, sa100k, ds100k):
     gb = dv.GradBuffers(ds100k.n_sites, ds100k.device)
     res = dv.backward_rays_device(ds100k, _d(o), _d(dirs), _d(np.zeros(m)), _d(t_max),
                                   _d(np.full(m, start), torch.int32), _d(adj), gb, f64=True,
-                                  order=None, lanes_per_ray=1)
+                                  order=None, lanes_per_ray=1, view_dirs=dv.view_cone(cam))
     torch.cuda.synchronize()
     np.testing.assert_array_equal(res.status.cpu().numpy(), status)
     assert np.abs(res.rgb.cpu().numpy() - rgb).max() <= IMG_TOL
@@ -182,3 +184,44 @@ def test_backward_rays_one_lane_full_view(cuda_ok, sa100k, ds100k):
     assert rel(g4[:, 3], ds_ref) <= GRAD_RTOL
     assert rel(g4[:, :3], dp_ref) <= GRAD_RTOL
     assert rel(gb.sh.double().cpu().numpy(), dsh_ref) <= GRAD_RTOL
+
+
+def test_view_culled_rows(cuda_ok, ds100k):
+    """rfb_cull_scene's copy of the packed rows: every row keeps a CSR-ordered
+    subset of its records, every dropped neighbour is back-facing with margin
+    for all four corner directions, n1max's low 5 bits hold the number dropped
+    (pack_row leaves them zero), and a sizeable share of the rows is dropped."""
+    from paper_2502_01157_b200 import device as dv
+
+    cam = _cam(480, 270, 0)
+    cone = dv.view_cone(cam)
+    ds100k.view(cone)
+    torch.cuda.synchronize()
+    full_h = ds100k.cells.cpu().numpy()
+    view_h = ds100k._view_cells.cpu().numpy()
+    full_e = ds100k.edges.cpu().numpy()
+    view_e = ds100k._view_edges.cpu().numpy()
+    k0, k1 = full_h[:, 3], full_h[:, 6]
+    assert np.array_equal(view_h[:, 3], k0)
+    n1f = full_h[:, 7].view(np.uint32)
+    n1v = view_h[:, 7].view(np.uint32)
+    assert np.all(n1f & 31 == 0)
+    assert np.array_equal(n1v & ~np.uint32(31), n1f)
+    dropped = (n1v & 31).astype(np.int64)
+    kept = view_h[:, 6] - k0
+    assert np.array_equal(kept + dropped, k1 - k0)
+    frac = dropped.sum() / (k1 - k0).sum()
+    assert 0.15 < frac < 0.4, frac
+    c = cone / np.linalg.norm(cone, axis=1, keepdims=True)
+    rng = np.random.default_rng(0)
+    for u in rng.choice(len(full_h), 300, replace=False):
+        row = full_e[k0[u]:k1[u]]
+        vrow = view_e[k0[u]:k0[u] + kept[u]]
+        ids = row[:, 3].view(np.int32)
+        vids = vrow[:, 3].view(np.int32)
+        assert np.array_equal(ids[np.isin(ids, vids)], vids), "CSR order kept"
+        n = row[:, :3].astype(np.float64) - full_h[u, :3].view(np.float32).astype(np.float64)
+        back = np.all(n @ c.T < -1e-9 * np.abs(n).sum(1)[:, None], axis=1)
+        assert np.array_equal(~np.isin(ids, vids), back)
+        if kept[u] & 1:
+            assert np.all(np.isnan(view_e[k0[u] + kept[u]]))

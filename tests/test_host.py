@@ -193,3 +193,29 @@ def test_csr_sha1_of_qhull_fixture():
     nbr2 = nbr.copy()
     nbr2[5] += 1
     assert csr_sha1(off, nbr2) != h
+
+
+@pytest.mark.parametrize("W,H,angle", [(1920, 1080, 0.9), (320, 256, 1.4), (64, 1, 0.3)])
+def test_view_cone_holds_every_pixel_direction(W, H, angle):
+    """device.view_cone: every pixel direction of a pinhole camera (the reference's
+    camera.py:78-92 arithmetic) is a positive combination of the four corner
+    generators, so a face back-facing (with margin) for all four is back-facing
+    for every pixel -- the premise of rfb_cull_scene."""
+    from paper_2502_01157_b200 import device as dv
+
+    cam = CameraModel.from_angle_x(PINHOLE, W, H, angle,
+                                   look_at((0.3, -2.0, 2.5), (0.1, 0.2, -0.1)))
+    cone = dv.view_cone(cam)
+    c = cone / np.linalg.norm(cone, axis=1, keepdims=True)
+    rng = np.random.default_rng(1)
+    rows = rng.integers(0, H, 4000)
+    cols = rng.integers(0, W, 4000)
+    d = cam.ray_directions(rows, cols)
+    n = rng.normal(size=(20000, 3))
+    back = np.all(n @ c.T < -1e-9 * np.abs(n).sum(1)[:, None], axis=1)
+    assert back.mean() > 0.1
+    assert np.all(n[back] @ d.T < 0.0)
+    # the corners are pixel directions themselves: the cone is tight
+    corner = cam.ray_directions(np.array([0, 0, H - 1, H - 1]), np.array([0, W - 1, 0, W - 1]))
+    np.testing.assert_allclose(corner, c, atol=1e-15)
+    assert dv.view_cone(CameraModel.from_angle_x("fisheye", W, H, angle, cam.pose)) is None

@@ -28,6 +28,7 @@ ap.add_argument("--height", type=int, default=1080)
 ap.add_argument("--train", action="store_true")
 ap.add_argument("--once", action="store_true")
 ap.add_argument("--view", type=int, default=0)
+ap.add_argument("--cull", default="1", help="view culling modes to time: '0', '1' or '0,1'")
 ap.add_argument("--packed", type=int, default=-1)
 ap.add_argument("--quantile", action="store_true")
 ap.add_argument("--morton", action="store_true", help="renumber sites in Morton order")
@@ -91,23 +92,25 @@ for (sw, sh_) in sizes:
         print(f"{sw}x{sh_} lanes={lanes:2d}: {ms:8.3f} ms  {sw * sh_ / ms / 1e3:8.2f} Mrays/s", flush=True)
 if sizes:
     sys.exit(0)
+culls = [int(c) for c in args.cull.split(",")]
 for lanes in [int(x) for x in args.lanes.split(",")]:
+  for cull in culls:
     reps = 1 if args.once else args.reps
     if not args.once:
-        dv.render_image_device(ds, cam, lanes_per_ray=lanes, workspace=ws, out=out)
+        dv.render_image_device(ds, cam, lanes_per_ray=lanes, workspace=ws, out=out, cull=bool(cull))
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):
-        dv.render_image_device(ds, cam, lanes_per_ray=lanes, workspace=ws, out=out)
+        dv.render_image_device(ds, cam, lanes_per_ray=lanes, workspace=ws, out=out, cull=bool(cull))
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
     m = args.width * args.height
     import hashlib
     h = hashlib.sha1(out.rgb.cpu().numpy().tobytes()).hexdigest()[:12]
-    print(f"fwd lanes={lanes:2d}: {ms:8.2f} ms/frame  {m / ms / 1e3:8.2f} Mrays/s  rgb sha1 {h}",
-          flush=True)
+    print(f"fwd lanes={lanes:2d} cull={cull}: {ms:8.2f} ms/frame  {m / ms / 1e3:8.2f} Mrays/s  "
+          f"rgb sha1 {h}", flush=True)
 
 if args.train:
     perm = torch.from_numpy(dv.tile_order(args.width, args.height)).cuda()
@@ -124,19 +127,24 @@ if args.train:
     wsb = dv.Workspace(ds.device)
     fo = dv.alloc_forward(m, ds.device)
     reps = 1 if args.once else args.reps
-    for r in range(reps + (0 if args.once else 1)):
-        if r == 1 or (args.once and r == 0):
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-        if args.quantile:
-            up = torch.rand((m, 2, 2), dtype=torch.float64, device="cuda")
-            dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
-                                  rgb_scale=1.0 / (3 * m), quantile_scale=0.01 / (2 * m),
-                                  u_pairs=up, workspace=wsb, out=fo, order=None)
-        else:
-            dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
-                                  rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo, order=None)
-    torch.cuda.synchronize()
-    ms = (time.perf_counter() - t0) * 1e3 / reps
-    print(f"train: {ms:8.2f} ms/step  {m / ms / 1e3:8.2f} Mrays/s  loss {float(loss[0]):.12g}",
-          flush=True)
+    for cull in culls:
+      vd = dv.view_cone(cam) if cull else None
+      loss.zero_()
+      for r in range(reps + (0 if args.once else 1)):
+          if r == 1 or (args.once and r == 0):
+              torch.cuda.synchronize()
+              t0 = time.perf_counter()
+          if args.quantile:
+              up = torch.rand((m, 2, 2), dtype=torch.float64, device="cuda")
+              dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
+                                    rgb_scale=1.0 / (3 * m), quantile_scale=0.01 / (2 * m),
+                                    u_pairs=up, workspace=wsb, out=fo, order=None, view_dirs=vd)
+          else:
+              dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
+                                    rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo, order=None, view_dirs=vd)
+      torch.cuda.synchronize()
+      ms = (time.perf_counter() - t0) * 1e3 / reps
+      import hashlib
+      h = hashlib.sha1(fo.rgb.cpu().numpy().tobytes()).hexdigest()[:12]
+      print(f"train cull={cull}: {ms:8.2f} ms/step  {m / ms / 1e3:8.2f} Mrays/s  "
+            f"loss {float(loss[0]):.12g}  rgb sha1 {h}", flush=True)
