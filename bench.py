@@ -453,7 +453,7 @@ def grad_parity(ds, sa, cam, args, threads):
     res = dv.train_batch_device(ds, d(o), d(dirs), d(np.zeros(m)), d(np.full(m, t_max)),
                                 d(np.full(m, start), torch.int32), d(targets), gb, loss,
                                 rgb_scale=1.0 / (3 * m), f64=True, order=None,
-                                view_dirs=dv.view_cone(cam))
+                                view=(cam, torch.from_numpy(perm)))
     torch.cuda.synchronize()
 
     def rel(a, b):
@@ -558,7 +558,7 @@ def main():
     # (n1max's low bits), so count them once more on the view with those bits cleared
     V_walk = V_tot
     if ds.packed and dv.view_cone(views[0]) is not None and ds.VIEW_CULL:
-        ds.view(dv.view_cone(views[0]))
+        ds.view_camera(views[0])
         ds._view_cells[:, 7].bitwise_and_(~31)
         diag = dv.render_image_device(ds, views[0], per_ray=False, lanes_per_ray=lanes,
                                       workspace=ws, cull="last")
@@ -624,7 +624,7 @@ def main():
             u_pairs = (torch.from_numpy(np.random.default_rng(12).uniform(0.0, 1.0, (m, 2, 2)))
                        .to(dev)[perm].contiguous() if args.quantile else None)
             batches.append((origins, dirs, t_min, t_max, start, targets, u_pairs,
-                            dv.view_cone(cam)))
+                            (cam, perm)))
         m = W * H
         n_train_views = len(train_views) * world if args.config in (1, 2) else 8
         gb = dv.GradBuffers(ds.n_sites, dev)
@@ -637,13 +637,13 @@ def main():
         def fb_step():
             gb.zero_()
             loss.zero_()
-            for (origins, dirs, t_min, t_max, start, targets, u_pairs, cone) in batches:
-                # rays already in tile order; the view's culled rows (rfb_cull_scene) are
-                # re-derived inside every step
+            for (origins, dirs, t_min, t_max, start, targets, u_pairs, view) in batches:
+                # rays already in tile order; the view's region-culled rows (rfb_cull_view)
+                # are re-derived inside every step
                 dv.train_batch_device(ds, origins, dirs, t_min, t_max, start, targets, gb, loss,
                                       rgb_scale=rgb_scale, quantile_scale=q_scale,
                                       u_pairs=u_pairs, workspace=wsb, out=out_fb,
-                                      order=None, view_dirs=cone)
+                                      order=None, view=view)
             if dist_on:
                 dist.all_reduce(gb.flat)
                 dist.all_reduce(loss)
@@ -930,7 +930,7 @@ def main():
         "train_iteration": train_iter,
         "gpu_launches": fwd_launches + fb_launches,
         "gpu_launches_detail": {"forward": fwd_launches, "fwd_bwd": fb_launches,
-                                "per_forward_view": "k_cull_rows, k_nearest_dist, "
+                                "per_forward_view": "k_cull_rows (4x2 regions), k_nearest_dist, "
                                                     "k_nearest_id, k_render",
                                 "per_fwd_bwd_view": "k_cull_rows, k_train"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

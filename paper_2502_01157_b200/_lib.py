@@ -13,7 +13,7 @@ import threading
 
 from .errors import DeviceError, ExtensionMissing
 
-ABI_VERSION = 14  # include/rfb.h RFB_ABI_VERSION
+ABI_VERSION = 15  # include/rfb.h RFB_ABI_VERSION
 _lock = threading.Lock()
 _lib = None
 
@@ -40,6 +40,8 @@ class rfb_scene(ctypes.Structure):
         ("sh_absmax_dev", ctypes.c_void_p),
         ("pk_of", ctypes.c_void_p),
         ("pk_id", ctypes.c_void_p),
+        ("view_rx", ctypes.c_int32),
+        ("view_ry", ctypes.c_int32),
     ]
 
 
@@ -61,6 +63,7 @@ class rfb_rays(ctypes.Structure):
         ("t_max", ctypes.c_void_p),
         ("start_sites", ctypes.c_void_p),
         ("order", ctypes.c_void_p),
+        ("region", ctypes.c_void_p),
     ]
 
 
@@ -156,6 +159,8 @@ SIGNATURES = {
     "rfb_workspace_bytes": (SZ, [I64, I32, I32]),
     "rfb_cull_scene": (ctypes.c_int, [P(rfb_scene), P(ctypes.c_double), I32, VP, VP, P(rfb_scene),
                                       VP]),
+    "rfb_cull_view": (ctypes.c_int, [P(rfb_scene), P(rfb_camera), I32, I32, VP, VP, P(rfb_scene),
+                                     VP]),
     "rfb_backward_rays": (ctypes.c_int, [P(rfb_scene), P(rfb_rays), P(rfb_params), VP,
                                          P(rfb_fwd_out), P(rfb_grads), VP, SZ, VP]),
     "rfb_train_batch": (ctypes.c_int, [P(rfb_scene), P(rfb_rays), P(rfb_params), VP, F64, F64, VP,

@@ -37,7 +37,12 @@ struct ArrayRays {
     const int32_t *start;
     int64_t m;
     const int32_t *order;  // optional processing order (a permutation of 0..m-1)
+    const uint8_t *region;  // optional: view region per ray (rfb_rays.region)
     __host__ __device__ __forceinline__ int64_t count() const { return m; }
+    // region of a view-culled scene ray q walks
+    __device__ __forceinline__ int32_t region_of(int64_t q, int32_t, int32_t) const {
+        return region ? (int32_t)region[q] : 0;
+    }
     __device__ __forceinline__ int64_t index(int64_t slot) const {
         return order ? (int64_t)order[slot] : slot;
     }
@@ -101,6 +106,12 @@ struct TileRays {
     double t_min, t_max;
     const int32_t *start_ptr;  // device scalar (located start cell)
     __host__ __device__ __forceinline__ int64_t count() const { return n_tiles * tile_w * tile_h; }
+    // region of pixel oidx in an rx x ry grid (rfb.h: rfb_scene.view_rx)
+    __device__ __forceinline__ int32_t region_of(int64_t oidx, int32_t rx, int32_t ry) const {
+        if (rx <= 0) return 0;
+        const int32_t py = (int32_t)(oidx / cam.width), px = (int32_t)(oidx - (int64_t)py * cam.width);
+        return (py * ry / cam.height) * rx + px * rx / cam.width;
+    }
     __device__ __forceinline__ void uniform(double *u) const {
         u[0] = cam.o[0];
         u[1] = cam.o[1];
@@ -174,7 +185,7 @@ __device__ __forceinline__ void write_fwd(const FwdOut &O, int64_t q, int status
 // ---------------------------------------------------------------------------
 template <int G, int PACKED, class RayT, class Rec>
 __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, int32_t start,
-                                    double epsilon,
+                                    int32_t hoff, double epsilon,
                                     double log_eps, double width_floor, int32_t step_limit,
                                     int gl, unsigned gmask, int32_t &nseg, int32_t &cells,
                                     int32_t &visits, Rec &&rec) {
@@ -191,7 +202,7 @@ __device__ __forceinline__ int walk(const SceneView<PACKED> &S, const RayT &r, i
             cells = step_limit;
             return RFB_STATUS_STEP_LIMIT;
         }
-        const Cell c = S.cell(i);
+        const Cell c = S.cell(i + hoff);  // hoff: the ray's region copy (view-culled scenes)
         // packed: + the neighbours a view-culled row dropped (k_cull_rows)
         visits += c.k1 - c.k0 + (PACKED ? (__float_as_int(c.n1max) & 31) : 0);
         double best_t;
@@ -332,8 +343,11 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
         float cr = 0.f, cg = 0.f, cb = 0.f;
         const bool dump = O.seg_cap > 0;
         int32_t nseg, cells, visits;
+        const int32_t hoff =
+            PACKED ? src.region_of(oidx, S.view_rx, S.view_ry) * (int32_t)S.n_sites : 0;
         int status = walk<G, PACKED>(
-            S, r, start, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells, visits,
+            S, r, start, hoff, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells,
+            visits,
             [&](int32_t s, int32_t cell, double sigma, double t0, double t1) {
                 double delta = t1 - t0;
                 const double alpha = (double)(-expm1f(-(float)(sigma * delta)));
@@ -604,9 +618,11 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 double bsum = basis_setup(rr, bas);
                 ctol = color_tol(S, SHDEG > 0 ? bsum : kC0);
             }
+            const int32_t hoff =
+                PACKED ? src.region_of(q, S.view_rx, S.view_ry) * (int32_t)S.n_sites : 0;
             status = walk<G, PACKED>(
-                S, r, start, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg, cells,
-                visits,
+                S, r, start, hoff, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg,
+                cells, visits,
                 [&](int32_t s, int32_t cell, double sigma, double t0, double t1) {
                     const double e = exp(-sigma * (t1 - t0));
                     double col[3];
@@ -1528,62 +1544,149 @@ __global__ void k_refresh_rows(int64_t n, const double *pos, CellHdr *cells, con
 // |coordinate|), covered by widening the margin by 2^-21 X.  One row per 16
 // lanes; the kept records are compacted with a ballot.
 // ---------------------------------------------------------------------------
-constexpr int kCullMaxDirs = 8;
+constexpr int kCullMaxDirs = 8;     // generators of one cone (rfb_cull_scene)
+constexpr int kCullMaxRegions = 32;  // regions of a view (rfb_cull_view)
+constexpr int kCullMaxGen = 72;  // (rx + 1)(ry + 1) for rx * ry <= 32
 constexpr int kCullMaxDrop = 31;
 struct CullCone {
-    double c[kCullMaxDirs][3];
-    int32_t nd;
+    // grid mode (rx > 0): the (rx + 1) x (ry + 1) region-corner directions, row-major;
+    // region (ix, iy) is the cone of corners (ix, iy), (ix + 1, iy), (ix, iy + 1),
+    // (ix + 1, iy + 1).  Single-cone mode (rx == 0): nd generators, one region.
+    float c[kCullMaxGen][3];  // unit vectors (fp32: the margin covers their rounding)
+    int32_t rx, ry, nd;
+    int64_t stride;  // edge slots between region copies
 };
-__global__ void k_cull_rows(const CellHdr *cells, const float4 *edges, int64_t n, CullCone cone,
+// Record e of the row of a cell at (xi, yi, zi): bit k set when the face is back-facing
+// with margin for generator k.  fp32: n = fl(x_j - x_i) and the dot product round by
+// <= 8 2^-24 |n|_1 (|c| = 1), so `dot < -2^-18 |n|_1` implies an exact c . n below
+// -3e-6 |n|_1 (>> the 1e-9 the reference's fp64 `denom` needs); fp64 sites: + 2^-21 X.
+__device__ __forceinline__ uint64_t cull_bits(const CullCone &cone, int nc, float xi, float yi,
+                                              float zi, float xa, const float4 &e, int pos64) {
+    const float nx = e.x - xi, ny = e.y - yi, nz = e.z - zi;
+    float marg = 0x1p-18f * (fabsf(nx) + fabsf(ny) + fabsf(nz));
+    if (pos64) marg += 0x1p-21f * fmaxf(xa, fmaxf(fabsf(e.x), fmaxf(fabsf(e.y), fabsf(e.z))));
+    uint64_t b = 0;
+    for (int k = 0; k < nc; ++k) {
+        const float d = __fmaf_rn(cone.c[k][2], nz, __fmaf_rn(cone.c[k][1], ny, cone.c[k][0] * nx));
+        b |= (uint64_t)(d < -marg) << k;
+    }
+    return b;
+}
+// bit p of the result: region p culled (grid: bit iy (rx + 1) + ix)
+__device__ __forceinline__ uint64_t region_bits(const CullCone &cone, uint64_t b) {
+    if (cone.rx == 0) return b == (1ull << cone.nd) - 1 ? 1ull : 0ull;
+    const int w = cone.rx + 1;
+    return b & (b >> 1) & (b >> w) & (b >> (w + 1));
+}
+#ifndef RFB_CULL_ROWS
+#define RFB_CULL_ROWS 1  // rows per 16-lane group (their loads issued together)
+#endif
+#ifndef RFB_CULL_MINB
+#define RFB_CULL_MINB 8  // resident 256-thread blocks per SM (memory-level parallelism)
+#endif
+constexpr int kCullRows = RFB_CULL_ROWS;
+__global__ void __launch_bounds__(256, RFB_CULL_MINB) k_cull_rows(const CellHdr *cells, const float4 *edges, int64_t n, CullCone cone,
                             int pos64, CellHdr *cells_out, float4 *edges_out) {
-    const int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kRowLanes;
-    if (u >= n) return;  // whole 16-lane groups
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kRowLanes;
+    if (g * kCullRows >= n) return;  // whole 16-lane groups
     const int gl = threadIdx.x & (kRowLanes - 1);
     const unsigned gshift = threadIdx.x & 16;
     const unsigned gmask = 0xffffu << gshift;
-    const CellHdr h = cells[u];
-    const double xi = h.x, yi = h.y, zi = h.z;
-    const double xa = fmax(fabs(xi), fmax(fabs(yi), fabs(zi)));
-    const int32_t deg = h.k1 - h.k0;
-    int32_t m = 0;
-    for (int pass = 0; pass < 2; ++pass) {  // pass 1: the row would drop > 31, copy it whole
-        m = 0;
-        for (int32_t t0 = 0; t0 < deg; t0 += kRowLanes) {
-            const int32_t t = t0 + gl;
-            const bool real = t < deg;
-            bool keep = real;
-            float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (real) {
-                e = edges[h.k0 + t];
-                if (pass == 0) {
-                    const double nx = (double)e.x - xi, ny = (double)e.y - yi,
-                                 nz = (double)e.z - zi;
-                    double marg = 1e-9 * (fabs(nx) + fabs(ny) + fabs(nz));
-                    if (pos64)
-                        marg += 0x1p-21 * fmax(xa, fmax(fabs((double)e.x),
-                                                        fmax(fabs((double)e.y), fabs((double)e.z))));
-                    bool back = true;
-                    for (int k = 0; k < cone.nd; ++k)
-                        back = back &&
-                               (cone.c[k][0] * nx + cone.c[k][1] * ny + cone.c[k][2] * nz < -marg);
-                    keep = !back;
+    const unsigned lt = (1u << gl) - 1u;
+    const int nc = cone.rx ? (cone.rx + 1) * (cone.ry + 1) : cone.nd;
+    const int nr = cone.rx ? cone.rx * cone.ry : 1;
+    const float qnan = __int_as_float(0x7fffffff);
+    const float4 pad = make_float4(qnan, qnan, qnan, qnan);
+    // the group's rows: headers, then the (<= 2 per lane) records of every short row,
+    // all loads in flight together (the kernel is latency-bound otherwise)
+    CellHdr h[kCullRows];
+    float4 e0[kCullRows], e1[kCullRows];
+#pragma unroll
+    for (int q = 0; q < kCullRows; ++q) {
+        const int64_t u = g * kCullRows + q;
+        if (u < n) h[q] = cells[u];
+        else h[q].k0 = h[q].k1 = 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kCullRows; ++q) {
+        const int32_t deg = h[q].k1 - h[q].k0;
+        e0[q] = gl < deg ? edges[h[q].k0 + gl] : pad;
+        e1[q] = gl + kRowLanes < deg && deg <= kCullMaxDrop ? edges[h[q].k0 + kRowLanes + gl] : pad;
+    }
+#pragma unroll
+    for (int q = 0; q < kCullRows; ++q) {
+        const int64_t u = g * kCullRows + q;
+        if (u >= n) break;
+        const CellHdr hq = h[q];
+        const float xa = fmaxf(fabsf(hq.x), fmaxf(fabsf(hq.y), fabsf(hq.z)));
+        const int32_t deg = hq.k1 - hq.k0;
+        auto header = [&](int r, int64_t k0, int32_t m) {
+            CellHdr o = hq;
+            o.k0 = (int32_t)k0;
+            o.k1 = (int32_t)(k0 + m);
+            o.n1max = __uint_as_float((__float_as_uint(hq.n1max) & ~31u) | (unsigned)(deg - m));
+            cells_out[r * n + u] = o;
+        };
+        if (deg <= kCullMaxDrop) {
+            // every region from the same bits of the (<= 2) records each lane holds
+            const bool real0 = gl < deg, real1 = gl + kRowLanes < deg;
+            const uint64_t c0 =
+                real0 ? region_bits(cone, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e0[q], pos64)) : 0;
+            const uint64_t c1 =
+                real1 ? region_bits(cone, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e1[q], pos64)) : 0;
+            int ix = 0, iy = 0;
+            for (int r = 0; r < nr; ++r) {
+                const int p = cone.rx ? iy * (cone.rx + 1) + ix : 0;
+                const bool k0b = real0 && !((c0 >> p) & 1), k1b = real1 && !((c1 >> p) & 1);
+                const unsigned b0 = (__ballot_sync(gmask, k0b) >> gshift) & 0xffffu;
+                const unsigned b1 = (__ballot_sync(gmask, k1b) >> gshift) & 0xffffu;
+                const int64_t k0 = r * cone.stride + hq.k0;
+                const int32_t m = __popc(b0) + __popc(b1);
+                // the rest of the row's original extent gets pads: whole 32-byte sectors
+                // written (a partly written sector costs HBM a read-modify-write)
+                const int32_t degp = (deg + 1) & ~1;
+                if (k0b) edges_out[k0 + __popc(b0 & lt)] = e0[q];
+                if (k1b) edges_out[k0 + __popc(b0) + __popc(b1 & lt)] = e1[q];
+                if (gl >= m && gl < degp) edges_out[k0 + gl] = pad;
+                if (gl + kRowLanes >= m && gl + kRowLanes < degp) edges_out[k0 + kRowLanes + gl] = pad;
+                if (gl == 0) header(r, k0, m);
+                if (++ix == cone.rx) {
+                    ix = 0;
+                    ++iy;
                 }
             }
-            const unsigned bal = (__ballot_sync(gmask, keep) >> gshift) & 0xffffu;
-            if (keep) edges_out[h.k0 + m + __popc(bal & ((1u << gl) - 1u))] = e;
-            m += __popc(bal);
+            continue;
         }
-        if (deg - m <= kCullMaxDrop) break;
-    }
-    if (gl == 0) {
-        if (m & 1) {
-            const float qnan = __int_as_float(0x7fffffff);
-            edges_out[h.k0 + m] = make_float4(qnan, qnan, qnan, qnan);
+        // long rows (rare): per region, over chunks of 16; a region that would drop more
+        // than 31 records (the n1max field holds 5 bits) keeps the row whole
+        int ix = 0, iy = 0;
+        for (int r = 0; r < nr; ++r) {
+            const int p = cone.rx ? iy * (cone.rx + 1) + ix : 0;
+            const int64_t k0 = r * cone.stride + hq.k0;
+            int32_t m = 0;
+            for (int pass = 0; pass < 2; ++pass) {
+                m = 0;
+                for (int32_t t0 = 0; t0 < deg; t0 += kRowLanes) {
+                    const int32_t t = t0 + gl;
+                    const bool real = t < deg;
+                    const float4 e = real ? edges[hq.k0 + t] : pad;
+                    bool keep = real;
+                    if (real && pass == 0)
+                        keep = !((region_bits(cone, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e,
+                                                              pos64)) >> p) & 1);
+                    const unsigned bal = (__ballot_sync(gmask, keep) >> gshift) & 0xffffu;
+                    if (keep) edges_out[k0 + m + __popc(bal & lt)] = e;
+                    m += __popc(bal);
+                }
+                if (deg - m <= kCullMaxDrop) break;
+            }
+            for (int32_t t = m + gl; t < ((deg + 1) & ~1); t += kRowLanes) edges_out[k0 + t] = pad;
+            if (gl == 0) header(r, k0, m);
+            if (++ix == cone.rx) {
+                ix = 0;
+                ++iy;
+            }
         }
-        CellHdr o = h;
-        o.k1 = h.k0 + m;
-        o.n1max = __uint_as_float((__float_as_uint(h.n1max) & ~31u) | (unsigned)(deg - m));
-        cells_out[u] = o;
     }
 }
 
@@ -1621,6 +1724,11 @@ static SceneView<PACKED> view(const rfb_scene *s) {
     v.bg[2] = s->background[2];
     v.n_sites = s->n_sites;
     v.n_edges = s->n_edges;
+    v.view_rx = s->view_rx > 0 ? s->view_rx : 0;
+    v.view_ry = s->view_rx > 0 ? s->view_ry : 0;
+    v.n_views = s->view_rx > 0 ? s->view_rx * s->view_ry : 1;
+    v.edge_slots = s->view_rx > 0 ? (int64_t)v.n_views * RFB_VIEW_STRIDE(s->n_sites, s->n_edges)
+                                  : (int64_t)RFB_PACKED_EDGE_SLOTS(s->n_sites, s->n_edges);
     return v;
 }
 
@@ -1652,6 +1760,9 @@ static bool scene_ok(const rfb_scene *s) {
         s->n_sites >= (1 << 29) || (s->sh_degree != 0 && s->sh_degree != 3))
         return false;
     if (s->packed && (!s->cells || !s->edges || !s->edge_nbr || !s->sh32)) return false;
+    if (s->view_rx < 0 || s->view_ry < 0 || (s->view_rx > 0) != (s->view_ry > 0) ||
+        s->view_rx * s->view_ry > kCullMaxRegions || (s->view_rx > 0 && !s->packed))
+        return false;
     if (s->packed && ((reinterpret_cast<uintptr_t>(s->cells) | reinterpret_cast<uintptr_t>(s->edges) |
                        reinterpret_cast<uintptr_t>(s->sh32)) & 31u))
         return false;  // 256-bit loads
@@ -1868,7 +1979,7 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
     FwdOut O = dev_out(out);
     ArrayRays src{rays->origins, rays->directions, rays->t_min, rays->t_max, rays->start_sites,
-                  rays->m, rays->order};
+                  rays->m, rays->order, rays->region};
     Grads G{grads->site4g, grads->sh};
     double log_eps = p->epsilon > 0.0 ? std::log(p->epsilon) : 0.0;
     dim3 grid((unsigned)(slots / kTrainBlock));
@@ -2160,7 +2271,7 @@ int rfb_render_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_para
     if (!rays->origins || !rays->directions || !rays->t_min || !rays->t_max || !rays->start_sites)
         return RFB_EINVAL;
     ArrayRays src{rays->origins, rays->directions, rays->t_min, rays->t_max, rays->start_sites,
-                  rays->m, rays->order};
+                  rays->m, rays->order, rays->region};
     return launch_render(scene, src, params, out, workspace, workspace_bytes,
                          (cudaStream_t)stream);
 }
@@ -2196,31 +2307,83 @@ int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb
     return launch_render(scene, src, params, out, workspace, workspace_bytes, st);
 }
 
-int rfb_cull_scene(const rfb_scene *scene, const double *dirs, int32_t n_dirs, void *cells_out,
-                   void *edges_out, rfb_scene *view_out, void *stream) {
-    if (!scene_ok(scene) || !scene->packed || !dirs || n_dirs < 1 || n_dirs > kCullMaxDirs ||
-        !cells_out || !edges_out || !view_out ||
-        (reinterpret_cast<uintptr_t>(cells_out) & 31) || (reinterpret_cast<uintptr_t>(edges_out) & 31))
-        return RFB_EINVAL;
-    CullCone cone;
-    for (int k = 0; k < kCullMaxDirs; ++k)
-        for (int a = 0; a < 3; ++a) cone.c[k][a] = k < n_dirs ? dirs[3 * k + a] : 0.0;
-    for (int k = 0; k < n_dirs; ++k) {  // unit generators (the margin is relative to |c| = 1)
-        const double l = std::sqrt(cone.c[k][0] * cone.c[k][0] + cone.c[k][1] * cone.c[k][1] +
-                                   cone.c[k][2] * cone.c[k][2]);
-        if (!(l > 0.0) || !std::isfinite(l)) return RFB_EINVAL;
-        for (int a = 0; a < 3; ++a) cone.c[k][a] /= l;
-    }
-    cone.nd = n_dirs;
+static int launch_cull(const rfb_scene *scene, const CullCone &cone, void *cells_out,
+                       void *edges_out, rfb_scene *view_out, int32_t rx, int32_t ry,
+                       cudaStream_t st) {
     *view_out = *scene;
     view_out->cells = cells_out;
     view_out->edges = edges_out;
-    if (scene->n_sites == 0) return RFB_OK;
-    cudaStream_t st = (cudaStream_t)stream;
-    k_cull_rows<<<(unsigned)((scene->n_sites * kRowLanes + 255) / 256), 256, 0, st>>>(
+    view_out->view_rx = rx;
+    view_out->view_ry = ry;
+    const int64_t groups = (scene->n_sites + kCullRows - 1) / kCullRows;
+    k_cull_rows<<<(unsigned)((groups * kRowLanes + 255) / 256), 256, 0, st>>>(
         (const CellHdr *)scene->cells, (const float4 *)scene->edges, scene->n_sites, cone,
         scene->positions_f64 ? 1 : 0, (CellHdr *)cells_out, (float4 *)edges_out);
     return (int)cudaGetLastError();
+}
+
+static bool cull_args_ok(const rfb_scene *scene, const void *cells_out, const void *edges_out,
+                         const rfb_scene *view_out) {
+    return scene_ok(scene) && scene->packed && scene->view_rx == 0 && cells_out && edges_out &&
+           view_out && !(reinterpret_cast<uintptr_t>(cells_out) & 31) &&
+           !(reinterpret_cast<uintptr_t>(edges_out) & 31);
+}
+
+// unit generator k of cone `c` from a direction (false: zero or non-finite)
+static bool set_gen(CullCone &c, int k, const double *d) {
+    const double l = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (!(l > 0.0) || !std::isfinite(l)) return false;
+    for (int a = 0; a < 3; ++a) c.c[k][a] = (float)(d[a] / l);
+    return true;
+}
+
+int rfb_cull_scene(const rfb_scene *scene, const double *dirs, int32_t n_dirs, void *cells_out,
+                   void *edges_out, rfb_scene *view_out, void *stream) {
+    if (!cull_args_ok(scene, cells_out, edges_out, view_out) || !dirs || n_dirs < 1 ||
+        n_dirs > kCullMaxDirs)
+        return RFB_EINVAL;
+    CullCone cone{};
+    for (int k = 0; k < n_dirs; ++k)
+        if (!set_gen(cone, k, dirs + 3 * k)) return RFB_EINVAL;
+    cone.rx = cone.ry = 0;
+    cone.nd = n_dirs;
+    cone.stride = 0;
+    return launch_cull(scene, cone, cells_out, edges_out, view_out, 0, 0, (cudaStream_t)stream);
+}
+
+int rfb_cull_view(const rfb_scene *scene, const rfb_camera *camera, int32_t rx, int32_t ry,
+                  void *cells_out, void *edges_out, rfb_scene *view_out, void *stream) {
+    if (!cull_args_ok(scene, cells_out, edges_out, view_out) || !camera || camera->kind != 0 ||
+        rx < 1 || ry < 1 || rx * ry > kCullMaxRegions || (rx + 1) * (ry + 1) > kCullMaxGen ||
+        camera->width < rx ||
+        camera->height < ry || !(camera->focal > 0.0))
+        return RFB_EINVAL;
+    const int64_t stride = RFB_VIEW_STRIDE(scene->n_sites, scene->n_edges);
+    if ((int64_t)rx * ry * stride >= (int64_t)INT32_MAX ||
+        (int64_t)rx * ry * scene->n_sites >= (int64_t)INT32_MAX)
+        return RFB_EINVAL;  // header / slot indices are int32
+    CullCone cone{};
+    cone.rx = rx;
+    cone.ry = ry;
+    cone.nd = 4;
+    cone.stride = stride;
+    const int64_t W = camera->width, H = camera->height;
+    // region ix holds the pixels with px * rx / W == ix, i.e. columns ceil(ix W / rx) ..
+    // ceil((ix + 1) W / rx) - 1: their centres lie strictly inside the pixel-edge lines
+    // col = ceil(ix W / rx) and ceil((ix + 1) W / rx), which the regions share
+    for (int iy = 0; iy <= ry; ++iy)
+        for (int ix = 0; ix <= rx; ++ix) {
+            const double col = (double)((ix * W + rx - 1) / rx);
+            const double row = (double)((iy * H + ry - 1) / ry);
+            // camera.py:78-92: d_cam = (u, v, -1), d = R d_cam (here at pixel edges)
+            const double u = (col - camera->cx) / camera->focal;
+            const double v = -(row - camera->cy) / camera->focal;
+            double d[3];
+            for (int a = 0; a < 3; ++a)
+                d[a] = camera->pose[4 * a] * u + camera->pose[4 * a + 1] * v - camera->pose[4 * a + 2];
+            if (!set_gen(cone, iy * (rx + 1) + ix, d)) return RFB_EINVAL;
+        }
+    return launch_cull(scene, cone, cells_out, edges_out, view_out, rx, ry, (cudaStream_t)stream);
 }
 
 int rfb_backward_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,

@@ -140,6 +140,10 @@ struct SceneView {
     const float *absmax_p;  // nullable device copy of the bound (training: raised by Adam)
     double bg[3];
     int64_t n_sites, n_edges;  // extents (RFB_CHECK builds assert every index against them)
+    // view-culled scenes (rfb_cull_view): view_rx * view_ry region copies of the
+    // headers (region r's at hdr + r * n_sites; the walk adds the ray's offset) and rows
+    int32_t view_rx, view_ry, n_views;
+    int64_t edge_slots;  // records in `edge` (every region)
 
     // site id <-> packed index (identity for the generic layout)
     __device__ __forceinline__ int32_t to_pk(int32_t i) const {
@@ -154,7 +158,7 @@ struct SceneView {
     // when a segment is recorded) -- fewer live registers across the
     // neighbour loop.
     __device__ __forceinline__ Cell cell(int32_t i) const {
-        RFB_BOUND(i, n_sites);
+        RFB_BOUND(i, n_sites * n_views);
         Cell c;
         if (PACKED) {
             const float4 *p = reinterpret_cast<const float4 *>(hdr + i);
@@ -165,7 +169,7 @@ struct SceneView {
             c.k1 = __float_as_int(b.x);
             c.n1max = b.y;
             RFB_BOUND(c.k0, c.k1 + 1);
-            RFB_BOUND(c.k1, n_edges + n_sites + 3);  // padded rows (RFB_PACKED_EDGE_SLOTS)
+            RFB_BOUND(c.k1, edge_slots + 1);  // padded rows (RFB_PACKED_EDGE_SLOTS / view)
             RFB_BOUND(c.k0 & 1, 1);                  // rows start at even slots
         } else {
             double4 s = ld_site(site4 + i);
@@ -631,7 +635,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     int32_t best_k = 0x7fffffff;
     // phase 2 on slot k: kernels.py:116-133 in fp64
     auto exact = [&](int32_t k) {
-        RFB_BOUND(k, S.n_edges + S.n_sites + 2);
+        RFB_BOUND(k, S.edge_slots);
         const float4 ej = rec_site(S.edge, k);  // (in L1: phase 1 just read it)
         const int32_t j = __float_as_int(ej.w);
         RFB_BOUND(j, S.n_sites);
@@ -690,7 +694,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
         RFB_PRAGMA_UNROLL(RFB_PAIR_UNROLL)
         for (int32_t kp = c.k0; kp < c.k1; kp += 2) {
             float4 e0, e1;
-            RFB_BOUND(kp + 1, S.n_edges + S.n_sites + 2);
+            RFB_BOUND(kp + 1, S.edge_slots);
 #if RFB_CHECK
             assert((reinterpret_cast<uintptr_t>(S.edge + kp) & 31) == 0);
 #endif
@@ -743,7 +747,7 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
     int32_t nk = 0;
     RFB_PRAGMA_UNROLL(RFB_F32_UNROLL)
     for (int32_t k = k0; k < c.k1; k += G, ++nk) {
-        RFB_BOUND(k, S.n_edges + S.n_sites + 2);
+        RFB_BOUND(k, S.edge_slots);
         const float4 e = rec_site(S.edge, k);
         float lb, ub;
         bool front, sure;

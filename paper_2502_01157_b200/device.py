@@ -260,15 +260,55 @@ class DeviceScene:
         if dirs is None or not self.packed or not self.VIEW_CULL or self.n_sites == 0:
             return self.c
         d = np.ascontiguousarray(np.asarray(dirs, dtype=np.float64).reshape(-1, 3))
-        if getattr(self, "_view_cells", None) is None:
-            self._view_cells = torch.empty_like(self.cells)
-            self._view_edges = torch.empty_like(self.edges)
-            self._view_c = _lib.rfb_scene()
+        self._view_alloc(1)
         _lib.check(self.lib.rfb_cull_scene(
             self.c, d.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(len(d)),
             _ptr(self._view_cells), _ptr(self._view_edges), ctypes.byref(self._view_c),
             _stream(stream)), "rfb_cull_scene")
         return ctypes.byref(self._view_c)
+
+    # image regions culled separately by render_image_device (rfb_cull_view): smaller
+    # cones drop more faces; "RX"x"RY" from RFB_VIEW_REGIONS (e.g. "4x4"), "1x1" = one cone
+    VIEW_REGIONS = tuple(int(v) for v in os.environ.get("RFB_VIEW_REGIONS", "4x2").split("x"))
+
+    def _view_alloc(self, regions: int):
+        if getattr(self, "_view_regions", 0) < regions:
+            self._view_cells = self._view_edges = None
+            stride = (self.n_edges + self.n_sites + 3) & ~1  # RFB_VIEW_STRIDE
+            self._view_cells = torch.empty((regions * self.n_sites, 8), dtype=torch.int32,
+                                           device=self.device)
+            self._view_edges = torch.empty((regions * stride, 4), dtype=torch.float32,
+                                           device=self.device)
+            self._view_regions = regions
+            self._view_c = _lib.rfb_scene()
+
+    def view_camera(self, camera, regions=None, stream=None):
+        """``view`` per image region of a pinhole camera (rfb_cull_view): an RX x RY
+        grid of pixel rectangles, each culled against its own corner cone; the
+        walk picks each pixel's region (rfb_render_image) or takes it from
+        ``region_ids`` (ray batches).  Falls back like ``view``."""
+        rx, ry = regions or self.VIEW_REGIONS
+        rx, ry = max(1, min(int(rx), int(camera.width))), max(1, min(int(ry), int(camera.height)))
+        if (not self.packed or not self.VIEW_CULL or self.n_sites == 0
+                or getattr(camera, "kind", "pinhole") == "fisheye"):
+            return self.c
+        self._view_alloc(rx * ry)
+        cam = camera_struct(camera)
+        _lib.check(self.lib.rfb_cull_view(self.c, ctypes.byref(cam), rx, ry,
+                                          _ptr(self._view_cells), _ptr(self._view_edges),
+                                          ctypes.byref(self._view_c), _stream(stream)),
+                   "rfb_cull_view")
+        return ctypes.byref(self._view_c)
+
+    def region_ids(self, camera, pixels: torch.Tensor, regions=None) -> torch.Tensor:
+        """uint8 region of each row-major pixel index for ``view_camera(camera,
+        regions)`` (rfb.h: (py * ry / H) * rx + px * rx / W)."""
+        rx, ry = regions or self.VIEW_REGIONS
+        W, H = int(camera.width), int(camera.height)
+        rx, ry = max(1, min(int(rx), W)), max(1, min(int(ry), H))
+        p = pixels.to(self.device, torch.int64)
+        py, px = p // W, p % W
+        return ((py * ry // H) * rx + px * rx // W).to(torch.uint8)
 
     # -- device-resident updates (training) ------------------------------
     def rebuild_adjacency(self, positions: torch.Tensor | None = None, packed=None,
@@ -472,6 +512,19 @@ def fwd_struct(r: ForwardResult) -> _lib.rfb_fwd_out:
     return o
 
 
+def _view_for(ds: DeviceScene, view_dirs, view, stream):
+    """(scene struct, region ids) for a ray batch: ``view`` = (camera, pixels) walks
+    the camera's region-culled rows with each ray's region from its row-major pixel
+    index; ``view_dirs`` = a cone holding every direction (one region)."""
+    if view is not None:
+        cam, pixels = view
+        sc = ds.view_camera(cam, stream=stream)
+        if sc is ds.c or getattr(ds._view_c, "view_rx", 0) == 0:
+            return sc, None
+        return sc, ds.region_ids(cam, pixels).contiguous()
+    return ds.view(view_dirs, stream), None
+
+
 def rays_struct(origins, directions, t_min, t_max, start, order=None) -> _lib.rfb_rays:
     r = _lib.rfb_rays()
     r.m = origins.shape[0]
@@ -521,12 +574,15 @@ def render_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
                        per_ray=True, seg_capacity=0, lanes_per_ray=DEFAULT_LANES,
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
-                       order=None, stream=None, view_dirs=None) -> ForwardResult:
+                       order=None, stream=None, view_dirs=None, view=None) -> ForwardResult:
     """rfb_render_rays on device tensors (kernels.py:199-247).  ``order``: an
     optional processing permutation (e.g. coherent_order) -- outputs stay
     indexed by ray.  ``view_dirs``: generators of a cone holding every ray
     direction (``view_cone(camera)`` for a camera's pixels): the walk then
-    uses the view-culled rows (``DeviceScene.view``; same output)."""
+    uses the view-culled rows (``DeviceScene.view``; same output).  ``view``:
+    (camera, pixels) -- the rays are those pixels (row-major indices) of a
+    pinhole camera: the walk uses the camera's region-culled rows
+    (``DeviceScene.view_camera``), a smaller cone per ray."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=per_ray, seg_capacity=seg_capacity)
     ws = (workspace or Workspace(ds.device)).get(256)
@@ -534,7 +590,9 @@ def render_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start
     order = _order32(order, m, ds.device)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
     o = fwd_struct(res)
-    sc = ds.view(view_dirs, stream)
+    sc, reg = _view_for(ds, view_dirs, view, stream)
+    if reg is not None:
+        rays.region = reg.data_ptr()
     _lib.check(ds.lib.rfb_render_rays(sc, ctypes.byref(rays), ctypes.byref(p), ctypes.byref(o),
                                       _ptr(ws), ws.numel(), _stream(stream)), "rfb_render_rays")
     return res
@@ -602,7 +660,7 @@ def render_image_device(ds: DeviceScene, camera, *, epsilon=DEFAULT_EPSILON,
     if cull == "last":  # diagnostics: the view the previous call derived, as it is now
         sc = ctypes.byref(ds._view_c)
     else:
-        sc = ds.view(view_cone(camera), stream) if cull else ds.c
+        sc = ds.view_camera(camera, stream=stream) if cull else ds.c
     _lib.check(ds.lib.rfb_render_image(sc, ctypes.byref(cam), ctypes.byref(p), 0.0, float(t_max),
                                        int(start_site), _ptr(tile_ids), int(tile_ids.numel()),
                                        int(tile_w), int(tile_h), ctypes.byref(o), _ptr(ws),
@@ -647,10 +705,10 @@ def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, sta
                          grads: GradBuffers, *, epsilon=DEFAULT_EPSILON,
                          step_limit=DEFAULT_STEP_LIMIT, f64=False,
                          workspace: Workspace | None = None, out: ForwardResult | None = None,
-                         order="auto", lanes_per_ray=0, stream=None, view_dirs=None) -> ForwardResult:
+                         order="auto", lanes_per_ray=0, stream=None, view_dirs=None, view=None) -> ForwardResult:
     """rfb_backward_rays (render.py:152-221 generic adjoint).  ``order``: see _order32;
     ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule;
-    ``view_dirs``: see render_rays_device."""
+    ``view_dirs``, ``view``: see render_rays_device."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(
@@ -661,7 +719,9 @@ def backward_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, sta
     o = fwd_struct(res)
     g = grads.struct()
     adj = adjoints.to(ds.device, torch.float64).contiguous()
-    sc = ds.view(view_dirs, stream)
+    sc, reg = _view_for(ds, view_dirs, view, stream)
+    if reg is not None:
+        rays.region = reg.data_ptr()
     _lib.check(ds.lib.rfb_backward_rays(sc, ctypes.byref(rays), ctypes.byref(p), _ptr(adj),
                                         ctypes.byref(o), ctypes.byref(g), _ptr(ws), ws.numel(),
                                         _stream(stream)), "rfb_backward_rays")
@@ -673,11 +733,11 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
                        quantile_scale: float = 0.0, u_pairs=None, weight_floor: float = 1e-4,
                        epsilon=DEFAULT_EPSILON, step_limit=DEFAULT_STEP_LIMIT, f64=False,
                        workspace: Workspace | None = None, out: ForwardResult | None = None,
-                       order="auto", lanes_per_ray=0, stream=None, view_dirs=None) -> ForwardResult:
+                       order="auto", lanes_per_ray=0, stream=None, view_dirs=None, view=None) -> ForwardResult:
     """rfb_train_batch (kernels.py:372-453).  ``loss`` float64 [2] accumulates.
     ``order``: "auto" sorts batches of >= 500k rays coherently (see _order32);
     ``lanes_per_ray``: 1 or 2 forces the kernel variant, 0 = the library's rule;
-    ``view_dirs``: see render_rays_device."""
+    ``view_dirs``, ``view``: see render_rays_device."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=True)
     ws = (workspace or Workspace(ds.device)).get(
@@ -692,7 +752,9 @@ def train_batch_device(ds: DeviceScene, origins, directions, t_min, t_max, start
     if quantile_scale > 0.0:
         up = u_pairs.to(ds.device, torch.float64).contiguous()
         n_pairs = up.shape[1]
-    sc = ds.view(view_dirs, stream)
+    sc, reg = _view_for(ds, view_dirs, view, stream)
+    if reg is not None:
+        rays.region = reg.data_ptr()
     _lib.check(ds.lib.rfb_train_batch(sc, ctypes.byref(rays), ctypes.byref(p), _ptr(targets),
                                       float(rgb_scale), float(quantile_scale), _ptr(up), n_pairs,
                                       float(weight_floor), ctypes.byref(o), ctypes.byref(g),

@@ -41,7 +41,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version_and_errors(lib):
-    assert lib.rfb_abi_version() == 14
+    assert lib.rfb_abi_version() == 15
     assert lib.rfb_error_string(0) == b"ok"
     assert lib.rfb_error_string(-1) == b"invalid argument"
 
@@ -58,7 +58,7 @@ int main(void) {
          sizeof(rfb_scene), sizeof(rfb_params), sizeof(rfb_rays), sizeof(rfb_fwd_out),
          sizeof(rfb_grads), sizeof(rfb_camera));
   F(rfb_scene, sh32) F(rfb_scene, packed) F(rfb_scene, sh_absmax) F(rfb_scene, background)
-  F(rfb_scene, sh_absmax_dev)
+  F(rfb_scene, sh_absmax_dev) F(rfb_scene, view_ry) F(rfb_rays, region)
   F(rfb_fwd_out, f64_outputs) F(rfb_fwd_out, seg_t1) F(rfb_fwd_out, seg_count) F(rfb_camera, focal) F(rfb_params, lanes_per_ray)
   return 0;
 }

@@ -124,11 +124,12 @@ def _d(a, dt=torch.float64):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", dt)
 
 
-@pytest.mark.parametrize("quantile,cull", [(False, True), (True, True), (False, False)])
+@pytest.mark.parametrize("quantile,cull", [(False, "regions"), (True, "regions"),
+                                           (False, "cone"), (False, None)])
 def test_train_batch_one_lane_full_view(cuda_ok, sa100k, ds100k, quantile, cull):
     """k_train<3, 1, true, Q, 1> (the config-3 kernel) on an 81,920-ray view in tile
     order, against the oracle's train_batch (kernels.py:372-453); the bench walks
-    the view-culled rows (view_dirs = the camera's cone)."""
+    the camera's region-culled rows (view = (camera, pixels), rfb_cull_view)."""
     from paper_2502_01157_b200 import device as dv
 
     W, H = 320, 256
@@ -149,7 +150,10 @@ def test_train_batch_one_lane_full_view(cuda_ok, sa100k, ds100k, quantile, cull)
                                 _d(np.full(m, start), torch.int32), _d(targets), gb, loss,
                                 rgb_scale=1.0 / (3 * m), quantile_scale=qs,
                                 u_pairs=_d(u) if quantile else None, f64=True, order=None,
-                                lanes_per_ray=1, view_dirs=dv.view_cone(cam) if cull else None)
+                                lanes_per_ray=1,
+                                view_dirs=dv.view_cone(cam) if cull == "cone" else None,
+                                view=(cam, torch.from_numpy(dv.tile_order(W, H)))
+                                if cull == "regions" else None)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
     np.testing.assert_array_equal(res.counters.cpu().numpy(), ref["counters"].sum(axis=0))
@@ -186,42 +190,74 @@ def test_backward_rays_one_lane_full_view(cuda_ok, sa100k, ds100k):
     assert rel(gb.sh.double().cpu().numpy(), dsh_ref) <= GRAD_RTOL
 
 
+def _check_culled(full_h, full_e, view_h, view_e, cones, n, stride, rows):
+    """Region r of a culled view: headers offset by r*stride, every row a CSR-ordered
+    subset of the full row, dropped records back-facing with margin for the region's
+    generators (kernel: fp32, 2^-18 |n|_1; checked here in fp64 with slack), kept ones
+    not back-facing with a clear margin, n1max's low 5 bits = number dropped."""
+    k0, k1 = full_h[:, 3], full_h[:, 6]
+    n1f = full_h[:, 7].view(np.uint32)
+    assert np.all(n1f & 31 == 0)
+    tot_drop = tot = 0
+    for r, cone in enumerate(cones):
+        vh = view_h[r * n:(r + 1) * n]
+        assert np.array_equal(vh[:, 3], k0 + r * stride)
+        n1v = vh[:, 7].view(np.uint32)
+        assert np.array_equal(n1v & ~np.uint32(31), n1f)
+        dropped = (n1v & 31).astype(np.int64)
+        kept = (vh[:, 6] - vh[:, 3]).astype(np.int64)
+        assert np.array_equal(kept + dropped, k1 - k0)
+        tot_drop += dropped.sum()
+        tot += (k1 - k0).sum()
+        c = cone / np.linalg.norm(cone, axis=1, keepdims=True)
+        for u in rows:
+            row = full_e[k0[u]:k1[u]]
+            vrow = view_e[vh[u, 3]:vh[u, 3] + kept[u]]
+            ids = row[:, 3].view(np.int32)
+            vids = vrow[:, 3].view(np.int32)
+            keep = np.isin(ids, vids)
+            assert np.array_equal(ids[keep], vids), "CSR order kept"
+            nn = row[:, :3].astype(np.float64) - full_h[u, :3].view(np.float32).astype(np.float64)
+            dots = nn @ c.T
+            l1 = np.abs(nn).sum(1)[:, None]
+            assert np.all(dots[~keep] < -2.0 ** -19 * l1[~keep]), "dropped a face not back-facing"
+            assert not np.any(np.all(dots[keep] < -2.0 ** -17 * l1[keep], axis=1)), "kept a back face"
+            if kept[u] & 1:
+                assert np.all(np.isnan(view_e[vh[u, 3] + kept[u]]))
+    return tot_drop / tot
+
+
 def test_view_culled_rows(cuda_ok, ds100k):
-    """rfb_cull_scene's copy of the packed rows: every row keeps a CSR-ordered
-    subset of its records, every dropped neighbour is back-facing with margin
-    for all four corner directions, n1max's low 5 bits hold the number dropped
-    (pack_row leaves them zero), and a sizeable share of the rows is dropped."""
+    """rfb_cull_scene (one cone: the 4 corner-pixel directions) and rfb_cull_view (a
+    4 x 2 grid of image regions, each with its own pixel-edge corner cone): the copies
+    of the packed rows hold exactly the faces that are not back-facing for the cone."""
     from paper_2502_01157_b200 import device as dv
 
     cam = _cam(480, 270, 0)
-    cone = dv.view_cone(cam)
-    ds100k.view(cone)
-    torch.cuda.synchronize()
+    n = ds100k.n_sites
     full_h = ds100k.cells.cpu().numpy()
-    view_h = ds100k._view_cells.cpu().numpy()
     full_e = ds100k.edges.cpu().numpy()
-    view_e = ds100k._view_edges.cpu().numpy()
-    k0, k1 = full_h[:, 3], full_h[:, 6]
-    assert np.array_equal(view_h[:, 3], k0)
-    n1f = full_h[:, 7].view(np.uint32)
-    n1v = view_h[:, 7].view(np.uint32)
-    assert np.all(n1f & 31 == 0)
-    assert np.array_equal(n1v & ~np.uint32(31), n1f)
-    dropped = (n1v & 31).astype(np.int64)
-    kept = view_h[:, 6] - k0
-    assert np.array_equal(kept + dropped, k1 - k0)
-    frac = dropped.sum() / (k1 - k0).sum()
-    assert 0.15 < frac < 0.4, frac
-    c = cone / np.linalg.norm(cone, axis=1, keepdims=True)
-    rng = np.random.default_rng(0)
-    for u in rng.choice(len(full_h), 300, replace=False):
-        row = full_e[k0[u]:k1[u]]
-        vrow = view_e[k0[u]:k0[u] + kept[u]]
-        ids = row[:, 3].view(np.int32)
-        vids = vrow[:, 3].view(np.int32)
-        assert np.array_equal(ids[np.isin(ids, vids)], vids), "CSR order kept"
-        n = row[:, :3].astype(np.float64) - full_h[u, :3].view(np.float32).astype(np.float64)
-        back = np.all(n @ c.T < -1e-9 * np.abs(n).sum(1)[:, None], axis=1)
-        assert np.array_equal(~np.isin(ids, vids), back)
-        if kept[u] & 1:
-            assert np.all(np.isnan(view_e[k0[u] + kept[u]]))
+    rows = np.random.default_rng(0).choice(n, 200, replace=False)
+    ds100k.view(dv.view_cone(cam))
+    torch.cuda.synchronize()
+    frac1 = _check_culled(full_h, full_e, ds100k._view_cells.cpu().numpy(),
+                          ds100k._view_edges.cpu().numpy(), [dv.view_cone(cam)], n, 0, rows)
+    assert 0.15 < frac1 < 0.4, frac1
+    rx, ry = 4, 2
+    ds100k.view_camera(cam, regions=(rx, ry))
+    torch.cuda.synchronize()
+    W, H = cam.width, cam.height
+    R = np.asarray(cam.pose)[:3, :3]
+    edges_c = [-(-ix * W // rx) for ix in range(rx + 1)]
+    edges_r = [-(-iy * H // ry) for iy in range(ry + 1)]
+    cones = []
+    for iy in range(ry):
+        for ix in range(rx):
+            pts = [(edges_c[ix + a], edges_r[iy + b]) for b in (0, 1) for a in (0, 1)]
+            d = np.array([[(c - cam.cx) / cam.focal, -(r - cam.cy) / cam.focal, -1.0]
+                          for c, r in pts])
+            cones.append(d @ R.T)
+    stride = (ds100k.n_edges + n + 3) & ~1
+    frac8 = _check_culled(full_h, full_e, ds100k._view_cells.cpu().numpy(),
+                          ds100k._view_edges.cpu().numpy(), cones, n, stride, rows)
+    assert frac8 > frac1

@@ -128,7 +128,7 @@ if args.train:
     fo = dv.alloc_forward(m, ds.device)
     reps = 1 if args.once else args.reps
     for cull in culls:
-      vd = dv.view_cone(cam) if cull else None
+      vw = (cam, perm) if cull else None
       loss.zero_()
       for r in range(reps + (0 if args.once else 1)):
           if r == 1 or (args.once and r == 0):
@@ -138,10 +138,10 @@ if args.train:
               up = torch.rand((m, 2, 2), dtype=torch.float64, device="cuda")
               dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
                                     rgb_scale=1.0 / (3 * m), quantile_scale=0.01 / (2 * m),
-                                    u_pairs=up, workspace=wsb, out=fo, order=None, view_dirs=vd)
+                                    u_pairs=up, workspace=wsb, out=fo, order=None, view=vw)
           else:
               dv.train_batch_device(ds, o, dirs, tmin, tmax, start, tg, gb, loss,
-                                    rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo, order=None, view_dirs=vd)
+                                    rgb_scale=1.0 / (3 * m), workspace=wsb, out=fo, order=None, view=vw)
       torch.cuda.synchronize()
       ms = (time.perf_counter() - t0) * 1e3 / reps
       import hashlib
