@@ -32,8 +32,13 @@ lines = [f"# {tag} launch list: ncu --metrics gpu__time_duration.sum --clock-con
 for k, (n, t) in agg.items():
     lines.append(f"{k[:70]:70s} {n:8d} {t / 1e6:10.3f} {t / n / 1e6:10.3f}")
 rend = sum(v[1] for k, v in agg.items() if "k_render" in k)
-fwd = sum(v[1] for k, v in agg.items() if "k_render" in k or "k_nearest" in k)
-lines += ["", f"k_render share of the forward step's kernel time: {100 * rend / fwd:.1f}%"]
+# k_cull_rows launches: one per forward view and one per training view (bench order)
+n_rend = sum(v[0] for k, v in agg.items() if "k_render" in k)
+n_cull = sum(v[0] for k, v in agg.items() if "k_cull_rows" in k)
+cull_avg = sum(v[1] for k, v in agg.items() if "k_cull_rows" in k) / max(n_cull, 1)
+fwd = sum(v[1] for k, v in agg.items() if "k_render" in k or "k_nearest" in k) + cull_avg * n_rend
+lines += ["", f"k_render share of the forward step's kernel time (k_cull_rows, k_nearest_*, "
+              f"k_render): {100 * rend / fwd:.1f}%"]
 open(f"profiles/{tag}_launches_summary.txt", "w").write("\n".join(lines) + "\n")
 subprocess.run(["cp", launches, f"profiles/{tag}_launches.csv"])
 summ = "\n".join(f"# {rep} (ncu --set full)\n" + ncu_summary.summarise(rep) for rep in reps)
