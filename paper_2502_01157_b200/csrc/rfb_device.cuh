@@ -24,6 +24,9 @@
 #ifndef RFB_LDG256
 #define RFB_LDG256 1  // 256-bit loads for edge pairs and SH rows (packed layout)
 #endif
+#ifndef RFB_SH_NOALLOC
+#define RFB_SH_NOALLOC 1  // SH row loads: 1 L1::no_allocate, 2 L1::evict_first, 0 default
+#endif
 #ifndef RFB_SH_PIPE
 #define RFB_SH_PIPE 1  // SH colour: the next channel's row loads overlap this channel's sum
 #endif
@@ -119,6 +122,27 @@ __device__ __forceinline__ void ldg256(const void *p, float4 &a, float4 &b) {
         : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
           "=f"(b.w)
         : "l"(p));
+}
+
+// The same for data used once per lane (SH rows): not allocated in L1, so the
+// step's header and row sectors stay there for their second use (sigma, phase 2)
+// instead of being evicted by the 192-byte rows (1080p config 2: 13.38 -> 12.32 ms;
+// evict_first: 13.11 ms; hints on the edge pairs / header / reverse-pass records:
+// no change).
+__device__ __forceinline__ void ldg256_stream(const void *p, float4 &a, float4 &b) {
+#if RFB_SH_NOALLOC == 1
+    asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+          "=f"(b.w)
+        : "l"(p));
+#elif RFB_SH_NOALLOC == 2
+    asm("ld.global.nc.L1::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z),
+          "=f"(b.w)
+        : "l"(p));
+#else
+    ldg256(p, a, b);
+#endif
 }
 
 // PACKED: 0 generic (site4 + int32 CSR), 1 packed with fp32-exact sites,
@@ -279,10 +303,10 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
             // two channels' loads in flight: channel ch+1's 64 B arrive while ch is summed
             const float4 *r4 = reinterpret_cast<const float4 *>(row);
             float4 va[4], vb[4];
-            ldg256(r4, va[0], va[1]);
-            ldg256(r4 + 2, va[2], va[3]);
-            ldg256(r4 + 4, vb[0], vb[1]);
-            ldg256(r4 + 6, vb[2], vb[3]);
+            ldg256_stream(r4, va[0], va[1]);
+            ldg256_stream(r4 + 2, va[2], va[3]);
+            ldg256_stream(r4 + 4, vb[0], vb[1]);
+            ldg256_stream(r4 + 6, vb[2], vb[3]);
             auto dot = [&](const float4 *v) {
                 float a = 0.5f;
 #pragma unroll
@@ -295,8 +319,8 @@ __device__ __forceinline__ int cell_color(const SceneView<PACKED> &S, int32_t i,
                 return (double)a;
             };
             acc[0] = dot(va);
-            ldg256(r4 + 8, va[0], va[1]);
-            ldg256(r4 + 10, va[2], va[3]);
+            ldg256_stream(r4 + 8, va[0], va[1]);
+            ldg256_stream(r4 + 10, va[2], va[3]);
             acc[1] = dot(vb);
             acc[2] = dot(va);
         } else {
