@@ -1582,9 +1582,20 @@ __device__ __forceinline__ uint64_t region_bits(const CullCone &cone, uint64_t b
 #define RFB_CULL_ROWS 1  // rows per 16-lane group (their loads issued together)
 #endif
 #ifndef RFB_CULL_MINB
-#define RFB_CULL_MINB 8  // resident 256-thread blocks per SM (memory-level parallelism)
+#define RFB_CULL_MINB 6  // resident 256-thread blocks per SM (memory-level parallelism)
 #endif
 constexpr int kCullRows = RFB_CULL_ROWS;
+// bit r: region r culls the record (from cull_bits' generator bits)
+__device__ __forceinline__ uint32_t region_mask(const CullCone &cone, int nr, uint64_t b) {
+    const uint64_t rb = region_bits(cone, b);
+    if (cone.rx == 0) return (uint32_t)(rb & 1u);
+    uint32_t m = 0;
+    int r = 0;
+    for (int iy = 0; iy < cone.ry; ++iy)
+        for (int ix = 0; ix < cone.rx; ++ix, ++r)
+            m |= (uint32_t)((rb >> (iy * (cone.rx + 1) + ix)) & 1u) << r;
+    return m;
+}
 __global__ void __launch_bounds__(256, RFB_CULL_MINB) k_cull_rows(const CellHdr *cells, const float4 *edges, int64_t n, CullCone cone,
                             int pos64, CellHdr *cells_out, float4 *edges_out) {
     const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kRowLanes;
@@ -1628,33 +1639,29 @@ __global__ void __launch_bounds__(256, RFB_CULL_MINB) k_cull_rows(const CellHdr 
             cells_out[r * n + u] = o;
         };
         if (deg <= kCullMaxDrop) {
-            // every region from the same bits of the (<= 2) records each lane holds
+            // every region from the same bits of the (<= 2) records each lane holds:
+            // bit r of m0 / m1 = the record is dropped from region r's copy
             const bool real0 = gl < deg, real1 = gl + kRowLanes < deg;
-            const uint64_t c0 =
-                real0 ? region_bits(cone, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e0[q], pos64)) : 0;
-            const uint64_t c1 =
-                real1 ? region_bits(cone, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e1[q], pos64)) : 0;
-            int ix = 0, iy = 0;
-            for (int r = 0; r < nr; ++r) {
-                const int p = cone.rx ? iy * (cone.rx + 1) + ix : 0;
-                const bool k0b = real0 && !((c0 >> p) & 1), k1b = real1 && !((c1 >> p) & 1);
+            const uint32_t m0 =
+                real0 ? region_mask(cone, nr, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e0[q], pos64)) : ~0u;
+            const uint32_t m1 =
+                real1 ? region_mask(cone, nr, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e1[q], pos64)) : ~0u;
+            const int32_t degp = (deg + 1) & ~1;
+            int32_t my_m = 0;  // lane r < nr: region r's kept count (it writes that header)
+            float4 *out = edges_out + hq.k0;
+            for (int r = 0; r < nr; ++r, out += cone.stride) {
+                const bool k0b = !((m0 >> r) & 1u), k1b = !((m1 >> r) & 1u);
                 const unsigned b0 = (__ballot_sync(gmask, k0b) >> gshift) & 0xffffu;
                 const unsigned b1 = (__ballot_sync(gmask, k1b) >> gshift) & 0xffffu;
-                const int64_t k0 = r * cone.stride + hq.k0;
-                const int32_t m = __popc(b0) + __popc(b1);
-                // the rest of the row's original extent gets pads: whole 32-byte sectors
-                // written (a partly written sector costs HBM a read-modify-write)
-                const int32_t degp = (deg + 1) & ~1;
-                if (k0b) edges_out[k0 + __popc(b0 & lt)] = e0[q];
-                if (k1b) edges_out[k0 + __popc(b0) + __popc(b1 & lt)] = e1[q];
-                if (gl >= m && gl < degp) edges_out[k0 + gl] = pad;
-                if (gl + kRowLanes >= m && gl + kRowLanes < degp) edges_out[k0 + kRowLanes + gl] = pad;
-                if (gl == 0) header(r, k0, m);
-                if (++ix == cone.rx) {
-                    ix = 0;
-                    ++iy;
-                }
+                const int32_t n0 = __popc(b0), m = n0 + __popc(b1);
+                if (k0b) out[__popc(b0 & lt)] = e0[q];
+                if (k1b) out[n0 + __popc(b1 & lt)] = e1[q];
+                // the rest of the row's extent gets pads (whole 32-byte sectors written)
+                if (gl >= m && gl < degp) out[gl] = pad;
+                if (gl + kRowLanes >= m && gl + kRowLanes < degp) out[kRowLanes + gl] = pad;
+                my_m = gl == r ? m : my_m;
             }
+            if (gl < nr) header(gl, gl * cone.stride + hq.k0, my_m);
             continue;
         }
         // long rows (rare): per region, over chunks of 16; a region that would drop more

@@ -1,4 +1,4 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
-REGIONS="1x1 2x2 4x2 4x4" python tools/cull_probe.py
-for f in build/variants/*.so; do echo "== $f"; REGIONS="1x1 2x2 4x2 4x4" RFB_LIB=$f python tools/cull_probe.py; done
+REGIONS="${REGIONS:-2x2 4x2 4x4}" python tools/cull_probe.py
+for f in build/variants/*.so; do echo "== $f"; REGIONS="${REGIONS:-2x2 4x2 4x4}" RFB_LIB=$f python tools/cull_probe.py; done
