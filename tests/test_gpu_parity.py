@@ -344,13 +344,13 @@ def test_effect_rays_device(cuda_ok, kind):
         np.testing.assert_allclose(od.cpu().numpy()[i], r.direction, rtol=0, atol=1e-14)
 
 
-@pytest.mark.parametrize("packed", [True, False])
-def test_fp64_positions_vs_oracle(cuda_ok, packed):
+@pytest.mark.parametrize("packed,cull", [(True, False), (True, True), (False, False)])
+def test_fp64_positions_vs_oracle(cuda_ok, packed, cull):
     """Sites that are not fp32-representable (as after an Adam step on the
     positions): the packed layout with the widened pre-filter bound
-    (positions_f64) and the generic fp64 layout; per-ray cell sequences,
-    counters and status must be the oracle's bit for bit, the image within
-    1e-4."""
+    (positions_f64), also over view-culled rows (rfb_cull_scene with the fp64-site
+    margin), and the generic fp64 layout; per-ray cell sequences, counters and
+    status must be the oracle's bit for bit, the image within 1e-4."""
     from paper_2502_01157_b200 import device as dv
     from paper_2502_01157_b200.synthetic import delaunay_csr
 
@@ -373,9 +373,19 @@ def test_fp64_positions_vs_oracle(cuda_ok, packed):
     start = int(orc.nearest_sites(pos, o[:1])[0])
     tmax = ds.default_t_max(o[:1])
     ref = orc.render_rays(sa, o, d, 0.0, tmax, start)
+    cone = None
+    if cull:  # every direction is a positive multiple of (u, v, -1), (u, v) in this box
+        uv = d[:, :2] / -d[:, 2:3]
+        lo, hi = uv.min(0), uv.max(0)
+        cone = np.array([[lo[0], lo[1], -1.0], [hi[0], lo[1], -1.0], [lo[0], hi[1], -1.0],
+                         [hi[0], hi[1], -1.0]])
     res = dv.render_rays_device(ds, _dev(o), _dev(d), _dev(np.zeros(m)), _dev(np.full(m, tmax)),
-                                _dev(np.full(m, start), torch.int32), f64=True, seg_capacity=512)
+                                _dev(np.full(m, start), torch.int32), f64=True, seg_capacity=512,
+                                view_dirs=cone)
     torch.cuda.synchronize()
+    if cull:
+        dropped = int((ds._view_cells[:, 7] & 31).sum().item())
+        assert dropped > 0.05 * ds.n_edges, dropped
     np.testing.assert_array_equal(res.status.cpu().numpy(), ref["status"])
     np.testing.assert_array_equal(res.ray_counters.cpu().numpy(), ref["counters"])
     assert np.abs(res.rgb.cpu().numpy() - ref["rgb"]).max() <= IMG_TOL
