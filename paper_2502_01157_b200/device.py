@@ -41,6 +41,65 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+class _Uploader:
+    """Host -> device copies of large numpy arrays through a reusable pinned staging
+    ring: the host side fills one chunk with several threads (numpy releases the GIL)
+    while the previous chunk's DMA runs, instead of torch's single-threaded pageable
+    copy (~10 GB/s for the 548 MB of a 1M-site scene)."""
+
+    CHUNK = 32 << 20
+    RING = 3
+    THREADS = 8
+
+    def __init__(self):
+        self.bufs = None
+        self.events = None
+        self.pool = None
+
+    def _setup(self):
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.bufs = [torch.empty(self.CHUNK, dtype=torch.uint8, pin_memory=True)
+                     for _ in range(self.RING)]
+        self.views = [b.numpy() for b in self.bufs]
+        self.events = [None] * self.RING
+        self.pool = ThreadPoolExecutor(self.THREADS)
+
+    def _fill(self, dst: np.ndarray, src: np.ndarray):
+        n = len(src)
+        step = max(1, -(-n // self.THREADS))
+        futs = [self.pool.submit(np.copyto, dst[i:i + step], src[i:i + step])
+                for i in range(0, n, step)]
+        for f in futs:
+            f.result()
+
+    def __call__(self, arr: np.ndarray, device) -> torch.Tensor:
+        arr = np.ascontiguousarray(arr)
+        out = torch.empty(arr.shape, dtype=torch.from_numpy(arr[:0]).dtype, device=device)
+        if arr.nbytes < 2 * self.CHUNK:
+            out.copy_(torch.from_numpy(arr))
+            return out
+        if self.bufs is None:
+            self._setup()
+        src = arr.reshape(-1).view(np.uint8)
+        dst = out.view(-1).view(torch.uint8)
+        stream = torch.cuda.current_stream(device)
+        for k, off in enumerate(range(0, src.nbytes, self.CHUNK)):
+            b = k % self.RING
+            if self.events[b] is not None:
+                self.events[b].synchronize()  # the DMA that last read this buffer is done
+            n = min(self.CHUNK, src.nbytes - off)
+            self._fill(self.views[b][:n], src[off:off + n])
+            dst[off:off + n].copy_(self.bufs[b][:n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self.events[b] = ev
+        return out
+
+
+_upload = _Uploader()
+
+
 def sh_degree_of(sh_coeffs: np.ndarray) -> int:
     """0 when bands 1..15 are all exactly zero (the DC-only kernel is then
     bit-identical), else 3."""
@@ -95,11 +154,11 @@ class DeviceScene:
         with torch.cuda.device(dev):
             # upload first; the scene statistics the layout needs are reductions on
             # the device (one sync) instead of host passes over the 384 MB SH table
-            self.sh = torch.from_numpy(sh).to(dev)
-            pos_d = torch.from_numpy(pos).to(dev)
-            sig_d = torch.from_numpy(sigma).to(dev)
-            off_d = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64)).to(dev)
-            nbr_d = torch.from_numpy(np.ascontiguousarray(neighbors, dtype=np.int64)).to(dev)
+            self.sh = _upload(sh, dev)
+            pos_d = _upload(pos, dev)
+            sig_d = _upload(sigma, dev)
+            off_d = _upload(np.ascontiguousarray(offsets, dtype=np.int64), dev)
+            nbr_d = _upload(np.ascontiguousarray(neighbors, dtype=np.int64), dev)
             if n:
                 st = torch.stack([self.sh.abs().max(),
                                   (self.sh.view(n, 16, 3)[:, 1:, :] != 0).any().double(),
