@@ -486,6 +486,11 @@ __device__ __forceinline__ unsigned order_key(double t) {
 #ifndef RFB_REV_COLREG
 #define RFB_REV_COLREG 1  // reverse pass: load cell + colour together when advancing
 #endif
+#ifndef RFB_REV_SHARED_K
+#define RFB_REV_SHARED_K 1  // reverse reduction: both sums of a lane share one basis column
+                            // (one shared load less per member: 26.0 -> 24.6 ms per config-3
+                            // view; the two values as one 8-byte load (16-float rows): 27.2)
+#endif
 #ifndef RFB_REV_PREFETCH
 #define RFB_REV_PREFETCH 0  // reverse pass: L2 prefetch distance (segments) of the records
 #endif
@@ -583,9 +588,20 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
     bas[16] = 1.0f;
     // reverse-pass output o (two per lane): o < 48 -> dSH[k][ch] = sum f[ch] * basis[k];
     // 48..51 -> (dpos_i xyz, dsigma_i); 52..54 -> dpos_j xyz
+#if RFB_REV_SHARED_K
+    // lane = (half h, basis k): both of its sums use basis[l][k] (one shared load per
+    // member for the two): h 0 -> dSH[k][0], dSH[k][1]; h 1 -> dSH[k][2] and, for k < 7,
+    // the plain sum of value 3 + k (dpos_i xyz, dsigma_i, dpos_j xyz; weight 1)
+    const int kk = lane & 15, hh = lane >> 4;
+    const int c0i = hh ? 2 : 0, c1i = hh ? 3 + (kk < 7 ? kk : 6) : 1;  // (kk >= 7: unused)
+    const int o0 = 3 * kk + c0i;                       // dSH index of acc0
+    const int o1 = hh ? (kk < 7 ? 48 + kk : 64) : 3 * kk + 1;  // acc1: dSH / 48.. / none
+    const float one_sel = hh ? 1.f : 0.f;
+#else
     const int o0 = lane, o1 = lane + 32;
     const int k0 = o0 / 3, c0i = o0 % 3;
     const int k1 = o1 < 48 ? o1 / 3 : 16, c1i = o1 < 48 ? o1 % 3 : 3 + (o1 - 48);
+#endif
     constexpr int RPW = 32 / G;
     const int gl = lane & (G - 1);
     const unsigned gmask = G == 1 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
@@ -970,13 +986,23 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int l = 4 * qd + e;
+#if RFB_REV_SHARED_K
+                        const float b = s_basis[warp][l][kk];
+                        acc0 = __fmaf_rn(s_f[warp][l][c0i], b, acc0);
+                        acc1 = __fmaf_rn(s_f[warp][l][c1i], hh ? one_sel : b, acc1);
+#else
                         acc0 = __fmaf_rn(s_f[warp][l][c0i], s_basis[warp][l][k0], acc0);
                         acc1 = __fmaf_rn(s_f[warp][l][c1i], s_basis[warp][l][k1], acc1);
+#endif
                     }
                 }
             }
             float *row = gr.sh + 48 * (int64_t)lc;
+#if RFB_REV_SHARED_K
+            atomicAdd(row + o0, acc0);  // dSH[k][0] / dSH[k][2]
+#else
             atomicAdd(row + o0, acc0);  // dSH, 32 contiguous floats
+#endif
             if (o1 < 48) {
                 atomicAdd(row + o1, acc1);  // dSH, 16 contiguous floats
             } else if (o1 < 52) {
