@@ -491,6 +491,9 @@ __device__ __forceinline__ unsigned order_key(double t) {
                             // (one shared load less per member: 26.0 -> 24.6 ms per config-3
                             // view; the two values as one 8-byte load (16-float rows): 27.2)
 #endif
+#ifndef RFB_TRAIN_ALPHA32
+#define RFB_TRAIN_ALPHA32 1  // k_train segments: fp32 alpha as k_render (else fp64 exp)
+#endif
 #ifndef RFB_REV_PREFETCH
 #define RFB_REV_PREFETCH 0  // reverse pass: L2 prefetch distance (segments) of the records
 #endif
@@ -640,11 +643,19 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 S, r, start, hoff, epsilon, log_eps, width_floor, step_limit, gl, gmask, nseg,
                 cells, visits,
                 [&](int32_t s, int32_t cell, double sigma, double t0, double t1) {
-                    const double e = exp(-sigma * (t1 - t0));
                     double col[3];
                     const int mask = cell_color<SHDEG, PACKED>(S, cell, bas, r, ctol, col);
+#if RFB_TRAIN_ALPHA32
+                    // k_render's compositing arithmetic (fp32 alpha, fp64 T and weights):
+                    // the training forward outputs equal the render's bit for bit
+                    const double alpha = (double)(-expm1f(-(float)(sigma * (t1 - t0))));
+                    const double w = Tb * alpha;
+                    const double Tn = Tb * (1.0 - alpha);  // T_before[s+1] (kernels.py:275)
+#else
+                    const double e = exp(-sigma * (t1 - t0));
                     const double Tn = Tb * e;  // T_before[s+1] (kernels.py:275)
                     const double w = Tb - Tn;  // T_before[s] * alpha
+#endif
                     wsum += w;
                     const float wf = (float)w;
                     cr += wf * (float)col[0];
