@@ -494,6 +494,9 @@ __device__ __forceinline__ unsigned order_key(double t) {
 #ifndef RFB_TRAIN_ALPHA32
 #define RFB_TRAIN_ALPHA32 1  // k_train segments: fp32 alpha as k_render (else fp64 exp)
 #endif
+#ifndef RFB_REV_SMALL
+#define RFB_REV_SMALL 2  // reverse pass: groups of at most this many lanes scatter per lane
+#endif
 #ifndef RFB_REV_PREFETCH
 #define RFB_REV_PREFETCH 0  // reverse pass: L2 prefetch distance (segments) of the records
 #endif
@@ -947,7 +950,14 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                     }
                 }
             }
-            if (per_lane) {  // this lane's segment straight to its cell (kernels.py:309-337)
+#if RFB_REV_SMALL > 0
+            // a group this small scatters its members' values directly (vector atomics)
+            // instead of paying the shared-memory reduction
+            const bool scatter = per_lane || __popc(__ballot_sync(kFull, in)) <= RFB_REV_SMALL;
+#else
+            const bool scatter = per_lane;
+#endif
+            if (scatter) {  // this lane's segment straight to its cell (kernels.py:309-337)
                 if (in) {
                     const float *b = &s_basis[warp][lane][0];
                     RFB_BOUND(lc, S.n_sites);
