@@ -909,6 +909,7 @@ def main():
                if scene_mb > 126 else
                f"scene ({scene_mb:.0f} MB) fits in L2; no flush (small-config case)")
     fwd_launches = 4 * args.steps * len(views) if args.config != 5 else 0
+    gc = gather_ceilings()
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -949,7 +950,11 @@ def main():
                                      "SURVEY §8d) can exceed 1",
                      "binding_frac": binding_frac,
                      "traffic_source": traffic_src,
-                     "gather_ceilings": gather_ceilings()},
+                     "gather_ceilings": gc,
+                     # the walk's gathers are served by L2 (97% hits): the same achieved
+                     # bytes against the measured per-lane 32-byte L2 gather ceiling
+                     "l2_gather_frac": (achieved / gc["l2_lane32"]
+                                        if achieved and gc and gc.get("l2_lane32") else None)},
         "cpu_baseline": cpu,
         "clocks": clocks if clocks is not None else (fb or {}).get("clocks"),
     }
