@@ -486,19 +486,8 @@ __device__ __forceinline__ unsigned order_key(double t) {
 #ifndef RFB_REV_COLREG
 #define RFB_REV_COLREG 1  // reverse pass: load cell + colour together when advancing
 #endif
-#ifndef RFB_REV_SHARED_K
-#define RFB_REV_SHARED_K 1  // reverse reduction: both sums of a lane share one basis column
-                            // (one shared load less per member: 26.0 -> 24.6 ms per config-3
-                            // view; the two values as one 8-byte load (16-float rows): 27.2)
-#endif
-#ifndef RFB_TRAIN_ALPHA32
-#define RFB_TRAIN_ALPHA32 1  // k_train segments: fp32 alpha as k_render (else fp64 exp)
-#endif
 #ifndef RFB_REV_SMALL
 #define RFB_REV_SMALL 2  // reverse pass: groups of at most this many lanes scatter per lane
-#endif
-#ifndef RFB_REV_PREFETCH
-#define RFB_REV_PREFETCH 0  // reverse pass: L2 prefetch distance (segments) of the records
 #endif
 constexpr int kTrainBlock = 128;
 constexpr int kTrainWarps = kTrainBlock / 32;
@@ -594,7 +583,6 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
     bas[16] = 1.0f;
     // reverse-pass output o (two per lane): o < 48 -> dSH[k][ch] = sum f[ch] * basis[k];
     // 48..51 -> (dpos_i xyz, dsigma_i); 52..54 -> dpos_j xyz
-#if RFB_REV_SHARED_K
     // lane = (half h, basis k): both of its sums use basis[l][k] (one shared load per
     // member for the two): h 0 -> dSH[k][0], dSH[k][1]; h 1 -> dSH[k][2] and, for k < 7,
     // the plain sum of value 3 + k (dpos_i xyz, dsigma_i, dpos_j xyz; weight 1)
@@ -603,11 +591,6 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
     const int o0 = 3 * kk + c0i;                       // dSH index of acc0
     const int o1 = hh ? (kk < 7 ? 48 + kk : 64) : 3 * kk + 1;  // acc1: dSH / 48.. / none
     const float one_sel = hh ? 1.f : 0.f;
-#else
-    const int o0 = lane, o1 = lane + 32;
-    const int k0 = o0 / 3, c0i = o0 % 3;
-    const int k1 = o1 < 48 ? o1 / 3 : 16, c1i = o1 < 48 ? o1 % 3 : 3 + (o1 - 48);
-#endif
     constexpr int RPW = 32 / G;
     const int gl = lane & (G - 1);
     const unsigned gmask = G == 1 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
@@ -648,17 +631,11 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                 [&](int32_t s, int32_t cell, double sigma, double t0, double t1) {
                     double col[3];
                     const int mask = cell_color<SHDEG, PACKED>(S, cell, bas, r, ctol, col);
-#if RFB_TRAIN_ALPHA32
-                    // k_render's compositing arithmetic (fp32 alpha, fp64 T and weights):
-                    // the training forward outputs equal the render's bit for bit
+                    // k_render's compositing arithmetic (fp32 alpha, fp64 T and weights;
+                    // an fp64 exp here measured 0.2 ms slower per config-3 view)
                     const double alpha = (double)(-expm1f(-(float)(sigma * (t1 - t0))));
                     const double w = Tb * alpha;
                     const double Tn = Tb * (1.0 - alpha);  // T_before[s+1] (kernels.py:275)
-#else
-                    const double e = exp(-sigma * (t1 - t0));
-                    const double Tn = Tb * e;  // T_before[s+1] (kernels.py:275)
-                    const double w = Tb - Tn;  // T_before[s] * alpha
-#endif
                     wsum += w;
                     const float wf = (float)w;
                     cr += wf * (float)col[0];
@@ -932,14 +909,6 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
                     cmask = (cm >> 29) & 7;
                     t1 = t0;
                     tb1 = tb0;
-#if RFB_REV_PREFETCH > 0
-                    // the records RFB_REV_PREFETCH segments further back were written
-                    // early in the walk and have left L2: bring them back ahead of use
-                    if (s > RFB_REV_PREFETCH) {
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(rec_a + (s - RFB_REV_PREFETCH) * SL4));
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(rec_b + (s - 1 - RFB_REV_PREFETCH) * SL4));
-                    }
-#endif
                     if (s > 0) {
                         const double2 rb = rec_b[(s - 1) * SL4];  // {t0, T_before[s]}
                         t0 = rb.x;
@@ -1007,23 +976,14 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
                         const int l = 4 * qd + e;
-#if RFB_REV_SHARED_K
                         const float b = s_basis[warp][l][kk];
                         acc0 = __fmaf_rn(s_f[warp][l][c0i], b, acc0);
                         acc1 = __fmaf_rn(s_f[warp][l][c1i], hh ? one_sel : b, acc1);
-#else
-                        acc0 = __fmaf_rn(s_f[warp][l][c0i], s_basis[warp][l][k0], acc0);
-                        acc1 = __fmaf_rn(s_f[warp][l][c1i], s_basis[warp][l][k1], acc1);
-#endif
                     }
                 }
             }
             float *row = gr.sh + 48 * (int64_t)lc;
-#if RFB_REV_SHARED_K
             atomicAdd(row + o0, acc0);  // dSH[k][0] / dSH[k][2]
-#else
-            atomicAdd(row + o0, acc0);  // dSH, 32 contiguous floats
-#endif
             if (o1 < 48) {
                 atomicAdd(row + o1, acc1);  // dSH, 16 contiguous floats
             } else if (o1 < 52) {
@@ -1631,10 +1591,6 @@ __device__ __forceinline__ uint64_t region_bits(const CullCone &cone, uint64_t b
 #ifndef RFB_CULL_MINB
 #define RFB_CULL_MINB 6  // resident 256-thread blocks per SM (memory-level parallelism)
 #endif
-#ifndef RFB_CULL_FILLPAD
-#define RFB_CULL_FILLPAD 0  // pad a culled row to its full original extent (else: to even;
-                            // measured faster: 4x2 cull 0.60 -> 0.56 ms)
-#endif
 constexpr int kCullRows = RFB_CULL_ROWS;
 // Compile-time region grids (RX > 0, (RX + 1)(RY + 1) <= 32 corners): unrolled corner
 // tests on a 32-bit mask and constant shifts; RX == 0: the runtime shape (any grid, or one
@@ -1727,7 +1683,6 @@ __global__ void __launch_bounds__(256, RFB_CULL_MINB) k_cull_rows(const CellHdr 
                 if (real0) m0 = region_mask(cone, nr, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e0[q], pos64));
                 if (real1) m1 = region_mask(cone, nr, cull_bits(cone, nc, hq.x, hq.y, hq.z, xa, e1[q], pos64));
             }
-            const int32_t degp = (deg + 1) & ~1;
             int32_t my_m = 0;  // lane r < nr: region r's kept count (it writes that header)
             float4 *out = edges_out + hq.k0;
 #pragma unroll
@@ -1738,13 +1693,9 @@ __global__ void __launch_bounds__(256, RFB_CULL_MINB) k_cull_rows(const CellHdr 
                 const int32_t n0 = __popc(b0), m = n0 + __popc(b1);
                 if (k0b) out[__popc(b0 & lt)] = e0[q];
                 if (k1b) out[n0 + __popc(b1 & lt)] = e1[q];
-#if RFB_CULL_FILLPAD
-                // the rest of the row's extent gets pads (whole 32-byte sectors written)
-                if (gl >= m && gl < degp) out[gl] = pad;
-                if (gl + kRowLanes >= m && gl + kRowLanes < degp) out[kRowLanes + gl] = pad;
-#else
-                if (gl == 0 && (m & 1)) out[m] = pad;  // the odd row's one pad
-#endif
+                // the odd row's one pad (filling the row's whole original extent so
+                // every sector is written measured slower: 0.60 vs 0.56 ms at 4 x 2)
+                if (gl == 0 && (m & 1)) out[m] = pad;
                 my_m = gl == r ? m : my_m;
             }
             if (gl < nr) header(gl, gl * cone.stride + hq.k0, my_m);

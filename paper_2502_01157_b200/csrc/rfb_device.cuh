@@ -573,8 +573,8 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 // reference's first minimum (their fp64 t is strictly larger than some other
 // neighbour's).
 // Phase 2 (fp64, exactly the reference's expressions on the exact sites):
-// every uncertain neighbour and every front-facing one that was within the
-// running band when it was seen (a superset of the final band) is
+// every uncertain neighbour and every front-facing one whose lower bound is
+// within the final band (one lane: the running band while it is visited) is
 // re-evaluated in CSR order with `denom <= 0 -> skip`, `t < best_t` -- so
 // best_t / best_j are bit-identical to kernels.py:116-133.  With the final-
 // band filter (below) usually only one neighbour is.  Rows longer than 32
@@ -585,18 +585,6 @@ __device__ __forceinline__ void exit_face(const SceneView<PACKED> &S, const Cell
 #endif
 #ifndef RFB_PAIR_UNROLL
 #define RFB_PAIR_UNROLL 2  // edge pairs per unrolled phase-1 iteration (16-byte records)
-#endif
-#ifndef RFB_FINAL_BAND
-#define RFB_FINAL_BAND 1  // drop candidates the final band excludes (one exact evaluation)
-#endif
-#ifndef RFB_UNIFY_P2
-#define RFB_UNIFY_P2 1  // the single-candidate case goes through the candidate loop (one inlined copy)
-#endif
-#ifndef RFB_TWO_PASS
-#define RFB_TWO_PASS 1  // no running candidate mask; several candidates: second pass vs the final U
-#endif
-#if RFB_TWO_PASS && !RFB_FINAL_BAND
-#error "RFB_TWO_PASS needs RFB_FINAL_BAND"
 #endif
 typedef unsigned int cand_mask_t;
 constexpr int kMaskBits = 32;
@@ -682,16 +670,17 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
         }
     };
     if (G == 1) {
-        // Final-band filter: the running band admits every neighbour whose lower
-        // bound beats the upper bound seen SO FAR, so a row visited in CSR order
-        // keeps each new running minimum (~ln(front-facing) + 0.6 ~ 2.7 per
-        // step).  Only the neighbours whose lower bound beats the FINAL band can
-        // be the reference's first minimum; tracked as the two smallest
-        // candidate lower bounds L1 <= L2 and L1's slot: if L2 > U_final, only
-        // L1's neighbour can beat the final band, and it is the best upper
-        // bound's (lb <= ub = U_final), so phase 2 evaluates it alone -- the
-        // same first minimum, bit for bit.  (Folding in a non-candidate's lower
-        // bound, > U_running >= U_final, only makes the test more conservative.)
+        // Final-band filter: only the neighbours whose lower bound beats the FINAL
+        // upper bound U (the minimum over the row of the certain upper bounds) can be
+        // the reference's first minimum.  Phase 1 tracks U, the two smallest candidate
+        // lower bounds L1 <= L2 and L1's slot: if L2 > U, only L1's neighbour can beat
+        // the final band, and it is the best upper bound's (lb <= ub = U), so phase 2
+        // evaluates it alone -- the same first minimum, bit for bit (~1.0 exact
+        // evaluations per step; a running band in CSR order keeps every new running
+        // minimum, ~2.7).  Otherwise (ties, uncertain facing) a second pass over the
+        // row (L1-resident) collects every candidate against the final U.  Either way
+        // the candidates go through one phase-2 loop, so the lanes of a warp never
+        // split over different phase-2 code (round 2: 19.05 -> 18.29 ms per frame).
         float L1 = kInf, L2 = kInf;
         int32_t t1 = -1, slot = 0;
         // slot t of the row ends up as bit (nslots - 1 - t) of `mask`
@@ -700,16 +689,10 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
             bool front, sure;
             bounds(e, lb, ub, front, sure);
             const float lbm = sure ? lb : -kInf;  // uncertain facing: always a candidate
-#if !RFB_TWO_PASS
-            const bool cand = front && lbm <= U;
-            mask = (mask << 1) | (cand ? 1u : 0u);
-#endif
-#if RFB_FINAL_BAND
             const float lbc = front ? lbm : kInf;
             t1 = lbc < L1 ? slot : t1;
             L2 = fminf(L2, fmaxf(L1, lbc));
             L1 = fminf(L1, lbc);
-#endif
             U = sure ? fminf(U, ub) : U;
             ++slot;
         };
@@ -726,24 +709,13 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
             visit(e0);
             visit(e1);
         }
-        if (nslots > kMaskBits) {  // rare: the mask lost bits -- every neighbour exactly
+        if (nslots > kMaskBits) {  // rare: the mask would lose bits -- every neighbour exactly
             for (int32_t k = c.k0; k < c.k1; ++k) exact(k);
             return;
         }
-#if RFB_FINAL_BAND
         if (t1 >= 0 && L2 > U && L1 <= U) {  // only L1's neighbour can be the first minimum
-#if RFB_UNIFY_P2
-            mask = 1u << (nslots - 1 - t1);  // one phase-2 site for every lane (no divergence)
-#else
-            exact(c.k0 + t1);
-            return;
-#endif
-        }
-#if RFB_TWO_PASS
-        else if (t1 >= 0) {
-            // several candidates beat the final band: collect them against the final U
-            // (a subset of the running band, same guarantee) in a second pass over the row
-            // (L1-resident); only here does the candidate mask get built
+            mask = 1u << (nslots - 1 - t1);
+        } else if (t1 >= 0) {  // several candidates: collect them against the final U
             for (int32_t kp = c.k0; kp < c.k1; kp += 2) {
                 float4 e0, e1;
                 ldg256(S.edge + kp, e0, e1);
@@ -757,8 +729,6 @@ __device__ __forceinline__ void exit_face_f32(const SceneView<PK> &S, int32_t ci
                 }
             }
         }
-#endif
-#endif
         while (mask) {  // highest bit = lowest slot: CSR order
             const int b = 31 - __clz((int)mask);
             mask &= ~(1u << b);
