@@ -376,7 +376,11 @@ int rfb_render_image(const rfb_scene *scene, const rfb_camera *camera, const rfb
 
 /* Workspace bytes needed by the calls above for m rays (kind: 0 forward,
  * 1 backward/train with any loss, 2 backward / train without the quantile
- * term: 8-byte segment records instead of 32). */
+ * term).  Forward calls accept >= 256 bytes; from 256 + 8 (SMs + 1) on they
+ * keep one work queue per SM (an SM's warps walk neighbouring pixel patches
+ * together and share the cells' data in L1; same results).  Backward / train:
+ * a 4 KB header of work counters, then the segment records of the resident
+ * rays. */
 size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind);
 
 /* Forward + reverse pass for arbitrary colour adjoints [m][3] f64.  out.rgb

@@ -267,6 +267,29 @@ __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
 // result equals compositing after the walk).  Warps fetch 32/G rays at a
 // time from a global counter (persistent grid).
 // ---------------------------------------------------------------------------
+#ifndef RFB_SM_LOCAL
+#define RFB_SM_LOCAL 1  // per-SM tile queues (fetch_unit) when the workspace has room
+#endif
+// Work distribution over units of RPW rays (consecutive units = neighbouring warp patches,
+// 32 of them = one 32 x 32 image tile in rfb_render_image's tile order).  n_v > 0: the
+// grid is n_v x (blocks per SM), and block b works for virtual SM v = b % n_v (blocks of
+// one wave are spread one per SM, so the blocks sharing v normally sit on one SM): 95% of
+// the 32-unit groups are dealt round-robin to the virtual SMs, each with its own counter
+// (ctr[1 + v]), so an SM's warps walk one image tile together and share its cells'
+// headers, rows and SH rows in L1; the rest are handed out from ctr[0] (the tail).
+// n_v == 0: one global counter (ctr[0]).
+__device__ __forceinline__ int64_t fetch_unit(unsigned long long *ctr, int64_t U, int n_v) {
+    if (n_v <= 0) return (int64_t)atomicAdd(ctr, 1ull);
+    const int64_t T = (U + 31) / 32;
+    const int64_t per = (T * 19 / 20) / n_v;  // static 32-unit groups per virtual SM
+    const int v = blockIdx.x % n_v;  // (%smid itself: 11.80 vs 11.87 ms, but ids need not be dense)
+    if (per > 0) {
+        const unsigned long long u = atomicAdd(ctr + 1 + v, 1ull);
+        if ((int64_t)u < per * 32) return (v + (int64_t)n_v * (int64_t)(u >> 5)) * 32 + (int64_t)(u & 31);
+    }
+    return per * n_v * 32 + (int64_t)atomicAdd(ctr, 1ull);
+}
+
 #ifndef RFB_FWD_MINB
 #define RFB_FWD_MINB 4
 #endif
@@ -278,7 +301,7 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
                                                 const __grid_constant__ Src src, double epsilon,
                                                 double log_eps, double width_floor,
                                                 int32_t step_limit, FwdOut O,
-                                                unsigned long long *ray_counter) {
+                                                unsigned long long *ray_counter, int32_t n_v) {
     constexpr int RPW = 32 / G;
     // per thread: the ray's fp64 constants + sum|basis| (field-major, conflict-free);
     // shared-origin sources keep only the direction per thread
@@ -294,14 +317,15 @@ __global__ void __launch_bounds__(256, RFB_FWD_MINB) k_render(SceneView<PACKED> 
     const int gl = lane & (G - 1);
     const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
     const int64_t total = src.count();
+    const int64_t units = (total + RPW - 1) / RPW;
     unsigned int my_cells = 0, my_visits = 0;
 
     for (;;) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(ray_counter, (unsigned long long)RPW);
-        base = __shfl_sync(kFull, base, 0);
-        if ((int64_t)base >= total) break;
-        int64_t q = (int64_t)base + lane / G;
+        long long unit = 0;
+        if (lane == 0) unit = (long long)fetch_unit(ray_counter, units, n_v);
+        unit = __shfl_sync(kFull, unit, 0);
+        if ((int64_t)unit >= units) break;
+        int64_t q = (int64_t)unit * RPW + lane / G;
         if (q >= total) continue;
         int64_t oidx;
         int32_t start;
@@ -490,6 +514,7 @@ __device__ __forceinline__ unsigned order_key(double t) {
 #define RFB_REV_SMALL 2  // reverse pass: groups of at most this many lanes scatter per lane
 #endif
 constexpr int kTrainBlock = 128;
+constexpr size_t kTrainWsHdr = 4096;  // training workspace: work counters, then the records
 constexpr int kTrainWarps = kTrainBlock / 32;
 
 // resident blocks per SM (register budget): 7 x 128 threads (72 regs) for the
@@ -552,7 +577,7 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
     SceneView<PACKED> S, ArrayRays src, double epsilon, double log_eps, double width_floor,
     int32_t step_limit, const double *adjoints, const double *targets, double rgb_scale,
     double q_scale, const double *u_pairs, int32_t n_pairs, double weight_floor, FwdOut O,
-    Grads gr, double *loss, Scratch scr, unsigned long long *ray_counter) {
+    Grads gr, double *loss, Scratch scr, unsigned long long *ray_counter, int32_t n_v) {
     // per lane: 16 basis values + a constant 1 (column 16) used by the plain sums
     __shared__ float s_basis[kTrainWarps][32][17];
     // per lane per reverse iteration: f_r, f_g, f_b, dpos_i xyz, dsigma_i, dpos_j xyz
@@ -595,12 +620,13 @@ __global__ void __launch_bounds__(kTrainBlock, QUANT ? RFB_TRAIN_MINB_Q : RFB_TR
     const int gl = lane & (G - 1);
     const unsigned gmask = G == 1 ? kFull : (((1u << G) - 1u) << (lane & ~(G - 1)));
 
+    const int64_t units = (total + RPW - 1) / RPW;
     for (;;) {
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(ray_counter, (unsigned long long)RPW);
-        base = __shfl_sync(kFull, base, 0);
-        if ((int64_t)base >= total) break;
-        const int64_t qs = (int64_t)base + lane / G;
+        long long unit = 0;
+        if (lane == 0) unit = (long long)fetch_unit(ray_counter, units, n_v);
+        unit = __shfl_sync(kFull, unit, 0);
+        if ((int64_t)unit >= units) break;
+        const int64_t qs = (int64_t)unit * RPW + lane / G;
         const bool have_ray = qs < total;
         const int64_t q = have_ray ? src.index(qs) : 0;  // ray id (optional order)
 
@@ -1875,39 +1901,45 @@ static void prefer_carveout() {
 template <int G, int PACKED, class Src>
 static void launch_render_g(const rfb_scene *scene, const Src &src, double eps, double log_eps,
                             double wf, int32_t sl, const FwdOut &O, unsigned long long *ctr,
-                            cudaStream_t st) {
+                            int sm_local, cudaStream_t st) {
     SceneView<PACKED> S = view<PACKED>(scene);
     int per_sm = 0;
     if (scene->sh_degree == 0) {
         auto k = k_render<G, 0, PACKED, Src>;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
-        k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr);
+        k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr,
+                                                           sm_local ? num_sms() : 0);
     } else {
         auto k = k_render<G, 3, PACKED, Src>;
         prefer_carveout<k_render<G, 3, PACKED, Src>>();
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 256, 0);
-        k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr);
+        k<<<num_sms() * std::max(per_sm, 1), 256, 0, st>>>(S, src, eps, log_eps, wf, sl, O, ctr,
+                                                           sm_local ? num_sms() : 0);
     }
 }
 
 template <int G, class Src>
 static void launch_render_p(const rfb_scene *scene, const Src &src, double eps, double log_eps,
                             double wf, int32_t sl, const FwdOut &O, unsigned long long *ctr,
-                            cudaStream_t st) {
+                            int sm_local, cudaStream_t st) {
     if (scene->packed && !scene->positions_f64)
-        launch_render_g<G, 1>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
+        launch_render_g<G, 1>(scene, src, eps, log_eps, wf, sl, O, ctr, sm_local, st);
     else if (scene->packed && G <= 2)  // fp64 sites: widened bound (G > 2: generic walk)
-        launch_render_g<G, 2>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
+        launch_render_g<G, 2>(scene, src, eps, log_eps, wf, sl, O, ctr, sm_local, st);
     else
-        launch_render_g<G, 0>(scene, src, eps, log_eps, wf, sl, O, ctr, st);
+        launch_render_g<G, 0>(scene, src, eps, log_eps, wf, sl, O, ctr, sm_local, st);
 }
 
 template <class Src>
 static int launch_render(const rfb_scene *scene, const Src &src, const rfb_params *p,
                          const rfb_fwd_out *out, void *ws, size_t ws_bytes, cudaStream_t st) {
     if (!ws || ws_bytes < 256) return RFB_EINVAL;
-    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(ws);
-    cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
+    // counters at ws + 256: [0] global, [1 + v] per virtual SM (when the workspace has room)
+    unsigned long long *ctr = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(ws) + 256);
+    const size_t sm_bytes = 8 * (size_t)(num_sms() + 1);
+    int sm_local = RFB_SM_LOCAL && ws_bytes >= 256 + sm_bytes;
+    if (ws_bytes < 256 + 8) ctr = reinterpret_cast<unsigned long long *>(ws);  // (legacy 256 B)
+    cudaMemsetAsync(ctr, 0, sm_local ? sm_bytes : 8, st);
     FwdOut O = dev_out(out);
     double log_eps = p->epsilon > 0.0 ? std::log(p->epsilon) : 0.0;
     int g = p->lanes_per_ray;
@@ -1924,12 +1956,12 @@ static int launch_render(const rfb_scene *scene, const Src &src, const rfb_param
     const double e = p->epsilon, wf = p->width_floor;
     const int32_t sl = p->step_limit;
     switch (g) {
-        case 1: launch_render_p<1>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
-        case 2: launch_render_p<2>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
-        case 4: launch_render_p<4>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
-        case 8: launch_render_p<8>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
-        case 16: launch_render_p<16>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
-        case 32: launch_render_p<32>(scene, src, e, log_eps, wf, sl, O, ctr, st); break;
+        case 1: launch_render_p<1>(scene, src, e, log_eps, wf, sl, O, ctr, sm_local, st); break;
+        case 2: launch_render_p<2>(scene, src, e, log_eps, wf, sl, O, ctr, sm_local, st); break;
+        case 4: launch_render_p<4>(scene, src, e, log_eps, wf, sl, O, ctr, sm_local, st); break;
+        case 8: launch_render_p<8>(scene, src, e, log_eps, wf, sl, O, ctr, sm_local, st); break;
+        case 16: launch_render_p<16>(scene, src, e, log_eps, wf, sl, O, ctr, sm_local, st); break;
+        case 32: launch_render_p<32>(scene, src, e, log_eps, wf, sl, O, ctr, sm_local, st); break;
         default: return RFB_EINVAL;
     }
     return (int)cudaGetLastError();
@@ -1962,12 +1994,12 @@ static void launch_train_p(const rfb_scene *scene, dim3 grid, cudaStream_t st, b
                            int32_t sl, const double *adj, const double *tg, double rgb_scale,
                            double q_scale, const double *up, int32_t np, double wfloor,
                            const FwdOut &O, const Grads &G, double *loss, const Scratch &scr,
-                           unsigned long long *ctr) {
+                           unsigned long long *ctr, int32_t n_v) {
     SceneView<PACKED> S = view<PACKED>(scene);
 #define RFB_TRAIN1(SH, TR, QU, L)                                                             \
     k_train<SH, PACKED, TR, QU, L><<<grid, kTrainBlock, 0, st>>>(                               \
         S, src, eps, log_eps, wf, sl, adj, tg, rgb_scale, q_scale, up, np, wfloor, O, G, loss, \
-        scr, ctr)
+        scr, ctr, n_v)
 #define RFB_TRAIN(SH, TR, QU)                                                                 \
     do {                                                                                       \
         if (lanes == 2) RFB_TRAIN1(SH, TR, QU, 2); else RFB_TRAIN1(SH, TR, QU, 1);             \
@@ -2002,8 +2034,8 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     if (!train && !adjoints) return RFB_EINVAL;
     const bool quant = train && q_scale > 0.0;
     const int64_t per = bwd_slot_bytes(p->step_limit, quant);
-    if (!ws || ws_bytes < 256 + (size_t)per * kTrainBlock) return RFB_EINVAL;
-    int64_t slots = (int64_t)((ws_bytes - 256) / (size_t)per);
+    if (!ws || ws_bytes < kTrainWsHdr + (size_t)per * kTrainBlock) return RFB_EINVAL;
+    int64_t slots = (int64_t)((ws_bytes - kTrainWsHdr) / (size_t)per);
     if (p->lanes_per_ray < 0 || p->lanes_per_ray > 2) return RFB_EINVAL;
     const int lanes = p->lanes_per_ray > 0 ? p->lanes_per_ray : train_lanes(rays->m, quant);
     slots = std::min<int64_t>(slots, bwd_slots_max(quant));
@@ -2015,12 +2047,15 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     Scratch scr;
     scr.slots = slots;
     const int64_t cap = p->step_limit;
-    char *c = base + 256;
+    char *c = base + kTrainWsHdr;
     scr.a = reinterpret_cast<float4 *>(c);
     scr.c = reinterpret_cast<uint2 *>(c);  // (compact and full records share the space)
     c += cap * slots * 16;
     scr.b = reinterpret_cast<double2 *>(c);
-    cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st);
+    // per-SM work queues (fetch_unit) when the grid is whole waves of num_sms() blocks
+    const int64_t nblk = slots / kTrainBlock;
+    const int32_t n_v = (RFB_SM_LOCAL && nblk % num_sms() == 0 && nblk >= num_sms()) ? num_sms() : 0;
+    cudaMemsetAsync(ctr, 0, 8 * (size_t)(n_v + 1), st);
     FwdOut O = dev_out(out);
     ArrayRays src{rays->origins, rays->directions, rays->t_min, rays->t_max, rays->start_sites,
                   rays->m, rays->order, rays->region};
@@ -2030,15 +2065,15 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     if (scene->packed && !scene->positions_f64)
         launch_train_p<1>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
                           p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
-                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
+                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr, n_v);
     else if (scene->packed)
         launch_train_p<2>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
                           p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
-                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
+                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr, n_v);
     else
         launch_train_p<0>(scene, grid, st, train, lanes, src, p->epsilon, log_eps,
                           p->width_floor, p->step_limit, adjoints, targets, rgb_scale, q_scale,
-                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr);
+                          u_pairs, n_pairs, wfloor, O, G, loss, scr, ctr, n_v);
     return (int)cudaGetLastError();
 }
 
@@ -2297,13 +2332,13 @@ int rfb_locate_seeded(const rfb_scene *scene, const double *queries, int64_t m,
 }
 
 size_t rfb_workspace_bytes(int64_t m, int32_t step_limit, int32_t kind) {
-    if (kind == 0) return 256;
+    if (kind == 0) return 256 + 8 * (size_t)(num_sms() + 1);  // + the per-SM work counters
     const bool quant = kind != 2;  // 2: no quantile term (compact records)
     int64_t slots = std::min<int64_t>(quant ? std::max(bwd_slots_max(false), bwd_slots_max(true))
                                             : bwd_slots_max(false),
                                       ((2 * m + kTrainBlock - 1) / kTrainBlock) * kTrainBlock);
     slots = std::max<int64_t>(slots, kTrainBlock);
-    return 256 + (size_t)slots * (size_t)bwd_slot_bytes(step_limit, quant);
+    return kTrainWsHdr + (size_t)slots * (size_t)bwd_slot_bytes(step_limit, quant);
 }
 
 int rfb_render_rays(const rfb_scene *scene, const rfb_rays *rays, const rfb_params *params,

@@ -30,6 +30,8 @@ DEFAULT_EPSILON = 1e-3     # tracer/rays.py:12
 DEFAULT_STEP_LIMIT = 4096  # tracer/rays.py:13
 WIDTH_FLOOR_SCALE = 1e-12  # tracer/rays.py:14
 DEFAULT_LANES = 0  # auto (rfb.h: rfb_params.lanes_per_ray)
+# forward workspace: 256 bytes + room for the per-SM work counters (rfb.h rfb_render_rays)
+FWD_WORKSPACE_BYTES = 4096
 
 
 def _ptr(t):
@@ -644,7 +646,7 @@ def render_rays_device(ds: DeviceScene, origins, directions, t_min, t_max, start
     (``DeviceScene.view_camera``), a smaller cone per ray."""
     m = origins.shape[0]
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=per_ray, seg_capacity=seg_capacity)
-    ws = (workspace or Workspace(ds.device)).get(256)
+    ws = (workspace or Workspace(ds.device)).get(FWD_WORKSPACE_BYTES)
     p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
     order = _order32(order, m, ds.device)
     rays = rays_struct(origins, directions, t_min, t_max, start, order)
@@ -708,7 +710,7 @@ def render_image_device(ds: DeviceScene, camera, *, epsilon=DEFAULT_EPSILON,
         tx, ty = tile_grid(W, H, tile_w, tile_h)
         tile_ids = torch.arange(tx * ty, dtype=torch.int32, device=ds.device)
     res = out or alloc_forward(m, ds.device, f64=f64, per_ray=per_ray)
-    ws = (workspace or Workspace(ds.device)).get(256)
+    ws = (workspace or Workspace(ds.device)).get(FWD_WORKSPACE_BYTES)
     if t_max is None:
         t_max = ds.default_t_max(np.asarray(camera.pose)[:3, 3][None, :])
     p = make_params(epsilon, ds.width_floor, step_limit, lanes_per_ray)
