@@ -267,6 +267,12 @@ __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
 // result equals compositing after the walk).  Warps fetch 32/G rays at a
 // time from a global counter (persistent grid).
 // ---------------------------------------------------------------------------
+#ifndef RFB_SM_STATIC_PCT
+#define RFB_SM_STATIC_PCT 80  // share of the 32-unit groups dealt statically to the SM queues
+#endif
+#ifndef RFB_TRAIN_SM_LOCAL
+#define RFB_TRAIN_SM_LOCAL 0  // (config 5: 258 vs 244 ms with; config 3: same)
+#endif
 #ifndef RFB_SM_LOCAL
 #define RFB_SM_LOCAL 1  // per-SM tile queues (fetch_unit) when the workspace has room
 #endif
@@ -281,7 +287,7 @@ __device__ __forceinline__ double basis_setup(const Ray &r, float *basis_f) {
 __device__ __forceinline__ int64_t fetch_unit(unsigned long long *ctr, int64_t U, int n_v) {
     if (n_v <= 0) return (int64_t)atomicAdd(ctr, 1ull);
     const int64_t T = (U + 31) / 32;
-    const int64_t per = (T * 19 / 20) / n_v;  // static 32-unit groups per virtual SM
+    const int64_t per = (T * RFB_SM_STATIC_PCT / 100) / n_v;  // static 32-unit groups per virtual SM
     const int v = blockIdx.x % n_v;  // (%smid itself: 11.80 vs 11.87 ms, but ids need not be dense)
     if (per > 0) {
         const unsigned long long u = atomicAdd(ctr + 1 + v, 1ull);
@@ -514,7 +520,10 @@ __device__ __forceinline__ unsigned order_key(double t) {
 #define RFB_REV_SMALL 2  // reverse pass: groups of at most this many lanes scatter per lane
 #endif
 constexpr int kTrainBlock = 128;
-constexpr size_t kTrainWsHdr = 4096;  // training workspace: work counters, then the records
+#ifndef RFB_TRAIN_WS_HDR
+#define RFB_TRAIN_WS_HDR 4096
+#endif
+constexpr size_t kTrainWsHdr = RFB_TRAIN_WS_HDR;  // training workspace: work counters, then records
 constexpr int kTrainWarps = kTrainBlock / 32;
 
 // resident blocks per SM (register budget): 7 x 128 threads (72 regs) for the
@@ -2054,7 +2063,9 @@ static int launch_backward(const rfb_scene *scene, const rfb_rays *rays, const r
     scr.b = reinterpret_cast<double2 *>(c);
     // per-SM work queues (fetch_unit) when the grid is whole waves of num_sms() blocks
     const int64_t nblk = slots / kTrainBlock;
-    const int32_t n_v = (RFB_SM_LOCAL && nblk % num_sms() == 0 && nblk >= num_sms()) ? num_sms() : 0;
+    const int32_t n_v = (RFB_SM_LOCAL && RFB_TRAIN_SM_LOCAL && nblk % num_sms() == 0 &&
+                         nblk >= num_sms() && kTrainWsHdr >= 8 * (size_t)(num_sms() + 1))
+                            ? num_sms() : 0;
     cudaMemsetAsync(ctr, 0, 8 * (size_t)(n_v + 1), st);
     FwdOut O = dev_out(out);
     ArrayRays src{rays->origins, rays->directions, rays->t_min, rays->t_max, rays->start_sites,
