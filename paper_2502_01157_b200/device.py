@@ -49,9 +49,9 @@ class _Uploader:
     while the previous chunk's DMA runs, instead of torch's single-threaded pageable
     copy (~10 GB/s for the 548 MB of a 1M-site scene)."""
 
-    CHUNK = 32 << 20
+    CHUNK = int(os.environ.get("RFB_UPLOAD_CHUNK_MB", "32")) << 20
     RING = 3
-    THREADS = 8
+    THREADS = int(os.environ.get("RFB_UPLOAD_THREADS", "8"))
 
     def __init__(self):
         self.bufs = None
