@@ -557,7 +557,7 @@ def main():
     # back-facing for the whole frame (rfb_cull_scene); the visit counter adds them back
     # (n1max's low bits), so count them once more on the view with those bits cleared
     V_walk = V_tot
-    if ds.packed and dv.view_cone(views[0]) is not None and ds.VIEW_CULL:
+    if ds.can_cull(views[0], W * H // world):
         ds.view_camera(views[0])
         ds._view_cells[:, 7].bitwise_and_(~31)
         diag = dv.render_image_device(ds, views[0], per_ray=False, lanes_per_ray=lanes,
@@ -666,7 +666,8 @@ def main():
         torch.cuda.synchronize()
         barrier()
         fb_ms = e0.elapsed_time(e1)
-        fb_launches = args.steps * len(batches)
+        fb_launches = args.steps * sum(2 if ds.can_cull(b[-1][0], len(b[-1][1])) else 1
+                                       for b in batches)
         clocks_fb = clk2.stop() if rank == 0 else None
         t = torch.tensor([fb_ms], dtype=torch.float64, device=dev)
         if dist_on:
@@ -908,7 +909,8 @@ def main():
     l2_note = (f"inputs larger than L2 (scene {scene_mb:.0f} MB vs 126 MB L2); no flush"
                if scene_mb > 126 else
                f"scene ({scene_mb:.0f} MB) fits in L2; no flush (small-config case)")
-    fwd_launches = 4 * args.steps * len(views) if args.config != 5 else 0
+    culled = ds.can_cull(views[0], W * H // world)
+    fwd_launches = (4 if culled else 3) * args.steps * len(views) if args.config != 5 else 0
     gc = gather_ceilings()
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -931,9 +933,9 @@ def main():
         "train_iteration": train_iter,
         "gpu_launches": fwd_launches + fb_launches,
         "gpu_launches_detail": {"forward": fwd_launches, "fwd_bwd": fb_launches,
-                                "per_forward_view": "k_cull_rows (4x2 regions), k_nearest_dist, "
+                                "per_forward_view": ("k_cull_rows (4x2 regions), " if culled else "") + "k_nearest_dist, "
                                                     "k_nearest_id, k_render",
-                                "per_fwd_bwd_view": "k_cull_rows, k_train"},
+                                "per_fwd_bwd_view": ("k_cull_rows, " if culled else "") + "k_train"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if achieved else None, "traffic": traffic,
                      "peak_kind": peak_kind, "kernel": roof_kernel,
