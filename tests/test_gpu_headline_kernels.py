@@ -302,3 +302,24 @@ def test_render_image_per_sm_queues_960x540(cuda_ok, sa100k, ds100k):
     # every pixel written by exactly one ray: the frame's counters add up to the per-ray sums
     np.testing.assert_array_equal(res.counters.cpu().numpy(),
                                   res.ray_counters.to(torch.int64).sum(0).cpu().numpy())
+
+
+def test_view_batch_without_culling(cuda_ok, sa100k, ds100k, monkeypatch):
+    """A ray batch passed with view=(camera, pixels) when culling does not apply (culling
+    off, or a batch too small to pay for the pass) walks the full rows: same outputs."""
+    from paper_2502_01157_b200 import device as dv
+
+    W, H = 160, 96
+    cam = _cam(W, H, 1)
+    o, dirs, start, t_max = _view_batch(cam, ds100k)
+    m = len(dirs)
+    perm = torch.from_numpy(dv.tile_order(W, H))
+    args = (_d(o), _d(dirs), _d(np.zeros(m)), _d(t_max), _d(np.full(m, start), torch.int32))
+    assert not ds100k.can_cull(cam, m)  # 15,360 rays: below the floor
+    a = dv.render_rays_device(ds100k, *args, f64=True, view=(cam, perm))
+    monkeypatch.setattr(ds100k, "VIEW_CULL", False)
+    b = dv.render_rays_device(ds100k, *args, f64=True, view=(cam, perm))
+    c = dv.render_rays_device(ds100k, *args, f64=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a.rgb, c.rgb) and torch.equal(b.rgb, c.rgb)
+    assert torch.equal(a.ray_counters, c.ray_counters)
